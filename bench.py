@@ -1,0 +1,434 @@
+#!/usr/bin/env python3
+"""Benchmark of the arXiv 1811.11226 Sec. IV augmentation hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c3|c5|c2|c4] [--variant auto|gather|staged]
+
+One step = one pass of the whole hot path (affine warp of image + labels with
+noise, window/clamp and gamma) over one batch.
+Default workload = BASELINE.json configs[2] ("c3": 16 x 128x128x160 volumes
+per GPU, the training-iteration shape); N GPUs shard volumes by GLOBAL index
+(weak scaling, no collective on the data path; NCCL only gathers timings).
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "augmented GVoxel/s (image+label)"
+UNIT = "GVoxel/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+WORKLOADS = {
+    "c3": dict(shape=(160, 128, 128), per_gpu=16, ranges="train",
+               desc="16 x 128x128x160 f32 CT + u8 labels per GPU (BASELINE configs[2])"),
+    "c5": dict(shape=(160, 128, 128), total=256, ranges="train",
+               desc="256 x 128x128x160 f32 CT + u8 labels sharded over N GPUs (configs[4])"),
+    "c2": dict(shape=(160, 128, 128), per_gpu=1, ranges="train",
+               desc="1 x 128x128x160 f32 CT + u8 labels per GPU (configs[1])"),
+    "c4": dict(shape=(512, 512, 512), per_gpu=1, ranges="large",
+               desc="1 x 512^3 f32 CT + u8 labels per GPU, large rotations (configs[3])"),
+}
+N_DISTINCT_PHANTOMS = 4  # input volumes cycle over 4 seeded phantoms (DESIGN.md input recipe)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--variant", choices=["auto", "gather", "staged"], default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work of the bounded oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def shard(workload, world, rank):
+    """Global volume indices of this rank (contiguous block)."""
+    w = WORKLOADS[workload]
+    if "per_gpu" in w:
+        per = w["per_gpu"]
+        return list(range(rank * per, (rank + 1) * per)), per * world
+    total = w["total"]
+    lo = rank * total // world
+    hi = (rank + 1) * total // world
+    return list(range(lo, hi)), total
+
+
+def ranges_of(workload):
+    return synth.TRAIN if WORKLOADS[workload]["ranges"] == "train" else synth.LARGE
+
+
+def host_inputs(shape, vids):
+    """Seeded phantoms (cycled) for the given global volume ids; uint8 labels."""
+    base = {}
+    imgs = np.empty((len(vids), *shape), np.float32)
+    lbls = np.empty((len(vids), *shape), np.uint8)
+    for i, v in enumerate(vids):
+        k = v % N_DISTINCT_PHANTOMS
+        if k not in base:
+            base[k] = synth.phantom(shape, seed=synth.MASTER_SEED + k)
+        imgs[i], lbls[i] = base[k]
+    return imgs, lbls
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload, variant):
+    """dram bytes per launch of the warp kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(f"{workload}/{variant}")
+    return None if e is None else float(e["dram_bytes_per_launch"])
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:  # noqa: BLE001
+            self._ok = False
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._ok:
+            self._t.join()
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        reasons = [n for b, n in self.NAMES.items() if self.reasons & b and b != 0x1]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(shape, vids, ranges, imgs, lbls, cpu_seconds, max_voxels=None):
+    """Time the oracle (as it stands) on whole volumes of the workload, threads =
+    host cores, one oracle call per (volume, z-slab).  Returns (voxels, seconds, cores)."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    nz, ny, nx = shape
+    slab = max(1, nz // 8)
+    jobs = []
+    for i, v in enumerate(vids):
+        d = synth.draw(ranges, v)
+        A = O.compose_affine(O.make_geom(d.rot_rad, d.scale, d.shear, d.flip, d.generic, d.disp),
+                             shape, shape)[1]
+        ph = O.photometric(O.NOISE | O.WINDOW | O.CLAMP | O.GAMMA, window=d.window,
+                           gamma=d.gamma, sigma=d.sigma, seed=synth.MASTER_SEED, volume_id=v)
+        for z0 in range(0, nz, slab):
+            zz = np.arange(z0, min(nz, z0 + slab))
+            xyz = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), zz, indexing="ij"),
+                           -1).reshape(-1, 3).astype(np.int32)
+            jobs.append((i, A, ph, xyz))
+    # calibrate: one slab single-threaded, then size the sample to ~cpu_seconds of CPU work
+    t0 = time.perf_counter()
+    i, A, ph, xyz = jobs[0]
+    O.warp_points(imgs[i], lbls[i], A, xyz, shape, 0, -1000.0, 0, ph)
+    per_vox = (time.perf_counter() - t0) / len(xyz)
+    budget_vox = int(cpu_seconds / max(per_vox, 1e-12))
+    if max_voxels:
+        budget_vox = min(budget_vox, max_voxels)
+    sel, acc = [], 0
+    k = 0
+    while acc < budget_vox:
+        sel.append(jobs[k % len(jobs)])
+        acc += len(jobs[k % len(jobs)][3])
+        k += 1
+
+    def run(job):
+        i, A, ph, xyz = job
+        O.warp_points(imgs[i], lbls[i], A, xyz, shape, 0, -1000.0, 0, ph)
+        return len(xyz)
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
+        vox = sum(ex.map(run, sel))
+    return vox, time.perf_counter() - t0, cores
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    wl = WORKLOADS[args.workload]
+    shape = wl["shape"]
+    vids, total = shard(args.workload, world, 0)
+    ranges = ranges_of(args.workload)
+    imgs, lbls = host_inputs(shape, vids[:N_DISTINCT_PHANTOMS])
+    vids = vids[:N_DISTINCT_PHANTOMS]
+    # each step: a bounded sample (~0.25 s of CPU work) of the same workload
+    per_step = max(0.05, min(0.25, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(shape, vids, ranges, imgs, lbls, per_step)
+    tot_vox, tot_s, cores = 0, 0.0, 1
+    for _ in range(args.steps):
+        v, s, cores = oracle_sample(shape, vids, ranges, imgs, lbls, per_step)
+        tot_vox += v
+        tot_s += s
+    value = tot_vox / tot_s / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{tot_vox} output voxels of the workload's volumes "
+                                   f"(z-slabs, {len(vids)} volumes cycled), oracle_warp_points "
+                                   f"on {cores} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(args, world):
+    wl = WORKLOADS[args.workload]
+    nz, ny, nx = wl["shape"]
+    per = wl.get("per_gpu")
+    return {"workload": f"{args.workload}: {wl['desc']}", "dims_xyz": [nx, ny, nz],
+            "volumes_per_gpu": per if per else wl["total"] // world,
+            "global_batch": per * world if per else wl["total"],
+            "transforms": wl["ranges"], "photometric": "noise+window+clamp+gamma",
+            "kernel_variant": args.variant,
+            "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"dp{world} (volume shards, no data-path collective)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    import build
+    if rank == 0:
+        build.build_cuda()
+    if world > 1:
+        dist.barrier()
+    import paper_1811_11226_b200 as W
+    from paper_1811_11226_b200.augment import FULL, build_params
+
+    variant = {"auto": W.KERNEL_AUTO, "gather": W.KERNEL_GATHER, "staged": W.KERNEL_STAGED}[
+        args.variant]
+    wl = WORKLOADS[args.workload]
+    shape = wl["shape"]
+    vids, global_batch = shard(args.workload, world, rank)
+    ranges = ranges_of(args.workload)
+    draws = [synth.draw(ranges, v) for v in vids]
+    params = build_params(draws, vids, shape, shape, FULL, seed=synth.MASTER_SEED)
+    imgs, lbls = host_inputs(shape, vids)
+    B = len(vids)
+    nvox_out = int(np.prod(shape))
+    t_img = torch.from_numpy(imgs).to(dev)
+    t_lbl = torch.from_numpy(lbls).to(dev)
+    batch = W.AugmentBatch(t_img, t_lbl, params, fill=-1000.0, label_fill=0, variant=variant)
+
+    # algorithmic bytes: 5 B written per output voxel
+    # + 4 B per distinct input image voxel read + 1 B per distinct label voxel read
+    f_img = f_lbl = 0
+    for c0 in range(0, B, 64):
+        a, b = W.warp3d_footprint_batched(params[c0:c0 + 64], shape, shape, device=dev)
+        f_img += a
+        f_lbl += b
+    alg_bytes = 5 * B * nvox_out + 4 * f_img + 1 * f_lbl
+    naive_bytes = 10 * B * nvox_out
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, args.warmup)):
+        flush.fill_(1)
+        batch.run()
+    torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = W.warp3d_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)            # L2 flush between timed steps (not timed)
+            starts[k].record(stream)
+            batch.run()
+            ends[k].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = W.warp3d_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = global_batch * nvox_out * args.steps / (max_ms * 1e-3) / 1e9
+
+    # e2e: pinned host buffers -> H2D -> warp -> D2H, inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(W, torch, dev, imgs, lbls, params, shape, min(args.steps, 20), world,
+                      global_batch, nvox_out)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, s, cores = oracle_sample(shape, vids, ranges, imgs, lbls, args.cpu_seconds)
+        cpu = {"value": v / s / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{v} output voxels of this workload (z-slabs of its volumes), "
+                         f"oracle_warp_points on {cores} threads, {s:.1f} s wall"}
+
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        avg_launch_s = (total_ms / args.steps) * 1e-3 / max(1, launches // max(1, args.steps))
+        per_launch_bytes = alg_bytes / max(1, launches // max(1, args.steps))
+        achieved = per_launch_bytes / avg_launch_s / 1e9
+        traffic = ncu_traffic(args.workload, args.variant)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_of(args, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "alg_bytes_per_launch": per_launch_bytes,
+                         "alg_bytes_per_voxel": alg_bytes / (B * nvox_out),
+                         "naive_frac": naive_bytes / (total_ms / args.steps * 1e-3) / 1e9 / peak,
+                         "footprint": {"F_img": f_img, "F_lbl": f_lbl}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms),
+                        "max": max(step_ms)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch, nvox_out):
+    import torch.distributed as dist
+    B = imgs.shape[0]
+    h_img = torch.from_numpy(imgs).pin_memory()
+    h_lbl = torch.from_numpy(lbls).pin_memory()
+    h_out = torch.empty((B, *shape), dtype=torch.float32).pin_memory()
+    h_out_l = torch.empty((B, *shape), dtype=torch.uint8).pin_memory()
+    d_img = torch.empty_like(h_img, device=dev)
+    d_lbl = torch.empty_like(h_lbl, device=dev)
+    d_out = torch.empty((B, *shape), dtype=torch.float32, device=dev)
+    d_out_l = torch.empty((B, *shape), dtype=torch.uint8, device=dev)
+
+    def step():
+        d_img.copy_(h_img, non_blocking=True)
+        d_lbl.copy_(h_lbl, non_blocking=True)
+        W.warp3d_affine_batched(d_img, d_lbl, params, fill=-1000.0, out=d_out, out_labels=d_out_l)
+        h_out.copy_(d_out, non_blocking=True)
+        h_out_l.copy_(d_out_l, non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize(dev)
+    ms = s.elapsed_time(e)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = global_batch * nvox_out * steps / (float(t.item()) * 1e-3) / 1e9
+    return {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(B * nvox_out * 5),
+            "d2h_bytes_per_step": int(B * nvox_out * 5), "steps": steps,
+            "path": "pinned host -> cudaMemcpyAsync -> warp3d_affine_batched -> pinned host, "
+                    "one stream (sequential)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

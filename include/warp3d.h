@@ -1,0 +1,201 @@
+/*
+ * warp3d.h -- C ABI of the B200 (sm_100a) 3D CT augmentation library.
+ *
+ * Implements the per-training-iteration augmentation of Rister et al.,
+ * "CT organ segmentation using GPU data augmentation, unsupervised labels and
+ * IOU loss", arXiv 1811.11226, Sec. IV:
+ *
+ *   I_affine(x) = I_in(A x + b)
+ *   image: trilinear; labels: nearest neighbour
+ *   I_occ(x)    = 0 inside an axis-aligned prism in z
+ *   I_noise(x)  = I_occ(x) + n(x), n ~ N(0, sigma^2) iid
+ *   I_window(x) = min(max((I_noise(x) - a)/(b - a), 0), 1) PAPER.md:455-467
+ *   gamma: w <- w^gamma (north-star addition; not in the paper)
+ *
+ * The arithmetic contract the paper leaves open (voxel centres, border mode,
+ * rounding of p, tie rule, RNG mapping, ...) is DESIGN.md readings R1-R21;
+ * the numbers below (R4, R6, ...) refer to them.
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ * - Layout: volumes are dense [batch][nz][ny][nx], x fastest (R1).  Voxel
+ *   (x,y,z) has its centre at integer coordinates.  w3d_dims is (nx, ny, nz).
+ * - Pointers named in/out/labels/ctr are DEVICE pointers owned by the caller;
+ *   structs and the affine of warp3d_affine are HOST pointers, read before the
+ *   call returns.  The library never allocates, frees or synchronises on the
+ *   hot path; launches are asynchronous on `stream` (a cudaStream_t; NULL =
+ *   legacy default stream).
+ * - Errors: every function returns a w3d_status.  Invalid arguments are
+ *   rejected BEFORE any launch with W3D_ERR_INVALID_ARG; a failed launch
+ *   returns W3D_ERR_CUDA.  warp3d_last_error() gives a thread-local message
+ *   for the last non-OK status.  Asynchronous kernel faults surface at the
+ *   caller's next synchronisation.  No C++ exception crosses this ABI.
+ * - Output must not overlap input (gathers read arbitrary input voxels).
+ */
+#ifndef WARP3D_H
+#define WARP3D_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WARP3D_ABI_VERSION 1
+
+typedef enum {
+  W3D_OK = 0,
+  W3D_ERR_INVALID_ARG = 1, /* bad pointer / dims / params; nothing launched   */
+  W3D_ERR_UNSUPPORTED = 2, /* valid but outside this build (e.g. > 2^31 voxels
+                              per volume)                                      */
+  W3D_ERR_CUDA = 3,        /* a CUDA runtime call or launch failed              */
+  W3D_ERR_INTERNAL = 4
+} w3d_status;
+
+typedef enum {
+  W3D_INTERP_LINEAR = 0,   /* trilinear                        */
+  W3D_INTERP_NEAREST = 1   /* nearest, round half up (R7)                        */
+} w3d_interp;
+
+/* Kernel variant selector for warp3d_affine_batched_ex (tests / benchmarks). */
+typedef enum {
+  W3D_KERNEL_AUTO = 0,     /* library choice (staged, gather fallback per tile)  */
+  W3D_KERNEL_GATHER = 1,   /* every corner gathered through L1/L2 (__ldg)        */
+  W3D_KERNEL_STAGED = 2    /* per-tile source footprint staged in shared memory
+                              (falls back to gathers for tiles whose footprint
+                              exceeds the shared-memory budget)                  */
+} w3d_kernel;
+
+typedef struct {
+  int32_t nx, ny, nz;      /* each in [1, 2^24); nx*ny*nz < 2^31                 */
+} w3d_dims;
+
+/* Photometric flag bits (w3d_photometric.flags). */
+enum {
+  W3D_PH_NOISE = 1u,   /* v += sigma * n, Philox4x32-10 + Box-Muller (R10)       */
+  W3D_PH_WINDOW = 2u,  /* v = (v - a)/(b - a)  (R14)               */
+  W3D_PH_CLAMP = 4u,   /* v = min(max(v, 0), 1); requires WINDOW                 */
+  W3D_PH_GAMMA = 8u,   /* v = v^gamma; requires WINDOW|CLAMP (R13)               */
+  W3D_PH_OCCLUDE = 16u /* image = 0 for occ_z0 <= z <= occ_z0 + occ_height, all
+                          later steps skipped, labels untouched (R15)            */
+};
+
+typedef struct {
+  uint32_t flags;      /* W3D_PH_* bits; unknown bits -> INVALID_ARG              */
+  float window_lo;     /* a (HU), finite; a < b when WINDOW        */
+  float window_hi;     /* b (HU), finite                                          */
+  float gamma;         /* > 0, finite when GAMMA; gamma == 1 skips the step       */
+  float noise_sigma;   /* >= 0, finite, HU                     */
+  uint32_t _reserved;  /* must be 0                                               */
+  uint64_t seed;       /* Philox key (key0 = low 32 bits, key1 = high)            */
+  uint64_t volume_id;  /* GLOBAL sample index: Philox counter words 2,3 (R10)     */
+  float occ_z0;        /* occlusion prism start (output z), finite                */
+  float occ_height;    /* delta >= 0, finite                                      */
+} w3d_photometric;     /* 48 bytes */
+
+typedef struct {
+  float affine[12];    /* row-major [A | b]: OUTPUT voxel coords -> INPUT coords,
+                          p_k = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b_k))) in
+                          fp32 (R4).  Finite, |A_kj| <= 2^20, |b_k| <= 2^30.      */
+  w3d_photometric ph;
+} w3d_volume_params;   /* 96 bytes */
+
+/* Host-side description of a random geometric transform. */
+typedef struct {
+  double rot_rad[3];   /* Euler angles about x, y, z                            */
+  double scale[3];     /* per-axis, > 0                                         */
+  double shear[3];     /* xy, xz, yz entries of a unit upper-triangular Sh      */
+  int32_t flip[3];     /* 0/1 per axis -> F = diag(+-1) (footnote PAPER.md:408)  */
+  int32_t _reserved;
+  double generic[9];   /* G = I + generic, row-major ("generic affine warping") */
+  double disp[3];      /* d (voxels): output centre maps to input centre + d     */
+} w3d_geom;
+
+/*
+ * warp3d_affine -- one volume.  out(x) = photometric(I_in(A x + b)).
+ *   in       device float [in.nz][in.ny][in.nx]
+ *   affine   host float[12], see w3d_volume_params.affine
+ *   interp   image interpolation (trilinear per PAPER.md:416-417, or nearest)
+ *   fill     image value of out-of-volume trilinear corners (R6), finite
+ *   ph       host, NULL = no photometric step
+ *   out      device float [out.nz][out.ny][out.nx], must not overlap `in`
+ */
+w3d_status warp3d_affine(const float* in, w3d_dims in_dims, const float affine[12],
+                         w3d_interp interp, float fill, const w3d_photometric* ph,
+                         float* out, w3d_dims out_dims, void* stream);
+
+/*
+ * warp3d_affine_batched -- `batch` volumes of identical in_dims / out_dims,
+ * each with its own transform and photometric parameters (PAPER.md:406-410,
+ * 445-446, 460-461: parameters are drawn per training example), plus the
+ * matching nearest-neighbour label warp.
+ *   in         device float [batch][in]
+ *   in_labels  device uint8 [batch][in], or NULL (no label warp)
+ *   params     host array [batch]
+ *   label_fill label of voxels whose nearest input voxel is outside (R8)
+ *   out        device float [batch][out]
+ *   out_labels device uint8 [batch][out]; NULL iff in_labels is NULL
+ * Volume i's noise stream is keyed by params[i].ph.(seed, volume_id) only,
+ * so results do not depend on batch size, order, split or GPU count.
+ */
+w3d_status warp3d_affine_batched(int32_t batch, const float* in, const uint8_t* in_labels,
+                                 w3d_dims in_dims, const w3d_volume_params* params,
+                                 w3d_interp interp, float fill, uint8_t label_fill,
+                                 float* out, uint8_t* out_labels, w3d_dims out_dims,
+                                 void* stream);
+
+/* Same, with an explicit kernel variant (results are identical by contract). */
+w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_t* in_labels,
+                                    w3d_dims in_dims, const w3d_volume_params* params,
+                                    w3d_interp interp, float fill, uint8_t label_fill,
+                                    float* out, uint8_t* out_labels, w3d_dims out_dims,
+                                    w3d_kernel variant, void* stream);
+
+/*
+ * warp3d_compose_affine -- host only (no GPU needed).  A = F Rz Ry Rx Sh S G
+ * (R16), b = c_in + d - A c_out with c = (n - 1)/2 per axis (PAPER.md:411-413,
+ * R3), evaluated in double and rounded once to fp32 into affine_out[12].
+ */
+w3d_status warp3d_compose_affine(const w3d_geom* g, w3d_dims in_dims, w3d_dims out_dims,
+                                 float affine_out[12]);
+
+/*
+ * warp3d_noise -- test hook: out[v] = sigma * n(seed, volume_id, v) over a
+ * dense volume of `dims` (the noise term of PAPER.md:442 alone, R10).
+ */
+w3d_status warp3d_noise(float* out, w3d_dims dims, float sigma, uint64_t seed,
+                        uint64_t volume_id, void* stream);
+
+/*
+ * warp3d_philox4x32_10 -- test hook: n independent Philox4x32-10 blocks.
+ *   ctr  device uint32 [n][4];  out device uint32 [n][4];  key = (lo, hi) of `key`.
+ */
+w3d_status warp3d_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out, int64_t n,
+                                void* stream);
+
+/*
+ * warp3d_footprint_batched -- measurement helper (not on the hot path).
+ * Counts the distinct input voxels the warp touches: counts[0] = #F_img
+ * (in-volume trilinear corners with nonzero extent, i.e. every corner of every
+ * sample whose p is not fully out of bounds), counts[1] = #F_lbl (in-volume
+ * nearest voxels).  marks: device uint8 scratch [2][batch][in] (overwritten);
+ * counts: device uint64 [2] (overwritten).  Used for the algorithmic-bytes
+ * roofline.
+ */
+w3d_status warp3d_footprint_batched(int32_t batch, w3d_dims in_dims,
+                                    const w3d_volume_params* params, w3d_dims out_dims,
+                                    uint8_t* marks, unsigned long long* counts, void* stream);
+
+/* Number of kernels this library has launched in this process (evidence for
+ * bench.py's gpu_launches). */
+uint64_t warp3d_launch_count(void);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char* warp3d_last_error(void);
+
+int warp3d_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WARP3D_H */

@@ -1,0 +1,161 @@
+"""Python entry points with the C-ABI's names (include/warp3d.h).
+
+PyTorch provides device memory and the current CUDA stream; every step of
+the augmentation runs in libwarp3d.so.  Tensors are passed
+as raw device pointers; shapes are numpy-style [batch, nz, ny, nx].
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import (INTERP_LINEAR, INTERP_NEAREST, KERNEL_AUTO, KERNEL_GATHER, KERNEL_STAGED,
+                   PH_CLAMP, PH_GAMMA, PH_NOISE, PH_OCCLUDE, PH_WINDOW, Geom, Photometric,
+                   VolumeParams, Warp3DError)
+
+__all__ = [
+    "warp3d_affine", "warp3d_affine_batched", "warp3d_compose_affine", "warp3d_noise",
+    "warp3d_philox4x32_10", "warp3d_footprint_batched", "warp3d_launch_count",
+    "warp3d_abi_version", "photometric", "volume_params", "make_geom", "Warp3DError",
+    "INTERP_LINEAR", "INTERP_NEAREST", "KERNEL_AUTO", "KERNEL_GATHER", "KERNEL_STAGED",
+    "PH_NOISE", "PH_WINDOW", "PH_CLAMP", "PH_GAMMA", "PH_OCCLUDE",
+]
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev(t, dtype, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def photometric(flags=0, window=(0.0, 1.0), gamma=1.0, sigma=0.0, seed=0, volume_id=0,
+                occ_z0=0.0, occ_height=0.0) -> Photometric:
+    return Photometric(int(flags), float(window[0]), float(window[1]), float(gamma),
+                       float(sigma), 0, int(seed), int(volume_id), float(occ_z0),
+                       float(occ_height))
+
+
+def make_geom(rot=(0, 0, 0), scale=(1, 1, 1), shear=(0, 0, 0), flip=(0, 0, 0), generic=None,
+              disp=(0, 0, 0)) -> Geom:
+    g = Geom()
+    g.rot_rad[:] = [float(v) for v in rot]
+    g.scale[:] = [float(v) for v in scale]
+    g.shear[:] = [float(v) for v in shear]
+    g.flip[:] = [int(bool(v)) for v in flip]
+    g.generic[:] = [0.0] * 9 if generic is None else [float(v) for v in np.ravel(generic)]
+    g.disp[:] = [float(v) for v in disp]
+    return g
+
+
+def warp3d_compose_affine(geom: Geom, in_shape_zyx, out_shape_zyx=None) -> np.ndarray:
+    """Host-only: [A|b] (float32 [3,4]) for a w3d_geom."""
+    out_shape_zyx = in_shape_zyx if out_shape_zyx is None else out_shape_zyx
+    out = (ctypes.c_float * 12)()
+    L.check(L.load().warp3d_compose_affine(ctypes.byref(geom), L.dims(in_shape_zyx),
+                                           L.dims(out_shape_zyx), out))
+    return np.array(out, dtype=np.float32).reshape(3, 4)
+
+
+def volume_params(affine, ph: Photometric | None = None) -> VolumeParams:
+    p = VolumeParams()
+    p.affine[:] = [float(v) for v in np.asarray(affine, dtype=np.float32).ravel()]
+    if ph is not None:
+        p.ph = ph
+    return p
+
+
+def warp3d_affine(inp: torch.Tensor, affine, interp=INTERP_LINEAR, fill=0.0, ph=None,
+                  out_shape=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """One volume: inp float32 [nz,ny,nx] on the GPU -> out float32 [mz,my,mx]."""
+    if inp.dim() != 3:
+        raise ValueError("inp must be [nz, ny, nx]")
+    out_shape = tuple(inp.shape) if out_shape is None else tuple(out_shape)
+    if out is None:
+        out = torch.empty(out_shape, dtype=torch.float32, device=inp.device)
+    A = (ctypes.c_float * 12)(*[float(v) for v in np.asarray(affine, dtype=np.float32).ravel()])
+    L.check(L.load().warp3d_affine(_dev(inp, torch.float32, "inp"), L.dims(inp.shape), A,
+                                   int(interp), float(fill),
+                                   None if ph is None else ctypes.byref(ph),
+                                   _dev(out, torch.float32, "out"), L.dims(out.shape), _stream()))
+    return out
+
+
+def warp3d_affine_batched(inp: torch.Tensor, labels: torch.Tensor | None, params,
+                          interp=INTERP_LINEAR, fill=0.0, label_fill=0, out_shape=None,
+                          out: torch.Tensor | None = None, out_labels: torch.Tensor | None = None,
+                          variant=KERNEL_AUTO):
+    """Batch: inp float32 [B,nz,ny,nx], labels uint8 [B,nz,ny,nx] or None,
+    params: sequence of B VolumeParams (or a ctypes array of them)."""
+    if inp.dim() != 4:
+        raise ValueError("inp must be [batch, nz, ny, nx]")
+    B = inp.shape[0]
+    out_shape = tuple(inp.shape[1:]) if out_shape is None else tuple(out_shape)
+    if out is None:
+        out = torch.empty((B, *out_shape), dtype=torch.float32, device=inp.device)
+    if labels is not None and out_labels is None:
+        out_labels = torch.empty((B, *out_shape), dtype=torch.uint8, device=inp.device)
+    if isinstance(params, ctypes.Array):
+        arr = params
+    else:
+        arr = (VolumeParams * B)(*params)
+    if len(arr) != B:
+        raise ValueError(f"{len(arr)} params for a batch of {B}")
+    L.check(L.load().warp3d_affine_batched_ex(
+        B, _dev(inp, torch.float32, "inp"),
+        None if labels is None else _dev(labels, torch.uint8, "labels"),
+        L.dims(inp.shape[1:]), arr, int(interp), float(fill), int(label_fill),
+        _dev(out, torch.float32, "out"),
+        None if out_labels is None else _dev(out_labels, torch.uint8, "out_labels"),
+        L.dims(out.shape[1:]), int(variant), _stream()))
+    return out, out_labels
+
+
+def warp3d_noise(shape_zyx, sigma, seed, volume_id, device="cuda") -> torch.Tensor:
+    out = torch.empty(tuple(shape_zyx), dtype=torch.float32, device=device)
+    L.check(L.load().warp3d_noise(_dev(out, torch.float32, "out"), L.dims(shape_zyx),
+                                  float(sigma), int(seed), int(volume_id), _stream()))
+    return out
+
+
+def warp3d_philox4x32_10(ctr: torch.Tensor, key: int) -> torch.Tensor:
+    """ctr: int32/uint32 CUDA tensor [n,4] (bit pattern) -> out same shape."""
+    if ctr.dim() != 2 or ctr.shape[1] != 4:
+        raise ValueError("ctr must be [n, 4]")
+    out = torch.empty_like(ctr)
+    L.check(L.load().warp3d_philox4x32_10(_dev(ctr, ctr.dtype, "ctr"), int(key),
+                                          _dev(out, ctr.dtype, "out"), ctr.shape[0], _stream()))
+    return out
+
+
+def warp3d_footprint_batched(params, in_shape_zyx, out_shape_zyx=None, device="cuda"):
+    """(#F_img, #F_lbl): distinct input voxels the warp reads (measurement only)."""
+    out_shape_zyx = in_shape_zyx if out_shape_zyx is None else out_shape_zyx
+    arr = params if isinstance(params, ctypes.Array) else (VolumeParams * len(params))(*params)
+    B = len(arr)
+    nin = int(np.prod(in_shape_zyx))
+    marks = torch.empty(2 * B * nin, dtype=torch.uint8, device=device)
+    counts = torch.zeros(2, dtype=torch.int64, device=device)
+    L.check(L.load().warp3d_footprint_batched(B, L.dims(in_shape_zyx), arr, L.dims(out_shape_zyx),
+                                              ctypes.c_void_p(marks.data_ptr()),
+                                              ctypes.c_void_p(counts.data_ptr()), _stream()))
+    c = counts.cpu().tolist()
+    return int(c[0]), int(c[1])
+
+
+def warp3d_launch_count() -> int:
+    return int(L.load().warp3d_launch_count())
+
+
+def warp3d_abi_version() -> int:
+    return int(L.load().warp3d_abi_version())

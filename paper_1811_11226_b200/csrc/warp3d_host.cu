@@ -1,0 +1,379 @@
+// warp3d_host.cu -- C-ABI entry points (include/warp3d.h): argument
+// validation, per-volume parameter derivation, launch chunking, errors.
+//
+// Validation rejects everything outside the contract BEFORE launching
+// (W3D_ERR_INVALID_ARG).  Per-volume parameters travel by value as a
+// __grid_constant__ kernel argument (up to kMaxVolPerLaunch volumes per
+// launch), so the hot path performs no allocation, copy or synchronisation.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "warp3d.h"
+#include "warp3d_internal.cuh"
+
+namespace w3d {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n)); }
+
+static w3d_status fail(w3d_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+static w3d_status ok() {
+  g_last_error.clear();
+  return W3D_OK;
+}
+
+static w3d_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(W3D_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+constexpr int32_t kMaxDim = 1 << 23;  // n - 0.5 exact in fp32 (R8)
+constexpr int64_t kMaxVoxels = (int64_t(1) << 31) - 1;
+
+static w3d_status check_dims(const w3d_dims& d, const char* name) {
+  if (d.nx < 1 || d.ny < 1 || d.nz < 1 || d.nx >= kMaxDim || d.ny >= kMaxDim || d.nz >= kMaxDim)
+    return fail(W3D_ERR_INVALID_ARG, "%s = (%d, %d, %d): each must be in [1, 2^23)", name, d.nx,
+                d.ny, d.nz);
+  const int64_t n = int64_t(d.nx) * d.ny * d.nz;
+  if (n > kMaxVoxels)
+    return fail(W3D_ERR_UNSUPPORTED, "%s has %lld voxels (> 2^31 - 1 per volume)", name,
+                static_cast<long long>(n));
+  return W3D_OK;
+}
+
+static int64_t nvox(const w3d_dims& d) { return int64_t(d.nx) * d.ny * d.nz; }
+
+static bool overlap(const void* a, int64_t abytes, const void* b, int64_t bbytes) {
+  if (!a || !b) return false;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return a0 < b0 + static_cast<uintptr_t>(bbytes) && b0 < a0 + static_cast<uintptr_t>(abytes);
+}
+
+static w3d_status check_affine(const float* A, int i) {
+  for (int k = 0; k < 12; ++k) {
+    const float v = A[k];
+    const float lim = (k % 4 == 3) ? 1073741824.0f /* 2^30 */ : 1048576.0f /* 2^20 */;
+    if (!std::isfinite(v) || std::fabs(v) > lim)
+      return fail(W3D_ERR_INVALID_ARG,
+                  "volume %d: affine[%d] = %g (must be finite, |A| <= 2^20, |b| <= 2^30)", i, k,
+                  static_cast<double>(v));
+  }
+  return W3D_OK;
+}
+
+static w3d_status check_ph(const w3d_photometric& ph, int i) {
+  const uint32_t known = W3D_PH_NOISE | W3D_PH_WINDOW | W3D_PH_CLAMP | W3D_PH_GAMMA |
+                         W3D_PH_OCCLUDE;
+  if (ph.flags & ~known) return fail(W3D_ERR_INVALID_ARG, "volume %d: unknown flags 0x%x", i, ph.flags);
+  if (ph._reserved != 0) return fail(W3D_ERR_INVALID_ARG, "volume %d: _reserved must be 0", i);
+  if ((ph.flags & W3D_PH_CLAMP) && !(ph.flags & W3D_PH_WINDOW))
+    return fail(W3D_ERR_INVALID_ARG, "volume %d: CLAMP requires WINDOW", i);
+  if ((ph.flags & W3D_PH_GAMMA) && !((ph.flags & W3D_PH_WINDOW) && (ph.flags & W3D_PH_CLAMP)))
+    return fail(W3D_ERR_INVALID_ARG, "volume %d: GAMMA requires WINDOW and CLAMP", i);
+  if (ph.flags & W3D_PH_WINDOW) {
+    if (!std::isfinite(ph.window_lo) || !std::isfinite(ph.window_hi) ||
+        !(ph.window_lo < ph.window_hi))
+      return fail(W3D_ERR_INVALID_ARG, "volume %d: window needs finite a < b (a=%g, b=%g)", i,
+                  double(ph.window_lo), double(ph.window_hi));
+    const double s = 1.0 / (double(ph.window_hi) - double(ph.window_lo));
+    if (!std::isfinite(static_cast<float>(s)))
+      return fail(W3D_ERR_INVALID_ARG, "volume %d: 1/(b-a) overflows fp32", i);
+  }
+  if ((ph.flags & W3D_PH_GAMMA) && !(std::isfinite(ph.gamma) && ph.gamma > 0.0f))
+    return fail(W3D_ERR_INVALID_ARG, "volume %d: gamma must be finite and > 0", i);
+  if ((ph.flags & W3D_PH_NOISE) && !(std::isfinite(ph.noise_sigma) && ph.noise_sigma >= 0.0f))
+    return fail(W3D_ERR_INVALID_ARG, "volume %d: noise_sigma must be finite and >= 0", i);
+  if ((ph.flags & W3D_PH_OCCLUDE) &&
+      !(std::isfinite(ph.occ_z0) && std::isfinite(ph.occ_height) && ph.occ_height >= 0.0f))
+    return fail(W3D_ERR_INVALID_ARG, "volume %d: occlusion needs finite z0 and height >= 0", i);
+  return W3D_OK;
+}
+
+// Host-side derivation of the kernel's per-volume parameters.
+static VolDev derive(const float* A, const w3d_photometric* ph) {
+  VolDev P;
+  std::memset(&P, 0, sizeof(P));
+  std::memcpy(P.A, A, sizeof(P.A));
+  P.gamma = 1.0f;
+  if (!ph) return P;
+  uint32_t f = 0;
+  if ((ph->flags & W3D_PH_NOISE) && ph->noise_sigma > 0.0f) f |= kNoise;
+  if (ph->flags & W3D_PH_WINDOW) {
+    f |= kWindow;
+    const double a = ph->window_lo, b = ph->window_hi;
+    P.win_s = static_cast<float>(1.0 / (b - a));
+    P.win_off = static_cast<float>(-a * double(P.win_s));
+  }
+  if (ph->flags & W3D_PH_CLAMP) f |= kClamp;
+  if ((ph->flags & W3D_PH_GAMMA) && ph->gamma != 1.0f) f |= kGamma;
+  if (ph->flags & W3D_PH_OCCLUDE) {
+    // z0 <= z <= z0 + delta over integer z  <=>  ceil(z0) <= z <= floor(z0 + delta),
+    // the sum in double exactly as the oracle evaluates it (R15).
+    const double lo = std::ceil(double(ph->occ_z0));
+    const double hi = std::floor(double(ph->occ_z0) + double(ph->occ_height));
+    const double clo = lo < -2e9 ? -2e9 : (lo > 2e9 ? 2e9 : lo);
+    const double chi = hi < -2e9 ? -2e9 : (hi > 2e9 ? 2e9 : hi);
+    P.occ_lo = static_cast<int32_t>(clo);
+    P.occ_hi = static_cast<int32_t>(chi);
+    if (P.occ_lo <= P.occ_hi) f |= kOcclude;
+  }
+  P.flags = f;
+  P.sigma = ph->noise_sigma;
+  P.gamma = ph->gamma;
+  P.key0 = static_cast<uint32_t>(ph->seed);
+  P.key1 = static_cast<uint32_t>(ph->seed >> 32);
+  P.vid0 = static_cast<uint32_t>(ph->volume_id);
+  P.vid1 = static_cast<uint32_t>(ph->volume_id >> 32);
+  return P;
+}
+
+// One batch, already validated; chunks of kMaxVolPerLaunch volumes.
+static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_labels,
+                              w3d_dims in_dims, const float* const* affines,
+                              const w3d_photometric* const* phs, w3d_interp interp, float fill,
+                              uint8_t label_fill, float* out, uint8_t* out_labels,
+                              w3d_dims out_dims, w3d_kernel variant, cudaStream_t stream) {
+  static thread_local WarpArgs args;  // ~14 KB: keep off the stack
+  const int64_t in_n = nvox(in_dims), out_n = nvox(out_dims);
+  for (int32_t v0 = 0; v0 < batch; v0 += kMaxVolPerLaunch) {
+    const int32_t nv = (batch - v0 < kMaxVolPerLaunch) ? batch - v0 : kMaxVolPerLaunch;
+    args.in = in + v0 * in_n;
+    args.in_lbl = in_labels ? in_labels + v0 * in_n : nullptr;
+    args.out = out + v0 * out_n;
+    args.out_lbl = out_labels ? out_labels + v0 * out_n : nullptr;
+    args.nx = in_dims.nx; args.ny = in_dims.ny; args.nz = in_dims.nz;
+    args.mx = out_dims.nx; args.my = out_dims.ny; args.mz = out_dims.nz;
+    args.in_stride = in_n;
+    args.out_stride = out_n;
+    args.fill = fill;
+    args.label_fill = label_fill;
+    args.interp = interp;
+    args.nvol = nv;
+    for (int32_t i = 0; i < nv; ++i) args.vol[i] = derive(affines[v0 + i], phs[v0 + i]);
+    const cudaError_t e = (variant == W3D_KERNEL_GATHER) ? launch_gather(args, stream)
+                                                         : launch_staged(args, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");
+  }
+  return ok();
+}
+
+static w3d_status check_common(const float* in, w3d_dims in_dims, w3d_interp interp, float fill,
+                               float* out, w3d_dims out_dims) {
+  if (!in || !out) return fail(W3D_ERR_INVALID_ARG, "in/out must be non-NULL device pointers");
+  if (reinterpret_cast<uintptr_t>(in) % 4 || reinterpret_cast<uintptr_t>(out) % 4)
+    return fail(W3D_ERR_INVALID_ARG, "in/out must be 4-byte aligned float pointers");
+  w3d_status st = check_dims(in_dims, "in_dims");
+  if (st != W3D_OK) return st;
+  st = check_dims(out_dims, "out_dims");
+  if (st != W3D_OK) return st;
+  if (interp != W3D_INTERP_LINEAR && interp != W3D_INTERP_NEAREST)
+    return fail(W3D_ERR_INVALID_ARG, "interp = %d is not a w3d_interp", int(interp));
+  if (!std::isfinite(fill)) return fail(W3D_ERR_INVALID_ARG, "fill must be finite");
+  return W3D_OK;
+}
+
+}  // namespace w3d
+
+using namespace w3d;
+
+extern "C" {
+
+int warp3d_abi_version(void) { return WARP3D_ABI_VERSION; }
+
+const char* warp3d_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t warp3d_launch_count(void) { return g_launches.load(); }
+
+w3d_status warp3d_affine(const float* in, w3d_dims in_dims, const float affine[12],
+                         w3d_interp interp, float fill, const w3d_photometric* ph, float* out,
+                         w3d_dims out_dims, void* stream) {
+  w3d_status st = check_common(in, in_dims, interp, fill, out, out_dims);
+  if (st != W3D_OK) return st;
+  if (!affine) return fail(W3D_ERR_INVALID_ARG, "affine must be a non-NULL host pointer");
+  if ((st = check_affine(affine, 0)) != W3D_OK) return st;
+  if (ph && (st = check_ph(*ph, 0)) != W3D_OK) return st;
+  if (overlap(in, nvox(in_dims) * 4, out, nvox(out_dims) * 4))
+    return fail(W3D_ERR_INVALID_ARG, "out overlaps in (in-place warps are not allowed)");
+  const float* A = affine;
+  return run_batched(1, in, nullptr, in_dims, &A, &ph, interp, fill, 0, out, nullptr, out_dims,
+                     W3D_KERNEL_AUTO, static_cast<cudaStream_t>(stream));
+}
+
+w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_t* in_labels,
+                                    w3d_dims in_dims, const w3d_volume_params* params,
+                                    w3d_interp interp, float fill, uint8_t label_fill,
+                                    float* out, uint8_t* out_labels, w3d_dims out_dims,
+                                    w3d_kernel variant, void* stream) {
+  if (batch < 1) return fail(W3D_ERR_INVALID_ARG, "batch = %d must be >= 1", batch);
+  w3d_status st = check_common(in, in_dims, interp, fill, out, out_dims);
+  if (st != W3D_OK) return st;
+  if (!params) return fail(W3D_ERR_INVALID_ARG, "params must be a non-NULL host array");
+  if ((in_labels == nullptr) != (out_labels == nullptr))
+    return fail(W3D_ERR_INVALID_ARG, "out_labels must be NULL iff in_labels is NULL");
+  if (variant != W3D_KERNEL_AUTO && variant != W3D_KERNEL_GATHER && variant != W3D_KERNEL_STAGED)
+    return fail(W3D_ERR_INVALID_ARG, "variant = %d is not a w3d_kernel", int(variant));
+  for (int32_t i = 0; i < batch; ++i) {
+    if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;
+    if ((st = check_ph(params[i].ph, i)) != W3D_OK) return st;
+  }
+  const int64_t in_b = int64_t(batch) * nvox(in_dims), out_b = int64_t(batch) * nvox(out_dims);
+  if (overlap(in, in_b * 4, out, out_b * 4) || overlap(in_labels, in_b, out_labels, out_b) ||
+      overlap(in, in_b * 4, out_labels, out_b) || overlap(in_labels, in_b, out, out_b * 4) ||
+      overlap(out, out_b * 4, out_labels, out_b))
+    return fail(W3D_ERR_INVALID_ARG, "output buffers overlap inputs or each other");
+  const int n = batch;
+  static thread_local const float* A[1 << 16];
+  static thread_local const w3d_photometric* P[1 << 16];
+  for (int32_t v0 = 0; v0 < n; v0 += (1 << 16)) {
+    const int32_t nv = (n - v0 < (1 << 16)) ? n - v0 : (1 << 16);
+    for (int32_t i = 0; i < nv; ++i) {
+      A[i] = params[v0 + i].affine;
+      P[i] = &params[v0 + i].ph;
+    }
+    st = run_batched(nv, in + int64_t(v0) * nvox(in_dims),
+                     in_labels ? in_labels + int64_t(v0) * nvox(in_dims) : nullptr, in_dims, A, P,
+                     interp, fill, label_fill, out + int64_t(v0) * nvox(out_dims),
+                     out_labels ? out_labels + int64_t(v0) * nvox(out_dims) : nullptr, out_dims,
+                     variant, static_cast<cudaStream_t>(stream));
+    if (st != W3D_OK) return st;
+  }
+  return ok();
+}
+
+w3d_status warp3d_affine_batched(int32_t batch, const float* in, const uint8_t* in_labels,
+                                 w3d_dims in_dims, const w3d_volume_params* params,
+                                 w3d_interp interp, float fill, uint8_t label_fill, float* out,
+                                 uint8_t* out_labels, w3d_dims out_dims, void* stream) {
+  return warp3d_affine_batched_ex(batch, in, in_labels, in_dims, params, interp, fill, label_fill,
+                                  out, out_labels, out_dims, W3D_KERNEL_AUTO, stream);
+}
+
+// A = F Rz Ry Rx Sh S G (R16), b = c_in + d - A c_out, double.
+w3d_status warp3d_compose_affine(const w3d_geom* g, w3d_dims in_dims, w3d_dims out_dims,
+                                 float affine_out[12]) {
+  if (!g || !affine_out) return fail(W3D_ERR_INVALID_ARG, "g and affine_out must be non-NULL");
+  w3d_status st = check_dims(in_dims, "in_dims");
+  if (st != W3D_OK) return st;
+  if ((st = check_dims(out_dims, "out_dims")) != W3D_OK) return st;
+  for (int k = 0; k < 3; ++k)
+    if (!std::isfinite(g->rot_rad[k]) || !std::isfinite(g->scale[k]) || !(g->scale[k] > 0) ||
+        !std::isfinite(g->shear[k]) || !std::isfinite(g->disp[k]))
+      return fail(W3D_ERR_INVALID_ARG, "geom: non-finite entry or scale <= 0 on axis %d", k);
+  for (int k = 0; k < 9; ++k)
+    if (!std::isfinite(g->generic[k])) return fail(W3D_ERR_INVALID_ARG, "geom: generic[%d]", k);
+  struct M3 {
+    double m[3][3];
+  };
+  auto mul = [](const M3& a, const M3& b) {
+    M3 c;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        c.m[i][j] = a.m[i][0] * b.m[0][j] + a.m[i][1] * b.m[1][j] + a.m[i][2] * b.m[2][j];
+    return c;
+  };
+  const double cx = std::cos(g->rot_rad[0]), sx = std::sin(g->rot_rad[0]);
+  const double cy = std::cos(g->rot_rad[1]), sy = std::sin(g->rot_rad[1]);
+  const double cz = std::cos(g->rot_rad[2]), sz = std::sin(g->rot_rad[2]);
+  const M3 F{{{g->flip[0] ? -1.0 : 1.0, 0, 0}, {0, g->flip[1] ? -1.0 : 1.0, 0},
+              {0, 0, g->flip[2] ? -1.0 : 1.0}}};
+  const M3 Rz{{{cz, -sz, 0}, {sz, cz, 0}, {0, 0, 1}}};
+  const M3 Ry{{{cy, 0, sy}, {0, 1, 0}, {-sy, 0, cy}}};
+  const M3 Rx{{{1, 0, 0}, {0, cx, -sx}, {0, sx, cx}}};
+  const M3 Sh{{{1, g->shear[0], g->shear[1]}, {0, 1, g->shear[2]}, {0, 0, 1}}};
+  const M3 S{{{g->scale[0], 0, 0}, {0, g->scale[1], 0}, {0, 0, g->scale[2]}}};
+  M3 G;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) G.m[i][j] = g->generic[3 * i + j] + (i == j ? 1.0 : 0.0);
+  const M3 A = mul(mul(mul(mul(mul(mul(F, Rz), Ry), Rx), Sh), S), G);
+  const double n_in[3] = {double(in_dims.nx), double(in_dims.ny), double(in_dims.nz)};
+  const double n_out[3] = {double(out_dims.nx), double(out_dims.ny), double(out_dims.nz)};
+  for (int k = 0; k < 3; ++k) {
+    double Ac = 0.0;
+    for (int j = 0; j < 3; ++j) Ac += A.m[k][j] * 0.5 * (n_out[j] - 1.0);
+    const double b = 0.5 * (n_in[k] - 1.0) + g->disp[k] - Ac;
+    for (int j = 0; j < 3; ++j) affine_out[4 * k + j] = static_cast<float>(A.m[k][j]);
+    affine_out[4 * k + 3] = static_cast<float>(b);
+  }
+  return ok();
+}
+
+w3d_status warp3d_noise(float* out, w3d_dims dims, float sigma, uint64_t seed, uint64_t volume_id,
+                        void* stream) {
+  if (!out) return fail(W3D_ERR_INVALID_ARG, "out must be non-NULL");
+  w3d_status st = check_dims(dims, "dims");
+  if (st != W3D_OK) return st;
+  if (!(std::isfinite(sigma) && sigma >= 0.0f))
+    return fail(W3D_ERR_INVALID_ARG, "sigma must be finite and >= 0");
+  const cudaError_t e = launch_noise(out, nvox(dims), sigma, uint32_t(seed), uint32_t(seed >> 32),
+                                     uint32_t(volume_id), uint32_t(volume_id >> 32),
+                                     static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "warp3d_noise launch");
+  return ok();
+}
+
+w3d_status warp3d_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out, int64_t n,
+                                void* stream) {
+  if (!ctr || !out) return fail(W3D_ERR_INVALID_ARG, "ctr/out must be non-NULL");
+  if (n < 0) return fail(W3D_ERR_INVALID_ARG, "n must be >= 0");
+  if (reinterpret_cast<uintptr_t>(ctr) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+    return fail(W3D_ERR_INVALID_ARG, "ctr/out must be 16-byte aligned");
+  if (n == 0) return ok();
+  if (overlap(ctr, n * 16, out, n * 16) && ctr != out)
+    return fail(W3D_ERR_INVALID_ARG, "ctr and out partially overlap");
+  const cudaError_t e = launch_philox(ctr, uint32_t(key), uint32_t(key >> 32), out, n,
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "warp3d_philox4x32_10 launch");
+  return ok();
+}
+
+w3d_status warp3d_footprint_batched(int32_t batch, w3d_dims in_dims,
+                                    const w3d_volume_params* params, w3d_dims out_dims,
+                                    uint8_t* marks, unsigned long long* counts, void* stream) {
+  if (batch < 1 || !params || !marks || !counts)
+    return fail(W3D_ERR_INVALID_ARG, "footprint: batch >= 1 and non-NULL params/marks/counts");
+  if (batch > kMaxVolPerLaunch)
+    return fail(W3D_ERR_UNSUPPORTED, "footprint: batch <= %d", kMaxVolPerLaunch);
+  w3d_status st = check_dims(in_dims, "in_dims");
+  if (st != W3D_OK) return st;
+  if ((st = check_dims(out_dims, "out_dims")) != W3D_OK) return st;
+  for (int32_t i = 0; i < batch; ++i) {
+    if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;
+    if ((st = check_ph(params[i].ph, i)) != W3D_OK) return st;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  static thread_local WarpArgs args;
+  std::memset(&args, 0, sizeof(args));
+  args.nx = in_dims.nx; args.ny = in_dims.ny; args.nz = in_dims.nz;
+  args.mx = out_dims.nx; args.my = out_dims.ny; args.mz = out_dims.nz;
+  args.in_stride = nvox(in_dims);
+  args.out_stride = nvox(out_dims);
+  args.interp = W3D_INTERP_LINEAR;
+  args.nvol = batch;
+  for (int32_t i = 0; i < batch; ++i) args.vol[i] = derive(params[i].affine, &params[i].ph);
+  const int64_t total = args.in_stride * batch;
+  cudaError_t e = cudaMemsetAsync(marks, 0, size_t(total) * 2, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = launch_footprint(args, marks, s);
+  if (e == cudaSuccess) e = launch_count_marks(marks, total, counts, s);
+  if (e == cudaSuccess) e = launch_count_marks(marks + total, total, counts + 1, s);
+  if (e != cudaSuccess) return cuda_fail(e, "warp3d_footprint_batched");
+  return ok();
+}
+
+}  // extern "C"

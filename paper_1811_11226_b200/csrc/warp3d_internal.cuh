@@ -1,0 +1,68 @@
+// warp3d_internal.cuh -- launch-argument structs shared by the host entry
+// points (warp3d_host.cu) and the kernels (warp3d_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "warp3d.h"
+
+namespace w3d {
+
+// Effective per-volume flags after host-side simplification.
+enum : uint32_t {
+  kNoise = 1u,    // sigma > 0
+  kWindow = 2u,
+  kClamp = 4u,
+  kGamma = 8u,    // gamma != 1
+  kOcclude = 16u  // non-empty integer z range
+};
+
+// Per-volume parameters as the kernels see them (derived on the host from
+// w3d_volume_params).
+struct alignas(16) VolDev {
+  float A[12];        // [A | b] row-major, R4
+  uint32_t flags;     // effective kNoise | kWindow | ...
+  float sigma;        // HU
+  float win_s;        // s = fp32(1 / (b - a))
+  float win_off;      // fp32(-a * s): w = fma(v, s, off)
+  float gamma;
+  uint32_t key0, key1;  // Philox key = seed
+  uint32_t vid0, vid1;  // Philox counter words 2,3 = volume_id
+  int32_t occ_lo, occ_hi;  // occluded output z in [occ_lo, occ_hi]
+  uint32_t _pad[3];
+};
+static_assert(sizeof(VolDev) == 112, "VolDev layout");
+
+constexpr int kMaxVolPerLaunch = 128;
+
+struct WarpArgs {
+  const float* in;
+  const uint8_t* in_lbl;  // may be null
+  float* out;
+  uint8_t* out_lbl;       // null iff in_lbl null
+  int32_t nx, ny, nz;     // input dims
+  int32_t mx, my, mz;     // output dims
+  int64_t in_stride;      // voxels per input volume
+  int64_t out_stride;     // voxels per output volume
+  float fill;
+  uint32_t label_fill;
+  int32_t interp;         // W3D_INTERP_*
+  int32_t nvol;           // volumes in this launch
+  VolDev vol[kMaxVolPerLaunch];
+};
+
+// Launchers (warp3d_kernels.cu).  All return cudaGetLastError() of the launch.
+cudaError_t launch_gather(const WarpArgs& a, cudaStream_t s);
+cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s);
+cudaError_t launch_noise(float* out, int64_t n, float sigma, uint32_t k0, uint32_t k1,
+                         uint32_t v0, uint32_t v1, cudaStream_t s);
+cudaError_t launch_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
+                          int64_t n, cudaStream_t s);
+cudaError_t launch_footprint(const WarpArgs& a, uint8_t* marks, cudaStream_t s);
+cudaError_t launch_count_marks(const uint8_t* marks, int64_t n, unsigned long long* counts,
+                               cudaStream_t s);
+
+void note_launch(int n = 1);
+
+}  // namespace w3d

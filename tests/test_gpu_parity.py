@@ -1,0 +1,370 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element on seeded inputs, at sizes spanning many tiles and ragged tails, and at
+BASELINE.json's full sizes on sampled voxels.  Labels and Philox words are
+bit-exact; images within the north-star tolerance (tests/tolerance.py)."""
+import concurrent.futures as cf
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from tolerance import assert_image_close
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FULL = O.NOISE | O.WINDOW | O.CLAMP | O.GAMMA
+SEED = synth.MASTER_SEED
+
+
+@pytest.fixture(scope="module")
+def W():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import build
+    build.build_cuda()
+    import paper_1811_11226_b200 as W
+    return W
+
+
+def _oracle_affine(d, in_shape, out_shape):
+    return O.compose_affine(O.make_geom(d.rot_rad, d.scale, d.shear, d.flip, d.generic, d.disp),
+                            in_shape, out_shape)[1]
+
+
+def _oph(d, flags, vid, seed=SEED):
+    return O.photometric(flags, window=d.window, gamma=d.gamma, sigma=d.sigma, seed=seed,
+                         volume_id=vid)
+
+
+def _wph(W, d, flags, vid, seed=SEED):
+    return W.photometric(flags, window=d.window, gamma=d.gamma, sigma=d.sigma, seed=seed,
+                         volume_id=vid)
+
+
+def _pool():
+    return cf.ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 4))
+
+
+def run_case(W, images, labels, affines, draws, flags, vids, out_shape=None, interp=0,
+             fill=-1000.0, label_fill=0, variant=0, oracle_volumes=None):
+    """GPU batch + oracle on the selected volumes; returns (gpu_img, gpu_lbl, ref)."""
+    B = len(affines)
+    in_shape = images.shape[1:]
+    out_shape = tuple(in_shape) if out_shape is None else tuple(out_shape)
+    params = [W.volume_params(affines[i], _wph(W, draws[i], flags, vids[i])) for i in range(B)]
+    ti = torch.from_numpy(images).cuda()
+    tl = None if labels is None else torch.from_numpy(labels).cuda()
+    out, out_l = W.warp3d_affine_batched(ti, tl, params, interp=interp, fill=fill,
+                                         label_fill=label_fill, out_shape=out_shape,
+                                         variant=variant)
+    torch.cuda.synchronize()
+    g_img = out.cpu().numpy()
+    g_lbl = None if out_l is None else out_l.cpu().numpy()
+    sel = range(B) if oracle_volumes is None else oracle_volumes
+
+    def one(i):
+        return i, O.warp_volume(images[i], None if labels is None else labels[i], affines[i],
+                                out_shape, interp, fill, label_fill,
+                                _oph(draws[i], flags, vids[i]))
+    with _pool() as ex:
+        ref = dict(ex.map(one, sel))
+    return g_img, g_lbl, ref
+
+
+def check(g_img, g_lbl, ref, draws, flags, what=""):
+    for i, (r_img, r_lbl) in ref.items():
+        d = draws[i]
+        win = d.window if flags & O.WINDOW else None
+        gam = d.gamma if flags & O.GAMMA else 1.0
+        assert_image_close(g_img[i], r_img, win, gam, bool(flags & O.CLAMP), f"{what} vol {i}")
+        if r_lbl is not None:
+            mism = int(np.sum(g_lbl[i] != r_lbl))
+            assert mism == 0, f"{what} vol {i}: {mism} label mismatches"
+
+
+# ----------------------------------------------------------------------------- RNG hooks
+def test_philox_hook_bit_exact(W):
+    rng = np.random.default_rng(1)
+    n = 4096
+    ctr = rng.integers(0, 2 ** 32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+    ctr[0] = 0
+    ctr[1] = 0xFFFFFFFF
+    for key in (0, 0xFFFFFFFFFFFFFFFF, 0x299F31D0A4093822, SEED):
+        out = W.warp3d_philox4x32_10(torch.from_numpy(ctr.view(np.int32)).cuda(), key)
+        got = out.cpu().numpy().view(np.uint32)
+        k = [key & 0xFFFFFFFF, key >> 32]
+        for i in range(0, n, 37):
+            assert list(got[i]) == list(O.philox4x32_10(ctr[i], k)), (key, i)
+    # the Random123 known answers through the device path
+    kat = np.array([[0, 0, 0, 0], [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344]], np.uint32)
+    out = W.warp3d_philox4x32_10(torch.from_numpy(kat.view(np.int32)).cuda(),
+                                 0x299F31D0A4093822).cpu().numpy().view(np.uint32)
+    assert [hex(v) for v in out[1]] == ["0xd16cfe09", "0x94fdcceb", "0x5001e420", "0x24126ea1"]
+
+
+@pytest.mark.parametrize("shape", [(7, 9, 13), (32, 32, 32), (160, 128, 128)])
+def test_noise_hook_matches_oracle(W, shape):
+    sigma = 20.0
+    for vid in (0, 5, 2 ** 40 + 3):
+        g = W.warp3d_noise(shape, sigma, SEED, vid).cpu().numpy()
+        r = O.noise_field(shape, sigma, SEED, vid)
+        assert_image_close(g, r, what=f"noise {shape} vid {vid}")
+    g = W.warp3d_noise((4, 4, 4), 0.0, SEED, 0).cpu().numpy()
+    assert not g.any()
+
+
+# ----------------------------------------------------------------------------- configs[0] (C1)
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_c1_fixed_affine_noise(W, variant):
+    """32^3 float32 + uint8 labels, one fixed affine, trilinear + nearest, sigma = 10 HU."""
+    img, lbl = synth.phantom((32, 32, 32))
+    d = synth.C1_DRAW
+    A = _oracle_affine(d, img.shape, img.shape)
+    g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], O.NOISE, [0],
+                                 variant=variant)
+    check(g_img, g_lbl, ref, [d], O.NOISE, "C1")
+
+
+# ----------------------------------------------------------------------------- small / ragged
+SMALL = [
+    # (in_shape, out_shape, ranges, flags, interp, batch)
+    ((23, 29, 37), None, "train", FULL, 0, 3),            # nx % 4 != 0: scalar path
+    ((40, 36, 44), (33, 30, 28), "train", FULL, 0, 2),    # crop, ragged out dims
+    ((48, 40, 64), None, "large", FULL, 0, 2),
+    ((48, 40, 64), None, "train", O.NOISE | O.WINDOW, 0, 2),   # window without clamp
+    ((48, 40, 64), None, "train", O.WINDOW | O.CLAMP, 1, 2),   # nearest image
+    ((24, 32, 32), (24, 40, 48), "large", 0, 0, 2),            # out larger than in
+    ((1, 1, 1), (3, 5, 8), "train", FULL, 0, 1),               # degenerate 1-voxel input
+    ((5, 3, 4), (1, 1, 4), "train", FULL, 0, 2),
+]
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("case", range(len(SMALL)))
+def test_small_cases(W, case, variant):
+    in_shape, out_shape, rname, flags, interp, B = SMALL[case]
+    ranges = synth.TRAIN if rname == "train" else synth.LARGE
+    out_shape = in_shape if out_shape is None else out_shape
+    imgs, lbls, As, ds = [], [], [], []
+    for i in range(B):
+        im, lb = synth.phantom(in_shape, seed=100 + i) if min(in_shape) >= 8 else \
+            synth.random_volume(in_shape, 100 + i)
+        d = synth.draw(ranges, 1000 * case + i)
+        imgs.append(im); lbls.append(lb); ds.append(d)
+        As.append(_oracle_affine(d, in_shape, out_shape))
+    g_img, g_lbl, ref = run_case(W, np.stack(imgs), np.stack(lbls), As, ds, flags,
+                                 [50 + i for i in range(B)], out_shape=out_shape, interp=interp,
+                                 variant=variant, label_fill=7)
+    check(g_img, g_lbl, ref, ds, flags, f"small {case}")
+
+
+def test_exact_permutations_on_gpu(W):
+    """Identity, integer shifts, flips and 90-degree rotations: exact (no tolerance)."""
+    img, lbl = synth.random_volume((16, 16, 16), 3)
+    n = 16
+    mats = {
+        "identity": (np.eye(3), (0, 0, 0)),
+        "shift": (np.eye(3), (3, -2, 1)),
+        "flipx": (np.diag([-1.0, 1, 1]), (n - 1, 0, 0)),
+        "rotz90": (np.array([[0, 1, 0], [-1, 0, 0], [0, 0, 1]]), (0, n - 1, 0)),
+    }
+    d = synth.C1_DRAW
+    for name, (M, b) in mats.items():
+        A = np.zeros((3, 4), np.float32)
+        A[:, :3] = M
+        A[:, 3] = b
+        for variant in (1, 2):
+            g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], 0, [0],
+                                         variant=variant, fill=-5.0, label_fill=9)
+            assert np.array_equal(g_img[0], ref[0][0]), name
+            assert np.array_equal(g_lbl[0], ref[0][1]), name
+    assert np.array_equal(g_img[0], np.rot90(img, k=-1, axes=(1, 2)))
+
+
+def test_fully_out_of_bounds_and_occlusion(W):
+    img, lbl = synth.random_volume((12, 12, 12), 4)
+    d = synth.draw(synth.TRAIN, 3)
+    A = np.zeros((3, 4), np.float32)
+    A[:, 3] = (-40, 3, 3)
+    for variant in (1, 2):
+        g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], 0, [0], variant=variant,
+                                     fill=-1000.0, label_fill=6)
+        assert np.all(g_img == np.float32(-1000.0)) and np.all(g_lbl == 6)
+    # occlusion: prism in output z; exact zeros there, labels untouched
+    A = _oracle_affine(d, img.shape, img.shape)
+    params = [W.volume_params(A, W.photometric(FULL | O.OCCLUDE, window=d.window, gamma=d.gamma,
+                                               sigma=d.sigma, seed=1, volume_id=0, occ_z0=2.5,
+                                               occ_height=4.0))]
+    oph = O.photometric(FULL | O.OCCLUDE, window=d.window, gamma=d.gamma, sigma=d.sigma, seed=1,
+                        volume_id=0, occ_z0=2.5, occ_height=4.0)
+    r_img, r_lbl = O.warp_volume(img, lbl, A, None, 0, -1000.0, 0, oph)
+    for variant in (1, 2):
+        out, out_l = W.warp3d_affine_batched(torch.from_numpy(img[None]).cuda(),
+                                             torch.from_numpy(lbl[None]).cuda(), params,
+                                             fill=-1000.0, variant=variant)
+        g = out.cpu().numpy()[0]
+        assert np.all(g[3:7] == 0.0)
+        assert np.array_equal(out_l.cpu().numpy()[0], r_lbl)
+        assert_image_close(g, r_img, d.window, d.gamma, True, "occlusion")
+
+
+def test_single_volume_entry_point(W):
+    img, _ = synth.phantom((20, 24, 28))
+    d = synth.draw(synth.TRAIN, 9)
+    A = _oracle_affine(d, img.shape, img.shape)
+    ph = W.photometric(FULL, window=d.window, gamma=d.gamma, sigma=d.sigma, seed=SEED, volume_id=4)
+    g = W.warp3d_affine(torch.from_numpy(img).cuda(), A, fill=-1000.0, ph=ph).cpu().numpy()
+    r, _ = O.warp_volume(img, None, A, None, 0, -1000.0, 0, _oph(d, FULL, 4))
+    assert_image_close(g, r, d.window, d.gamma, True, "warp3d_affine")
+    g0 = W.warp3d_affine(torch.from_numpy(img).cuda(), A, fill=-1000.0).cpu().numpy()
+    r0, _ = O.warp_volume(img, None, A, None, 0, -1000.0, 0, None)
+    assert_image_close(g0, r0, what="warp3d_affine no photometric")
+
+
+# ----------------------------------------------------------------------------- configs[1..2]
+def _batch_inputs(shape, B, ranges, first_vid=0, n_distinct=4):
+    base = [synth.phantom(shape, seed=synth.MASTER_SEED + k) for k in range(min(B, n_distinct))]
+    imgs = np.stack([base[i % len(base)][0] for i in range(B)])
+    lbls = np.stack([base[i % len(base)][1] for i in range(B)])
+    ds = [synth.draw(ranges, first_vid + i) for i in range(B)]
+    As = [_oracle_affine(d, shape, shape) for d in ds]
+    return imgs, lbls, ds, As
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_c2_single_ct_volume(W, variant):
+    imgs, lbls, ds, As = _batch_inputs((160, 128, 128), 1, synth.TRAIN)
+    g_img, g_lbl, ref = run_case(W, imgs, lbls, As, ds, FULL, [0], variant=variant)
+    check(g_img, g_lbl, ref, ds, FULL, "C2")
+
+
+def test_c3_batch16(W):
+    imgs, lbls, ds, As = _batch_inputs((160, 128, 128), 16, synth.TRAIN)
+    g_img, g_lbl, ref = run_case(W, imgs, lbls, As, ds, FULL, list(range(16)))
+    check(g_img, g_lbl, ref, ds, FULL, "C3")
+
+
+# ----------------------------------------------------------------------------- configs[3] (C4)
+def _sampled_check(W, imgs, lbls, As, ds, flags, vids, n_pts, variant=0, seed=0):
+    B = len(As)
+    shape = imgs.shape[1:]
+    params = [W.volume_params(As[i], _wph(W, ds[i], flags, vids[i])) for i in range(B)]
+    out, out_l = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(),
+                                         torch.from_numpy(lbls).cuda(), params, fill=-1000.0,
+                                         variant=variant)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(seed)
+    nz, ny, nx = shape
+    for i in range(B):
+        xyz = np.stack([rng.integers(0, nx, n_pts), rng.integers(0, ny, n_pts),
+                        rng.integers(0, nz, n_pts)], axis=1).astype(np.int32)
+        # plus whole rows at the volume's boundary and the ragged end
+        vals, lb = O.warp_points(imgs[i], lbls[i], As[i], xyz, None, 0, -1000.0, 0,
+                                 _oph(ds[i], flags, vids[i]))
+        idx = (torch.from_numpy(xyz[:, 2].astype(np.int64)).cuda(),
+               torch.from_numpy(xyz[:, 1].astype(np.int64)).cuda(),
+               torch.from_numpy(xyz[:, 0].astype(np.int64)).cuda())
+        g = out[i][idx].cpu().numpy()
+        gl = out_l[i][idx].cpu().numpy()
+        d = ds[i]
+        assert_image_close(g, vals, d.window, d.gamma, True, f"sampled vol {i}")
+        assert np.array_equal(gl, lb), f"sampled labels vol {i}: {int(np.sum(gl != lb))}"
+    return out, out_l
+
+
+def test_c4_512cubed_large_rotations_sampled(W):
+    shape = (512, 512, 512)
+    img, lbl = synth.phantom(shape)
+    ds = [synth.draw(synth.LARGE, 7)]
+    As = [_oracle_affine(ds[0], shape, shape)]
+    for variant in (0, 1):
+        out, out_l = _sampled_check(W, img[None], lbl[None], As, ds, FULL, [0], 200_000,
+                                    variant=variant)
+        # full z-slices (several thousand contiguous rows) through the oracle
+        for z in (0, 255, 511):
+            xyz = np.stack(np.meshgrid(np.arange(512), np.arange(512), [z], indexing="xy"),
+                           -1).reshape(-1, 3).astype(np.int32)
+            vals, lb = O.warp_points(img, lbl, As[0], xyz, None, 0, -1000.0, 0,
+                                     _oph(ds[0], FULL, 0))
+            g = out[0, z].cpu().numpy().ravel()
+            gl = out_l[0, z].cpu().numpy().ravel()
+            assert_image_close(g, vals, ds[0].window, ds[0].gamma, True, f"C4 slice {z}")
+            assert np.array_equal(gl, lb)
+        del out, out_l
+
+
+# ----------------------------------------------------------------------------- configs[4] (C5)
+def test_c5_256_volumes_sampled_and_shard_invariant(W):
+    """Full C5 batch in the launch configuration bench.py uses, sampled against the
+    oracle; any contiguous shard (what a rank computes) is bit-identical."""
+    imgs, lbls, ds, As = _batch_inputs((160, 128, 128), 256, synth.TRAIN)
+    out, out_l = _sampled_check(W, imgs, lbls, As, ds, FULL, list(range(256)), 2000)
+    ti, tl = torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda()
+    for world in (2, 8):
+        per = 256 // world
+        for r in (0, world - 1):
+            sl = slice(r * per, (r + 1) * per)
+            params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(256)[sl]]
+            o, ol = W.warp3d_affine_batched(ti[sl].contiguous(), tl[sl].contiguous(), params,
+                                            fill=-1000.0)
+            assert torch.equal(o, out[sl]) and torch.equal(ol, out_l[sl]), (world, r)
+
+
+# ----------------------------------------------------------------------------- invariances
+def test_variants_batch_splits_and_determinism_bitwise(W):
+    imgs, lbls, ds, As = _batch_inputs((64, 48, 56), 6, synth.TRAIN)
+    ti, tl = torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda()
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, 100 + i)) for i in range(6)]
+    ref, ref_l = W.warp3d_affine_batched(ti, tl, params, fill=-1000.0, variant=1)
+    for variant in (0, 1, 2):
+        o, ol = W.warp3d_affine_batched(ti, tl, params, fill=-1000.0, variant=variant)
+        assert torch.equal(o, ref) and torch.equal(ol, ref_l), variant
+    for i in range(6):  # single calls
+        o, ol = W.warp3d_affine_batched(ti[i:i + 1], tl[i:i + 1], params[i:i + 1], fill=-1000.0)
+        assert torch.equal(o[0], ref[i]) and torch.equal(ol[0], ref_l[i])
+    o, ol = W.warp3d_affine_batched(ti[[4, 1]].contiguous(), tl[[4, 1]].contiguous(),
+                                    [params[4], params[1]], fill=-1000.0)
+    assert torch.equal(o[0], ref[4]) and torch.equal(o[1], ref[1])
+    # labels invariant to photometrics
+    params2 = [W.volume_params(As[i], W.photometric(FULL, window=(-100.0, 100.0), gamma=1.3,
+                                                    sigma=3.0, seed=7, volume_id=i))
+               for i in range(6)]
+    _, ol2 = W.warp3d_affine_batched(ti, tl, params2, fill=-1000.0)
+    assert torch.equal(ol2, ref_l)
+
+
+def test_more_volumes_than_one_launch(W):
+    """batch > kMaxVolPerLaunch (128) is chunked; volume ids stay per volume."""
+    shape = (8, 8, 12)
+    B = 131
+    img, lbl = synth.random_volume(shape, 5)
+    imgs = np.repeat(img[None], B, 0)
+    lbls = np.repeat(lbl[None], B, 0)
+    ds = [synth.draw(synth.TRAIN, i) for i in range(B)]
+    As = [_oracle_affine(d, shape, shape) for d in ds]
+    g_img, g_lbl, ref = run_case(W, imgs, lbls, As, ds, FULL, list(range(B)),
+                                 oracle_volumes=[0, 1, 127, 128, 129, 130])
+    check(g_img, g_lbl, ref, ds, FULL, "chunked")
+
+
+def test_footprint_counts_match_oracle_marking(W):
+    """#F_img / #F_lbl (roofline accounting) equal a host count of the same sets."""
+    shape = (20, 18, 24)
+    img, lbl = synth.random_volume(shape, 6)
+    ds = [synth.draw(synth.TRAIN, i) for i in range(2)]
+    As = [_oracle_affine(d, shape, shape) for d in ds]
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(2)]
+    f_img, f_lbl = W.warp3d_footprint_batched(params, shape)
+    # nearest set from the oracle: nearest-interpolate a coordinate-coded volume
+    # (values < 2^24 are exact in fp32) and count the distinct in-volume codes
+    nz, ny, nx = shape
+    tot_l = 0
+    for i in range(2):
+        code = np.arange(nz * ny * nx, dtype=np.float32).reshape(shape)
+        nimg, _ = O.warp_volume(code, None, As[i], None, O.NEAREST, -1.0, 0, None)
+        tot_l += len(np.unique(nimg[nimg >= 0]))
+    assert f_lbl == tot_l
+    assert f_img >= f_lbl
