@@ -65,8 +65,10 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         P = ctypes.c_void_p
         L.oracle_philox4x32_10.argtypes = [P, P, P]
-        L.oracle_noise_uniforms.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, P, P]
-        L.oracle_noise_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
+        I32 = ctypes.c_int32
+        L.oracle_noise_uniforms.argtypes = [ctypes.c_uint64, ctypes.c_uint64, P, I32, I32, I32,
+                                            P, P]
+        L.oracle_noise_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint64, P, I32, I32, I32]
         L.oracle_noise_normal.restype = ctypes.c_double
         L.oracle_compose_affine.argtypes = [P, P, P, P, P]
         L.oracle_warp_volume.argtypes = [P, P, P, P, ctypes.c_int32, ctypes.c_float,
@@ -102,14 +104,15 @@ def philox4x32_10(ctr, key):
     return out
 
 
-def noise_uniforms(seed, volume_id, v_lin):
+def noise_uniforms(seed, volume_id, shape_zyx, x, y, z):
     u1, s = ctypes.c_double(), ctypes.c_double()
-    lib().oracle_noise_uniforms(seed, volume_id, v_lin, ctypes.byref(u1), ctypes.byref(s))
+    lib().oracle_noise_uniforms(seed, volume_id, _ptr(_dims(shape_zyx)), x, y, z,
+                                ctypes.byref(u1), ctypes.byref(s))
     return u1.value, s.value
 
 
-def noise_normal(seed, volume_id, v_lin):
-    return lib().oracle_noise_normal(seed, volume_id, v_lin)
+def noise_normal(seed, volume_id, shape_zyx, x, y, z):
+    return lib().oracle_noise_normal(seed, volume_id, _ptr(_dims(shape_zyx)), x, y, z)
 
 
 def noise_field(shape_zyx, sigma, seed, volume_id):

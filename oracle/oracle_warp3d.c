@@ -50,14 +50,16 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
   out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* Noise counter mapping (R10): voxel v_lin of volume `volume_id`
- * uses Philox block q = v_lin >> 2 with counter (lo q, hi q, lo id, hi id)
- * and key (lo seed, hi seed).  Lanes 0,1 share words (r0, r1); lanes 2,3
- * share (r2, r3).  u1 in (0,1) and s in [-1,1) are exact in fp32. */
-void oracle_noise_uniforms(uint64_t seed, uint64_t volume_id, uint64_t v_lin,
-                           double* u1, double* s) {
-  uint64_t q = v_lin >> 2;
-  unsigned lane = (unsigned)(v_lin & 3u);
+/* Noise counter mapping (R10): output voxel (x, y, z) of a volume of
+ * dims (mx, my, mz) uses Philox block q = x + mx * (floor(y/4) + Gy * z),
+ * Gy = ceil(my/4), with counter (lo q, hi q, lo id, hi id) and key
+ * (lo seed, hi seed); its lane is y mod 4.  Lanes 0,1 share words (r0, r1),
+ * lanes 2,3 share (r2, r3).  u1 in (0,1) and s in [-1,1) are exact in fp32. */
+void oracle_noise_uniforms(uint64_t seed, uint64_t volume_id, const int32_t dims[3],
+                           int32_t x, int32_t y, int32_t z, double* u1, double* s) {
+  uint64_t Gy = ((uint64_t)dims[1] + 3u) / 4u;
+  uint64_t q = (uint64_t)x + (uint64_t)dims[0] * ((uint64_t)(y / 4) + Gy * (uint64_t)z);
+  unsigned lane = (unsigned)(y % 4);
   uint32_t ctr[4] = {(uint32_t)q, (uint32_t)(q >> 32), (uint32_t)volume_id,
                      (uint32_t)(volume_id >> 32)};
   uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
@@ -69,21 +71,24 @@ void oracle_noise_uniforms(uint64_t seed, uint64_t volume_id, uint64_t v_lin,
   *s = 2.0 * ((double)(ub >> 8) * ldexp(1.0, -24)) - 1.0;
 }
 
-/* Box-Muller: n = sqrt(-2 ln u1) * (cos | sin)(pi s); even lanes take the
- * cosine, odd lanes the sine.  Standard normal. */
-double oracle_noise_normal(uint64_t seed, uint64_t volume_id, uint64_t v_lin) {
+/* Box-Muller: n = sqrt(-2 ln u1) * (cos | sin)(pi s); even lanes (y even) take
+ * the cosine, odd lanes the sine.  Standard normal. */
+double oracle_noise_normal(uint64_t seed, uint64_t volume_id, const int32_t dims[3],
+                           int32_t x, int32_t y, int32_t z) {
   double u1, s;
-  oracle_noise_uniforms(seed, volume_id, v_lin, &u1, &s);
+  oracle_noise_uniforms(seed, volume_id, dims, x, y, z, &u1, &s);
   double R = sqrt(-2.0 * log(u1));
   double angle = M_PI * s;
-  return (v_lin & 1u) ? R * sin(angle) : R * cos(angle);
+  return (y % 2) ? R * sin(angle) : R * cos(angle);
 }
 
 void oracle_noise_field(float* out, const int32_t dims[3], float sigma, uint64_t seed,
                         uint64_t volume_id) {
-  uint64_t n = (uint64_t)dims[0] * (uint64_t)dims[1] * (uint64_t)dims[2];
-  for (uint64_t v = 0; v < n; ++v)
-    out[v] = (float)((double)sigma * oracle_noise_normal(seed, volume_id, v));
+  size_t idx = 0;
+  for (int32_t z = 0; z < dims[2]; ++z)
+    for (int32_t y = 0; y < dims[1]; ++y)
+      for (int32_t x = 0; x < dims[0]; ++x, ++idx)
+        out[idx] = (float)((double)sigma * oracle_noise_normal(seed, volume_id, dims, x, y, z));
 }
 
 /* ------------------------------------------------------------------------ */
@@ -225,8 +230,7 @@ static voxel_result one_voxel(const float* in, const uint8_t* in_lbl, const int3
   /* Step 3 -- additive Gaussian noise I_noise = I + n, n ~ N(0, sigma^2)
    * (PAPER.md:440-446), on every voxel including fill voxels (R9). */
   if ((flags & ORC_NOISE) && ph->noise_sigma > 0.0f) {
-    uint64_t v_lin = (uint64_t)x + (uint64_t)m[0] * ((uint64_t)y + (uint64_t)m[1] * (uint64_t)z);
-    v += (double)ph->noise_sigma * oracle_noise_normal(ph->seed, ph->volume_id, v_lin);
+    v += (double)ph->noise_sigma * oracle_noise_normal(ph->seed, ph->volume_id, m, x, y, z);
   }
 
   /* Step 4 -- window: (v - a)/(b - a), then clamp to [0,1]. */

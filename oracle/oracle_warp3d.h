@@ -57,10 +57,12 @@ typedef struct {
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 
 /* The (u1, s) uniforms and the standard normal n used for output voxel
- * v_lin of volume `volume_id` (reading R10). */
-void oracle_noise_uniforms(uint64_t seed, uint64_t volume_id, uint64_t v_lin,
-                           double* u1, double* s);
-double oracle_noise_normal(uint64_t seed, uint64_t volume_id, uint64_t v_lin);
+ * (x, y, z) of a volume of dims (mx, my, mz) with id `volume_id`
+ * (reading R10). */
+void oracle_noise_uniforms(uint64_t seed, uint64_t volume_id, const int32_t dims[3],
+                           int32_t x, int32_t y, int32_t z, double* u1, double* s);
+double oracle_noise_normal(uint64_t seed, uint64_t volume_id, const int32_t dims[3],
+                           int32_t x, int32_t y, int32_t z);
 
 /* A = F Rz Ry Rx Sh S G, b = c_in + d - A c_out.
  * Writes the double matrix [A|b] (row-major 3x4) and its fp32 rounding. */

@@ -46,35 +46,55 @@ def test_philox_known_answers():
 # ----------------------------------------------------------------------------- P9 noise
 def test_noise_uniforms_exact_lattice():
     # u1 = odd multiple of 2^-24 in (0,1); s = multiple of 2^-23 in [-1, 1)
-    for v in range(0, 4000, 7):
-        u1, s = O.noise_uniforms(123, 4, v)
+    shp = (5, 10, 7)
+    for v in range(0, 350, 3):
+        x, y, z = v % 7, (v // 7) % 10, v // 70
+        u1, s = O.noise_uniforms(123, 4, shp, x, y, z)
         k = u1 * 2.0 ** 24
         assert 0 < u1 < 1 and k == int(k) and int(k) % 2 == 1
         assert -1.0 <= s < 1.0 and s * 2.0 ** 23 == int(s * 2.0 ** 23)
-    # voxels 4q..4q+3 share one Philox block: lanes (0,1) and (2,3) share uniforms
-    a = [O.noise_uniforms(9, 1, 4 * 11 + l) for l in range(4)]
+    # R10: voxels (x, 4g..4g+3, z) share one Philox block; rows (4g, 4g+1) and
+    # (4g+2, 4g+3) share uniforms; neighbours along x use different blocks
+    a = [O.noise_uniforms(9, 1, shp, 3, 4 + l, 2) for l in range(4)]
     assert a[0] == a[1] and a[2] == a[3] and a[0] != a[2]
+    assert O.noise_uniforms(9, 1, shp, 4, 4, 2) != a[0]
+    # the last (partial) y-group: my = 10 -> rows 8, 9 are lanes 0, 1 of their block
+    b = [O.noise_uniforms(9, 1, shp, 0, 8 + l, 0) for l in range(2)]
+    assert b[0] == b[1]
 
 
 def test_noise_uniforms_come_from_philox_words():
-    seed, vid, v = 0x1234_5678_9ABC, 0xDEAD_BEEF_01, 4 * 1000 + 2
-    q = v >> 2
+    seed, vid = 0x1234_5678_9ABC, 0xDEAD_BEEF_01
+    shp = (20, 30, 40)                    # (nz, ny, nx): mx = 40, my = 30 -> Gy = 8
+    x, y, z = 17, 22, 13                  # y-group 5, lane 2
+    q = x + 40 * (22 // 4 + 8 * 13)
     r = O.philox4x32_10([q & 0xFFFFFFFF, q >> 32, vid & 0xFFFFFFFF, vid >> 32],
                         [seed & 0xFFFFFFFF, seed >> 32])
-    u1, s = O.noise_uniforms(seed, vid, v)
+    u1, s = O.noise_uniforms(seed, vid, shp, x, y, z)
     assert u1 == (2 * (int(r[2]) >> 9) + 1) / 2.0 ** 24
     assert s == 2 * ((int(r[3]) >> 8) / 2.0 ** 24) - 1
+    # Box-Muller closed form: even row -> R cos(pi s), odd row -> R sin(pi s)
+    R = math.sqrt(-2 * math.log(u1))
+    assert O.noise_normal(seed, vid, shp, x, y, z) == pytest.approx(R * math.cos(math.pi * s),
+                                                                    rel=1e-14, abs=1e-14)
+    assert O.noise_normal(seed, vid, shp, x, y + 1, z) == pytest.approx(R * math.sin(math.pi * s),
+                                                                        rel=1e-14, abs=1e-14)
 
 
 def test_noise_statistics_1e6():
     # SPEC.md:381 / S:639: 1e6 samples at sigma=1: |mean|<0.004, |sd-1|<0.01, |lag-1 rho|<0.005
-    n = O.noise_field((100, 100, 100), 1.0, 0x181111226, 3).ravel().astype(np.float64)
+    f = O.noise_field((100, 100, 100), 1.0, 0x181111226, 3).astype(np.float64)
+    n = f.ravel()
     assert abs(n.mean()) < 0.004
     assert abs(n.std() - 1.0) < 0.01
-    rho = np.corrcoef(n[:-1], n[1:])[0, 1]
-    assert abs(rho) < 0.005
-    # cos/sin partners (even/odd voxels of one Box-Muller pair) are uncorrelated
-    assert abs(np.corrcoef(n[0::2], n[1::2])[0, 1]) < 0.005
+    # lag-1 correlation along every axis (x: different blocks; y: cos/sin partners
+    # and block-mates; z: different blocks)
+    for ax in range(3):
+        a = np.moveaxis(f, ax, -1)
+        rho = np.corrcoef(a[..., :-1].ravel(), a[..., 1:].ravel())[0, 1]
+        assert abs(rho) < 0.005, (ax, rho)
+    # cos/sin partners (rows 2k, 2k+1 of one Box-Muller pair) are uncorrelated
+    assert abs(np.corrcoef(f[:, 0::2, :].ravel(), f[:, 1::2, :].ravel())[0, 1]) < 0.005
     # whole-distribution check against the standard normal CDF (Kolmogorov-Smirnov)
     from scipy import stats
     assert stats.kstest(n[::7], "norm").pvalue > 1e-3
