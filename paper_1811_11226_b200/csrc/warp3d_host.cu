@@ -320,9 +320,9 @@ w3d_status warp3d_noise(float* out, w3d_dims dims, float sigma, uint64_t seed, u
   if (st != W3D_OK) return st;
   if (!(std::isfinite(sigma) && sigma >= 0.0f))
     return fail(W3D_ERR_INVALID_ARG, "sigma must be finite and >= 0");
-  const cudaError_t e = launch_noise(out, nvox(dims), sigma, uint32_t(seed), uint32_t(seed >> 32),
-                                     uint32_t(volume_id), uint32_t(volume_id >> 32),
-                                     static_cast<cudaStream_t>(stream));
+  const cudaError_t e = launch_noise(out, dims.nx, dims.ny, dims.nz, sigma, uint32_t(seed),
+                                     uint32_t(seed >> 32), uint32_t(volume_id),
+                                     uint32_t(volume_id >> 32), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "warp3d_noise launch");
   return ok();
 }

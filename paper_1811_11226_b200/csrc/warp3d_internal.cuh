@@ -36,6 +36,12 @@ static_assert(sizeof(VolDev) == 112, "VolDev layout");
 
 constexpr int kMaxVolPerLaunch = 128;
 
+// Output tile of one CTA: lane = x, warp = z.
+constexpr int kTX = 32, kTY = 8, kTZ = 8, kThreads = 256;
+static_assert(kTX == 32 && kTZ * 32 == kThreads && kTY % 4 == 0, "tile shape");
+// Shared-memory capacity of the staged footprint box, in voxels (5 B each).
+constexpr int kDefaultCapVox = 10240;
+
 struct WarpArgs {
   const float* in;
   const uint8_t* in_lbl;  // may be null
@@ -55,8 +61,11 @@ struct WarpArgs {
 // Launchers (warp3d_kernels.cu).  All return cudaGetLastError() of the launch.
 cudaError_t launch_gather(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s);
-cudaError_t launch_noise(float* out, int64_t n, float sigma, uint32_t k0, uint32_t k1,
-                         uint32_t v0, uint32_t v1, cudaStream_t s);
+cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,
+                         uint32_t k1, uint32_t v0, uint32_t v1, cudaStream_t s);
+bool staged_supported(const WarpArgs& a);
+int stage_capacity();
+void set_stage_capacity(int cap_vox);
 cudaError_t launch_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                           int64_t n, cudaStream_t s);
 cudaError_t launch_footprint(const WarpArgs& a, uint8_t* marks, cudaStream_t s);
