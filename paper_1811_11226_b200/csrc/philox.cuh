@@ -30,18 +30,42 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Box-Muller on one Philox word pair (R10):
 //   u1 = (2*(ua >> 9) + 1) * 2^-24  in (0,1), exact in fp32
 //   s  = (ub >> 8) * 2^-23 - 1      in [-1,1), exact in fp32
 //   R  = sqrt(-2 ln u1);  n_even = R cos(pi s), n_odd = R sin(pi s)
-// logf is the accurate libdevice version (the fast __logf's absolute error
-// near u1 -> 1 breaks the 1e-3 HU tolerance, SURVEY.md key finding 5).
+// Error budget: -2 ln u1 uses MUFU.LG2 for
+// u1 <= 15/16 (absolute error ~2^-22.6 in lg2, relative < 2e-6 there) and the
+// series ln(1-t) = -t(1 + t/2 + t^2/3 + t^3/4 + t^4/5), t = 1 - u1 exact, for
+// u1 > 15/16 where the MUFU's absolute error would dominate (truncation
+// < 2e-7 relative).  R = x * rsqrt(x); sin/cos by MUFU on pi*s in [-pi, pi)
+// (absolute error ~2^-20.5).  Worst case |n_gpu - n| < 1e-5, i.e. < 2e-4 HU
+// at sigma = 20 HU, inside the 1e-3 HU image tolerance.
 __device__ __forceinline__ float2 box_muller(uint32_t ua, uint32_t ub) {
   const float u1 = __int2float_rn(static_cast<int>(((ua >> 9) << 1) | 1u)) * 0x1.0p-24f;
   const float s = __fmaf_rn(__int2float_rn(static_cast<int>(ub >> 8)), 0x1.0p-23f, -1.0f);
-  const float R = sqrtf(-2.0f * logf(u1));
+  const float t = 1.0f - u1;  // exact wherever the series is used (u1 > 1/2)
+  float ser = __fmaf_rn(t, 0.2f, 0.25f);
+  ser = __fmaf_rn(t, ser, 0.333333343f);
+  ser = __fmaf_rn(t, ser, 0.5f);
+  ser = __fmaf_rn(t, ser, 1.0f);
+  const float m2ln_series = 2.0f * t * ser;                       // -2 ln(1 - t)
+  const float m2ln_mufu = lg2_approx(u1) * -1.38629436f;         // -2 ln 2 * lg2(u1)
+  const float r2 = (t < 0.0625f) ? m2ln_series : m2ln_mufu;      // > 0
+  const float R = r2 * rsqrtf(r2);
   float sn, cs;
-  sincospif(s, &sn, &cs);
+  __sincosf(3.14159274f * s, &sn, &cs);
   return make_float2(R * cs, R * sn);
 }
 

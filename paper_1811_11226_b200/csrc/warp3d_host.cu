@@ -111,17 +111,29 @@ static VolDev derive(const float* A, const w3d_photometric* ph) {
   std::memset(&P, 0, sizeof(P));
   std::memcpy(P.A, A, sizeof(P.A));
   P.gamma = 1.0f;
+  P.win_s = 1.0f;
+  P.win_off = 0.0f;
+  P.clamp_lo = -INFINITY;
+  P.clamp_hi = INFINITY;
   if (!ph) return P;
   uint32_t f = 0;
-  if ((ph->flags & W3D_PH_NOISE) && ph->noise_sigma > 0.0f) f |= kNoise;
+  if ((ph->flags & W3D_PH_NOISE) && ph->noise_sigma > 0.0f) {
+    f |= kNoise;
+    P.sigma = ph->noise_sigma;
+  }
   if (ph->flags & W3D_PH_WINDOW) {
-    f |= kWindow;
     const double a = ph->window_lo, b = ph->window_hi;
     P.win_s = static_cast<float>(1.0 / (b - a));
     P.win_off = static_cast<float>(-a * double(P.win_s));
   }
-  if (ph->flags & W3D_PH_CLAMP) f |= kClamp;
-  if ((ph->flags & W3D_PH_GAMMA) && ph->gamma != 1.0f) f |= kGamma;
+  if (ph->flags & W3D_PH_CLAMP) {
+    P.clamp_lo = 0.0f;
+    P.clamp_hi = 1.0f;
+  }
+  if ((ph->flags & W3D_PH_GAMMA) && ph->gamma != 1.0f) {
+    f |= kGamma;
+    P.gamma = ph->gamma;
+  }
   if (ph->flags & W3D_PH_OCCLUDE) {
     // z0 <= z <= z0 + delta over integer z  <=>  ceil(z0) <= z <= floor(z0 + delta),
     // the sum in double exactly as the oracle evaluates it (R15).
@@ -134,8 +146,6 @@ static VolDev derive(const float* A, const w3d_photometric* ph) {
     if (P.occ_lo <= P.occ_hi) f |= kOcclude;
   }
   P.flags = f;
-  P.sigma = ph->noise_sigma;
-  P.gamma = ph->gamma;
   P.key0 = static_cast<uint32_t>(ph->seed);
   P.key1 = static_cast<uint32_t>(ph->seed >> 32);
   P.vid0 = static_cast<uint32_t>(ph->volume_id);

@@ -19,18 +19,23 @@ enum : uint32_t {
 };
 
 // Per-volume parameters as the kernels see them (derived on the host from
-// w3d_volume_params).
+// w3d_volume_params).  Disabled photometric
+// steps get neutral values, so the kernel evaluates the chain branch-free:
+//   v = fma(sigma, n, v); w = fma(v, win_s, win_off); w = min(max(w, lo), hi);
+//   out = (flags & kGamma) ? w^gamma : w
 struct alignas(16) VolDev {
   float A[12];        // [A | b] row-major, R4
-  uint32_t flags;     // effective kNoise | kWindow | ...
-  float sigma;        // HU
-  float win_s;        // s = fp32(1 / (b - a))
-  float win_off;      // fp32(-a * s): w = fma(v, s, off)
+  uint32_t flags;     // kNoise (sigma > 0) | kGamma (gamma != 1) | kOcclude
+  float sigma;        // HU; 0 without NOISE
+  float win_s;        // fp32(1 / (b - a)); 1 without WINDOW
+  float win_off;      // fp32(-a * s);      0 without WINDOW
+  float clamp_lo;     // 0 with CLAMP, else -inf
+  float clamp_hi;     // 1 with CLAMP, else +inf
   float gamma;
   uint32_t key0, key1;  // Philox key = seed
   uint32_t vid0, vid1;  // Philox counter words 2,3 = volume_id
   int32_t occ_lo, occ_hi;  // occluded output z in [occ_lo, occ_hi]
-  uint32_t _pad[3];
+  uint32_t _pad[2];
 };
 static_assert(sizeof(VolDev) == 112, "VolDev layout");
 
@@ -41,6 +46,7 @@ constexpr int kTX = 32, kTY = 8, kTZ = 8, kThreads = 256;
 static_assert(kTX == 32 && kTZ * 32 == kThreads && kTY % 4 == 0, "tile shape");
 // Shared-memory capacity of the staged footprint box, in voxels (5 B each).
 constexpr int kDefaultCapVox = 10240;
+constexpr int kMinBlocksPerSM = 3;
 
 struct WarpArgs {
   const float* in;

@@ -17,38 +17,56 @@ namespace w3d {
 // ----------------------------------------------------------------------------
 // Shared per-voxel pieces
 // ----------------------------------------------------------------------------
+extern __shared__ __align__(16) unsigned char g_smem[];
 
-// lerp(a, b, t) = a + t (b - a), one rounding for the difference, one FMA (R5).
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+// packed fp32x2 (sm_100 FADD2/FFMA2): per-lane IEEE rounding identical to scalar
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+// lerp(a, b, t) = a + t (b - a): one rounding for the difference, one FMA (R5).
 __device__ __forceinline__ float lerp(float a, float b, float t) {
   return __fmaf_rn(t, __fsub_rn(b, a), a);
 }
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float lg2_approx(float x) {
-  float y;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) {
+  return __ffma2_rn(t, sub2(b, a), a);
 }
 
-// Photometric tail for one voxel (PAPER.md:440-467 + gamma, R9-R14).
-// n is the standard normal of this voxel (ignored without kNoise).
-__device__ __forceinline__ float photometric(float v, float n, const VolDev& P) {
-  const uint32_t f = P.flags;
-  if (f & kNoise) v = __fmaf_rn(P.sigma, n, v);
-  if (f & kWindow) {
-    v = __fmaf_rn(v, P.win_s, P.win_off);  // (v - a) / (b - a)
-    if (f & kClamp) v = __saturatef(v);    // min(max(., 0), 1)
+// Per-volume parameters held in registers for the whole CTA (uniform).
+struct Params {
+  float A[12];
+  float sigma, win_s, win_off, lo, hi, gamma;
+  uint32_t flags, key0, key1, vid0, vid1;
+  int occ_lo, occ_hi;
+};
+
+__device__ __forceinline__ Params load_params(const VolDev& P) {
+  Params p;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) p.A[k] = P.A[k];
+  p.sigma = P.sigma; p.win_s = P.win_s; p.win_off = P.win_off;
+  p.lo = P.clamp_lo; p.hi = P.clamp_hi; p.gamma = P.gamma;
+  p.flags = P.flags; p.key0 = P.key0; p.key1 = P.key1; p.vid0 = P.vid0; p.vid1 = P.vid1;
+  p.occ_lo = P.occ_lo; p.occ_hi = P.occ_hi;
+  return p;
+}
+
+// Photometric tail for two voxels (PAPER.md:440-467 + gamma, R9-R14), branch
+// free: disabled steps carry neutral parameters (VolDev).
+__device__ __forceinline__ float2 photometric2(float2 v, float2 n, const Params& p) {
+  v = __ffma2_rn(f2(p.sigma), n, v);                      // I + sigma n
+  float2 w = __ffma2_rn(v, f2(p.win_s), f2(p.win_off));   // (I - a) / (b - a)
+  w.x = fminf(fmaxf(w.x, p.lo), p.hi);                    // clamp to [0, 1]
+  w.y = fminf(fmaxf(w.y, p.lo), p.hi);
+  if (p.flags & kGamma) {                                 // w^gamma
+    const float2 l = __fmul2_rn(make_float2(lg2_approx(w.x), lg2_approx(w.y)), f2(p.gamma));
+    w = make_float2(ex2_approx(l.x), ex2_approx(l.y));
   }
-  if (f & kGamma) v = ex2_approx(P.gamma * lg2_approx(v));  // w^gamma on [0,1]
-  return v;
+  return w;
 }
 
 // Normals of the 4 voxels (rows y = 4g .. 4g+3) of Philox block q (R10).
-__device__ __forceinline__ void normals4(uint32_t q, const VolDev& P, float n[4]) {
+__device__ __forceinline__ void normals4(uint32_t q, const Params& P, float n[4]) {
   const uint4 r = philox4x32_10(make_uint4(q, 0u, P.vid0, P.vid1), P.key0, P.key1);
   const float2 a = box_muller(r.x, r.y);
   const float2 b = box_muller(r.z, r.w);
@@ -115,88 +133,103 @@ __device__ __forceinline__ Sample sample_gather(const WarpArgs& a, const float* 
 }
 
 // ----------------------------------------------------------------------------
-// Staged sampling: the CTA's source footprint box is in shared memory with
-// `fill` / `label_fill` in its out-of-volume part, so no per-corner predicate is
-// needed.  p is clamped to [-1, n] first: a clamped coordinate reads only pad
-// voxels or gets weight 0 on in-volume ones, which reproduces the border-fill
-// rule (R6) and the label rule (R8) exactly.
+// Staged sampling of two voxels: the CTA's source footprint box is in shared
+// memory (g_smem) with `fill` / `label_fill` in its out-of-volume part, so no
+// per-corner predicate is needed.  Tiles whose transformed corners leave
+// [-1, n] clamp p to [-1, n] first: a clamped coordinate reads only pad voxels
+// or gets weight 0 on in-volume ones, which reproduces the border-fill rule
+// (R6) and the label rule (R8) exactly.
 // ----------------------------------------------------------------------------
-struct StageView {
-  const float* img;     // [D][H][W] floats
-  const uint8_t* lbl;   // [D][H][W] bytes, same index
-  int W, HW;            // row and plane pitch (elements)
+struct Stage {
+  int W, HW, lbl_off;   // row / plane pitch (elements); label region byte offset
   float bx, by, bz;     // box origin (input voxel coords of element 0)
   float Wf, HWf;
   float nx, ny, nz;     // clamp bounds
 };
 
-__device__ __forceinline__ Sample sample_staged(const StageView& v, float px, float py, float pz,
-                                                bool want_img, bool nearest_img,
-                                                bool has_lbl) {
-  Sample s;
-  px = fminf(fmaxf(px, -1.0f), v.nx);
-  py = fminf(fmaxf(py, -1.0f), v.ny);
-  pz = fminf(fmaxf(pz, -1.0f), v.nz);
-  const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
-  const float tx = __fsub_rn(px, fx), ty = __fsub_rn(py, fy), tz = __fsub_rn(pz, fz);
-  // local element index: all terms are small integers, exact in fp32
-  const float lf = __fmaf_rn(__fsub_rn(fz, v.bz), v.HWf,
-                             __fmaf_rn(__fsub_rn(fy, v.by), v.Wf, __fsub_rn(fx, v.bx)));
-  const int li = __float2int_rz(lf);
-  const int ln = li + (tx >= 0.5f ? 1 : 0) + (ty >= 0.5f ? v.W : 0) + (tz >= 0.5f ? v.HW : 0);
-  s.lbl = has_lbl ? v.lbl[ln] : 0u;
-  s.img = 0.0f;
-  if (!want_img) return s;
-  if (nearest_img) {
-    s.img = v.img[ln];
-    return s;
+template <bool kLabels, bool kNearest, bool kClamp>
+__device__ __forceinline__ void sample_staged2(const Stage& v, float2 px, float2 py, float2 pz,
+                                               bool want_img, float2& img, uint32_t& l0,
+                                               uint32_t& l1) {
+  const float* simg = reinterpret_cast<const float*>(g_smem);
+  const uint8_t* slbl = g_smem + v.lbl_off;
+  if (kClamp) {
+    px = make_float2(fminf(fmaxf(px.x, -1.0f), v.nx), fminf(fmaxf(px.y, -1.0f), v.nx));
+    py = make_float2(fminf(fmaxf(py.x, -1.0f), v.ny), fminf(fmaxf(py.y, -1.0f), v.ny));
+    pz = make_float2(fminf(fmaxf(pz.x, -1.0f), v.nz), fminf(fmaxf(pz.y, -1.0f), v.nz));
   }
-  const float* b = v.img + li;
+  const float2 fx = make_float2(floorf(px.x), floorf(px.y));
+  const float2 fy = make_float2(floorf(py.x), floorf(py.y));
+  const float2 fz = make_float2(floorf(pz.x), floorf(pz.y));
+  const float2 tx = sub2(px, fx), ty = sub2(py, fy), tz = sub2(pz, fz);
+  // local element index: all terms are small integers, exact in fp32
+  const float2 lf = __ffma2_rn(sub2(fz, f2(v.bz)), f2(v.HWf),
+                               __ffma2_rn(sub2(fy, f2(v.by)), f2(v.Wf), sub2(fx, f2(v.bx))));
+  const int li0 = __float2int_rz(lf.x), li1 = __float2int_rz(lf.y);
+  int ln0 = 0, ln1 = 0;
+  if (kLabels || kNearest) {
+    ln0 = li0 + (tx.x >= 0.5f ? 1 : 0) + (ty.x >= 0.5f ? v.W : 0) + (tz.x >= 0.5f ? v.HW : 0);
+    ln1 = li1 + (tx.y >= 0.5f ? 1 : 0) + (ty.y >= 0.5f ? v.W : 0) + (tz.y >= 0.5f ? v.HW : 0);
+  }
+  if (kLabels) {
+    l0 = slbl[ln0];
+    l1 = slbl[ln1];
+  }
+  if (!want_img) return;
+  if (kNearest) {
+    img = make_float2(simg[ln0], simg[ln1]);
+    return;
+  }
+  const float* b0 = simg + li0;
+  const float* b1 = simg + li1;
   const int W = v.W, HW = v.HW;
-  const float c000 = b[0], c100 = b[1], c010 = b[W], c110 = b[W + 1];
-  const float c001 = b[HW], c101 = b[HW + 1], c011 = b[HW + W], c111 = b[HW + W + 1];
-  const float c00 = lerp(c000, c100, tx), c10 = lerp(c010, c110, tx);
-  const float c01 = lerp(c001, c101, tx), c11 = lerp(c011, c111, tx);
-  s.img = lerp(lerp(c00, c10, ty), lerp(c01, c11, ty), tz);
-  return s;
+  const float2 c000 = make_float2(b0[0], b1[0]), c100 = make_float2(b0[1], b1[1]);
+  const float2 c010 = make_float2(b0[W], b1[W]), c110 = make_float2(b0[W + 1], b1[W + 1]);
+  const float2 c001 = make_float2(b0[HW], b1[HW]), c101 = make_float2(b0[HW + 1], b1[HW + 1]);
+  const float2 c011 = make_float2(b0[HW + W], b1[HW + W]);
+  const float2 c111 = make_float2(b0[HW + W + 1], b1[HW + W + 1]);
+  const float2 c00 = lerp2(c000, c100, tx), c10 = lerp2(c010, c110, tx);
+  const float2 c01 = lerp2(c001, c101, tx), c11 = lerp2(c011, c111, tx);
+  img = lerp2(lerp2(c00, c10, ty), lerp2(c01, c11, ty), tz);
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // ----------------------------------------------------------------------------
-// Output tile loop shared by both paths.  Thread (lane, warp) of the CTA owns
-// output column x = ox + lane at z = oz + warp and the kTY rows oy .. oy+kTY-1,
-// i.e. kTY/4 Philox blocks (R10: block = (x, y/4, z), lane = y mod 4).  A warp
-// writes 32 consecutive x of one row: 128 B image + 32 B label stores.
+// Output tile loop.  Thread (lane, warp) owns output column x = ox + lane at
+// z = oz + warp and rows oy .. oy+kTY-1, i.e. kTY/4 Philox blocks (R10: block =
+// (x, y/4, z), lane = y mod 4), evaluated as y-pairs with FFMA2/FADD2.  The
+// coordinate keeps the R4 nesting p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
+// A warp writes 32 consecutive x of one row: 128 B image + 32 B label stores.
 // ----------------------------------------------------------------------------
-template <bool kStagedPath>
-__device__ __forceinline__ void tile_compute(const WarpArgs& a, const VolDev& P,
+template <bool kStagedPath, bool kLabels, bool kNearest, bool kClamp>
+__device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
                                              const float* __restrict__ vin,
                                              const uint8_t* __restrict__ lin,
                                              float* __restrict__ vout,
-                                             uint8_t* __restrict__ lout, const StageView& sv,
+                                             uint8_t* __restrict__ lout, const Stage& sv,
                                              int ox, int oy, int oz) {
   const int X = ox + static_cast<int>(threadIdx.x & 31);
   const int Z = oz + static_cast<int>(threadIdx.x >> 5);
   if (X >= a.mx || Z >= a.mz) return;
   const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
-  float cz[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) cz[k] = __fmaf_rn(P.A[4 * k + 2], fZ, P.A[4 * k + 3]);
+  const float2 cz0 = f2(__fmaf_rn(P.A[2], fZ, P.A[3]));
+  const float2 cz1 = f2(__fmaf_rn(P.A[6], fZ, P.A[7]));
+  const float2 cz2 = f2(__fmaf_rn(P.A[10], fZ, P.A[11]));
   const bool occluded = (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;
-  const bool nearest_img = a.interp == W3D_INTERP_NEAREST;
   const int Gy = (a.my + 3) >> 2;
-  const int64_t zoff = static_cast<int64_t>(Z) * a.mx * a.my + X;
+  const int64_t o0 = (static_cast<int64_t>(Z) * a.my + oy) * a.mx + X;
+  float* po = vout + o0;
+  uint8_t* pl = kLabels ? lout + o0 : nullptr;
+  const int mx = a.mx;
 #pragma unroll
   for (int g = 0; g < kTY / 4; ++g) {
     const int Y0 = oy + 4 * g;
@@ -204,25 +237,39 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const VolDev& P,
     float n[4] = {0.f, 0.f, 0.f, 0.f};
     if ((P.flags & kNoise) && !occluded) {
       const uint32_t q = static_cast<uint32_t>(X) +
-                         static_cast<uint32_t>(a.mx) * static_cast<uint32_t>((Y0 >> 2) + Gy * Z);
+                         static_cast<uint32_t>(mx) * static_cast<uint32_t>((Y0 >> 2) + Gy * Z);
       normals4(q, P, n);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int Y = Y0 + k;
-      if (Y >= a.my) break;
-      const float fY = static_cast<float>(Y);
-      const float px = __fmaf_rn(P.A[0], fX, __fmaf_rn(P.A[1], fY, cz[0]));
-      const float py = __fmaf_rn(P.A[4], fX, __fmaf_rn(P.A[5], fY, cz[1]));
-      const float pz = __fmaf_rn(P.A[8], fX, __fmaf_rn(P.A[9], fY, cz[2]));
-      Sample s;
-      if (kStagedPath)
-        s = sample_staged(sv, px, py, pz, !occluded, nearest_img, lout != nullptr);
-      else
-        s = sample_gather(a, vin, lin, px, py, pz, !occluded);
-      const int64_t o = zoff + static_cast<int64_t>(Y) * a.mx;
-      vout[o] = occluded ? 0.0f : photometric(s.img, n[k], P);
-      if (lout) lout[o] = static_cast<uint8_t>(s.lbl);
+    for (int j = 0; j < 2; ++j) {
+      const int Ya = Y0 + 2 * j;
+      if (Ya >= a.my) break;
+      const bool second = Ya + 1 < a.my;   // the pair's second row exists
+      const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
+      const float2 px = __ffma2_rn(f2(P.A[0]), f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
+      const float2 py = __ffma2_rn(f2(P.A[4]), f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
+      const float2 pz = __ffma2_rn(f2(P.A[8]), f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
+      float2 img = make_float2(0.0f, 0.0f);
+      uint32_t l0 = 0, l1 = 0;
+      if (kStagedPath) {
+        sample_staged2<kLabels, kNearest, kClamp>(sv, px, py, pz, !occluded, img, l0, l1);
+      } else {
+        const Sample s0 = sample_gather(a, vin, lin, px.x, py.x, pz.x, !occluded);
+        const Sample s1 = sample_gather(a, vin, lin, px.y, py.y, pz.y, !occluded);
+        img = make_float2(s0.img, s1.img);
+        l0 = s0.lbl;
+        l1 = s1.lbl;
+      }
+      const float2 out = occluded ? make_float2(0.0f, 0.0f)
+                                  : photometric2(img, make_float2(n[2 * j], n[2 * j + 1]), P);
+      po[0] = out.x;
+      if (kLabels) pl[0] = static_cast<uint8_t>(l0);
+      if (second) {
+        po[mx] = out.y;
+        if (kLabels) pl[mx] = static_cast<uint8_t>(l1);
+      }
+      po += 2 * mx;
+      if (kLabels) pl += 2 * mx;
     }
   }
 }
@@ -234,26 +281,25 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const VolDev& P,
 // tile corners -- exact, because p is monotone in each output coordinate) in
 // shared memory with cp.async; tiles whose box exceeds cap_vox gather instead.
 // ----------------------------------------------------------------------------
-template <bool kStage>
-__global__ void __launch_bounds__(kThreads, 4)
+template <bool kStage, bool kLabels, bool kNearest>
+__global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
     warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_x, const int tiles_y,
                        const int cap_vox) {
-  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_box[8];
   const int vi = blockIdx.y;
-  const VolDev& P = a.vol[vi];
+  const Params P = load_params(a.vol[vi]);
   int t = blockIdx.x;
   const int ox = (t % tiles_x) * kTX;
   t /= tiles_x;
   const int oy = (t % tiles_y) * kTY;
   const int oz = (t / tiles_y) * kTZ;
   const float* __restrict__ vin = a.in + vi * a.in_stride;
-  const uint8_t* __restrict__ lin = a.in_lbl ? a.in_lbl + vi * a.in_stride : nullptr;
+  const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
   float* __restrict__ vout = a.out + vi * a.out_stride;
-  uint8_t* __restrict__ lout = a.out_lbl ? a.out_lbl + vi * a.out_stride : nullptr;
-  StageView sv;
+  uint8_t* __restrict__ lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
+  Stage sv;
   if (!kStage) {
-    tile_compute<false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+    tile_compute<false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
     return;
   }
   if (threadIdx.x < 32) {
@@ -264,8 +310,8 @@ __global__ void __launch_bounds__(kThreads, 4)
     float mn[3], mxv[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const float p = __fmaf_rn(P.A[4 * k], X,
-                                __fmaf_rn(P.A[4 * k + 1], Y, __fmaf_rn(P.A[4 * k + 2], Z, P.A[4 * k + 3])));
+      const float p = __fmaf_rn(P.A[4 * k], X, __fmaf_rn(P.A[4 * k + 1], Y,
+                                                         __fmaf_rn(P.A[4 * k + 2], Z, P.A[4 * k + 3])));
       mn[k] = p;
       mxv[k] = p;
     }
@@ -280,10 +326,12 @@ __global__ void __launch_bounds__(kThreads, 4)
       const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
                           static_cast<float>(a.nz)};
       int lo[3], hi[3];
+      bool inside = true;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         lo[k] = static_cast<int>(floorf(fminf(fmaxf(mn[k], -1.0f), n[k])));
         hi[k] = static_cast<int>(floorf(fminf(fmaxf(mxv[k], -1.0f), n[k]))) + 1;
+        inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
       }
       const int x0 = lo[0] >= 0 ? (lo[0] & ~3) : -4;
       const int W = (hi[0] + 1 - x0 + 3) & ~3;
@@ -291,54 +339,67 @@ __global__ void __launch_bounds__(kThreads, 4)
       s_box[0] = x0; s_box[1] = lo[1]; s_box[2] = lo[2];
       s_box[3] = W; s_box[4] = H; s_box[5] = D;
       s_box[6] = (static_cast<int64_t>(W) * H * D <= cap_vox) ? 1 : 0;
+      s_box[7] = inside ? 0 : 1;  // clamp needed
     }
   }
   __syncthreads();
   if (!s_box[6]) {
-    tile_compute<false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+    tile_compute<false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
     return;
   }
   const int bx = s_box[0], by = s_box[1], bz = s_box[2];
   const int W = s_box[3], H = s_box[4], D = s_box[5];
-  float* simg = reinterpret_cast<float*>(smem);
-  uint8_t* slbl = smem + static_cast<size_t>(cap_vox) * 4;
+  const bool need_clamp = s_box[7] != 0;
+  const uint32_t simg_s = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
+  const uint32_t slbl_s = simg_s + static_cast<uint32_t>(cap_vox) * 4u;
   {
-    // Stage rows of 16 B chunks (4 voxels): in-volume chunks by cp.async (image
-    // 16 B + label 4 B), out-of-volume chunks set to fill.  nx % 4 == 0 and
-    // x0 % 4 == 0, so a chunk is entirely inside or outside in x.
+    // Stage the box as 16 B chunks (4 voxels): in-volume chunks by cp.async
+    // (image 16 B + label 4 B), out-of-volume chunks set to fill.  nx % 4 == 0
+    // and x0 % 4 == 0, so a chunk is entirely inside or outside in x.  Thread
+    // i handles chunks i, i + 256, ...; (chunk, row, y, z) advance without
+    // division.
     const int CW = W >> 2;
     const int total = CW * H * D;
-    const float inv_cw = 1.0f / static_cast<float>(CW);
-    const float inv_h = 1.0f / static_cast<float>(H);
+    const int tid = static_cast<int>(threadIdx.x);
+    int c = tid % CW, r = tid / CW;
+    int ry = r % H, rz = r / H;
+    const int dc = kThreads % CW, dr = kThreads / CW;
     const float f = a.fill;
     const uint32_t lf4 = a.label_fill * 0x01010101u;
-    for (int i = threadIdx.x; i < total; i += kThreads) {
-      // float-reciprocal division, exact: the quotient q = (i + 0.5) / CW has
-      // relative error < 2^-22, i.e. absolute < (i + 0.5) 2^-22 / CW, below its
-      // distance 0.5 / CW to the nearest integer while i + 0.5 < 2^21.
-      const int row = __float2int_rz((static_cast<float>(i) + 0.5f) * inv_cw);
-      const int c = i - row * CW;
-      const int rz = __float2int_rz((static_cast<float>(row) + 0.5f) * inv_h);
-      const int ry = row - rz * H;
+    const int nx = a.nx, ny = a.ny, nz = a.nz;
+    for (int i = tid; i < total; i += kThreads) {
       const int gx = bx + 4 * c, gy = by + ry, gz = bz + rz;
-      const int li = row * W + 4 * c;
-      const bool in = (gx >= 0) & (gx < a.nx) & (gy >= 0) & (gy < a.ny) & (gz >= 0) & (gz < a.nz);
+      const uint32_t li = static_cast<uint32_t>(r * W + 4 * c);
+      const bool in = (static_cast<unsigned>(gx) < static_cast<unsigned>(nx)) &
+                      (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
+                      (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
       if (in) {
-        const int64_t g = (static_cast<int64_t>(gz) * a.ny + gy) * a.nx + gx;
-        cp_async16(simg + li, vin + g);
-        if (lin) cp_async4(slbl + li, lin + g);
+        const int g = (gz * ny + gy) * nx + gx;  // < 2^31 per volume
+        cp_async16(simg_s + 4u * li, vin + g);
+        if (kLabels) cp_async4(slbl_s + li, lin + g);
       } else {
-        *reinterpret_cast<float4*>(simg + li) = make_float4(f, f, f, f);
-        if (lin) *reinterpret_cast<uint32_t*>(slbl + li) = lf4;
+        *reinterpret_cast<float4*>(g_smem + 4u * li) = make_float4(f, f, f, f);
+        if (kLabels) *reinterpret_cast<uint32_t*>(g_smem + (slbl_s - simg_s) + li) = lf4;
+      }
+      c += dc;
+      r += dr;
+      ry += dr;
+      if (c >= CW) {
+        c -= CW;
+        ++r;
+        ++ry;
+      }
+      while (ry >= H) {
+        ry -= H;
+        ++rz;
       }
     }
     cp_async_wait_all();
   }
   __syncthreads();
-  sv.img = simg;
-  sv.lbl = slbl;
   sv.W = W;
   sv.HW = W * H;
+  sv.lbl_off = cap_vox * 4;
   sv.bx = static_cast<float>(bx);
   sv.by = static_cast<float>(by);
   sv.bz = static_cast<float>(bz);
@@ -347,7 +408,10 @@ __global__ void __launch_bounds__(kThreads, 4)
   sv.nx = static_cast<float>(a.nx);
   sv.ny = static_cast<float>(a.ny);
   sv.nz = static_cast<float>(a.nz);
-  tile_compute<true>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+  if (need_clamp)
+    tile_compute<true, kLabels, kNearest, true>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+  else
+    tile_compute<true, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
 }
 
 static int g_cap_vox = kDefaultCapVox;
@@ -355,29 +419,55 @@ static int g_cap_vox = kDefaultCapVox;
 int stage_capacity() { return g_cap_vox; }
 void set_stage_capacity(int cap) { g_cap_vox = cap; }
 
+template <bool kStage, bool kLabels, bool kNearest>
+static cudaError_t launch_variant(const WarpArgs& a, dim3 grid, int tiles_x, int tiles_y,
+                                  cudaStream_t s) {
+  if (kStage) {
+    const int cap = g_cap_vox;
+    const size_t smem = static_cast<size_t>(cap) * 5;
+    static size_t configured = 0;
+    if (configured != smem) {
+      const cudaError_t e = cudaFuncSetAttribute(warp3d_tile_kernel<kStage, kLabels, kNearest>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      configured = smem;
+    }
+    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, smem, s>>>(a, tiles_x,
+                                                                              tiles_y, cap);
+  } else {
+    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, 0, s>>>(a, tiles_x, tiles_y,
+                                                                           0);
+  }
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_tiles(const WarpArgs& a, bool staged, cudaStream_t s) {
   const int tiles_x = (a.mx + kTX - 1) / kTX, tiles_y = (a.my + kTY - 1) / kTY;
   const int tiles_z = (a.mz + kTZ - 1) / kTZ;
   const int64_t tiles = static_cast<int64_t>(tiles_x) * tiles_y * tiles_z;
   if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(a.nvol));
+  const bool labels = a.in_lbl != nullptr;
+  const bool nearest = a.interp == W3D_INTERP_NEAREST;
+  cudaError_t e;
   if (staged) {
-    const int cap = g_cap_vox;
-    const size_t smem = static_cast<size_t>(cap) * 5;
-    static size_t configured = 0;
-    if (configured != smem) {
-      const cudaError_t e = cudaFuncSetAttribute(
-          warp3d_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      configured = smem;
-    }
-    warp3d_tile_kernel<true><<<grid, kThreads, smem, s>>>(a, tiles_x, tiles_y, cap);
+    if (labels)
+      e = nearest ? launch_variant<true, true, true>(a, grid, tiles_x, tiles_y, s)
+                  : launch_variant<true, true, false>(a, grid, tiles_x, tiles_y, s);
+    else
+      e = nearest ? launch_variant<true, false, true>(a, grid, tiles_x, tiles_y, s)
+                  : launch_variant<true, false, false>(a, grid, tiles_x, tiles_y, s);
   } else {
-    warp3d_tile_kernel<false><<<grid, kThreads, 0, s>>>(a, tiles_x, tiles_y, 0);
+    if (labels)
+      e = nearest ? launch_variant<false, true, true>(a, grid, tiles_x, tiles_y, s)
+                  : launch_variant<false, true, false>(a, grid, tiles_x, tiles_y, s);
+    else
+      e = nearest ? launch_variant<false, false, true>(a, grid, tiles_x, tiles_y, s)
+                  : launch_variant<false, false, false>(a, grid, tiles_x, tiles_y, s);
   }
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 bool staged_supported(const WarpArgs& a) {
