@@ -150,6 +150,10 @@ static VolDev derive(const float* A, const w3d_photometric* ph) {
   P.key1 = static_cast<uint32_t>(ph->seed >> 32);
   P.vid0 = static_cast<uint32_t>(ph->volume_id);
   P.vid1 = static_cast<uint32_t>(ph->volume_id >> 32);
+  for (int r = 0; r < 10; ++r) {  // Philox key schedule (philox.cuh)
+    P.rk0[r] = P.key0 + static_cast<uint32_t>(r) * 0x9E3779B9u;
+    P.rk1[r] = P.key1 + static_cast<uint32_t>(r) * 0xBB67AE85u;
+  }
   return P;
 }
 

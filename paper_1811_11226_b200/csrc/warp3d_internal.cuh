@@ -36,17 +36,19 @@ struct alignas(16) VolDev {
   uint32_t vid0, vid1;  // Philox counter words 2,3 = volume_id
   int32_t occ_lo, occ_hi;  // occluded output z in [occ_lo, occ_hi]
   uint32_t _pad[2];
+  uint32_t rk0[10], rk1[10];  // Philox round keys k + r * (W0, W1), host-precomputed
+  uint32_t _pad2[4];
 };
-static_assert(sizeof(VolDev) == 112, "VolDev layout");
+static_assert(sizeof(VolDev) == 208, "VolDev layout");
 
 constexpr int kMaxVolPerLaunch = 128;
 
 // Output tile of one CTA: lane = x, warp = z.
-constexpr int kTX = 32, kTY = 8, kTZ = 8, kThreads = 256;
+constexpr int kTX = 32, kTY = 16, kTZ = 8, kThreads = 256;
 static_assert(kTX == 32 && kTZ * 32 == kThreads && kTY % 4 == 0, "tile shape");
 // Shared-memory capacity of the staged footprint box, in voxels (5 B each).
-constexpr int kDefaultCapVox = 10240;
-constexpr int kMinBlocksPerSM = 3;
+constexpr int kDefaultCapVox = 16384;
+constexpr int kMinBlocksPerSM = 2;
 
 struct WarpArgs {
   const float* in;

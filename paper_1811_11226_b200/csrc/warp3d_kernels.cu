@@ -36,8 +36,9 @@ __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) {
 struct Params {
   float A[12];
   float sigma, win_s, win_off, lo, hi, gamma;
-  uint32_t flags, key0, key1, vid0, vid1;
+  uint32_t flags, vid0, vid1;
   int occ_lo, occ_hi;
+  uint32_t rk0[10], rk1[10];
 };
 
 __device__ __forceinline__ Params load_params(const VolDev& P) {
@@ -46,8 +47,13 @@ __device__ __forceinline__ Params load_params(const VolDev& P) {
   for (int k = 0; k < 12; ++k) p.A[k] = P.A[k];
   p.sigma = P.sigma; p.win_s = P.win_s; p.win_off = P.win_off;
   p.lo = P.clamp_lo; p.hi = P.clamp_hi; p.gamma = P.gamma;
-  p.flags = P.flags; p.key0 = P.key0; p.key1 = P.key1; p.vid0 = P.vid0; p.vid1 = P.vid1;
+  p.flags = P.flags; p.vid0 = P.vid0; p.vid1 = P.vid1;
   p.occ_lo = P.occ_lo; p.occ_hi = P.occ_hi;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    p.rk0[r] = P.rk0[r];
+    p.rk1[r] = P.rk1[r];
+  }
   return p;
 }
 
@@ -67,7 +73,7 @@ __device__ __forceinline__ float2 photometric2(float2 v, float2 n, const Params&
 
 // Normals of the 4 voxels (rows y = 4g .. 4g+3) of Philox block q (R10).
 __device__ __forceinline__ void normals4(uint32_t q, const Params& P, float n[4]) {
-  const uint4 r = philox4x32_10(make_uint4(q, 0u, P.vid0, P.vid1), P.key0, P.key1);
+  const uint4 r = philox4x32_10_rk(make_uint4(q, 0u, P.vid0, P.vid1), P.rk0, P.rk1);
   const float2 a = box_muller(r.x, r.y);
   const float2 b = box_muller(r.z, r.w);
   n[0] = a.x; n[1] = a.y; n[2] = b.x; n[3] = b.y;
@@ -224,27 +230,24 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
   const float2 cz0 = f2(__fmaf_rn(P.A[2], fZ, P.A[3]));
   const float2 cz1 = f2(__fmaf_rn(P.A[6], fZ, P.A[7]));
   const float2 cz2 = f2(__fmaf_rn(P.A[10], fZ, P.A[11]));
-  const bool occluded = (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;
+  const bool occluded = (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;  // warp-uniform
+  const bool noise = (P.flags & kNoise) && !occluded;
   const int Gy = (a.my + 3) >> 2;
-  const int64_t o0 = (static_cast<int64_t>(Z) * a.my + oy) * a.mx + X;
-  float* po = vout + o0;
-  uint8_t* pl = kLabels ? lout + o0 : nullptr;
-  const int mx = a.mx;
-#pragma unroll
-  for (int g = 0; g < kTY / 4; ++g) {
-    const int Y0 = oy + 4 * g;
-    if (Y0 >= a.my) break;
+  const int mx = a.mx, my = a.my;
+  const int yend = min(oy + kTY, my);
+  // 32-bit offsets within the volume (< 2^31 voxels), one 64-bit add per store
+  uint32_t o = static_cast<uint32_t>((Z * my + oy) * mx + X);
+  const uint32_t q_base = static_cast<uint32_t>(X) + static_cast<uint32_t>(mx) *
+                                                      static_cast<uint32_t>(Gy * Z);
+#pragma unroll 1
+  for (int Y0 = oy; Y0 < yend; Y0 += 4) {
     float n[4] = {0.f, 0.f, 0.f, 0.f};
-    if ((P.flags & kNoise) && !occluded) {
-      const uint32_t q = static_cast<uint32_t>(X) +
-                         static_cast<uint32_t>(mx) * static_cast<uint32_t>((Y0 >> 2) + Gy * Z);
-      normals4(q, P, n);
-    }
+    if (noise) normals4(q_base + static_cast<uint32_t>(mx) * static_cast<uint32_t>(Y0 >> 2), P, n);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int Ya = Y0 + 2 * j;
-      if (Ya >= a.my) break;
-      const bool second = Ya + 1 < a.my;   // the pair's second row exists
+      if (Ya >= yend) break;
+      const bool second = Ya + 1 < yend;   // the pair's second row exists
       const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
       const float2 px = __ffma2_rn(f2(P.A[0]), f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
       const float2 py = __ffma2_rn(f2(P.A[4]), f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
@@ -262,14 +265,13 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
       }
       const float2 out = occluded ? make_float2(0.0f, 0.0f)
                                   : photometric2(img, make_float2(n[2 * j], n[2 * j + 1]), P);
-      po[0] = out.x;
-      if (kLabels) pl[0] = static_cast<uint8_t>(l0);
+      vout[o] = out.x;
+      if (kLabels) lout[o] = static_cast<uint8_t>(l0);
       if (second) {
-        po[mx] = out.y;
-        if (kLabels) pl[mx] = static_cast<uint8_t>(l1);
+        vout[o + mx] = out.y;
+        if (kLabels) lout[o + mx] = static_cast<uint8_t>(l1);
       }
-      po += 2 * mx;
-      if (kLabels) pl += 2 * mx;
+      o += 2 * mx;
     }
   }
 }
@@ -283,16 +285,13 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
 // ----------------------------------------------------------------------------
 template <bool kStage, bool kLabels, bool kNearest>
 __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
-    warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_x, const int tiles_y,
-                       const int cap_vox) {
+    warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap_vox) {
   __shared__ int s_box[8];
-  const int vi = blockIdx.y;
+  const int vi = static_cast<int>(blockIdx.z) / tiles_z;
   const Params P = load_params(a.vol[vi]);
-  int t = blockIdx.x;
-  const int ox = (t % tiles_x) * kTX;
-  t /= tiles_x;
-  const int oy = (t % tiles_y) * kTY;
-  const int oz = (t / tiles_y) * kTZ;
+  const int ox = static_cast<int>(blockIdx.x) * kTX;
+  const int oy = static_cast<int>(blockIdx.y) * kTY;
+  const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * kTZ;
   const float* __restrict__ vin = a.in + vi * a.in_stride;
   const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
   float* __restrict__ vout = a.out + vi * a.out_stride;
@@ -338,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
       const int H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
       s_box[0] = x0; s_box[1] = lo[1]; s_box[2] = lo[2];
       s_box[3] = W; s_box[4] = H; s_box[5] = D;
-      s_box[6] = (static_cast<int64_t>(W) * H * D <= cap_vox) ? 1 : 0;
+      s_box[6] = (static_cast<int64_t>(W) * H * D <= cap_vox && W <= 4 * kThreads) ? 1 : 0;
       s_box[7] = inside ? 0 : 1;  // clamp needed
     }
   }
@@ -350,48 +349,50 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
   const int bx = s_box[0], by = s_box[1], bz = s_box[2];
   const int W = s_box[3], H = s_box[4], D = s_box[5];
   const bool need_clamp = s_box[7] != 0;
-  const uint32_t simg_s = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
-  const uint32_t slbl_s = simg_s + static_cast<uint32_t>(cap_vox) * 4u;
   {
     // Stage the box as 16 B chunks (4 voxels): in-volume chunks by cp.async
     // (image 16 B + label 4 B), out-of-volume chunks set to fill.  nx % 4 == 0
     // and x0 % 4 == 0, so a chunk is entirely inside or outside in x.  Thread
-    // i handles chunks i, i + 256, ...; (chunk, row, y, z) advance without
-    // division.
+    // t owns chunk column c = t % CW of rows r = t / CW + k * (256 / CW)
+    // (W <= 1024 so CW <= 256); rows advance in (y, z) without division.
+    const uint32_t simg_s = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
+    const uint32_t slbl_s = simg_s + static_cast<uint32_t>(cap_vox) * 4u;
     const int CW = W >> 2;
-    const int total = CW * H * D;
+    const int rows_per_pass = kThreads / CW;
     const int tid = static_cast<int>(threadIdx.x);
-    int c = tid % CW, r = tid / CW;
-    int ry = r % H, rz = r / H;
-    const int dc = kThreads % CW, dr = kThreads / CW;
-    const float f = a.fill;
-    const uint32_t lf4 = a.label_fill * 0x01010101u;
-    const int nx = a.nx, ny = a.ny, nz = a.nz;
-    for (int i = tid; i < total; i += kThreads) {
-      const int gx = bx + 4 * c, gy = by + ry, gz = bz + rz;
-      const uint32_t li = static_cast<uint32_t>(r * W + 4 * c);
-      const bool in = (static_cast<unsigned>(gx) < static_cast<unsigned>(nx)) &
-                      (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
-                      (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
-      if (in) {
-        const int g = (gz * ny + gy) * nx + gx;  // < 2^31 per volume
-        cp_async16(simg_s + 4u * li, vin + g);
-        if (kLabels) cp_async4(slbl_s + li, lin + g);
-      } else {
-        *reinterpret_cast<float4*>(g_smem + 4u * li) = make_float4(f, f, f, f);
-        if (kLabels) *reinterpret_cast<uint32_t*>(g_smem + (slbl_s - simg_s) + li) = lf4;
-      }
-      c += dc;
-      r += dr;
-      ry += dr;
-      if (c >= CW) {
-        c -= CW;
-        ++r;
-        ++ry;
-      }
-      while (ry >= H) {
-        ry -= H;
-        ++rz;
+    const int c = tid % CW;
+    int r = tid / CW;
+    const int rows = H * D;
+    if (r < rows_per_pass) {
+      int rz = r / H, ry = r - (r / H) * H;
+      const int gx = bx + 4 * c;
+      const bool x_in = static_cast<unsigned>(gx) < static_cast<unsigned>(a.nx);
+      const int nx = a.nx, ny = a.ny, nz = a.nz;
+      const int plane = nx * ny;
+      const float f = a.fill;
+      const uint32_t lf4 = a.label_fill * 0x01010101u;
+      const int step_y = rows_per_pass % H, step_z = rows_per_pass / H;
+      uint32_t li = static_cast<uint32_t>(r * W + 4 * c);
+      const uint32_t lstep = static_cast<uint32_t>(rows_per_pass * W);
+      for (; r < rows; r += rows_per_pass) {
+        const int gy = by + ry, gz = bz + rz;
+        const bool in = x_in & (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
+                        (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
+        if (in) {
+          const uint32_t g = static_cast<uint32_t>(gz * plane + gy * nx + gx);
+          cp_async16(simg_s + 4u * li, vin + g);
+          if (kLabels) cp_async4(slbl_s + li, lin + g);
+        } else {
+          *reinterpret_cast<float4*>(g_smem + 4u * li) = make_float4(f, f, f, f);
+          if (kLabels) *reinterpret_cast<uint32_t*>(g_smem + (slbl_s - simg_s) + li) = lf4;
+        }
+        li += lstep;
+        ry += step_y;
+        rz += step_z;
+        if (ry >= H) {
+          ry -= H;
+          ++rz;
+        }
       }
     }
     cp_async_wait_all();
@@ -420,8 +421,7 @@ int stage_capacity() { return g_cap_vox; }
 void set_stage_capacity(int cap) { g_cap_vox = cap; }
 
 template <bool kStage, bool kLabels, bool kNearest>
-static cudaError_t launch_variant(const WarpArgs& a, dim3 grid, int tiles_x, int tiles_y,
-                                  cudaStream_t s) {
+static cudaError_t launch_variant(const WarpArgs& a, dim3 grid, int tiles_z, cudaStream_t s) {
   if (kStage) {
     const int cap = g_cap_vox;
     const size_t smem = static_cast<size_t>(cap) * 5;
@@ -433,11 +433,9 @@ static cudaError_t launch_variant(const WarpArgs& a, dim3 grid, int tiles_x, int
       if (e != cudaSuccess) return e;
       configured = smem;
     }
-    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, smem, s>>>(a, tiles_x,
-                                                                              tiles_y, cap);
+    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, smem, s>>>(a, tiles_z, cap);
   } else {
-    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, 0, s>>>(a, tiles_x, tiles_y,
-                                                                           0);
+    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, 0, s>>>(a, tiles_z, 0);
   }
   return cudaGetLastError();
 }
@@ -445,26 +443,27 @@ static cudaError_t launch_variant(const WarpArgs& a, dim3 grid, int tiles_x, int
 static cudaError_t launch_tiles(const WarpArgs& a, bool staged, cudaStream_t s) {
   const int tiles_x = (a.mx + kTX - 1) / kTX, tiles_y = (a.my + kTY - 1) / kTY;
   const int tiles_z = (a.mz + kTZ - 1) / kTZ;
-  const int64_t tiles = static_cast<int64_t>(tiles_x) * tiles_y * tiles_z;
-  if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
-  const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(a.nvol));
+  const int64_t gz = static_cast<int64_t>(tiles_z) * a.nvol;
+  if (tiles_y > 65535 || gz > 65535) return cudaErrorInvalidConfiguration;
+  const dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
+                  static_cast<unsigned>(gz));
   const bool labels = a.in_lbl != nullptr;
   const bool nearest = a.interp == W3D_INTERP_NEAREST;
   cudaError_t e;
   if (staged) {
     if (labels)
-      e = nearest ? launch_variant<true, true, true>(a, grid, tiles_x, tiles_y, s)
-                  : launch_variant<true, true, false>(a, grid, tiles_x, tiles_y, s);
+      e = nearest ? launch_variant<true, true, true>(a, grid, tiles_z, s)
+                  : launch_variant<true, true, false>(a, grid, tiles_z, s);
     else
-      e = nearest ? launch_variant<true, false, true>(a, grid, tiles_x, tiles_y, s)
-                  : launch_variant<true, false, false>(a, grid, tiles_x, tiles_y, s);
+      e = nearest ? launch_variant<true, false, true>(a, grid, tiles_z, s)
+                  : launch_variant<true, false, false>(a, grid, tiles_z, s);
   } else {
     if (labels)
-      e = nearest ? launch_variant<false, true, true>(a, grid, tiles_x, tiles_y, s)
-                  : launch_variant<false, true, false>(a, grid, tiles_x, tiles_y, s);
+      e = nearest ? launch_variant<false, true, true>(a, grid, tiles_z, s)
+                  : launch_variant<false, true, false>(a, grid, tiles_z, s);
     else
-      e = nearest ? launch_variant<false, false, true>(a, grid, tiles_x, tiles_y, s)
-                  : launch_variant<false, false, false>(a, grid, tiles_x, tiles_y, s);
+      e = nearest ? launch_variant<false, false, true>(a, grid, tiles_z, s)
+                  : launch_variant<false, false, false>(a, grid, tiles_z, s);
   }
   note_launch();
   return e;
