@@ -226,52 +226,64 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
   const int X = ox + static_cast<int>(threadIdx.x & 31);
   const int Z = oz + static_cast<int>(threadIdx.x >> 5);
   if (X >= a.mx || Z >= a.mz) return;
+  const int mx = a.mx, my = a.my;
+  const int yend = min(oy + kTY, my);
+  const bool occluded = (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;  // warp-uniform
+  // Noise for the thread's whole column first: kTY/4 independent Philox chains
+  // interleave (the 10-round chain is the kernel's longest dependency).
+  float n[kTY];
+#pragma unroll
+  for (int i = 0; i < kTY; ++i) n[i] = 0.0f;
+  if ((P.flags & kNoise) && !occluded) {
+    const int Gy = (my + 3) >> 2;
+    const uint32_t q0 = static_cast<uint32_t>(X) +
+                        static_cast<uint32_t>(mx) * static_cast<uint32_t>(Gy * Z + (oy >> 2));
+    uint4 r[kTY / 4];
+#pragma unroll
+    for (int g = 0; g < kTY / 4; ++g)
+      r[g] = philox4x32_10_rk(make_uint4(q0 + static_cast<uint32_t>(g * mx), 0u, P.vid0, P.vid1),
+                              P.rk0, P.rk1);
+#pragma unroll
+    for (int g = 0; g < kTY / 4; ++g) {
+      const float2 u = box_muller(r[g].x, r[g].y), v = box_muller(r[g].z, r[g].w);
+      n[4 * g] = u.x; n[4 * g + 1] = u.y; n[4 * g + 2] = v.x; n[4 * g + 3] = v.y;
+    }
+  }
   const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
   const float2 cz0 = f2(__fmaf_rn(P.A[2], fZ, P.A[3]));
   const float2 cz1 = f2(__fmaf_rn(P.A[6], fZ, P.A[7]));
   const float2 cz2 = f2(__fmaf_rn(P.A[10], fZ, P.A[11]));
-  const bool occluded = (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;  // warp-uniform
-  const bool noise = (P.flags & kNoise) && !occluded;
-  const int Gy = (a.my + 3) >> 2;
-  const int mx = a.mx, my = a.my;
-  const int yend = min(oy + kTY, my);
-  // 32-bit offsets within the volume (< 2^31 voxels), one 64-bit add per store
-  uint32_t o = static_cast<uint32_t>((Z * my + oy) * mx + X);
-  const uint32_t q_base = static_cast<uint32_t>(X) + static_cast<uint32_t>(mx) *
-                                                      static_cast<uint32_t>(Gy * Z);
-#pragma unroll 1
-  for (int Y0 = oy; Y0 < yend; Y0 += 4) {
-    float n[4] = {0.f, 0.f, 0.f, 0.f};
-    if (noise) normals4(q_base + static_cast<uint32_t>(mx) * static_cast<uint32_t>(Y0 >> 2), P, n);
+  const float2 ax0 = f2(P.A[0]), ax1 = f2(P.A[4]), ax2 = f2(P.A[8]);
+  // output offsets are 32-bit within a volume (< 2^31 voxels)
+  const uint32_t o0 = static_cast<uint32_t>((Z * my + oy) * mx + X);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int Ya = Y0 + 2 * j;
-      if (Ya >= yend) break;
-      const bool second = Ya + 1 < yend;   // the pair's second row exists
-      const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
-      const float2 px = __ffma2_rn(f2(P.A[0]), f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
-      const float2 py = __ffma2_rn(f2(P.A[4]), f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
-      const float2 pz = __ffma2_rn(f2(P.A[8]), f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
-      float2 img = make_float2(0.0f, 0.0f);
-      uint32_t l0 = 0, l1 = 0;
-      if (kStagedPath) {
-        sample_staged2<kLabels, kNearest, kClamp>(sv, px, py, pz, !occluded, img, l0, l1);
-      } else {
-        const Sample s0 = sample_gather(a, vin, lin, px.x, py.x, pz.x, !occluded);
-        const Sample s1 = sample_gather(a, vin, lin, px.y, py.y, pz.y, !occluded);
-        img = make_float2(s0.img, s1.img);
-        l0 = s0.lbl;
-        l1 = s1.lbl;
-      }
-      const float2 out = occluded ? make_float2(0.0f, 0.0f)
-                                  : photometric2(img, make_float2(n[2 * j], n[2 * j + 1]), P);
-      vout[o] = out.x;
-      if (kLabels) lout[o] = static_cast<uint8_t>(l0);
-      if (second) {
-        vout[o + mx] = out.y;
-        if (kLabels) lout[o + mx] = static_cast<uint8_t>(l1);
-      }
-      o += 2 * mx;
+  for (int j = 0; j < kTY / 2; ++j) {
+    const int Ya = oy + 2 * j;
+    if (Ya >= yend) break;
+    const bool second = Ya + 1 < yend;   // the pair's second row exists
+    const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
+    const float2 px = __ffma2_rn(ax0, f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
+    const float2 py = __ffma2_rn(ax1, f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
+    const float2 pz = __ffma2_rn(ax2, f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
+    float2 img = make_float2(0.0f, 0.0f);
+    uint32_t l0 = 0, l1 = 0;
+    if (kStagedPath) {
+      sample_staged2<kLabels, kNearest, kClamp>(sv, px, py, pz, !occluded, img, l0, l1);
+    } else {
+      const Sample s0 = sample_gather(a, vin, lin, px.x, py.x, pz.x, !occluded);
+      const Sample s1 = sample_gather(a, vin, lin, px.y, py.y, pz.y, !occluded);
+      img = make_float2(s0.img, s1.img);
+      l0 = s0.lbl;
+      l1 = s1.lbl;
+    }
+    const float2 out = occluded ? make_float2(0.0f, 0.0f)
+                                : photometric2(img, make_float2(n[2 * j], n[2 * j + 1]), P);
+    const uint32_t o = o0 + static_cast<uint32_t>(2 * j * mx);
+    vout[o] = out.x;
+    if (kLabels) lout[o] = static_cast<uint8_t>(l0);
+    if (second) {
+      vout[o + mx] = out.y;
+      if (kLabels) lout[o + mx] = static_cast<uint8_t>(l1);
     }
   }
 }
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
     // t owns chunk column c = t % CW of rows r = t / CW + k * (256 / CW)
     // (W <= 1024 so CW <= 256); rows advance in (y, z) without division.
     const uint32_t simg_s = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
-    const uint32_t slbl_s = simg_s + static_cast<uint32_t>(cap_vox) * 4u;
+    const uint32_t lbl_delta = static_cast<uint32_t>(cap_vox) * 4u;
     const int CW = W >> 2;
     const int rows_per_pass = kThreads / CW;
     const int tid = static_cast<int>(threadIdx.x);
@@ -364,34 +376,44 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
     int r = tid / CW;
     const int rows = H * D;
     if (r < rows_per_pass) {
-      int rz = r / H, ry = r - (r / H) * H;
-      const int gx = bx + 4 * c;
-      const bool x_in = static_cast<unsigned>(gx) < static_cast<unsigned>(a.nx);
       const int nx = a.nx, ny = a.ny, nz = a.nz;
-      const int plane = nx * ny;
+      int rz = r / H, ry = r - rz * H;
+      int gy = by + ry, gz = bz + rz;
+      const int gx = bx + 4 * c;
+      const bool x_in = static_cast<unsigned>(gx) < static_cast<unsigned>(nx);
+      // column base pointers (64-bit once); per row a 32-bit element offset
+      const float* gcol = vin + gx;
+      const uint8_t* lcol = kLabels ? lin + gx : nullptr;
+      int goff = gz * (nx * ny) + gy * nx;
+      const int step_y = rows_per_pass % H, step_z = rows_per_pass / H;
+      const int goff_step = step_z * (nx * ny) + step_y * nx;
+      const int goff_wrap = nx * ny - H * nx;
+      uint32_t sa = simg_s + 4u * static_cast<uint32_t>(r * W + 4 * c);
+      const uint32_t sa_step = 4u * static_cast<uint32_t>(rows_per_pass * W);
       const float f = a.fill;
       const uint32_t lf4 = a.label_fill * 0x01010101u;
-      const int step_y = rows_per_pass % H, step_z = rows_per_pass / H;
-      uint32_t li = static_cast<uint32_t>(r * W + 4 * c);
-      const uint32_t lstep = static_cast<uint32_t>(rows_per_pass * W);
       for (; r < rows; r += rows_per_pass) {
-        const int gy = by + ry, gz = bz + rz;
         const bool in = x_in & (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
                         (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
         if (in) {
-          const uint32_t g = static_cast<uint32_t>(gz * plane + gy * nx + gx);
-          cp_async16(simg_s + 4u * li, vin + g);
-          if (kLabels) cp_async4(slbl_s + li, lin + g);
+          cp_async16(sa, gcol + goff);
+          if (kLabels) cp_async4((sa - simg_s) / 4u + simg_s + lbl_delta, lcol + goff);
         } else {
-          *reinterpret_cast<float4*>(g_smem + 4u * li) = make_float4(f, f, f, f);
-          if (kLabels) *reinterpret_cast<uint32_t*>(g_smem + (slbl_s - simg_s) + li) = lf4;
+          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};\n" ::"r"(sa), "f"(f) : "memory");
+          if (kLabels)
+            asm volatile("st.shared.u32 [%0], %1;\n" ::"r"((sa - simg_s) / 4u + simg_s + lbl_delta),
+                         "r"(lf4) : "memory");
         }
-        li += lstep;
+        sa += sa_step;
         ry += step_y;
-        rz += step_z;
+        gy += step_y;
+        gz += step_z;
+        goff += goff_step;
         if (ry >= H) {
           ry -= H;
-          ++rz;
+          gy -= H;
+          ++gz;
+          goff += goff_wrap;
         }
       }
     }
