@@ -314,6 +314,7 @@ def main():
     naive_bytes = 10 * B * nvox_out
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    tiles_before = W.warp3d_tile_stats()
     stream = torch.cuda.current_stream(dev)
     for _ in range(max(3, args.warmup)):
         flush.fill_(1)
@@ -334,6 +335,7 @@ def main():
             ends[k].record(stream)
         torch.cuda.synchronize(dev)
     launches = W.warp3d_launch_count() - launches0
+    st0 = W.warp3d_tile_stats()
     if world > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -379,6 +381,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "tiles": {"staged": st0[0] - tiles_before[0], "gather": st0[1] - tiles_before[1]},
             "clocks": clk.summary(),
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms),
                         "max": max(step_ms)},

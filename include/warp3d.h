@@ -190,6 +190,12 @@ w3d_status warp3d_footprint_batched(int32_t batch, w3d_dims in_dims,
  * bench.py's gpu_launches). */
 uint64_t warp3d_launch_count(void);
 
+/* Diagnostics: out[0] = output tiles computed from a staged shared-memory box,
+ * out[1] = tiles computed by gathers (variant GATHER, unaligned inputs, or a
+ * footprint larger than the staging buffer), cumulative in this process.
+ * Synchronises the device (not for the hot path). */
+w3d_status warp3d_tile_stats(uint64_t out[2]);
+
 /* Thread-local message for the last non-OK status of this thread ("" if none). */
 const char* warp3d_last_error(void);
 

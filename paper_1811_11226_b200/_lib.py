@@ -25,7 +25,7 @@ EXPORTS = (
     "warp3d_affine", "warp3d_affine_batched", "warp3d_affine_batched_ex",
     "warp3d_compose_affine", "warp3d_noise", "warp3d_philox4x32_10",
     "warp3d_footprint_batched", "warp3d_launch_count", "warp3d_last_error",
-    "warp3d_abi_version",
+    "warp3d_abi_version", "warp3d_tile_stats",
 )
 
 
@@ -93,6 +93,8 @@ def load():
     L.warp3d_noise.argtypes = [P, Dims, F, U64, U64, P]
     L.warp3d_philox4x32_10.argtypes = [P, U64, P, I64, P]
     L.warp3d_footprint_batched.argtypes = [I32, Dims, P, Dims, P, P, P]
+    L.warp3d_tile_stats.argtypes = [P]
+    L.warp3d_tile_stats.restype = ctypes.c_int
     L.warp3d_launch_count.restype = U64
     L.warp3d_launch_count.argtypes = []
     L.warp3d_last_error.restype = ctypes.c_char_p

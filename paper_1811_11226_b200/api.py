@@ -19,6 +19,7 @@ from ._lib import (INTERP_LINEAR, INTERP_NEAREST, KERNEL_AUTO, KERNEL_GATHER, KE
 __all__ = [
     "warp3d_affine", "warp3d_affine_batched", "warp3d_compose_affine", "warp3d_noise",
     "warp3d_philox4x32_10", "warp3d_footprint_batched", "warp3d_launch_count",
+    "warp3d_tile_stats",
     "warp3d_abi_version", "photometric", "volume_params", "make_geom", "Warp3DError",
     "INTERP_LINEAR", "INTERP_NEAREST", "KERNEL_AUTO", "KERNEL_GATHER", "KERNEL_STAGED",
     "PH_NOISE", "PH_WINDOW", "PH_CLAMP", "PH_GAMMA", "PH_OCCLUDE",
@@ -155,6 +156,13 @@ def warp3d_footprint_batched(params, in_shape_zyx, out_shape_zyx=None, device="c
 
 def warp3d_launch_count() -> int:
     return int(L.load().warp3d_launch_count())
+
+
+def warp3d_tile_stats():
+    """(staged tiles, gather tiles) computed so far in this process (diagnostic)."""
+    out = (ctypes.c_uint64 * 2)()
+    L.check(L.load().warp3d_tile_stats(out))
+    return int(out[0]), int(out[1])
 
 
 def warp3d_abi_version() -> int:

@@ -180,8 +180,9 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
     args.interp = interp;
     args.nvol = nv;
     for (int32_t i = 0; i < nv; ++i) args.vol[i] = derive(affines[v0 + i], phs[v0 + i]);
-    const cudaError_t e = (variant == W3D_KERNEL_GATHER) ? launch_gather(args, stream)
-                                                         : launch_staged(args, stream);
+    const cudaError_t e = (variant == W3D_KERNEL_GATHER)   ? launch_gather(args, stream)
+                          : (variant == W3D_KERNEL_STAGED) ? launch_staged(args, stream)
+                                                           : launch_auto(args, stream);
     if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");
   }
   return ok();
@@ -213,6 +214,16 @@ int warp3d_abi_version(void) { return WARP3D_ABI_VERSION; }
 const char* warp3d_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t warp3d_launch_count(void) { return g_launches.load(); }
+
+w3d_status warp3d_tile_stats(uint64_t out[2]) {
+  if (!out) return fail(W3D_ERR_INVALID_ARG, "out must be non-NULL");
+  unsigned long long v[2] = {0, 0};
+  const cudaError_t e = read_tile_stats(v);
+  if (e != cudaSuccess) return cuda_fail(e, "warp3d_tile_stats");
+  out[0] = v[0];
+  out[1] = v[1];
+  return ok();
+}
 
 w3d_status warp3d_affine(const float* in, w3d_dims in_dims, const float affine[12],
                          w3d_interp interp, float fill, const w3d_photometric* ph, float* out,

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "philox.cuh"
 #include "warp3d_internal.cuh"
@@ -18,6 +19,12 @@ namespace w3d {
 // Shared per-voxel pieces
 // ----------------------------------------------------------------------------
 extern __shared__ __align__(16) unsigned char g_smem[];
+
+// Diagnostics (warp3d_tile_stats): tiles computed from a staged box / by gathers.
+__device__ unsigned long long g_tiles_staged = 0, g_tiles_gather = 0;
+__device__ __forceinline__ void count_tile(bool staged) {
+  if (threadIdx.x == 0) atomicAdd(staged ? &g_tiles_staged : &g_tiles_gather, 1ull);
+}
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 // packed fp32x2 (sm_100 FADD2/FFMA2): per-lane IEEE rounding identical to scalar
@@ -147,7 +154,8 @@ __device__ __forceinline__ Sample sample_gather(const WarpArgs& a, const float* 
 // (R6) and the label rule (R8) exactly.
 // ----------------------------------------------------------------------------
 struct Stage {
-  int W, HW, lbl_off;   // row / plane pitch (elements); label region byte offset
+  int W, HW;            // row / plane pitch (elements)
+  int img_off, lbl_off; // byte offsets of this buffer's image / label regions in g_smem
   float bx, by, bz;     // box origin (input voxel coords of element 0)
   float Wf, HWf;
   float nx, ny, nz;     // clamp bounds
@@ -157,7 +165,7 @@ template <bool kLabels, bool kNearest, bool kClamp>
 __device__ __forceinline__ void sample_staged2(const Stage& v, float2 px, float2 py, float2 pz,
                                                bool want_img, float2& img, uint32_t& l0,
                                                uint32_t& l1) {
-  const float* simg = reinterpret_cast<const float*>(g_smem);
+  const float* simg = reinterpret_cast<const float*>(g_smem + v.img_off);
   const uint8_t* slbl = g_smem + v.lbl_off;
   if (kClamp) {
     px = make_float2(fminf(fmaxf(px.x, -1.0f), v.nx), fminf(fmaxf(px.y, -1.0f), v.nx));
@@ -210,41 +218,57 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // ----------------------------------------------------------------------------
-// Output tile loop.  Thread (lane, warp) owns output column x = ox + lane at
-// z = oz + warp and rows oy .. oy+kTY-1, i.e. kTY/4 Philox blocks (R10: block =
-// (x, y/4, z), lane = y mod 4), evaluated as y-pairs with FFMA2/FADD2.  The
-// coordinate keeps the R4 nesting p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
-// A warp writes 32 consecutive x of one row: 128 B image + 32 B label stores.
+// Tile shapes.  Lane = output x (a warp covers 32 consecutive x of one row, so
+// stores are 128 B + 32 B and shared-memory gathers stay bank-friendly); warp
+// w covers z = w % TZ and the y-rows [yh * RPT, (yh + 1) * RPT), yh = w / TZ.
 // ----------------------------------------------------------------------------
-template <bool kStagedPath, bool kLabels, bool kNearest, bool kClamp>
+template <int TX_, int TY_, int TZ_, int THREADS_>
+struct Shape {
+  static constexpr int TX = TX_, TY = TY_, TZ = TZ_, THREADS = THREADS_;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int RPT = TY * TZ / WARPS;  // rows per thread
+  static_assert(TX == 32 && WARPS % TZ == 0 && RPT % 4 == 0 && TY % RPT == 0, "shape");
+};
+using TileShape = Shape<kTX, kTY, kTZ, kThreads>;   // one tile per CTA
+using PersShape = Shape<32, 16, 16, 1024>;           // persistent, double-buffered
+using PersShapeS = Shape<32, 16, 8, 512>;            // persistent, 2 CTAs / SM
+
+// ----------------------------------------------------------------------------
+// Output tile loop.  A thread owns output column x at one z and RPT rows, i.e.
+// RPT/4 Philox blocks (R10: block = (x, y/4, z), lane = y mod 4) computed first
+// as independent chains, then y-pairs with FFMA2/FADD2.  The coordinate keeps
+// the R4 nesting p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
+// ----------------------------------------------------------------------------
+template <class S, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp>
 __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
                                              const float* __restrict__ vin,
                                              const uint8_t* __restrict__ lin,
                                              float* __restrict__ vout,
                                              uint8_t* __restrict__ lout, const Stage& sv,
                                              int ox, int oy, int oz) {
+  constexpr int RPT = S::RPT;
+  const int w = static_cast<int>(threadIdx.x >> 5);
   const int X = ox + static_cast<int>(threadIdx.x & 31);
-  const int Z = oz + static_cast<int>(threadIdx.x >> 5);
-  if (X >= a.mx || Z >= a.mz) return;
+  const int Z = oz + w % S::TZ;
+  const int ybeg = oy + (w / S::TZ) * RPT;
   const int mx = a.mx, my = a.my;
-  const int yend = min(oy + kTY, my);
+  if (X >= mx || Z >= a.mz || ybeg >= my) return;
+  const int yend = min(ybeg + RPT, my);
   const bool occluded = (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;  // warp-uniform
-  // Noise for the thread's whole column first: kTY/4 independent Philox chains
-  // interleave (the 10-round chain is the kernel's longest dependency).
-  float n[kTY];
+  float n[RPT];
 #pragma unroll
-  for (int i = 0; i < kTY; ++i) n[i] = 0.0f;
+  for (int i = 0; i < RPT; ++i) n[i] = 0.0f;
   if ((P.flags & kNoise) && !occluded) {
     const int Gy = (my + 3) >> 2;
     const uint32_t q0 = static_cast<uint32_t>(X) +
-                        static_cast<uint32_t>(mx) * static_cast<uint32_t>(Gy * Z + (oy >> 2));
-    uint4 r[kTY / 4];
+                        static_cast<uint32_t>(mx) * static_cast<uint32_t>(Gy * Z + (ybeg >> 2));
+    uint4 r[RPT / 4];
 #pragma unroll
-    for (int g = 0; g < kTY / 4; ++g)
+    for (int g = 0; g < RPT / 4; ++g)
       r[g] = philox4x32_10_rk(make_uint4(q0 + static_cast<uint32_t>(g * mx), 0u, P.vid0, P.vid1),
                               P.rk0, P.rk1);
 #pragma unroll
-    for (int g = 0; g < kTY / 4; ++g) {
+    for (int g = 0; g < RPT / 4; ++g) {
       const float2 u = box_muller(r[g].x, r[g].y), v = box_muller(r[g].z, r[g].w);
       n[4 * g] = u.x; n[4 * g + 1] = u.y; n[4 * g + 2] = v.x; n[4 * g + 3] = v.y;
     }
@@ -253,18 +277,17 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
   const float2 cz0 = f2(__fmaf_rn(P.A[2], fZ, P.A[3]));
   const float2 cz1 = f2(__fmaf_rn(P.A[6], fZ, P.A[7]));
   const float2 cz2 = f2(__fmaf_rn(P.A[10], fZ, P.A[11]));
-  const float2 ax0 = f2(P.A[0]), ax1 = f2(P.A[4]), ax2 = f2(P.A[8]);
   // output offsets are 32-bit within a volume (< 2^31 voxels)
-  const uint32_t o0 = static_cast<uint32_t>((Z * my + oy) * mx + X);
+  const uint32_t o0 = static_cast<uint32_t>((Z * my + ybeg) * mx + X);
 #pragma unroll
-  for (int j = 0; j < kTY / 2; ++j) {
-    const int Ya = oy + 2 * j;
+  for (int j = 0; j < RPT / 2; ++j) {
+    const int Ya = ybeg + 2 * j;
     if (Ya >= yend) break;
     const bool second = Ya + 1 < yend;   // the pair's second row exists
     const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
-    const float2 px = __ffma2_rn(ax0, f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
-    const float2 py = __ffma2_rn(ax1, f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
-    const float2 pz = __ffma2_rn(ax2, f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
+    const float2 px = __ffma2_rn(f2(P.A[0]), f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
+    const float2 py = __ffma2_rn(f2(P.A[4]), f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
+    const float2 pz = __ffma2_rn(f2(P.A[8]), f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
     float2 img = make_float2(0.0f, 0.0f);
     uint32_t l0 = 0, l1 = 0;
     if (kStagedPath) {
@@ -288,156 +311,271 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
   }
 }
 
+// Box of one tile (warp 0): the bounding box of the 8 transformed tile corners
+// -- exact, because p is monotone in each output coordinate -- clamped to
+// [-1, n+1], x origin rounded down to a multiple of 4 and width up.
+// box = {x0, y0, z0, W, H, D, staged, clamp}.
+template <class S>
+__device__ __forceinline__ void tile_box(const WarpArgs& a, const Params& P, int ox, int oy,
+                                         int oz, int cap_vox, int* box) {
+  const int c = threadIdx.x & 7;
+  const float X = static_cast<float>((c & 1) ? min(ox + S::TX, a.mx) - 1 : ox);
+  const float Y = static_cast<float>((c & 2) ? min(oy + S::TY, a.my) - 1 : oy);
+  const float Z = static_cast<float>((c & 4) ? min(oz + S::TZ, a.mz) - 1 : oz);
+  float mn[3], mxv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float p = __fmaf_rn(P.A[4 * k], X, __fmaf_rn(P.A[4 * k + 1], Y,
+                                                       __fmaf_rn(P.A[4 * k + 2], Z, P.A[4 * k + 3])));
+    mn[k] = p;
+    mxv[k] = p;
+  }
+#pragma unroll
+  for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+      mxv[k] = fmaxf(mxv[k], __shfl_xor_sync(0xffffffffu, mxv[k], off));
+    }
+  if ((threadIdx.x & 31) == 0) {
+    const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                        static_cast<float>(a.nz)};
+    int lo[3], hi[3];
+    bool inside = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = static_cast<int>(floorf(fminf(fmaxf(mn[k], -1.0f), n[k])));
+      hi[k] = static_cast<int>(floorf(fminf(fmaxf(mxv[k], -1.0f), n[k]))) + 1;
+      inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
+    }
+    const int x0 = lo[0] >= 0 ? (lo[0] & ~3) : -4;
+    const int W = (hi[0] + 1 - x0 + 3) & ~3;
+    const int H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
+    box[0] = x0; box[1] = lo[1]; box[2] = lo[2];
+    box[3] = W; box[4] = H; box[5] = D;
+    box[6] = (static_cast<int64_t>(W) * H * D <= cap_vox && W <= 4 * S::THREADS) ? 1 : 0;
+    box[7] = inside ? 0 : 1;  // clamp needed
+  }
+}
+
+// Issue the staging of one box into the buffer at byte offsets (img_off,
+// lbl_off) of g_smem: 16 B chunks (4 voxels); in-volume chunks by cp.async
+// (image 16 B + label 4 B), out-of-volume chunks set to fill / label_fill.
+// nx % 4 == 0 and x0 % 4 == 0, so a chunk is entirely inside or outside in x.
+// Thread t owns chunk column c = t % CW of rows r = t / CW + k (THREADS / CW);
+// rows advance in (y, z) without division.  Completion: cp.async.wait_*.
+template <class S, bool kLabels>
+__device__ __forceinline__ void stage_box(const WarpArgs& a, const float* __restrict__ vin,
+                                          const uint8_t* __restrict__ lin, const int* box,
+                                          uint32_t img_off, uint32_t lbl_off) {
+  const int bx = box[0], by = box[1], bz = box[2], W = box[3], H = box[4], D = box[5];
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
+  const int CW = W >> 2;
+  const int rows_per_pass = S::THREADS / CW;
+  const int tid = static_cast<int>(threadIdx.x);
+  const int c = tid % CW;
+  int r = tid / CW;
+  if (r >= rows_per_pass) return;
+  const int rows = H * D;
+  const int nx = a.nx, ny = a.ny, nz = a.nz;
+  int rz = r / H, ry = r - rz * H;
+  int gy = by + ry, gz = bz + rz;
+  const int gx = bx + 4 * c;
+  const bool x_in = static_cast<unsigned>(gx) < static_cast<unsigned>(nx);
+  const float* gcol = vin + gx;
+  const uint8_t* lcol = kLabels ? lin + gx : nullptr;
+  int goff = gz * (nx * ny) + gy * nx;
+  const int step_y = rows_per_pass % H, step_z = rows_per_pass / H;
+  const int goff_step = step_z * (nx * ny) + step_y * nx;
+  const int goff_wrap = nx * ny - H * nx;
+  uint32_t li = static_cast<uint32_t>(r * W + 4 * c);
+  const uint32_t li_step = static_cast<uint32_t>(rows_per_pass * W);
+  const uint32_t simg = sbase + img_off, slbl = sbase + lbl_off;
+  const float f = a.fill;
+  const uint32_t lf4 = a.label_fill * 0x01010101u;
+  for (; r < rows; r += rows_per_pass) {
+    const bool in = x_in & (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
+                    (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
+    if (in) {
+      cp_async16(simg + 4u * li, gcol + goff);
+      if (kLabels) cp_async4(slbl + li, lcol + goff);
+    } else {
+      asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};\n" ::"r"(simg + 4u * li), "f"(f)
+                   : "memory");
+      if (kLabels) asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(slbl + li), "r"(lf4) : "memory");
+    }
+    li += li_step;
+    ry += step_y;
+    gy += step_y;
+    gz += step_z;
+    goff += goff_step;
+    if (ry >= H) {
+      ry -= H;
+      gy -= H;
+      ++gz;
+      goff += goff_wrap;
+    }
+  }
+}
+
+__device__ __forceinline__ Stage make_stage(const WarpArgs& a, const int* box, int img_off,
+                                            int lbl_off) {
+  Stage sv;
+  sv.W = box[3];
+  sv.HW = box[3] * box[4];
+  sv.img_off = img_off;
+  sv.lbl_off = lbl_off;
+  sv.bx = static_cast<float>(box[0]);
+  sv.by = static_cast<float>(box[1]);
+  sv.bz = static_cast<float>(box[2]);
+  sv.Wf = static_cast<float>(sv.W);
+  sv.HWf = static_cast<float>(sv.HW);
+  sv.nx = static_cast<float>(a.nx);
+  sv.ny = static_cast<float>(a.ny);
+  sv.nz = static_cast<float>(a.nz);
+  return sv;
+}
+
+template <class S, bool kLabels, bool kNearest>
+__device__ __forceinline__ void compute_staged(const WarpArgs& a, const Params& P,
+                                               const float* vin, const uint8_t* lin, float* vout,
+                                               uint8_t* lout, const int* box, int img_off,
+                                               int lbl_off, int ox, int oy, int oz) {
+  const Stage sv = make_stage(a, box, img_off, lbl_off);
+  if (box[7])
+    tile_compute<S, true, kLabels, kNearest, true>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+  else
+    tile_compute<S, true, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+}
+
 // ----------------------------------------------------------------------------
-// Kernel: one CTA per kTX x kTY x kTZ output tile; grid = (tiles, volumes),
-// tiles x-fastest so CTAs of one volume run together (L2 holds ~1 volume).
-// kStage: stage the tile's source footprint (bounding box of the 8 transformed
-// tile corners -- exact, because p is monotone in each output coordinate) in
-// shared memory with cp.async; tiles whose box exceeds cap_vox gather instead.
+// Kernel A (one tile per CTA): grid = (tiles_x, tiles_y, tiles_z * volumes).
+// kStage: stage the tile's footprint box; tiles whose box exceeds cap_vox (or
+// kStage = false: the W3D_KERNEL_GATHER variant) gather through L1/L2.
 // ----------------------------------------------------------------------------
 template <bool kStage, bool kLabels, bool kNearest>
 __global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
     warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap_vox) {
+  using S = TileShape;
   __shared__ int s_box[8];
   const int vi = static_cast<int>(blockIdx.z) / tiles_z;
   const Params P = load_params(a.vol[vi]);
-  const int ox = static_cast<int>(blockIdx.x) * kTX;
-  const int oy = static_cast<int>(blockIdx.y) * kTY;
-  const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * kTZ;
+  const int ox = static_cast<int>(blockIdx.x) * S::TX;
+  const int oy = static_cast<int>(blockIdx.y) * S::TY;
+  const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * S::TZ;
   const float* __restrict__ vin = a.in + vi * a.in_stride;
   const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
   float* __restrict__ vout = a.out + vi * a.out_stride;
   uint8_t* __restrict__ lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
   Stage sv;
   if (!kStage) {
-    tile_compute<false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+    count_tile(false);
+    tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
     return;
   }
-  if (threadIdx.x < 32) {
-    const int c = threadIdx.x & 7;
-    const float X = static_cast<float>((c & 1) ? min(ox + kTX, a.mx) - 1 : ox);
-    const float Y = static_cast<float>((c & 2) ? min(oy + kTY, a.my) - 1 : oy);
-    const float Z = static_cast<float>((c & 4) ? min(oz + kTZ, a.mz) - 1 : oz);
-    float mn[3], mxv[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float p = __fmaf_rn(P.A[4 * k], X, __fmaf_rn(P.A[4 * k + 1], Y,
-                                                         __fmaf_rn(P.A[4 * k + 2], Z, P.A[4 * k + 3])));
-      mn[k] = p;
-      mxv[k] = p;
-    }
-#pragma unroll
-    for (int off = 1; off < 8; off <<= 1)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
-        mxv[k] = fmaxf(mxv[k], __shfl_xor_sync(0xffffffffu, mxv[k], off));
-      }
-    if (threadIdx.x == 0) {
-      const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
-                          static_cast<float>(a.nz)};
-      int lo[3], hi[3];
-      bool inside = true;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        lo[k] = static_cast<int>(floorf(fminf(fmaxf(mn[k], -1.0f), n[k])));
-        hi[k] = static_cast<int>(floorf(fminf(fmaxf(mxv[k], -1.0f), n[k]))) + 1;
-        inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
-      }
-      const int x0 = lo[0] >= 0 ? (lo[0] & ~3) : -4;
-      const int W = (hi[0] + 1 - x0 + 3) & ~3;
-      const int H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
-      s_box[0] = x0; s_box[1] = lo[1]; s_box[2] = lo[2];
-      s_box[3] = W; s_box[4] = H; s_box[5] = D;
-      s_box[6] = (static_cast<int64_t>(W) * H * D <= cap_vox && W <= 4 * kThreads) ? 1 : 0;
-      s_box[7] = inside ? 0 : 1;  // clamp needed
-    }
-  }
+  if (threadIdx.x < 32) tile_box<S>(a, P, ox, oy, oz, cap_vox, s_box);
   __syncthreads();
-  if (!s_box[6]) {
-    tile_compute<false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+  int box[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) box[i] = s_box[i];
+  count_tile(box[6] != 0);
+  if (!box[6]) {
+    tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
     return;
   }
-  const int bx = s_box[0], by = s_box[1], bz = s_box[2];
-  const int W = s_box[3], H = s_box[4], D = s_box[5];
-  const bool need_clamp = s_box[7] != 0;
+  stage_box<S, kLabels>(a, vin, lin, box, 0u, static_cast<uint32_t>(cap_vox) * 4u);
+  cp_async_wait_all();
+  __syncthreads();
+  compute_staged<S, kLabels, kNearest>(a, P, vin, lin, vout, lout, box, 0, cap_vox * 4, ox, oy,
+                                       oz);
+}
+
+// ----------------------------------------------------------------------------
+// Kernel B (persistent): one 1024-thread CTA per SM walks the tiles t =
+// blockIdx.x + k * gridDim.x (volume-major order, so concurrently processed
+// tiles share the L2-resident part of one volume).  Two shared-memory buffers:
+// while tile k computes from buffer k & 1, the cp.async staging of tile k+1
+// fills buffer (k+1) & 1.  Box metadata uses 3 slots (k % 3) so warp 0 can
+// publish tile k+1's box while slow warps still read tile k-1's.
+// ----------------------------------------------------------------------------
+template <class S, bool kLabels, bool kNearest>
+__global__ void __launch_bounds__(S::THREADS, 1024 / S::THREADS)
+    warp3d_persistent_kernel(const __grid_constant__ WarpArgs a, const int tiles_x,
+                             const int tiles_y, const int tiles_z, const int total,
+                             const int cap_vox) {
+  __shared__ int s_box[3][8];
+  const int per_vol = tiles_x * tiles_y * tiles_z;
+  const uint32_t buf_bytes = static_cast<uint32_t>(cap_vox) * 5u;
+  int t = static_cast<int>(blockIdx.x);
+  if (t >= total) return;
+  auto coords = [&](int tt, int& vi, int& ox, int& oy, int& oz) {
+    vi = tt / per_vol;
+    int r = tt - vi * per_vol;
+    const int tzi = r / (tiles_x * tiles_y);
+    r -= tzi * tiles_x * tiles_y;
+    const int tyi = r / tiles_x;
+    ox = (r - tyi * tiles_x) * S::TX;
+    oy = tyi * S::TY;
+    oz = tzi * S::TZ;
+  };
+  // prologue: box + staging of the first tile into buffer 0
   {
-    // Stage the box as 16 B chunks (4 voxels): in-volume chunks by cp.async
-    // (image 16 B + label 4 B), out-of-volume chunks set to fill.  nx % 4 == 0
-    // and x0 % 4 == 0, so a chunk is entirely inside or outside in x.  Thread
-    // t owns chunk column c = t % CW of rows r = t / CW + k * (256 / CW)
-    // (W <= 1024 so CW <= 256); rows advance in (y, z) without division.
-    const uint32_t simg_s = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
-    const uint32_t lbl_delta = static_cast<uint32_t>(cap_vox) * 4u;
-    const int CW = W >> 2;
-    const int rows_per_pass = kThreads / CW;
-    const int tid = static_cast<int>(threadIdx.x);
-    const int c = tid % CW;
-    int r = tid / CW;
-    const int rows = H * D;
-    if (r < rows_per_pass) {
-      const int nx = a.nx, ny = a.ny, nz = a.nz;
-      int rz = r / H, ry = r - rz * H;
-      int gy = by + ry, gz = bz + rz;
-      const int gx = bx + 4 * c;
-      const bool x_in = static_cast<unsigned>(gx) < static_cast<unsigned>(nx);
-      // column base pointers (64-bit once); per row a 32-bit element offset
-      const float* gcol = vin + gx;
-      const uint8_t* lcol = kLabels ? lin + gx : nullptr;
-      int goff = gz * (nx * ny) + gy * nx;
-      const int step_y = rows_per_pass % H, step_z = rows_per_pass / H;
-      const int goff_step = step_z * (nx * ny) + step_y * nx;
-      const int goff_wrap = nx * ny - H * nx;
-      uint32_t sa = simg_s + 4u * static_cast<uint32_t>(r * W + 4 * c);
-      const uint32_t sa_step = 4u * static_cast<uint32_t>(rows_per_pass * W);
-      const float f = a.fill;
-      const uint32_t lf4 = a.label_fill * 0x01010101u;
-      for (; r < rows; r += rows_per_pass) {
-        const bool in = x_in & (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
-                        (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
-        if (in) {
-          cp_async16(sa, gcol + goff);
-          if (kLabels) cp_async4((sa - simg_s) / 4u + simg_s + lbl_delta, lcol + goff);
-        } else {
-          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};\n" ::"r"(sa), "f"(f) : "memory");
-          if (kLabels)
-            asm volatile("st.shared.u32 [%0], %1;\n" ::"r"((sa - simg_s) / 4u + simg_s + lbl_delta),
-                         "r"(lf4) : "memory");
-        }
-        sa += sa_step;
-        ry += step_y;
-        gy += step_y;
-        gz += step_z;
-        goff += goff_step;
-        if (ry >= H) {
-          ry -= H;
-          gy -= H;
-          ++gz;
-          goff += goff_wrap;
-        }
-      }
-    }
-    cp_async_wait_all();
+    int vi, ox, oy, oz;
+    coords(t, vi, ox, oy, oz);
+    if (threadIdx.x < 32) tile_box<S>(a, load_params(a.vol[vi]), ox, oy, oz, cap_vox, s_box[0]);
+    __syncthreads();
+    if (s_box[0][6])
+      stage_box<S, kLabels>(a, a.in + vi * a.in_stride,
+                            kLabels ? a.in_lbl + vi * a.in_stride : nullptr, s_box[0], 0u,
+                            static_cast<uint32_t>(cap_vox) * 4u);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
-  __syncthreads();
-  sv.W = W;
-  sv.HW = W * H;
-  sv.lbl_off = cap_vox * 4;
-  sv.bx = static_cast<float>(bx);
-  sv.by = static_cast<float>(by);
-  sv.bz = static_cast<float>(bz);
-  sv.Wf = static_cast<float>(W);
-  sv.HWf = static_cast<float>(W * H);
-  sv.nx = static_cast<float>(a.nx);
-  sv.ny = static_cast<float>(a.ny);
-  sv.nz = static_cast<float>(a.nz);
-  if (need_clamp)
-    tile_compute<true, kLabels, kNearest, true>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
-  else
-    tile_compute<true, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+  for (int k = 0;; ++k) {
+    const int tn = t + static_cast<int>(gridDim.x);
+    const int slot = k % 3, nslot = (k + 1) % 3;
+    const uint32_t buf = (k & 1) ? buf_bytes : 0u, nbuf = (k & 1) ? 0u : buf_bytes;
+    int nvi = 0, nox = 0, noy = 0, noz = 0;
+    if (tn < total) {
+      coords(tn, nvi, nox, noy, noz);
+      if (threadIdx.x < 32) tile_box<S>(a, load_params(a.vol[nvi]), nox, noy, noz, cap_vox,
+                                        s_box[nslot]);
+    }
+    __syncthreads();  // (1) next box visible; every warp is done with tile k-1's buffer
+    if (tn < total && s_box[nslot][6])
+      stage_box<S, kLabels>(a, a.in + nvi * a.in_stride,
+                            kLabels ? a.in_lbl + nvi * a.in_stride : nullptr, s_box[nslot],
+                            nbuf, nbuf + static_cast<uint32_t>(cap_vox) * 4u);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // tile k's group is complete
+    __syncthreads();  // (2) tile k's staged box visible to all
+    int box[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) box[i] = s_box[slot][i];
+    int vi, ox, oy, oz;
+    coords(t, vi, ox, oy, oz);
+    const Params P = load_params(a.vol[vi]);
+    const float* vin = a.in + vi * a.in_stride;
+    const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+    float* vout = a.out + vi * a.out_stride;
+    uint8_t* lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
+    count_tile(box[6] != 0);
+    if (box[6]) {
+      compute_staged<S, kLabels, kNearest>(a, P, vin, lin, vout, lout, box,
+                                           static_cast<int>(buf),
+                                           static_cast<int>(buf) + cap_vox * 4, ox, oy, oz);
+    } else {
+      Stage sv;
+      tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy,
+                                                        oz);
+    }
+    if (tn >= total) break;
+    t = tn;
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 static int g_cap_vox = kDefaultCapVox;
+static int g_pers_cap_vox = kPersCapVox;
 
 int stage_capacity() { return g_cap_vox; }
 void set_stage_capacity(int cap) { g_cap_vox = cap; }
@@ -460,6 +598,54 @@ static cudaError_t launch_variant(const WarpArgs& a, dim3 grid, int tiles_z, cud
     warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, 0, s>>>(a, tiles_z, 0);
   }
   return cudaGetLastError();
+}
+
+static int g_num_sms = 0;
+
+template <class S, bool kLabels, bool kNearest>
+static cudaError_t launch_persistent_variant(const WarpArgs& a, int cap, cudaStream_t s) {
+  const int tiles_x = (a.mx + S::TX - 1) / S::TX, tiles_y = (a.my + S::TY - 1) / S::TY;
+  const int tiles_z = (a.mz + S::TZ - 1) / S::TZ;
+  const int64_t total = static_cast<int64_t>(tiles_x) * tiles_y * tiles_z * a.nvol;
+  if (total >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
+  const size_t smem = static_cast<size_t>(cap) * 10;  // two buffers of cap * (4 + 1) B
+  static size_t configured = 0;
+  if (configured != smem) {
+    const cudaError_t e = cudaFuncSetAttribute(warp3d_persistent_kernel<S, kLabels, kNearest>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  const int64_t ctas = static_cast<int64_t>(g_num_sms) * (1024 / S::THREADS);
+  const int grid = static_cast<int>(total < ctas ? total : ctas);
+  warp3d_persistent_kernel<S, kLabels, kNearest><<<grid, S::THREADS, smem, s>>>(
+      a, tiles_x, tiles_y, tiles_z, static_cast<int>(total), cap);
+  return cudaGetLastError();
+}
+
+// Tuning knob for experiments (not part of the ABI): W3D_PERSISTENT_SHAPE=512
+// selects the 512-thread 32x16x8 persistent variant (2 CTAs / SM).
+static int pers_shape() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("W3D_PERSISTENT_SHAPE");
+    v = (e && atoi(e) == 512) ? 512 : 1024;
+  }
+  return v;
+}
+
+template <bool kLabels, bool kNearest>
+static cudaError_t launch_persistent_variant(const WarpArgs& a, cudaStream_t s) {
+  if (pers_shape() == 512)
+    return launch_persistent_variant<PersShapeS, kLabels, kNearest>(a, g_pers_cap_vox / 2, s);
+  return launch_persistent_variant<PersShape, kLabels, kNearest>(a, g_pers_cap_vox, s);
 }
 
 static cudaError_t launch_tiles(const WarpArgs& a, bool staged, cudaStream_t s) {
@@ -491,6 +677,26 @@ static cudaError_t launch_tiles(const WarpArgs& a, bool staged, cudaStream_t s) 
   return e;
 }
 
+static cudaError_t launch_persistent(const WarpArgs& a, cudaStream_t s) {
+  const bool labels = a.in_lbl != nullptr;
+  const bool nearest = a.interp == W3D_INTERP_NEAREST;
+  cudaError_t e;
+  if (labels)
+    e = nearest ? launch_persistent_variant<true, true>(a, s)
+                : launch_persistent_variant<true, false>(a, s);
+  else
+    e = nearest ? launch_persistent_variant<false, true>(a, s)
+                : launch_persistent_variant<false, false>(a, s);
+  note_launch();
+  return e;
+}
+
+cudaError_t read_tile_stats(unsigned long long out[2]) {
+  cudaError_t e = cudaMemcpyFromSymbol(&out[0], g_tiles_staged, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&out[1], g_tiles_gather, sizeof(unsigned long long));
+  return e;
+}
+
 bool staged_supported(const WarpArgs& a) {
   return (a.nx % 4 == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) &&
          (a.in_stride % 4 == 0) &&
@@ -501,6 +707,10 @@ cudaError_t launch_gather(const WarpArgs& a, cudaStream_t s) { return launch_til
 
 cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s) {
   return launch_tiles(a, staged_supported(a), s);
+}
+
+cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s) {
+  return staged_supported(a) ? launch_persistent(a, s) : launch_tiles(a, false, s);
 }
 
 // ----------------------------------------------------------------------------
