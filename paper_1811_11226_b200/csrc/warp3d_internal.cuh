@@ -43,12 +43,6 @@ static_assert(sizeof(VolDev) == 208, "VolDev layout");
 
 constexpr int kMaxVolPerLaunch = 128;
 
-// Output tile of one CTA: lane = x, warp = z.
-constexpr int kTX = 32, kTY = 16, kTZ = 8, kThreads = 256;
-static_assert(kTX == 32 && kTZ * 32 == kThreads && kTY % 4 == 0, "tile shape");
-// Shared-memory capacity of the staged footprint box, in voxels (5 B each).
-constexpr int kDefaultCapVox = 16384;
-constexpr int kMinBlocksPerSM = 2;
 // Persistent kernel: two buffers of kPersCapVox voxels (5 B each) per SM.
 constexpr int kPersCapVox = 22528;
 
@@ -76,8 +70,6 @@ cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32
                          uint32_t k1, uint32_t v0, uint32_t v1, cudaStream_t s);
 bool staged_supported(const WarpArgs& a);
 cudaError_t read_tile_stats(unsigned long long out[2]);
-int stage_capacity();
-void set_stage_capacity(int cap_vox);
 cudaError_t launch_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                           int64_t n, cudaStream_t s);
 cudaError_t launch_footprint(const WarpArgs& a, uint8_t* marks, cudaStream_t s);

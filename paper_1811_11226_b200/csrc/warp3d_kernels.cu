@@ -229,7 +229,18 @@ struct Shape {
   static constexpr int RPT = TY * TZ / WARPS;  // rows per thread
   static_assert(TX == 32 && WARPS % TZ == 0 && RPT % 4 == 0 && TY % RPT == 0, "shape");
 };
-using TileShape = Shape<kTX, kTY, kTZ, kThreads>;   // one tile per CTA
+// One-tile-per-CTA configurations: shape, CTAs per SM (register bound) and the
+// staging capacity in voxels (shared memory: CTAS * (CAP * 5 B + 1 KB) <= 228 KB).
+template <class S_, int MINB_, int CAP_>
+struct TileCfg {
+  using S = S_;
+  static constexpr int MINB = MINB_, CAP = CAP_;
+};
+using CfgA = TileCfg<Shape<32, 16, 8, 256>, 2, 16384>;  // 16 rows / thread
+using CfgB = TileCfg<Shape<32, 8, 8, 256>, 4, 11008>;   //  8 rows / thread, 32 warps / SM
+using CfgC = TileCfg<Shape<32, 16, 8, 256>, 3, 14592>;  // 16 rows / thread, 24 warps / SM
+using CfgD = TileCfg<Shape<32, 8, 16, 512>, 2, 16384>;  //  8 rows / thread, 32 warps / SM
+using CfgE = TileCfg<Shape<32, 16, 8, 512>, 2, 16384>;  //  8 rows / thread, 32 warps / SM
 using PersShape = Shape<32, 16, 16, 1024>;           // persistent, double-buffered
 using PersShapeS = Shape<32, 16, 8, 512>;            // persistent, 2 CTAs / SM
 
@@ -453,10 +464,10 @@ __device__ __forceinline__ void compute_staged(const WarpArgs& a, const Params& 
 // kStage: stage the tile's footprint box; tiles whose box exceeds cap_vox (or
 // kStage = false: the W3D_KERNEL_GATHER variant) gather through L1/L2.
 // ----------------------------------------------------------------------------
-template <bool kStage, bool kLabels, bool kNearest>
-__global__ void __launch_bounds__(kThreads, kMinBlocksPerSM)
+template <class Cfg, bool kStage, bool kLabels, bool kNearest>
+__global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
     warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap_vox) {
-  using S = TileShape;
+  using S = typename Cfg::S;
   __shared__ int s_box[8];
   const int vi = static_cast<int>(blockIdx.z) / tiles_z;
   const Params P = load_params(a.vol[vi]);
@@ -574,30 +585,62 @@ __global__ void __launch_bounds__(S::THREADS, 1024 / S::THREADS)
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-static int g_cap_vox = kDefaultCapVox;
 static int g_pers_cap_vox = kPersCapVox;
 
-int stage_capacity() { return g_cap_vox; }
-void set_stage_capacity(int cap) { g_cap_vox = cap; }
-
-template <bool kStage, bool kLabels, bool kNearest>
-static cudaError_t launch_variant(const WarpArgs& a, dim3 grid, int tiles_z, cudaStream_t s) {
+template <class Cfg, bool kStage, bool kLabels, bool kNearest>
+static cudaError_t launch_variant(const WarpArgs& a, cudaStream_t s) {
+  using S = typename Cfg::S;
+  const int tiles_x = (a.mx + S::TX - 1) / S::TX, tiles_y = (a.my + S::TY - 1) / S::TY;
+  const int tiles_z = (a.mz + S::TZ - 1) / S::TZ;
+  const int64_t gz = static_cast<int64_t>(tiles_z) * a.nvol;
+  if (tiles_y > 65535 || gz > 65535) return cudaErrorInvalidConfiguration;
+  const dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
+                  static_cast<unsigned>(gz));
   if (kStage) {
-    const int cap = g_cap_vox;
+    const int cap = Cfg::CAP;
     const size_t smem = static_cast<size_t>(cap) * 5;
-    static size_t configured = 0;
-    if (configured != smem) {
-      const cudaError_t e = cudaFuncSetAttribute(warp3d_tile_kernel<kStage, kLabels, kNearest>,
+    static bool configured = false;
+    if (!configured) {
+      const cudaError_t e = cudaFuncSetAttribute(warp3d_tile_kernel<Cfg, kStage, kLabels, kNearest>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(smem));
       if (e != cudaSuccess) return e;
-      configured = smem;
+      configured = true;
     }
-    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, smem, s>>>(a, tiles_z, cap);
+    warp3d_tile_kernel<Cfg, kStage, kLabels, kNearest><<<grid, S::THREADS, smem, s>>>(a, tiles_z,
+                                                                                    cap);
   } else {
-    warp3d_tile_kernel<kStage, kLabels, kNearest><<<grid, kThreads, 0, s>>>(a, tiles_z, 0);
+    warp3d_tile_kernel<Cfg, kStage, kLabels, kNearest><<<grid, S::THREADS, 0, s>>>(a, tiles_z, 0);
   }
   return cudaGetLastError();
+}
+
+template <class Cfg>
+static cudaError_t launch_cfg(const WarpArgs& a, bool staged, cudaStream_t s) {
+  const bool labels = a.in_lbl != nullptr;
+  const bool nearest = a.interp == W3D_INTERP_NEAREST;
+  if (staged) {
+    if (labels)
+      return nearest ? launch_variant<Cfg, true, true, true>(a, s)
+                     : launch_variant<Cfg, true, true, false>(a, s);
+    return nearest ? launch_variant<Cfg, true, false, true>(a, s)
+                   : launch_variant<Cfg, true, false, false>(a, s);
+  }
+  if (labels)
+    return nearest ? launch_variant<Cfg, false, true, true>(a, s)
+                   : launch_variant<Cfg, false, true, false>(a, s);
+  return nearest ? launch_variant<Cfg, false, false, true>(a, s)
+                 : launch_variant<Cfg, false, false, false>(a, s);
+}
+
+// Tuning knob for experiments (not part of the ABI): W3D_TILE_CFG = A..E.
+static char tile_cfg() {
+  static char v = 0;
+  if (!v) {
+    const char* e = getenv("W3D_TILE_CFG");
+    v = (e && e[0] >= 'A' && e[0] <= 'E') ? e[0] : 'A';
+  }
+  return v;
 }
 
 static int g_num_sms = 0;
@@ -649,29 +692,13 @@ static cudaError_t launch_persistent_variant(const WarpArgs& a, cudaStream_t s) 
 }
 
 static cudaError_t launch_tiles(const WarpArgs& a, bool staged, cudaStream_t s) {
-  const int tiles_x = (a.mx + kTX - 1) / kTX, tiles_y = (a.my + kTY - 1) / kTY;
-  const int tiles_z = (a.mz + kTZ - 1) / kTZ;
-  const int64_t gz = static_cast<int64_t>(tiles_z) * a.nvol;
-  if (tiles_y > 65535 || gz > 65535) return cudaErrorInvalidConfiguration;
-  const dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
-                  static_cast<unsigned>(gz));
-  const bool labels = a.in_lbl != nullptr;
-  const bool nearest = a.interp == W3D_INTERP_NEAREST;
   cudaError_t e;
-  if (staged) {
-    if (labels)
-      e = nearest ? launch_variant<true, true, true>(a, grid, tiles_z, s)
-                  : launch_variant<true, true, false>(a, grid, tiles_z, s);
-    else
-      e = nearest ? launch_variant<true, false, true>(a, grid, tiles_z, s)
-                  : launch_variant<true, false, false>(a, grid, tiles_z, s);
-  } else {
-    if (labels)
-      e = nearest ? launch_variant<false, true, true>(a, grid, tiles_z, s)
-                  : launch_variant<false, true, false>(a, grid, tiles_z, s);
-    else
-      e = nearest ? launch_variant<false, false, true>(a, grid, tiles_z, s)
-                  : launch_variant<false, false, false>(a, grid, tiles_z, s);
+  switch (tile_cfg()) {
+    case 'B': e = launch_cfg<CfgB>(a, staged, s); break;
+    case 'C': e = launch_cfg<CfgC>(a, staged, s); break;
+    case 'D': e = launch_cfg<CfgD>(a, staged, s); break;
+    case 'E': e = launch_cfg<CfgE>(a, staged, s); break;
+    default: e = launch_cfg<CfgA>(a, staged, s); break;
   }
   note_launch();
   return e;
@@ -709,8 +736,13 @@ cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s) {
   return launch_tiles(a, staged_supported(a), s);
 }
 
+// AUTO: the one-tile-per-CTA staged kernel; W3D_PERSISTENT=1 selects the
+// persistent double-buffered kernel (experiment knob).
 cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s) {
-  return staged_supported(a) ? launch_persistent(a, s) : launch_tiles(a, false, s);
+  if (!staged_supported(a)) return launch_tiles(a, false, s);
+  const char* e = getenv("W3D_PERSISTENT");
+  if (e && e[0] == '1') return launch_persistent(a, s);
+  return launch_tiles(a, true, s);
 }
 
 // ----------------------------------------------------------------------------
