@@ -250,6 +250,106 @@ using PersShapeS = Shape<32, 16, 8, 512>;            // persistent, 2 CTAs / SM
 // as independent chains, then y-pairs with FFMA2/FADD2.  The coordinate keeps
 // the R4 nesting p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
 // ----------------------------------------------------------------------------
+// 64-bit address base + 32-bit element offset in one IMAD.WIDE.U32
+__device__ __forceinline__ float* addr_f32(float* base, uint32_t off) {
+  float* p;
+  asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(p) : "r"(off), "l"(base));
+  return p;
+}
+__device__ __forceinline__ uint8_t* addr_u8(uint8_t* base, uint32_t off) {
+  uint8_t* p;
+  asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(p) : "r"(off), "l"(base));
+  return p;
+}
+
+// Rows ybeg .. ybeg+npairs*2 of one output column, as y-pairs.  kFull: every
+// pair has both rows (no per-pair bounds).
+template <class S, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp, bool kFull>
+__device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
+                                             const float* __restrict__ vin,
+                                             const uint8_t* __restrict__ lin,
+                                             float* __restrict__ vout,
+                                             uint8_t* __restrict__ lout, const Stage& sv,
+                                             int X, int Z, int ybeg, int yend, const float* n) {
+  const int mx = a.mx;
+  const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
+  const float2 cz0 = f2(__fmaf_rn(P.A[2], fZ, P.A[3]));
+  const float2 cz1 = f2(__fmaf_rn(P.A[6], fZ, P.A[7]));
+  const float2 cz2 = f2(__fmaf_rn(P.A[10], fZ, P.A[11]));
+  // output offsets are 32-bit within a volume (< 2^31 voxels)
+  const uint32_t o0 = static_cast<uint32_t>((Z * a.my + ybeg) * mx + X);
+#pragma unroll
+  for (int j = 0; j < S::RPT / 2; ++j) {
+    const int Ya = ybeg + 2 * j;
+    bool second = true;
+    if (!kFull) {
+      if (Ya >= yend) break;
+      second = Ya + 1 < yend;
+    }
+    const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
+    const float2 px = __ffma2_rn(f2(P.A[0]), f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
+    const float2 py = __ffma2_rn(f2(P.A[4]), f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
+    const float2 pz = __ffma2_rn(f2(P.A[8]), f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
+    float2 img = make_float2(0.0f, 0.0f);
+    uint32_t l0 = 0, l1 = 0;
+    if (kStagedPath) {
+      sample_staged2<kLabels, kNearest, kClamp>(sv, px, py, pz, true, img, l0, l1);
+    } else {
+      const Sample s0 = sample_gather(a, vin, lin, px.x, py.x, pz.x, true);
+      const Sample s1 = sample_gather(a, vin, lin, px.y, py.y, pz.y, true);
+      img = make_float2(s0.img, s1.img);
+      l0 = s0.lbl;
+      l1 = s1.lbl;
+    }
+    const float2 out = photometric2(img, make_float2(n[2 * j], n[2 * j + 1]), P);
+    const uint32_t o = o0 + static_cast<uint32_t>(2 * j * mx);
+    *addr_f32(vout, o) = out.x;
+    if (kLabels) *addr_u8(lout, o) = static_cast<uint8_t>(l0);
+    if (second) {
+      *addr_f32(vout, o + mx) = out.y;
+      if (kLabels) *addr_u8(lout, o + mx) = static_cast<uint8_t>(l1);
+    }
+  }
+}
+
+// Occluded output z (R15): image 0, every later step skipped;
+// labels are still warped.
+template <class S, bool kStagedPath, bool kLabels, bool kClamp>
+__device__ __forceinline__ void column_occluded(const WarpArgs& a, const Params& P,
+                                             const uint8_t* __restrict__ lin, float* vout,
+                                             uint8_t* lout, const Stage& sv, int X, int Z,
+                                             int ybeg, int yend) {
+  const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
+  const float cz0 = __fmaf_rn(P.A[2], fZ, P.A[3]), cz1 = __fmaf_rn(P.A[6], fZ, P.A[7]);
+  const float cz2 = __fmaf_rn(P.A[10], fZ, P.A[11]);
+  for (int Y = ybeg; Y < yend; ++Y) {
+    const float fY = static_cast<float>(Y);
+    const float px = __fmaf_rn(P.A[0], fX, __fmaf_rn(P.A[1], fY, cz0));
+    const float py = __fmaf_rn(P.A[4], fX, __fmaf_rn(P.A[5], fY, cz1));
+    const float pz = __fmaf_rn(P.A[8], fX, __fmaf_rn(P.A[9], fY, cz2));
+    uint32_t l = 0;
+    if (kLabels) {
+      if (kStagedPath) {
+        float2 img;
+        uint32_t l1;
+        sample_staged2<true, false, kClamp>(sv, make_float2(px, px), make_float2(py, py),
+                                           make_float2(pz, pz), false, img, l, l1);
+      } else {
+        l = sample_gather(a, nullptr, lin, px, py, pz, false).lbl;
+      }
+    }
+    const uint32_t o = static_cast<uint32_t>((Z * a.my + Y) * a.mx + X);
+    *addr_f32(vout, o) = 0.0f;
+    if (kLabels) *addr_u8(lout, o) = static_cast<uint8_t>(l);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Output tile loop.  A thread owns output column x at one z and RPT rows, i.e.
+// RPT/4 Philox blocks (R10: block = (x, y/4, z), lane = y mod 4) computed first
+// as independent chains, then y-pairs with FFMA2/FADD2.  The coordinate keeps
+// the R4 nesting p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
+// ----------------------------------------------------------------------------
 template <class S, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp>
 __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
                                              const float* __restrict__ vin,
@@ -265,11 +365,14 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
   const int mx = a.mx, my = a.my;
   if (X >= mx || Z >= a.mz || ybeg >= my) return;
   const int yend = min(ybeg + RPT, my);
-  const bool occluded = (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;  // warp-uniform
+  if ((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi) {  // warp-uniform
+    column_occluded<S, kStagedPath, kLabels, kClamp>(a, P, lin, vout, lout, sv, X, Z, ybeg, yend);
+    return;
+  }
   float n[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) n[i] = 0.0f;
-  if ((P.flags & kNoise) && !occluded) {
+  if (P.flags & kNoise) {
     const int Gy = (my + 3) >> 2;
     const uint32_t q0 = static_cast<uint32_t>(X) +
                         static_cast<uint32_t>(mx) * static_cast<uint32_t>(Gy * Z + (ybeg >> 2));
@@ -284,42 +387,12 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
       n[4 * g] = u.x; n[4 * g + 1] = u.y; n[4 * g + 2] = v.x; n[4 * g + 3] = v.y;
     }
   }
-  const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
-  const float2 cz0 = f2(__fmaf_rn(P.A[2], fZ, P.A[3]));
-  const float2 cz1 = f2(__fmaf_rn(P.A[6], fZ, P.A[7]));
-  const float2 cz2 = f2(__fmaf_rn(P.A[10], fZ, P.A[11]));
-  // output offsets are 32-bit within a volume (< 2^31 voxels)
-  const uint32_t o0 = static_cast<uint32_t>((Z * my + ybeg) * mx + X);
-#pragma unroll
-  for (int j = 0; j < RPT / 2; ++j) {
-    const int Ya = ybeg + 2 * j;
-    if (Ya >= yend) break;
-    const bool second = Ya + 1 < yend;   // the pair's second row exists
-    const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
-    const float2 px = __ffma2_rn(f2(P.A[0]), f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
-    const float2 py = __ffma2_rn(f2(P.A[4]), f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
-    const float2 pz = __ffma2_rn(f2(P.A[8]), f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
-    float2 img = make_float2(0.0f, 0.0f);
-    uint32_t l0 = 0, l1 = 0;
-    if (kStagedPath) {
-      sample_staged2<kLabels, kNearest, kClamp>(sv, px, py, pz, !occluded, img, l0, l1);
-    } else {
-      const Sample s0 = sample_gather(a, vin, lin, px.x, py.x, pz.x, !occluded);
-      const Sample s1 = sample_gather(a, vin, lin, px.y, py.y, pz.y, !occluded);
-      img = make_float2(s0.img, s1.img);
-      l0 = s0.lbl;
-      l1 = s1.lbl;
-    }
-    const float2 out = occluded ? make_float2(0.0f, 0.0f)
-                                : photometric2(img, make_float2(n[2 * j], n[2 * j + 1]), P);
-    const uint32_t o = o0 + static_cast<uint32_t>(2 * j * mx);
-    vout[o] = out.x;
-    if (kLabels) lout[o] = static_cast<uint8_t>(l0);
-    if (second) {
-      vout[o + mx] = out.y;
-      if (kLabels) lout[o + mx] = static_cast<uint8_t>(l1);
-    }
-  }
+  if (yend - ybeg == RPT)
+    column_pairs<S, kStagedPath, kLabels, kNearest, kClamp, true>(a, P, vin, lin, vout, lout, sv,
+                                                                  X, Z, ybeg, yend, n);
+  else
+    column_pairs<S, kStagedPath, kLabels, kNearest, kClamp, false>(a, P, vin, lin, vout, lout,
+                                                                   sv, X, Z, ybeg, yend, n);
 }
 
 // Box of one tile (warp 0): the bounding box of the 8 transformed tile corners
