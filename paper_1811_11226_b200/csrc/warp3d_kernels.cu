@@ -711,7 +711,7 @@ static char tile_cfg() {
   static char v = 0;
   if (!v) {
     const char* e = getenv("W3D_TILE_CFG");
-    v = (e && e[0] >= 'A' && e[0] <= 'E') ? e[0] : 'A';
+    v = (e && e[0] >= 'A' && e[0] <= 'E') ? e[0] : 'C';
   }
   return v;
 }
@@ -771,7 +771,8 @@ static cudaError_t launch_tiles(const WarpArgs& a, bool staged, cudaStream_t s) 
     case 'C': e = launch_cfg<CfgC>(a, staged, s); break;
     case 'D': e = launch_cfg<CfgD>(a, staged, s); break;
     case 'E': e = launch_cfg<CfgE>(a, staged, s); break;
-    default: e = launch_cfg<CfgA>(a, staged, s); break;
+    case 'A': e = launch_cfg<CfgA>(a, staged, s); break;
+    default: e = launch_cfg<CfgC>(a, staged, s); break;
   }
   note_launch();
   return e;
