@@ -82,6 +82,15 @@ def shard(workload, world, rank):
     return list(range(lo, hi)), total
 
 
+def reduce_max_ms(ms, dist, device):
+    """Max over ranks of a per-rank elapsed time (the contract's multi-GPU clock)."""
+    import torch
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def ranges_of(workload):
     return synth.TRAIN if WORKLOADS[workload]["ranges"] == "train" else synth.LARGE
 
@@ -340,10 +349,7 @@ def main():
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = reduce_max_ms(total_ms, dist if world > 1 else None, dev)
     value = global_batch * nvox_out * args.steps / (max_ms * 1e-3) / 1e9
 
     # e2e: pinned host buffers -> H2D -> warp -> D2H, inside the timed region
@@ -422,11 +428,8 @@ def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch
         step()
     e.record()
     torch.cuda.synchronize(dev)
-    ms = s.elapsed_time(e)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    value = global_batch * nvox_out * steps / (float(t.item()) * 1e-3) / 1e9
+    ms = reduce_max_ms(s.elapsed_time(e), dist if world > 1 else None, dev)
+    value = global_batch * nvox_out * steps / (ms * 1e-3) / 1e9
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(B * nvox_out * 5),
             "d2h_bytes_per_step": int(B * nvox_out * 5), "steps": steps,
             "path": "pinned host -> cudaMemcpyAsync -> warp3d_affine_batched -> pinned host, "
