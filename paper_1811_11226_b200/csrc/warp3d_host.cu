@@ -157,13 +157,83 @@ static VolDev derive(const float* A, const w3d_photometric* ph) {
   return P;
 }
 
+// ---------------------------------------------------------------------------
+// TMA tensor maps (one per width class) for the launch chunk's input volumes.
+// Encoded with the driver's cuTensorMapEncodeTiled (fetched through the
+// runtime), cached per (pointers, dims, volumes).
+// ---------------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+cudaError_t encode_tensor_maps(WarpArgs& a) {
+  EncodeFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dims[4] = {cuuint64_t(a.nx), cuuint64_t(a.ny), cuuint64_t(a.nz),
+                              cuuint64_t(a.nvol)};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  {
+    const cuuint64_t strides[3] = {cuuint64_t(a.nx) * 4, cuuint64_t(a.nx) * a.ny * 4,
+                                   cuuint64_t(a.in_stride) * 4};
+    for (int c = 0; c < kNumImgCls; ++c) {
+      const cuuint32_t box[4] = {cuuint32_t(img_cls_width(c)), cuuint32_t(kTmaRowsImg), 1, 1};
+      if (enc(&a.tm_img[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a.in), dims,
+              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+  }
+  if (a.in_lbl) {
+    const cuuint64_t strides[3] = {cuuint64_t(a.nx), cuuint64_t(a.nx) * a.ny,
+                                   cuuint64_t(a.in_stride)};
+    for (int c = 0; c < kNumLblCls; ++c) {
+      const cuuint32_t box[4] = {cuuint32_t(lbl_cls_width(c)), cuuint32_t(kTmaRowsLbl), 1, 1};
+      if (enc(&a.tm_lbl[c], CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(a.in_lbl), dims,
+              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
+  }
+  return cudaSuccess;
+}
+
+struct TmaKey {
+  const void* in = nullptr;
+  const void* lbl = nullptr;
+  int32_t nx = 0, ny = 0, nz = 0, nvol = 0;
+  bool valid = false;
+  bool operator==(const TmaKey& o) const {
+    return in == o.in && lbl == o.lbl && nx == o.nx && ny == o.ny && nz == o.nz &&
+           nvol == o.nvol && valid == o.valid;
+  }
+};
+
 // One batch, already validated; chunks of kMaxVolPerLaunch volumes.
 static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_labels,
                               w3d_dims in_dims, const float* const* affines,
                               const w3d_photometric* const* phs, w3d_interp interp, float fill,
                               uint8_t label_fill, float* out, uint8_t* out_labels,
                               w3d_dims out_dims, w3d_kernel variant, cudaStream_t stream) {
-  static thread_local WarpArgs args;  // ~14 KB: keep off the stack
+  static thread_local WarpArgs args;  // ~26 KB: keep off the stack
+  static thread_local TmaKey tma_key;  // tensor maps currently encoded in args
   const int64_t in_n = nvox(in_dims), out_n = nvox(out_dims);
   for (int32_t v0 = 0; v0 < batch; v0 += kMaxVolPerLaunch) {
     const int32_t nv = (batch - v0 < kMaxVolPerLaunch) ? batch - v0 : kMaxVolPerLaunch;
@@ -180,6 +250,24 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
     args.interp = interp;
     args.nvol = nv;
     for (int32_t i = 0; i < nv; ++i) args.vol[i] = derive(affines[v0 + i], phs[v0 + i]);
+    args.use_tma = 0;
+    if ((variant == W3D_KERNEL_AUTO || variant == W3D_KERNEL_TMA) && tma_supported(args)) {
+      TmaKey k;
+      k.in = args.in; k.lbl = args.in_lbl;
+      k.nx = args.nx; k.ny = args.ny; k.nz = args.nz; k.nvol = nv; k.valid = true;
+      if (k == tma_key) {
+        args.use_tma = 1;
+      } else if (encode_tensor_maps(args) == cudaSuccess) {
+        tma_key = k;
+        args.use_tma = 1;
+      } else {
+        tma_key = TmaKey();
+      }
+    }
+    if (variant == W3D_KERNEL_TMA && !args.use_tma)
+      return fail(W3D_ERR_UNSUPPORTED,
+                  "W3D_KERNEL_TMA needs nx %% 4 == 0 (labels: nx %% 16 == 0), 16 B aligned "
+                  "inputs and cuTensorMapEncodeTiled");
     const cudaError_t e = (variant == W3D_KERNEL_GATHER)   ? launch_gather(args, stream)
                           : (variant == W3D_KERNEL_STAGED) ? launch_staged(args, stream)
                                                            : launch_auto(args, stream);
@@ -251,7 +339,8 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
   if (!params) return fail(W3D_ERR_INVALID_ARG, "params must be a non-NULL host array");
   if ((in_labels == nullptr) != (out_labels == nullptr))
     return fail(W3D_ERR_INVALID_ARG, "out_labels must be NULL iff in_labels is NULL");
-  if (variant != W3D_KERNEL_AUTO && variant != W3D_KERNEL_GATHER && variant != W3D_KERNEL_STAGED)
+  if (variant != W3D_KERNEL_AUTO && variant != W3D_KERNEL_GATHER && variant != W3D_KERNEL_STAGED &&
+      variant != W3D_KERNEL_TMA)
     return fail(W3D_ERR_INVALID_ARG, "variant = %d is not a w3d_kernel", int(variant));
   for (int32_t i = 0; i < batch; ++i) {
     if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;

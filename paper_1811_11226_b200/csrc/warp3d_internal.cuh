@@ -1,6 +1,7 @@
 // warp3d_internal.cuh -- launch-argument structs shared by the host entry
 // points (warp3d_host.cu) and the kernels (warp3d_kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -41,12 +42,28 @@ struct alignas(16) VolDev {
 };
 static_assert(sizeof(VolDev) == 208, "VolDev layout");
 
-constexpr int kMaxVolPerLaunch = 128;
+constexpr int kMaxVolPerLaunch = 112;
+
+// TMA staging: the box is loaded with
+// cp.async.bulk.tensor boxes of kTmaRowsImg image rows x WI floats and
+// kTmaRowsLbl label rows x WL bytes; WI / WL come from these width classes
+// (one tensor map per class; WI*kTmaRowsImg*4 and WL*kTmaRowsLbl must be
+// multiples of 128 B so consecutive boxes stay 128 B aligned in smem).
+constexpr int kTmaRowsImg = 4, kTmaRowsLbl = 8;
+constexpr int kNumImgCls = 10, kNumLblCls = 7;
+__host__ __device__ constexpr int img_cls_width(int c) {
+  return c < 7 ? 16 + 8 * c : (c == 7 ? 80 : (c == 8 ? 96 : 128));
+}
+__host__ __device__ constexpr int lbl_cls_width(int c) { return c < 6 ? 16 * (c + 1) : 128; }
 
 // Persistent kernel: two buffers of kPersCapVox voxels (5 B each) per SM.
 constexpr int kPersCapVox = 22528;
 
-struct WarpArgs {
+struct alignas(64) WarpArgs {
+  CUtensorMap tm_img[kNumImgCls];  // 4D (nx, ny, nz, nvol) float32, box (w, 4, 1, 1)
+  CUtensorMap tm_lbl[kNumLblCls];  // 4D uint8, box (w, 8, 1, 1)
+  int32_t use_tma;                 // tensor maps valid
+  int32_t _pad_tma[15];
   const float* in;
   const uint8_t* in_lbl;  // may be null
   float* out;
@@ -66,6 +83,8 @@ struct WarpArgs {
 cudaError_t launch_gather(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s);
+bool tma_supported(const WarpArgs& a);
+cudaError_t encode_tensor_maps(WarpArgs& a);
 cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,
                          uint32_t k1, uint32_t v0, uint32_t v1, cudaStream_t s);
 bool staged_supported(const WarpArgs& a);

@@ -154,14 +154,15 @@ __device__ __forceinline__ Sample sample_gather(const WarpArgs& a, const float* 
 // (R6) and the label rule (R8) exactly.
 // ----------------------------------------------------------------------------
 struct Stage {
-  int W, HW;            // row / plane pitch (elements)
+  int W, HW;            // image row / plane pitch (elements)
+  int WL, HWL;          // label row / plane pitch (kSepLbl layouts; else = W, HW)
   int img_off, lbl_off; // byte offsets of this buffer's image / label regions in g_smem
   float bx, by, bz;     // box origin (input voxel coords of element 0)
-  float Wf, HWf;
+  float Wf, HWf, WLf, HWLf;
   float nx, ny, nz;     // clamp bounds
 };
 
-template <bool kLabels, bool kNearest, bool kClamp>
+template <bool kLabels, bool kNearest, bool kClamp, bool kSepLbl>
 __device__ __forceinline__ void sample_staged2(const Stage& v, float2 px, float2 py, float2 pz,
                                                bool want_img, float2& img, uint32_t& l0,
                                                uint32_t& l1) {
@@ -177,17 +178,26 @@ __device__ __forceinline__ void sample_staged2(const Stage& v, float2 px, float2
   const float2 fz = make_float2(floorf(pz.x), floorf(pz.y));
   const float2 tx = sub2(px, fx), ty = sub2(py, fy), tz = sub2(pz, fz);
   // local element index: all terms are small integers, exact in fp32
-  const float2 lf = __ffma2_rn(sub2(fz, f2(v.bz)), f2(v.HWf),
-                               __ffma2_rn(sub2(fy, f2(v.by)), f2(v.Wf), sub2(fx, f2(v.bx))));
+  const float2 rx = sub2(fx, f2(v.bx)), ry = sub2(fy, f2(v.by)), rz = sub2(fz, f2(v.bz));
+  const float2 lf = __ffma2_rn(rz, f2(v.HWf), __ffma2_rn(ry, f2(v.Wf), rx));
   const int li0 = __float2int_rz(lf.x), li1 = __float2int_rz(lf.y);
   int ln0 = 0, ln1 = 0;
-  if (kLabels || kNearest) {
+  if (kNearest || (kLabels && !kSepLbl)) {
     ln0 = li0 + (tx.x >= 0.5f ? 1 : 0) + (ty.x >= 0.5f ? v.W : 0) + (tz.x >= 0.5f ? v.HW : 0);
     ln1 = li1 + (tx.y >= 0.5f ? 1 : 0) + (ty.y >= 0.5f ? v.W : 0) + (tz.y >= 0.5f ? v.HW : 0);
   }
   if (kLabels) {
-    l0 = slbl[ln0];
-    l1 = slbl[ln1];
+    if (kSepLbl) {  // label box with its own pitches (TMA layout)
+      const float2 lfl = __ffma2_rn(rz, f2(v.HWLf), __ffma2_rn(ry, f2(v.WLf), rx));
+      const int m0 = __float2int_rz(lfl.x), m1 = __float2int_rz(lfl.y);
+      l0 = slbl[m0 + (tx.x >= 0.5f ? 1 : 0) + (ty.x >= 0.5f ? v.WL : 0) +
+                (tz.x >= 0.5f ? v.HWL : 0)];
+      l1 = slbl[m1 + (tx.y >= 0.5f ? 1 : 0) + (ty.y >= 0.5f ? v.WL : 0) +
+                (tz.y >= 0.5f ? v.HWL : 0)];
+    } else {
+      l0 = slbl[ln0];
+      l1 = slbl[ln1];
+    }
   }
   if (!want_img) return;
   if (kNearest) {
@@ -244,12 +254,6 @@ using CfgE = TileCfg<Shape<32, 16, 8, 512>, 2, 16384>;  //  8 rows / thread, 32 
 using PersShape = Shape<32, 16, 16, 1024>;           // persistent, double-buffered
 using PersShapeS = Shape<32, 16, 8, 512>;            // persistent, 2 CTAs / SM
 
-// ----------------------------------------------------------------------------
-// Output tile loop.  A thread owns output column x at one z and RPT rows, i.e.
-// RPT/4 Philox blocks (R10: block = (x, y/4, z), lane = y mod 4) computed first
-// as independent chains, then y-pairs with FFMA2/FADD2.  The coordinate keeps
-// the R4 nesting p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
-// ----------------------------------------------------------------------------
 // 64-bit address base + 32-bit element offset in one IMAD.WIDE.U32
 __device__ __forceinline__ float* addr_f32(float* base, uint32_t off) {
   float* p;
@@ -261,10 +265,17 @@ __device__ __forceinline__ uint8_t* addr_u8(uint8_t* base, uint32_t off) {
   asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(p) : "r"(off), "l"(base));
   return p;
 }
+__device__ __forceinline__ void st_f32(float* p, float v) {
+  asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_u8(uint8_t* p, uint32_t v) {
+  asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
-// Rows ybeg .. ybeg+npairs*2 of one output column, as y-pairs.  kFull: every
+// Rows ybeg .. of one output column, as y-pairs (NR / 2 of them).  kFull: every
 // pair has both rows (no per-pair bounds).
-template <class S, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp, bool kFull>
+template <int NR, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp, bool kSepLbl,
+          bool kFull>
 __device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
                                              const float* __restrict__ vin,
                                              const uint8_t* __restrict__ lin,
@@ -279,7 +290,7 @@ __device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
   // output offsets are 32-bit within a volume (< 2^31 voxels)
   const uint32_t o0 = static_cast<uint32_t>((Z * a.my + ybeg) * mx + X);
 #pragma unroll
-  for (int j = 0; j < S::RPT / 2; ++j) {
+  for (int j = 0; j < NR / 2; ++j) {
     const int Ya = ybeg + 2 * j;
     bool second = true;
     if (!kFull) {
@@ -293,7 +304,7 @@ __device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
     float2 img = make_float2(0.0f, 0.0f);
     uint32_t l0 = 0, l1 = 0;
     if (kStagedPath) {
-      sample_staged2<kLabels, kNearest, kClamp>(sv, px, py, pz, true, img, l0, l1);
+      sample_staged2<kLabels, kNearest, kClamp, kSepLbl>(sv, px, py, pz, true, img, l0, l1);
     } else {
       const Sample s0 = sample_gather(a, vin, lin, px.x, py.x, pz.x, true);
       const Sample s1 = sample_gather(a, vin, lin, px.y, py.y, pz.y, true);
@@ -303,22 +314,22 @@ __device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
     }
     const float2 out = photometric2(img, make_float2(n[2 * j], n[2 * j + 1]), P);
     const uint32_t o = o0 + static_cast<uint32_t>(2 * j * mx);
-    *addr_f32(vout, o) = out.x;
-    if (kLabels) *addr_u8(lout, o) = static_cast<uint8_t>(l0);
+    st_f32(addr_f32(vout, o), out.x);
+    if (kLabels) st_u8(addr_u8(lout, o), l0);
     if (second) {
-      *addr_f32(vout, o + mx) = out.y;
-      if (kLabels) *addr_u8(lout, o + mx) = static_cast<uint8_t>(l1);
+      st_f32(addr_f32(vout, o + mx), out.y);
+      if (kLabels) st_u8(addr_u8(lout, o + mx), l1);
     }
   }
 }
 
 // Occluded output z (R15): image 0, every later step skipped;
 // labels are still warped.
-template <class S, bool kStagedPath, bool kLabels, bool kClamp>
+template <bool kStagedPath, bool kLabels, bool kClamp, bool kSepLbl>
 __device__ __forceinline__ void column_occluded(const WarpArgs& a, const Params& P,
-                                             const uint8_t* __restrict__ lin, float* vout,
-                                             uint8_t* lout, const Stage& sv, int X, int Z,
-                                             int ybeg, int yend) {
+                                                const uint8_t* __restrict__ lin, float* vout,
+                                                uint8_t* lout, const Stage& sv, int X, int Z,
+                                                int ybeg, int yend) {
   const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
   const float cz0 = __fmaf_rn(P.A[2], fZ, P.A[3]), cz1 = __fmaf_rn(P.A[6], fZ, P.A[7]);
   const float cz2 = __fmaf_rn(P.A[10], fZ, P.A[11]);
@@ -332,24 +343,65 @@ __device__ __forceinline__ void column_occluded(const WarpArgs& a, const Params&
       if (kStagedPath) {
         float2 img;
         uint32_t l1;
-        sample_staged2<true, false, kClamp>(sv, make_float2(px, px), make_float2(py, py),
-                                           make_float2(pz, pz), false, img, l, l1);
+        sample_staged2<true, false, kClamp, kSepLbl>(sv, make_float2(px, px), make_float2(py, py),
+                                                    make_float2(pz, pz), false, img, l, l1);
       } else {
         l = sample_gather(a, nullptr, lin, px, py, pz, false).lbl;
       }
     }
     const uint32_t o = static_cast<uint32_t>((Z * a.my + Y) * a.mx + X);
-    *addr_f32(vout, o) = 0.0f;
-    if (kLabels) *addr_u8(lout, o) = static_cast<uint8_t>(l);
+    st_f32(addr_f32(vout, o), 0.0f);
+    if (kLabels) st_u8(addr_u8(lout, o), l);
   }
 }
 
 // ----------------------------------------------------------------------------
-// Output tile loop.  A thread owns output column x at one z and RPT rows, i.e.
-// RPT/4 Philox blocks (R10: block = (x, y/4, z), lane = y mod 4) computed first
-// as independent chains, then y-pairs with FFMA2/FADD2.  The coordinate keeps
-// the R4 nesting p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
+// Output column work.  A thread owns output column x at one z and NR rows
+// [ybeg, ybeg + NR), ybeg % 4 == 0, i.e. NR/4 Philox blocks (R10: block =
+// (x, y/4, z), lane = y mod 4) computed first as independent chains, then
+// y-pairs with FFMA2/FADD2.  The coordinate keeps the R4 nesting
+// p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
 // ----------------------------------------------------------------------------
+template <int NR, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp, bool kSepLbl>
+__device__ __forceinline__ void column_rows(const WarpArgs& a, const Params& P,
+                                            const float* __restrict__ vin,
+                                            const uint8_t* __restrict__ lin,
+                                            float* __restrict__ vout, uint8_t* __restrict__ lout,
+                                            const Stage& sv, int X, int Z, int ybeg) {
+  const int mx = a.mx, my = a.my;
+  if (X >= mx || Z >= a.mz || ybeg >= my) return;
+  const int yend = min(ybeg + NR, my);
+  if ((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi) {  // warp-uniform
+    column_occluded<kStagedPath, kLabels, kClamp, kSepLbl>(a, P, lin, vout, lout, sv, X, Z, ybeg,
+                                                           yend);
+    return;
+  }
+  float n[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) n[i] = 0.0f;
+  if (P.flags & kNoise) {
+    const int Gy = (my + 3) >> 2;
+    const uint32_t q0 = static_cast<uint32_t>(X) +
+                        static_cast<uint32_t>(mx) * static_cast<uint32_t>(Gy * Z + (ybeg >> 2));
+    uint4 r[NR / 4];
+#pragma unroll
+    for (int g = 0; g < NR / 4; ++g)
+      r[g] = philox4x32_10_rk(make_uint4(q0 + static_cast<uint32_t>(g * mx), 0u, P.vid0, P.vid1),
+                              P.rk0, P.rk1);
+#pragma unroll
+    for (int g = 0; g < NR / 4; ++g) {
+      const float2 u = box_muller(r[g].x, r[g].y), v = box_muller(r[g].z, r[g].w);
+      n[4 * g] = u.x; n[4 * g + 1] = u.y; n[4 * g + 2] = v.x; n[4 * g + 3] = v.y;
+    }
+  }
+  if (yend - ybeg == NR)
+    column_pairs<NR, kStagedPath, kLabels, kNearest, kClamp, kSepLbl, true>(
+        a, P, vin, lin, vout, lout, sv, X, Z, ybeg, yend, n);
+  else
+    column_pairs<NR, kStagedPath, kLabels, kNearest, kClamp, kSepLbl, false>(
+        a, P, vin, lin, vout, lout, sv, X, Z, ybeg, yend, n);
+}
+
 template <class S, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp>
 __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
                                              const float* __restrict__ vin,
@@ -357,42 +409,10 @@ __device__ __forceinline__ void tile_compute(const WarpArgs& a, const Params& P,
                                              float* __restrict__ vout,
                                              uint8_t* __restrict__ lout, const Stage& sv,
                                              int ox, int oy, int oz) {
-  constexpr int RPT = S::RPT;
   const int w = static_cast<int>(threadIdx.x >> 5);
-  const int X = ox + static_cast<int>(threadIdx.x & 31);
-  const int Z = oz + w % S::TZ;
-  const int ybeg = oy + (w / S::TZ) * RPT;
-  const int mx = a.mx, my = a.my;
-  if (X >= mx || Z >= a.mz || ybeg >= my) return;
-  const int yend = min(ybeg + RPT, my);
-  if ((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi) {  // warp-uniform
-    column_occluded<S, kStagedPath, kLabels, kClamp>(a, P, lin, vout, lout, sv, X, Z, ybeg, yend);
-    return;
-  }
-  float n[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) n[i] = 0.0f;
-  if (P.flags & kNoise) {
-    const int Gy = (my + 3) >> 2;
-    const uint32_t q0 = static_cast<uint32_t>(X) +
-                        static_cast<uint32_t>(mx) * static_cast<uint32_t>(Gy * Z + (ybeg >> 2));
-    uint4 r[RPT / 4];
-#pragma unroll
-    for (int g = 0; g < RPT / 4; ++g)
-      r[g] = philox4x32_10_rk(make_uint4(q0 + static_cast<uint32_t>(g * mx), 0u, P.vid0, P.vid1),
-                              P.rk0, P.rk1);
-#pragma unroll
-    for (int g = 0; g < RPT / 4; ++g) {
-      const float2 u = box_muller(r[g].x, r[g].y), v = box_muller(r[g].z, r[g].w);
-      n[4 * g] = u.x; n[4 * g + 1] = u.y; n[4 * g + 2] = v.x; n[4 * g + 3] = v.y;
-    }
-  }
-  if (yend - ybeg == RPT)
-    column_pairs<S, kStagedPath, kLabels, kNearest, kClamp, true>(a, P, vin, lin, vout, lout, sv,
-                                                                  X, Z, ybeg, yend, n);
-  else
-    column_pairs<S, kStagedPath, kLabels, kNearest, kClamp, false>(a, P, vin, lin, vout, lout,
-                                                                   sv, X, Z, ybeg, yend, n);
+  column_rows<S::RPT, kStagedPath, kLabels, kNearest, kClamp, false>(
+      a, P, vin, lin, vout, lout, sv, ox + static_cast<int>(threadIdx.x & 31), oz + w % S::TZ,
+      oy + (w / S::TZ) * S::RPT);
 }
 
 // Box of one tile (warp 0): the bounding box of the 8 transformed tile corners
@@ -514,6 +534,10 @@ __device__ __forceinline__ Stage make_stage(const WarpArgs& a, const int* box, i
   sv.bz = static_cast<float>(box[2]);
   sv.Wf = static_cast<float>(sv.W);
   sv.HWf = static_cast<float>(sv.HW);
+  sv.WL = sv.W;
+  sv.HWL = sv.HW;
+  sv.WLf = sv.Wf;
+  sv.HWLf = sv.HWf;
   sv.nx = static_cast<float>(a.nx);
   sv.ny = static_cast<float>(a.ny);
   sv.nz = static_cast<float>(a.nz);
@@ -792,6 +816,320 @@ static cudaError_t launch_persistent(const WarpArgs& a, cudaStream_t s) {
   return e;
 }
 
+// ----------------------------------------------------------------------------
+// Kernel C (TMA staging, the default): one CTA per output tile (cfg C shape,
+// WARPS == TZ so every thread owns all TY rows of its column).  Warp 0 plans
+// the tile: the footprint box of the whole tile, or of 2 / 4 y-parts when the
+// whole box exceeds the buffer (sub-tiling replaces the gather fallback).
+// Each part's box is loaded by cp.async.bulk.tensor (4D tensor map per width
+// class: image boxes of 4 rows, label boxes of 8 rows; out-of-tensor elements
+// arrive as 0), completion tracked by one mbarrier (one phase per part).
+// Boundary boxes with a nonzero fill / label_fill get their out-of-volume
+// elements overwritten before compute (R6, R8).
+// ----------------------------------------------------------------------------
+enum { kBx, kBy, kBz, kBW, kBH, kBD, kBCi, kBCl, kBClamp, kBFix, kBImgBytes, kBLblBytes,
+       kBPart, kBNF };
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "W3D_WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra W3D_DONE%=;\n"
+      " bra W3D_WAIT%=;\n"
+      "W3D_DONE%=:\n}\n" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            int z, int v, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(v), "r"(mbar)
+      : "memory");
+}
+
+// Warp 0: boxes of the tile split into nsub y-parts (nsub = 1, 2, 4: the
+// first that fits).  Lanes 8g .. 8g+7 evaluate part g's 8 corners.
+template <class S>
+__device__ __forceinline__ void tma_plan(const WarpArgs& a, const Params& P, int ox, int oy,
+                                         int oz, int capb, bool labels, int (*box)[kBNF],
+                                         int* nsub_out) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
+  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                      static_cast<float>(a.nz)};
+  const bool fill_nz = a.fill != 0.0f, lfill_nz = labels && a.label_fill != 0u;
+  for (int nsub = 1; nsub <= 4; nsub <<= 1) {
+    const int rows = S::TY / nsub;
+    const int y0 = oy + min(g, nsub - 1) * rows;
+    const bool empty = y0 >= a.my;
+    const float X = static_cast<float>((c & 1) ? min(ox + S::TX, a.mx) - 1 : ox);
+    const float Y = static_cast<float>((c & 2) ? min(y0 + rows, a.my) - 1 : min(y0, a.my - 1));
+    const float Z = static_cast<float>((c & 4) ? min(oz + S::TZ, a.mz) - 1 : oz);
+    float mn[3], mxv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float p = __fmaf_rn(P.A[4 * k], X, __fmaf_rn(P.A[4 * k + 1], Y,
+                                                         __fmaf_rn(P.A[4 * k + 2], Z, P.A[4 * k + 3])));
+      mn[k] = p;
+      mxv[k] = p;
+    }
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+        mxv[k] = fmaxf(mxv[k], __shfl_xor_sync(0xffffffffu, mxv[k], off));
+      }
+    int lo[3], hi[3];
+    bool inside = true, touches = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = static_cast<int>(floorf(fminf(fmaxf(mn[k], -1.0f), n[k])));
+      hi[k] = static_cast<int>(floorf(fminf(fmaxf(mxv[k], -1.0f), n[k]))) + 1;
+      inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
+      touches |= (lo[k] < 0) | (hi[k] >= static_cast<int>(n[k]));
+    }
+    const int W = hi[0] - lo[0] + 1, H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
+    int ci = -1, cl = -1;
+#pragma unroll
+    for (int q = kNumImgCls - 1; q >= 0; --q)
+      if (img_cls_width(q) >= W) ci = q;
+#pragma unroll
+    for (int q = kNumLblCls - 1; q >= 0; --q)
+      if (lbl_cls_width(q) >= W) cl = q;
+    const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
+    const int64_t bimg = ci < 0 ? 0 : static_cast<int64_t>(D) * H4 * img_cls_width(ci) * 4;
+    const int64_t blbl = (!labels || cl < 0) ? 0 : static_cast<int64_t>(D) * H8 * lbl_cls_width(cl);
+    const bool fits = empty || (ci >= 0 && (!labels || cl >= 0) && bimg + blbl <= capb);
+    const bool all_fit = __all_sync(0xffffffffu, (g >= nsub) || fits);
+    if (all_fit) {
+      if (c == 0 && g < nsub) {
+        int* b = box[g];
+        b[kBx] = lo[0]; b[kBy] = lo[1]; b[kBz] = lo[2];
+        b[kBW] = W; b[kBH] = H; b[kBD] = empty ? 0 : D;
+        b[kBCi] = ci; b[kBCl] = cl;
+        b[kBClamp] = inside ? 0 : 1;
+        b[kBFix] = touches ? ((fill_nz ? 1 : 0) | (lfill_nz ? 2 : 0)) : 0;
+        b[kBImgBytes] = static_cast<int>(bimg);
+        b[kBLblBytes] = static_cast<int>(blbl);
+        b[kBPart] = y0;
+      }
+      if (lane == 0) *nsub_out = nsub;
+      return;
+    }
+  }
+  if (lane == 0) *nsub_out = 0;
+}
+
+template <bool kLabels>
+__device__ __forceinline__ void tma_issue(const WarpArgs& a, const int* b, int vi, uint32_t sbase,
+                                          uint32_t mbar) {
+  const int lane = threadIdx.x & 31;
+  const int H4 = (b[kBH] + 3) & ~3, H8 = (b[kBH] + 7) & ~7, D = b[kBD];
+  const int WI = img_cls_width(b[kBCi]);
+  const int nimg_r = H4 / kTmaRowsImg, nimg = D * nimg_r;
+  const int nlbl_r = H8 / kTmaRowsLbl, nlbl = kLabels ? D * nlbl_r : 0;
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(mbar, static_cast<uint32_t>(b[kBImgBytes] + (kLabels ? b[kBLblBytes] : 0)));
+  }
+  __syncwarp();
+  const uint32_t lbase = sbase + static_cast<uint32_t>(b[kBImgBytes]);
+  const int WL = kLabels ? lbl_cls_width(b[kBCl]) : 0;
+  for (int i = lane; i < nimg + nlbl; i += 32) {
+    if (i < nimg) {
+      const int d = i / nimg_r, r = i - d * nimg_r;
+      const uint32_t dst = sbase + static_cast<uint32_t>(((d * H4) + kTmaRowsImg * r) * WI * 4);
+      tma_load_4d(dst, &a.tm_img[b[kBCi]], b[kBx], b[kBy] + kTmaRowsImg * r, b[kBz] + d, vi, mbar);
+    } else {
+      const int j = i - nimg, d = j / nlbl_r, r = j - d * nlbl_r;
+      const uint32_t dst = lbase + static_cast<uint32_t>(((d * H8) + kTmaRowsLbl * r) * WL);
+      tma_load_4d(dst, &a.tm_lbl[b[kBCl]], b[kBx], b[kBy] + kTmaRowsLbl * r, b[kBz] + d, vi, mbar);
+    }
+  }
+}
+
+// Overwrite the out-of-volume elements of a boundary box (TMA wrote 0) with
+// fill / label_fill.  The box is clamped to [-1, n+1], so per in-volume row at
+// most 3 columns are outside.
+template <class S, bool kLabels>
+__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b) {
+  const int W = b[kBW], H = b[kBH], D = b[kBD];
+  const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
+  const int WI = img_cls_width(b[kBCi]);
+  const int WL = kLabels ? lbl_cls_width(b[kBCl]) : 0;
+  float* simg = reinterpret_cast<float*>(g_smem);
+  uint8_t* slbl = g_smem + b[kBImgBytes];
+  const bool fi = b[kBFix] & 1, fl = kLabels && (b[kBFix] & 2);
+  const float f = a.fill;
+  const uint8_t lf = static_cast<uint8_t>(a.label_fill);
+  for (int r = threadIdx.x; r < H * D; r += S::THREADS) {
+    const int rz = r / H, ry = r - rz * H;
+    const int z = b[kBz] + rz, y = b[kBy] + ry;
+    float* irow = simg + (rz * H4 + ry) * WI;
+    uint8_t* lrow = slbl + (rz * H8 + ry) * WL;
+    const bool row_out = static_cast<unsigned>(z) >= static_cast<unsigned>(a.nz) ||
+                         static_cast<unsigned>(y) >= static_cast<unsigned>(a.ny);
+    const int x_first_out = a.nx - b[kBx];  // first column with x >= nx
+    for (int x = 0; x < W; ++x) {
+      const bool out = row_out || (b[kBx] + x < 0) || (x >= x_first_out);
+      if (!out) {
+        if (x + 1 < x_first_out) x = max(x, x_first_out - 1);  // jump to the right edge
+        continue;
+      }
+      if (fi) irow[x] = f;
+      if (fl) lrow[x] = lf;
+    }
+  }
+}
+
+__device__ __forceinline__ Stage make_stage_tma(const WarpArgs& a, const int* b) {
+  Stage sv;
+  const int H4 = (b[kBH] + 3) & ~3, H8 = (b[kBH] + 7) & ~7;
+  sv.W = img_cls_width(b[kBCi]);
+  sv.HW = sv.W * H4;
+  sv.WL = b[kBCl] >= 0 ? lbl_cls_width(b[kBCl]) : 0;
+  sv.HWL = sv.WL * H8;
+  sv.img_off = 0;
+  sv.lbl_off = b[kBImgBytes];
+  sv.bx = static_cast<float>(b[kBx]);
+  sv.by = static_cast<float>(b[kBy]);
+  sv.bz = static_cast<float>(b[kBz]);
+  sv.Wf = static_cast<float>(sv.W);
+  sv.HWf = static_cast<float>(sv.HW);
+  sv.WLf = static_cast<float>(sv.WL);
+  sv.HWLf = static_cast<float>(sv.HWL);
+  sv.nx = static_cast<float>(a.nx);
+  sv.ny = static_cast<float>(a.ny);
+  sv.nz = static_cast<float>(a.nz);
+  return sv;
+}
+
+template <int NR, bool kLabels, bool kNearest>
+__device__ __forceinline__ void tma_part_compute(const WarpArgs& a, const Params& P,
+                                                 float* vout, uint8_t* lout, const int* b,
+                                                 int X, int Z) {
+  const Stage sv = make_stage_tma(a, b);
+  if (b[kBClamp])
+    column_rows<NR, true, kLabels, kNearest, true, true>(a, P, nullptr, nullptr, vout, lout, sv,
+                                                         X, Z, b[kBPart]);
+  else
+    column_rows<NR, true, kLabels, kNearest, false, true>(a, P, nullptr, nullptr, vout, lout, sv,
+                                                          X, Z, b[kBPart]);
+}
+
+template <class Cfg, bool kLabels, bool kNearest>
+__global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
+    warp3d_tma_kernel(const __grid_constant__ WarpArgs a, const int tiles_z) {
+  using S = typename Cfg::S;
+  static_assert(S::WARPS == S::TZ && S::RPT == S::TY && S::TY % 16 == 0, "TMA kernel shape");
+  __shared__ int s_box[4][kBNF];
+  __shared__ int s_nsub;
+  __shared__ __align__(8) unsigned long long s_mbar;
+  const int vi = static_cast<int>(blockIdx.z) / tiles_z;
+  const Params P = load_params(a.vol[vi]);
+  const int ox = static_cast<int>(blockIdx.x) * S::TX;
+  const int oy = static_cast<int>(blockIdx.y) * S::TY;
+  const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * S::TZ;
+  float* __restrict__ vout = a.out + vi * a.out_stride;
+  uint8_t* __restrict__ lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
+  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    tma_plan<S>(a, P, ox, oy, oz, Cfg::CAP * 5, kLabels, s_box, &s_nsub);
+  }
+  __syncthreads();
+  const int nsub = s_nsub;
+  const int X = ox + static_cast<int>(threadIdx.x & 31);
+  const int Z = oz + static_cast<int>(threadIdx.x >> 5);
+  if (nsub == 0) {  // even a quarter of the tile does not fit: gathers
+    count_tile(false);
+    Stage sv;
+    const float* vin = a.in + vi * a.in_stride;
+    const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+    tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+    return;
+  }
+  count_tile(true);
+  uint32_t phase = 0;
+  for (int k = 0; k < nsub; ++k) {
+    int b[kBNF];
+#pragma unroll
+    for (int i = 0; i < kBNF; ++i) b[i] = s_box[k][i];
+    if (b[kBD] == 0) continue;  // part entirely beyond the volume's last row
+    if (threadIdx.x < 32) tma_issue<kLabels>(a, b, vi, sbase, mbar);
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+    if (b[kBFix]) {
+      tma_fixup<S, kLabels>(a, b);
+      __syncthreads();
+    }
+    if (nsub == 1)
+      tma_part_compute<S::TY, kLabels, kNearest>(a, P, vout, lout, b, X, Z);
+    else if (nsub == 2)
+      tma_part_compute<S::TY / 2, kLabels, kNearest>(a, P, vout, lout, b, X, Z);
+    else
+      tma_part_compute<S::TY / 4, kLabels, kNearest>(a, P, vout, lout, b, X, Z);
+    if (k + 1 < nsub) __syncthreads();  // buffer reuse by the next part
+  }
+}
+
+template <class Cfg, bool kLabels, bool kNearest>
+static cudaError_t launch_tma_variant(const WarpArgs& a, cudaStream_t s) {
+  using S = typename Cfg::S;
+  const int tiles_x = (a.mx + S::TX - 1) / S::TX, tiles_y = (a.my + S::TY - 1) / S::TY;
+  const int tiles_z = (a.mz + S::TZ - 1) / S::TZ;
+  const int64_t gz = static_cast<int64_t>(tiles_z) * a.nvol;
+  if (tiles_y > 65535 || gz > 65535) return cudaErrorInvalidConfiguration;
+  const dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
+                  static_cast<unsigned>(gz));
+  const size_t smem = static_cast<size_t>(Cfg::CAP) * 5;
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(warp3d_tma_kernel<Cfg, kLabels, kNearest>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  warp3d_tma_kernel<Cfg, kLabels, kNearest><<<grid, S::THREADS, smem, s>>>(a, tiles_z);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_tma(const WarpArgs& a, cudaStream_t s) {
+  const bool labels = a.in_lbl != nullptr;
+  const bool nearest = a.interp == W3D_INTERP_NEAREST;
+  cudaError_t e;
+  if (labels)
+    e = nearest ? launch_tma_variant<CfgC, true, true>(a, s)
+                : launch_tma_variant<CfgC, true, false>(a, s);
+  else
+    e = nearest ? launch_tma_variant<CfgC, false, true>(a, s)
+                : launch_tma_variant<CfgC, false, false>(a, s);
+  note_launch();
+  return e;
+}
+
+bool tma_supported(const WarpArgs& a) {
+  const bool img_ok = (a.nx % 4 == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0);
+  const bool lbl_ok = a.in_lbl == nullptr ||
+                      ((a.nx % 16 == 0) && (reinterpret_cast<uintptr_t>(a.in_lbl) % 16 == 0));
+  return img_ok && lbl_ok;
+}
+
 cudaError_t read_tile_stats(unsigned long long out[2]) {
   cudaError_t e = cudaMemcpyFromSymbol(&out[0], g_tiles_staged, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&out[1], g_tiles_gather, sizeof(unsigned long long));
@@ -810,12 +1148,14 @@ cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s) {
   return launch_tiles(a, staged_supported(a), s);
 }
 
-// AUTO: the one-tile-per-CTA staged kernel; W3D_PERSISTENT=1 selects the
-// persistent double-buffered kernel (experiment knob).
+// AUTO: the TMA-staged tile kernel when the tensor maps could be encoded, else
+// the cp.async-staged tile kernel; W3D_PERSISTENT=1 selects the persistent
+// double-buffered kernel (experiment knob).
 cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s) {
-  if (!staged_supported(a)) return launch_tiles(a, false, s);
   const char* e = getenv("W3D_PERSISTENT");
-  if (e && e[0] == '1') return launch_persistent(a, s);
+  if (e && e[0] == '1' && staged_supported(a)) return launch_persistent(a, s);
+  if (a.use_tma) return launch_tma(a, s);
+  if (!staged_supported(a)) return launch_tiles(a, false, s);
   return launch_tiles(a, true, s);
 }
 

@@ -117,7 +117,7 @@ def test_noise_hook_matches_oracle(W, shape):
 
 
 # ----------------------------------------------------------------------------- configs[0] (C1)
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_c1_fixed_affine_noise(W, variant):
     """32^3 float32 + uint8 labels, one fixed affine, trilinear + nearest, sigma = 10 HU."""
     img, lbl = synth.phantom((32, 32, 32))
@@ -142,7 +142,7 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("case", range(len(SMALL)))
 def test_small_cases(W, case, variant):
     in_shape, out_shape, rname, flags, interp, B = SMALL[case]
@@ -176,7 +176,7 @@ def test_exact_permutations_on_gpu(W):
         A = np.zeros((3, 4), np.float32)
         A[:, :3] = M
         A[:, 3] = b
-        for variant in (1, 2):
+        for variant in (1, 2, 3):
             g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], 0, [0],
                                          variant=variant, fill=-5.0, label_fill=9)
             assert np.array_equal(g_img[0], ref[0][0]), name
@@ -185,11 +185,11 @@ def test_exact_permutations_on_gpu(W):
 
 
 def test_fully_out_of_bounds_and_occlusion(W):
-    img, lbl = synth.random_volume((12, 12, 12), 4)
+    img, lbl = synth.random_volume((16, 16, 16), 4)
     d = synth.draw(synth.TRAIN, 3)
     A = np.zeros((3, 4), np.float32)
     A[:, 3] = (-40, 3, 3)
-    for variant in (1, 2):
+    for variant in (1, 2, 3):
         g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], 0, [0], variant=variant,
                                      fill=-1000.0, label_fill=6)
         assert np.all(g_img == np.float32(-1000.0)) and np.all(g_lbl == 6)
@@ -201,7 +201,7 @@ def test_fully_out_of_bounds_and_occlusion(W):
     oph = O.photometric(FULL | O.OCCLUDE, window=d.window, gamma=d.gamma, sigma=d.sigma, seed=1,
                         volume_id=0, occ_z0=2.5, occ_height=4.0)
     r_img, r_lbl = O.warp_volume(img, lbl, A, None, 0, -1000.0, 0, oph)
-    for variant in (1, 2):
+    for variant in (1, 2, 3):
         out, out_l = W.warp3d_affine_batched(torch.from_numpy(img[None]).cuda(),
                                              torch.from_numpy(lbl[None]).cuda(), params,
                                              fill=-1000.0, variant=variant)
@@ -209,6 +209,39 @@ def test_fully_out_of_bounds_and_occlusion(W):
         assert np.all(g[3:7] == 0.0)
         assert np.array_equal(out_l.cpu().numpy()[0], r_lbl)
         assert_image_close(g, r_img, d.window, d.gamma, True, "occlusion")
+
+
+def test_tma_variant_reports_unsupported_layouts(W):
+    img, lbl = synth.random_volume((8, 8, 12), 5)   # nx = 12: label rows not 16 B multiples
+    A = np.eye(3, 4, dtype=np.float32)
+    params = [W.volume_params(A)]
+    with pytest.raises(W.Warp3DError) as e:
+        W.warp3d_affine_batched(torch.from_numpy(img[None]).cuda(),
+                                torch.from_numpy(lbl[None]).cuda(), params, variant=3)
+    assert e.value.status == 2
+    # without labels nx % 4 == 0 suffices
+    out, _ = W.warp3d_affine_batched(torch.from_numpy(img[None]).cuda(), None, params, variant=3)
+    assert np.array_equal(out.cpu().numpy()[0], img)
+
+
+def test_tma_subtiling_and_fixup_paths(W):
+    """Large rotations on a big volume force 2- and 4-part sub-tiles; nonzero fill and
+    label_fill force the out-of-volume fix-up; results equal the gather variant bitwise
+    and the oracle within tolerance."""
+    shape = (96, 96, 96)
+    img, lbl = synth.phantom(shape)
+    ds = [synth.draw(synth.LARGE, 40 + i) for i in range(3)]
+    As = [_oracle_affine(d, shape, shape) for d in ds]
+    imgs = np.repeat(img[None], 3, 0)
+    lbls = np.repeat(lbl[None], 3, 0)
+    s0 = W.warp3d_tile_stats()
+    g_img, g_lbl, ref = run_case(W, imgs, lbls, As, ds, FULL, [0, 1, 2], variant=3,
+                                 fill=-1000.0, label_fill=5)
+    check(g_img, g_lbl, ref, ds, FULL, "tma large")
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(3)]
+    o1, l1 = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda(),
+                                     params, fill=-1000.0, label_fill=5, variant=1)
+    assert np.array_equal(o1.cpu().numpy(), g_img) and np.array_equal(l1.cpu().numpy(), g_lbl)
 
 
 def test_single_volume_entry_point(W):
@@ -234,7 +267,7 @@ def _batch_inputs(shape, B, ranges, first_vid=0, n_distinct=4):
     return imgs, lbls, ds, As
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 def test_c2_single_ct_volume(W, variant):
     imgs, lbls, ds, As = _batch_inputs((160, 128, 128), 1, synth.TRAIN)
     g_img, g_lbl, ref = run_case(W, imgs, lbls, As, ds, FULL, [0], variant=variant)
@@ -280,7 +313,7 @@ def test_c4_512cubed_large_rotations_sampled(W):
     img, lbl = synth.phantom(shape)
     ds = [synth.draw(synth.LARGE, 7)]
     As = [_oracle_affine(ds[0], shape, shape)]
-    for variant in (0, 1):
+    for variant in (0, 1, 2):
         out, out_l = _sampled_check(W, img[None], lbl[None], As, ds, FULL, [0], 200_000,
                                     variant=variant)
         # full z-slices (several thousand contiguous rows) through the oracle
@@ -319,7 +352,7 @@ def test_variants_batch_splits_and_determinism_bitwise(W):
     ti, tl = torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda()
     params = [W.volume_params(As[i], _wph(W, ds[i], FULL, 100 + i)) for i in range(6)]
     ref, ref_l = W.warp3d_affine_batched(ti, tl, params, fill=-1000.0, variant=1)
-    for variant in (0, 1, 2):
+    for variant in (0, 1, 2, 3):
         o, ol = W.warp3d_affine_batched(ti, tl, params, fill=-1000.0, variant=variant)
         assert torch.equal(o, ref) and torch.equal(ol, ref_l), variant
     for i in range(6):  # single calls
