@@ -837,16 +837,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes)
                : "memory");
 }
+// Bounded wait: a TMA that never completes traps (a launch error) instead of
+// hanging the device.
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred P1;\n"
-      "W3D_WAIT%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @P1 bra W3D_DONE%=;\n"
-      " bra W3D_WAIT%=;\n"
-      "W3D_DONE%=:\n}\n" ::"r"(mbar),
-      "r"(phase)
-      : "memory");
+  for (uint32_t tries = 0;; ++tries) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (tries > (1u << 24)) __trap();
+  }
 }
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int x, int y,
                                             int z, int v, uint32_t mbar) {
