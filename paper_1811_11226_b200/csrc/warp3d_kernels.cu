@@ -967,13 +967,13 @@ __device__ __forceinline__ void tma_issue(const WarpArgs& a, const int* b, int v
 // fill / label_fill.  The box is clamped to [-1, n+1], so per in-volume row at
 // most 3 columns are outside.
 template <class S, bool kLabels>
-__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b) {
+__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b, int pad) {
   const int W = b[kBW], H = b[kBH], D = b[kBD];
   const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
   const int WI = img_cls_width(b[kBCi]);
   const int WL = kLabels ? lbl_cls_width(b[kBCl]) : 0;
-  float* simg = reinterpret_cast<float*>(g_smem);
-  uint8_t* slbl = g_smem + b[kBImgBytes];
+  float* simg = reinterpret_cast<float*>(g_smem + pad);
+  uint8_t* slbl = g_smem + pad + b[kBImgBytes];
   const bool fi = b[kBFix] & 1, fl = kLabels && (b[kBFix] & 2);
   const float f = a.fill;
   const uint8_t lf = static_cast<uint8_t>(a.label_fill);
@@ -997,15 +997,15 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b) {
   }
 }
 
-__device__ __forceinline__ Stage make_stage_tma(const WarpArgs& a, const int* b) {
+__device__ __forceinline__ Stage make_stage_tma(const WarpArgs& a, const int* b, int pad) {
   Stage sv;
   const int H4 = (b[kBH] + 3) & ~3, H8 = (b[kBH] + 7) & ~7;
   sv.W = img_cls_width(b[kBCi]);
   sv.HW = sv.W * H4;
   sv.WL = b[kBCl] >= 0 ? lbl_cls_width(b[kBCl]) : 0;
   sv.HWL = sv.WL * H8;
-  sv.img_off = 0;
-  sv.lbl_off = b[kBImgBytes];
+  sv.img_off = pad;
+  sv.lbl_off = pad + b[kBImgBytes];
   sv.bx = static_cast<float>(b[kBx]);
   sv.by = static_cast<float>(b[kBy]);
   sv.bz = static_cast<float>(b[kBz]);
@@ -1022,8 +1022,8 @@ __device__ __forceinline__ Stage make_stage_tma(const WarpArgs& a, const int* b)
 template <int NR, bool kLabels, bool kNearest>
 __device__ __forceinline__ void tma_part_compute(const WarpArgs& a, const Params& P,
                                                  float* vout, uint8_t* lout, const int* b,
-                                                 int X, int Z) {
-  const Stage sv = make_stage_tma(a, b);
+                                                 int X, int Z, int pad) {
+  const Stage sv = make_stage_tma(a, b, pad);
   if (b[kBClamp])
     column_rows<NR, true, kLabels, kNearest, true, true>(a, P, nullptr, nullptr, vout, lout, sv,
                                                          X, Z, b[kBPart]);
@@ -1048,7 +1048,11 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
   float* __restrict__ vout = a.out + vi * a.out_stride;
   uint8_t* __restrict__ lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
   const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
+  // TMA destinations must be 128 B aligned: align the dynamic region at run time
+  // (the launch reserves 128 extra bytes)
+  const uint32_t sraw = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
+  const int pad = static_cast<int>((128u - (sraw & 127u)) & 127u);
+  const uint32_t sbase = sraw + static_cast<uint32_t>(pad);
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
       mbar_init(mbar, 1);
@@ -1079,15 +1083,15 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
     mbar_wait(mbar, phase);
     phase ^= 1u;
     if (b[kBFix]) {
-      tma_fixup<S, kLabels>(a, b);
+      tma_fixup<S, kLabels>(a, b, pad);
       __syncthreads();
     }
     if (nsub == 1)
-      tma_part_compute<S::TY, kLabels, kNearest>(a, P, vout, lout, b, X, Z);
+      tma_part_compute<S::TY, kLabels, kNearest>(a, P, vout, lout, b, X, Z, pad);
     else if (nsub == 2)
-      tma_part_compute<S::TY / 2, kLabels, kNearest>(a, P, vout, lout, b, X, Z);
+      tma_part_compute<S::TY / 2, kLabels, kNearest>(a, P, vout, lout, b, X, Z, pad);
     else
-      tma_part_compute<S::TY / 4, kLabels, kNearest>(a, P, vout, lout, b, X, Z);
+      tma_part_compute<S::TY / 4, kLabels, kNearest>(a, P, vout, lout, b, X, Z, pad);
     if (k + 1 < nsub) __syncthreads();  // buffer reuse by the next part
   }
 }
@@ -1101,7 +1105,7 @@ static cudaError_t launch_tma_variant(const WarpArgs& a, cudaStream_t s) {
   if (tiles_y > 65535 || gz > 65535) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
                   static_cast<unsigned>(gz));
-  const size_t smem = static_cast<size_t>(Cfg::CAP) * 5;
+  const size_t smem = static_cast<size_t>(Cfg::CAP) * 5 + 128;  // + alignment slack
   static bool configured = false;
   if (!configured) {
     const cudaError_t e = cudaFuncSetAttribute(warp3d_tma_kernel<Cfg, kLabels, kNearest>,
