@@ -827,8 +827,11 @@ static cudaError_t launch_persistent(const WarpArgs& a, cudaStream_t s) {
 // Boundary boxes with a nonzero fill / label_fill get their out-of-volume
 // elements overwritten before compute (R6, R8).
 // ----------------------------------------------------------------------------
-enum { kBx, kBy, kBz, kBW, kBH, kBD, kBCi, kBCl, kBClamp, kBFix, kBImgBytes, kBLblBytes,
-       kBPart, kBNF };
+// Box record: image origin x (multiple of 4: TMA needs 16 B aligned inner
+// coordinates), label origin x (multiple of 16), y, z, image / label widths
+// from those origins, H, D, classes, flags, byte sizes, first output row.
+enum { kBx, kBxl, kBy, kBz, kBW, kBWl, kBH, kBD, kBCi, kBCl, kBClamp, kBFix, kBImgBytes,
+       kBLblBytes, kBPart, kBNF };
 
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
@@ -903,14 +906,16 @@ __device__ __forceinline__ void tma_plan(const WarpArgs& a, const Params& P, int
       inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
       touches |= (lo[k] < 0) | (hi[k] >= static_cast<int>(n[k]));
     }
-    const int W = hi[0] - lo[0] + 1, H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
+    const int bxi = lo[0] & ~3, bxl = lo[0] & ~15;  // floor to 4 / 16 (lo >= -1)
+    const int W = hi[0] - bxi + 1, Wl = hi[0] - bxl + 1;
+    const int H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
     int ci = -1, cl = -1;
 #pragma unroll
     for (int q = kNumImgCls - 1; q >= 0; --q)
       if (img_cls_width(q) >= W) ci = q;
 #pragma unroll
     for (int q = kNumLblCls - 1; q >= 0; --q)
-      if (lbl_cls_width(q) >= W) cl = q;
+      if (lbl_cls_width(q) >= Wl) cl = q;
     const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
     const int64_t bimg = ci < 0 ? 0 : static_cast<int64_t>(D) * H4 * img_cls_width(ci) * 4;
     const int64_t blbl = (!labels || cl < 0) ? 0 : static_cast<int64_t>(D) * H8 * lbl_cls_width(cl);
@@ -919,8 +924,8 @@ __device__ __forceinline__ void tma_plan(const WarpArgs& a, const Params& P, int
     if (all_fit) {
       if (c == 0 && g < nsub) {
         int* b = box[g];
-        b[kBx] = lo[0]; b[kBy] = lo[1]; b[kBz] = lo[2];
-        b[kBW] = W; b[kBH] = H; b[kBD] = empty ? 0 : D;
+        b[kBx] = bxi; b[kBxl] = bxl; b[kBy] = lo[1]; b[kBz] = lo[2];
+        b[kBW] = W; b[kBWl] = Wl; b[kBH] = H; b[kBD] = empty ? 0 : D;
         b[kBCi] = ci; b[kBCl] = cl;
         b[kBClamp] = inside ? 0 : 1;
         b[kBFix] = touches ? ((fill_nz ? 1 : 0) | (lfill_nz ? 2 : 0)) : 0;
@@ -958,17 +963,21 @@ __device__ __forceinline__ void tma_issue(const WarpArgs& a, const int* b, int v
     } else {
       const int j = i - nimg, d = j / nlbl_r, r = j - d * nlbl_r;
       const uint32_t dst = lbase + static_cast<uint32_t>(((d * H8) + kTmaRowsLbl * r) * WL);
-      tma_load_4d(dst, &a.tm_lbl[b[kBCl]], b[kBx], b[kBy] + kTmaRowsLbl * r, b[kBz] + d, vi, mbar);
+      tma_load_4d(dst, &a.tm_lbl[b[kBCl]], b[kBxl], b[kBy] + kTmaRowsLbl * r, b[kBz] + d, vi,
+                  mbar);
     }
   }
 }
 
 // Overwrite the out-of-volume elements of a boundary box (TMA wrote 0) with
-// fill / label_fill.  The box is clamped to [-1, n+1], so per in-volume row at
-// most 3 columns are outside.
+// fill / label_fill.  The box is clamped to [-1, n+1]: per in-volume row only
+// a few columns at either end are outside.
+__device__ __forceinline__ bool col_out(int x, int nx) {
+  return static_cast<unsigned>(x) >= static_cast<unsigned>(nx);
+}
 template <class S, bool kLabels>
 __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b, int pad) {
-  const int W = b[kBW], H = b[kBH], D = b[kBD];
+  const int H = b[kBH], D = b[kBD];
   const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
   const int WI = img_cls_width(b[kBCi]);
   const int WL = kLabels ? lbl_cls_width(b[kBCl]) : 0;
@@ -980,19 +989,16 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b, int p
   for (int r = threadIdx.x; r < H * D; r += S::THREADS) {
     const int rz = r / H, ry = r - rz * H;
     const int z = b[kBz] + rz, y = b[kBy] + ry;
-    float* irow = simg + (rz * H4 + ry) * WI;
-    uint8_t* lrow = slbl + (rz * H8 + ry) * WL;
-    const bool row_out = static_cast<unsigned>(z) >= static_cast<unsigned>(a.nz) ||
-                         static_cast<unsigned>(y) >= static_cast<unsigned>(a.ny);
-    const int x_first_out = a.nx - b[kBx];  // first column with x >= nx
-    for (int x = 0; x < W; ++x) {
-      const bool out = row_out || (b[kBx] + x < 0) || (x >= x_first_out);
-      if (!out) {
-        if (x + 1 < x_first_out) x = max(x, x_first_out - 1);  // jump to the right edge
-        continue;
-      }
-      if (fi) irow[x] = f;
-      if (fl) lrow[x] = lf;
+    const bool row_out = col_out(z, a.nz) || col_out(y, a.ny);
+    if (fi) {
+      float* row = simg + (rz * H4 + ry) * WI;
+      for (int x = 0; x < b[kBW]; ++x)
+        if (row_out || col_out(b[kBx] + x, a.nx)) row[x] = f;
+    }
+    if (fl) {
+      uint8_t* row = slbl + (rz * H8 + ry) * WL;
+      for (int x = 0; x < b[kBWl]; ++x)
+        if (row_out || col_out(b[kBxl] + x, a.nx)) row[x] = lf;
     }
   }
 }
@@ -1005,7 +1011,9 @@ __device__ __forceinline__ Stage make_stage_tma(const WarpArgs& a, const int* b,
   sv.WL = b[kBCl] >= 0 ? lbl_cls_width(b[kBCl]) : 0;
   sv.HWL = sv.WL * H8;
   sv.img_off = pad;
-  sv.lbl_off = pad + b[kBImgBytes];
+  // label row origin is b[kBxl] <= b[kBx]: shift the label base so that the
+  // image-relative column index addresses the label buffer
+  sv.lbl_off = pad + b[kBImgBytes] + (b[kBx] - b[kBxl]);
   sv.bx = static_cast<float>(b[kBx]);
   sv.by = static_cast<float>(b[kBy]);
   sv.bz = static_cast<float>(b[kBz]);
