@@ -981,24 +981,42 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b, int p
   const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
   const int WI = img_cls_width(b[kBCi]);
   const int WL = kLabels ? lbl_cls_width(b[kBCl]) : 0;
-  float* simg = reinterpret_cast<float*>(g_smem + pad);
-  uint8_t* slbl = g_smem + pad + b[kBImgBytes];
+  const uint32_t simg = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem)) + pad;
+  const uint32_t slbl = simg + static_cast<uint32_t>(b[kBImgBytes]);
   const bool fi = b[kBFix] & 1, fl = kLabels && (b[kBFix] & 2);
   const float f = a.fill;
-  const uint8_t lf = static_cast<uint8_t>(a.label_fill);
+  const uint32_t lf4 = a.label_fill * 0x01010101u;
+  // columns [0, left) and [right, W) of an in-volume row are outside in x
+  const int left_i = min(b[kBW], max(0, -b[kBx])), right_i = max(0, a.nx - b[kBx]);
+  const int left_l = min(b[kBWl], max(0, -b[kBxl])), right_l = max(0, a.nx - b[kBxl]);
   for (int r = threadIdx.x; r < H * D; r += S::THREADS) {
     const int rz = r / H, ry = r - rz * H;
-    const int z = b[kBz] + rz, y = b[kBy] + ry;
-    const bool row_out = col_out(z, a.nz) || col_out(y, a.ny);
+    const bool row_out = col_out(b[kBz] + rz, a.nz) || col_out(b[kBy] + ry, a.ny);
     if (fi) {
-      float* row = simg + (rz * H4 + ry) * WI;
-      for (int x = 0; x < b[kBW]; ++x)
-        if (row_out || col_out(b[kBx] + x, a.nx)) row[x] = f;
+      const uint32_t row = simg + 4u * static_cast<uint32_t>((rz * H4 + ry) * WI);
+      if (row_out) {
+        for (int x = 0; x < WI; x += 4)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(row + 4u * x), "f"(f)
+                       : "memory");
+      } else {
+        for (int x = 0; x < left_i; ++x)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(row + 4u * x), "f"(f) : "memory");
+        for (int x = right_i; x < b[kBW]; ++x)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(row + 4u * x), "f"(f) : "memory");
+      }
     }
     if (fl) {
-      uint8_t* row = slbl + (rz * H8 + ry) * WL;
-      for (int x = 0; x < b[kBWl]; ++x)
-        if (row_out || col_out(b[kBxl] + x, a.nx)) row[x] = lf;
+      const uint32_t row = slbl + static_cast<uint32_t>((rz * H8 + ry) * WL);
+      if (row_out) {
+        for (int x = 0; x < WL; x += 16)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(row + x), "r"(lf4)
+                       : "memory");
+      } else {
+        for (int x = 0; x < left_l; ++x)
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(row + x), "r"(lf4) : "memory");
+        for (int x = right_l; x < b[kBWl]; ++x)
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(row + x), "r"(lf4) : "memory");
+      }
     }
   }
 }

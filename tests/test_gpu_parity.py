@@ -348,7 +348,7 @@ def test_c5_256_volumes_sampled_and_shard_invariant(W):
 
 # ----------------------------------------------------------------------------- invariances
 def test_variants_batch_splits_and_determinism_bitwise(W):
-    imgs, lbls, ds, As = _batch_inputs((64, 48, 56), 6, synth.TRAIN)
+    imgs, lbls, ds, As = _batch_inputs((64, 48, 64), 6, synth.TRAIN)
     ti, tl = torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda()
     params = [W.volume_params(As[i], _wph(W, ds[i], FULL, 100 + i)) for i in range(6)]
     ref, ref_l = W.warp3d_affine_batched(ti, tl, params, fill=-1000.0, variant=1)
