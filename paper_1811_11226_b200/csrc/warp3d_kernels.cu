@@ -1105,9 +1105,13 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
 #pragma unroll
     for (int i = 0; i < kBNF; ++i) b[i] = s_box[k][i];
     if (b[kBD] == 0) continue;  // part entirely beyond the volume's last row
-    if (threadIdx.x < 32) tma_issue<kLabels>(a, b, vi, sbase, mbar);
-    mbar_wait(mbar, phase);
+    // warp 0 issues and waits; the other warps block on bar.sync (no issue slots)
+    if (threadIdx.x < 32) {
+      tma_issue<kLabels>(a, b, vi, sbase, mbar);
+      mbar_wait(mbar, phase);
+    }
     phase ^= 1u;
+    __syncthreads();
     if (b[kBFix]) {
       tma_fixup<S, kLabels>(a, b, pad);
       __syncthreads();
