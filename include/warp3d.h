@@ -59,16 +59,20 @@ typedef enum {
 
 /* Kernel variant selector for warp3d_affine_batched_ex (tests / benchmarks). */
 typedef enum {
-  W3D_KERNEL_AUTO = 0,     /* library choice: TMA when possible, else STAGED,
+  W3D_KERNEL_AUTO = 0,     /* library choice: BULK when possible, else STAGED,
                               else GATHER                                         */
   W3D_KERNEL_GATHER = 1,   /* every corner gathered through L1/L2 (__ldg)        */
   W3D_KERNEL_STAGED = 2,   /* per-tile source footprint staged in shared memory
                               by cp.async (tiles whose footprint exceeds the
                               buffer gather instead)                              */
-  W3D_KERNEL_TMA = 3       /* footprint staged by cp.async.bulk.tensor (TMA),
-                              large footprints split into 2 / 4 y-parts; needs
-                              nx % 4 == 0 (with labels nx % 16 == 0) and 16 B
-                              aligned inputs, else W3D_ERR_UNSUPPORTED            */
+  W3D_KERNEL_TMA = 3,      /* footprint staged by cp.async.bulk.tensor (TMA
+                              tensor boxes), large footprints split into 2 / 4
+                              y-parts; needs nx % 4 == 0 (with labels
+                              nx % 16 == 0) and 16 B aligned inputs, else
+                              W3D_ERR_UNSUPPORTED                                 */
+  W3D_KERNEL_BULK = 4      /* as TMA, but each footprint row is one 1D
+                              cp.async.bulk copy (tight shared-memory layout);
+                              same requirements                                   */
 } w3d_kernel;
 
 typedef struct {

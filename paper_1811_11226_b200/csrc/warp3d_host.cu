@@ -251,7 +251,7 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
     args.nvol = nv;
     for (int32_t i = 0; i < nv; ++i) args.vol[i] = derive(affines[v0 + i], phs[v0 + i]);
     args.use_tma = 0;
-    if ((variant == W3D_KERNEL_AUTO || variant == W3D_KERNEL_TMA) && tma_supported(args)) {
+    if (variant == W3D_KERNEL_TMA && tma_supported(args)) {
       TmaKey k;
       k.in = args.in; k.lbl = args.in_lbl;
       k.nx = args.nx; k.ny = args.ny; k.nz = args.nz; k.nvol = nv; k.valid = true;
@@ -268,8 +268,14 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
       return fail(W3D_ERR_UNSUPPORTED,
                   "W3D_KERNEL_TMA needs nx %% 4 == 0 (labels: nx %% 16 == 0), 16 B aligned "
                   "inputs and cuTensorMapEncodeTiled");
+    if (variant == W3D_KERNEL_BULK && !tma_supported(args))
+      return fail(W3D_ERR_UNSUPPORTED,
+                  "W3D_KERNEL_BULK needs nx %% 4 == 0 (labels: nx %% 16 == 0) and 16 B aligned "
+                  "inputs");
     const cudaError_t e = (variant == W3D_KERNEL_GATHER)   ? launch_gather(args, stream)
                           : (variant == W3D_KERNEL_STAGED) ? launch_staged(args, stream)
+                          : (variant == W3D_KERNEL_TMA)    ? launch_tma(args, stream)
+                          : (variant == W3D_KERNEL_BULK)   ? launch_bulk(args, stream)
                                                            : launch_auto(args, stream);
     if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");
   }
@@ -340,7 +346,7 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
   if ((in_labels == nullptr) != (out_labels == nullptr))
     return fail(W3D_ERR_INVALID_ARG, "out_labels must be NULL iff in_labels is NULL");
   if (variant != W3D_KERNEL_AUTO && variant != W3D_KERNEL_GATHER && variant != W3D_KERNEL_STAGED &&
-      variant != W3D_KERNEL_TMA)
+      variant != W3D_KERNEL_TMA && variant != W3D_KERNEL_BULK)
     return fail(W3D_ERR_INVALID_ARG, "variant = %d is not a w3d_kernel", int(variant));
   for (int32_t i = 0; i < batch; ++i) {
     if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;

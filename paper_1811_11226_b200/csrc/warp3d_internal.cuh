@@ -83,6 +83,8 @@ struct alignas(64) WarpArgs {
 cudaError_t launch_gather(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s);
+cudaError_t launch_tma(const WarpArgs& a, cudaStream_t s);
+cudaError_t launch_bulk(const WarpArgs& a, cudaStream_t s);
 bool tma_supported(const WarpArgs& a);
 cudaError_t encode_tensor_maps(WarpArgs& a);
 cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,

@@ -831,7 +831,7 @@ static cudaError_t launch_persistent(const WarpArgs& a, cudaStream_t s) {
 // coordinates), label origin x (multiple of 16), y, z, image / label widths
 // from those origins, H, D, classes, flags, byte sizes, first output row.
 enum { kBx, kBxl, kBy, kBz, kBW, kBWl, kBH, kBD, kBCi, kBCl, kBClamp, kBFix, kBImgBytes,
-       kBLblBytes, kBPart, kBNF };
+       kBLblBytes, kBPart, kBPI, kBRI, kBPL, kBRL, kBNF };  // pitches / rows per plane
 
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
@@ -856,6 +856,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
     if (tries > (1u << 24)) __trap();
   }
 }
+__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int x, int y,
                                             int z, int v, uint32_t mbar) {
   asm volatile(
@@ -867,7 +881,7 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
 
 // Warp 0: boxes of the tile split into nsub y-parts (nsub = 1, 2, 4: the
 // first that fits).  Lanes 8g .. 8g+7 evaluate part g's 8 corners.
-template <class S>
+template <class S, bool kBulk>
 __device__ __forceinline__ void tma_plan(const WarpArgs& a, const Params& P, int ox, int oy,
                                          int oz, int capb, bool labels, int (*box)[kBNF],
                                          int* nsub_out) {
@@ -909,16 +923,23 @@ __device__ __forceinline__ void tma_plan(const WarpArgs& a, const Params& P, int
     const int bxi = lo[0] & ~3, bxl = lo[0] & ~15;  // floor to 4 / 16 (lo >= -1)
     const int W = hi[0] - bxi + 1, Wl = hi[0] - bxl + 1;
     const int H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
-    int ci = -1, cl = -1;
+    int ci = -1, cl = -1, PI, RI, PL, RL;
+    if (kBulk) {  // 1D bulk row copies: 16 B granularity only
+      ci = cl = 0;
+      PI = (W + 3) & ~3; RI = H;
+      PL = (Wl + 15) & ~15; RL = H;
+    } else {      // tensor boxes: width classes, 4 / 8-row groups
 #pragma unroll
-    for (int q = kNumImgCls - 1; q >= 0; --q)
-      if (img_cls_width(q) >= W) ci = q;
+      for (int q = kNumImgCls - 1; q >= 0; --q)
+        if (img_cls_width(q) >= W) ci = q;
 #pragma unroll
-    for (int q = kNumLblCls - 1; q >= 0; --q)
-      if (lbl_cls_width(q) >= Wl) cl = q;
-    const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
-    const int64_t bimg = ci < 0 ? 0 : static_cast<int64_t>(D) * H4 * img_cls_width(ci) * 4;
-    const int64_t blbl = (!labels || cl < 0) ? 0 : static_cast<int64_t>(D) * H8 * lbl_cls_width(cl);
+      for (int q = kNumLblCls - 1; q >= 0; --q)
+        if (lbl_cls_width(q) >= Wl) cl = q;
+      PI = ci < 0 ? 0 : img_cls_width(ci); RI = (H + 3) & ~3;
+      PL = cl < 0 ? 0 : lbl_cls_width(cl); RL = (H + 7) & ~7;
+    }
+    const int64_t bimg = static_cast<int64_t>(D) * RI * PI * 4;
+    const int64_t blbl = labels ? static_cast<int64_t>(D) * RL * PL : 0;
     const bool fits = empty || (ci >= 0 && (!labels || cl >= 0) && bimg + blbl <= capb);
     const bool all_fit = __all_sync(0xffffffffu, (g >= nsub) || fits);
     if (all_fit) {
@@ -932,6 +953,7 @@ __device__ __forceinline__ void tma_plan(const WarpArgs& a, const Params& P, int
         b[kBImgBytes] = static_cast<int>(bimg);
         b[kBLblBytes] = static_cast<int>(blbl);
         b[kBPart] = y0;
+        b[kBPI] = PI; b[kBRI] = RI; b[kBPL] = PL; b[kBRL] = RL;
       }
       if (lane == 0) *nsub_out = nsub;
       return;
@@ -944,8 +966,8 @@ template <bool kLabels>
 __device__ __forceinline__ void tma_issue(const WarpArgs& a, const int* b, int vi, uint32_t sbase,
                                           uint32_t mbar) {
   const int lane = threadIdx.x & 31;
-  const int H4 = (b[kBH] + 3) & ~3, H8 = (b[kBH] + 7) & ~7, D = b[kBD];
-  const int WI = img_cls_width(b[kBCi]);
+  const int H4 = b[kBRI], H8 = b[kBRL], D = b[kBD];
+  const int WI = b[kBPI];
   const int nimg_r = H4 / kTmaRowsImg, nimg = D * nimg_r;
   const int nlbl_r = H8 / kTmaRowsLbl, nlbl = kLabels ? D * nlbl_r : 0;
   if (lane == 0) {
@@ -954,7 +976,7 @@ __device__ __forceinline__ void tma_issue(const WarpArgs& a, const int* b, int v
   }
   __syncwarp();
   const uint32_t lbase = sbase + static_cast<uint32_t>(b[kBImgBytes]);
-  const int WL = kLabels ? lbl_cls_width(b[kBCl]) : 0;
+  const int WL = kLabels ? b[kBPL] : 0;
   for (int i = lane; i < nimg + nlbl; i += 32) {
     if (i < nimg) {
       const int d = i / nimg_r, r = i - d * nimg_r;
@@ -978,9 +1000,9 @@ __device__ __forceinline__ bool col_out(int x, int nx) {
 template <class S, bool kLabels>
 __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b, int pad) {
   const int H = b[kBH], D = b[kBD];
-  const int H4 = (H + 3) & ~3, H8 = (H + 7) & ~7;
-  const int WI = img_cls_width(b[kBCi]);
-  const int WL = kLabels ? lbl_cls_width(b[kBCl]) : 0;
+  const int H4 = b[kBRI], H8 = b[kBRL];
+  const int WI = b[kBPI];
+  const int WL = kLabels ? b[kBPL] : 0;
   const uint32_t simg = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem)) + pad;
   const uint32_t slbl = simg + static_cast<uint32_t>(b[kBImgBytes]);
   const bool fi = b[kBFix] & 1, fl = kLabels && (b[kBFix] & 2);
@@ -1021,13 +1043,80 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const int* b, int p
   }
 }
 
+// Bulk staging: every thread copies whole box rows with 1D cp.async.bulk
+// (image row [max(x0,0), min(x0+PI, nx)) and label row likewise; 16 B aligned
+// because x0 % 4 == 0 (labels x0 % 16 == 0) and nx % 4 (16) == 0) and writes
+// fill / label_fill into the out-of-volume rest of its rows.  Each copy adds
+// its bytes to the mbarrier's transaction count; every thread arrives once.
+template <class S, bool kLabels>
+__device__ __forceinline__ void bulk_issue(const WarpArgs& a, const int* b,
+                                           const float* __restrict__ vin,
+                                           const uint8_t* __restrict__ lin, uint32_t sbase,
+                                           uint32_t mbar) {
+  const int H = b[kBH], D = b[kBD], PI = b[kBPI], PL = b[kBPL];
+  const int bx = b[kBx], bxl = b[kBxl];
+  const int nx = a.nx, ny = a.ny, nz = a.nz;
+  const int xs = max(bx, 0), xe = min(bx + PI, nx);
+  const uint32_t bytes_i = xe > xs ? 4u * static_cast<uint32_t>(xe - xs) : 0u;
+  const int xsl = max(bxl, 0), xel = min(bxl + PL, nx);
+  const uint32_t bytes_l = xel > xsl ? static_cast<uint32_t>(xel - xsl) : 0u;
+  const uint32_t lbase = sbase + static_cast<uint32_t>(b[kBImgBytes]);
+  const float f = a.fill;
+  const uint32_t lf4 = a.label_fill * 0x01010101u;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  const int rows = H * D;
+  int r = threadIdx.x;
+  int rz = r / H, ry = r - (r / H) * H;
+  const int step_z = S::THREADS / H, step_y = S::THREADS - step_z * H;
+  for (; r < rows; r += S::THREADS) {
+    const int z = b[kBz] + rz, y = b[kBy] + ry;
+    const bool in_row = static_cast<unsigned>(z) < static_cast<unsigned>(nz) &&
+                        static_cast<unsigned>(y) < static_cast<unsigned>(ny);
+    const uint32_t irow = sbase + 4u * static_cast<uint32_t>(r * PI);
+    const int64_t g = (static_cast<int64_t>(z) * ny + y) * nx;
+    if (in_row && bytes_i) {
+      mbar_expect(mbar, bytes_i);
+      bulk_g2s(irow + 4u * static_cast<uint32_t>(xs - bx), vin + g + xs, bytes_i, mbar);
+      for (int x = 0; x < xs - bx; ++x)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(irow + 4u * x), "f"(f) : "memory");
+      for (int x = xe - bx; x < PI; ++x)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(irow + 4u * x), "f"(f) : "memory");
+    } else {
+      for (int x = 0; x < PI; x += 4)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(irow + 4u * x), "f"(f)
+                     : "memory");
+    }
+    if (kLabels) {
+      const uint32_t lrow = lbase + static_cast<uint32_t>(r * PL);
+      if (in_row && bytes_l) {
+        mbar_expect(mbar, bytes_l);
+        bulk_g2s(lrow + static_cast<uint32_t>(xsl - bxl), lin + g + xsl, bytes_l, mbar);
+        for (int x = 0; x < xsl - bxl; ++x)
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
+        for (int x = xel - bxl; x < PL; ++x)
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
+      } else {
+        for (int x = 0; x < PL; x += 16)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(lrow + x), "r"(lf4)
+                       : "memory");
+      }
+    }
+    rz += step_z;
+    ry += step_y;
+    if (ry >= H) {
+      ry -= H;
+      ++rz;
+    }
+  }
+  mbar_arrive(mbar);
+}
+
 __device__ __forceinline__ Stage make_stage_tma(const WarpArgs& a, const int* b, int pad) {
   Stage sv;
-  const int H4 = (b[kBH] + 3) & ~3, H8 = (b[kBH] + 7) & ~7;
-  sv.W = img_cls_width(b[kBCi]);
-  sv.HW = sv.W * H4;
-  sv.WL = b[kBCl] >= 0 ? lbl_cls_width(b[kBCl]) : 0;
-  sv.HWL = sv.WL * H8;
+  sv.W = b[kBPI];
+  sv.HW = sv.W * b[kBRI];
+  sv.WL = b[kBPL];
+  sv.HWL = sv.WL * b[kBRL];
   sv.img_off = pad;
   // label row origin is b[kBxl] <= b[kBx]: shift the label base so that the
   // image-relative column index addresses the label buffer
@@ -1058,7 +1147,7 @@ __device__ __forceinline__ void tma_part_compute(const WarpArgs& a, const Params
                                                           X, Z, b[kBPart]);
 }
 
-template <class Cfg, bool kLabels, bool kNearest>
+template <class Cfg, bool kBulk, bool kLabels, bool kNearest>
 __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
     warp3d_tma_kernel(const __grid_constant__ WarpArgs a, const int tiles_z) {
   using S = typename Cfg::S;
@@ -1081,10 +1170,10 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
   const uint32_t sbase = sraw + static_cast<uint32_t>(pad);
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
-      mbar_init(mbar, 1);
+      mbar_init(mbar, kBulk ? S::THREADS : 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    tma_plan<S>(a, P, ox, oy, oz, Cfg::CAP * 5, kLabels, s_box, &s_nsub);
+    tma_plan<S, kBulk>(a, P, ox, oy, oz, Cfg::CAP * 5, kLabels, s_box, &s_nsub);
   }
   __syncthreads();
   const int nsub = s_nsub;
@@ -1105,14 +1194,18 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
 #pragma unroll
     for (int i = 0; i < kBNF; ++i) b[i] = s_box[k][i];
     if (b[kBD] == 0) continue;  // part entirely beyond the volume's last row
-    // warp 0 issues and waits; the other warps block on bar.sync (no issue slots)
+    // bulk: every thread issues its rows; tensor: warp 0 issues.  Warp 0 waits
+    // on the mbarrier, the other warps block on bar.sync (no issue slots).
+    if (kBulk)
+      bulk_issue<S, kLabels>(a, b, a.in + vi * a.in_stride,
+                             kLabels ? a.in_lbl + vi * a.in_stride : nullptr, sbase, mbar);
     if (threadIdx.x < 32) {
-      tma_issue<kLabels>(a, b, vi, sbase, mbar);
+      if (!kBulk) tma_issue<kLabels>(a, b, vi, sbase, mbar);
       mbar_wait(mbar, phase);
     }
     phase ^= 1u;
     __syncthreads();
-    if (b[kBFix]) {
+    if (!kBulk && b[kBFix]) {
       tma_fixup<S, kLabels>(a, b, pad);
       __syncthreads();
     }
@@ -1126,7 +1219,7 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
   }
 }
 
-template <class Cfg, bool kLabels, bool kNearest>
+template <class Cfg, bool kBulk, bool kLabels, bool kNearest>
 static cudaError_t launch_tma_variant(const WarpArgs& a, cudaStream_t s) {
   using S = typename Cfg::S;
   const int tiles_x = (a.mx + S::TX - 1) / S::TX, tiles_y = (a.my + S::TY - 1) / S::TY;
@@ -1138,29 +1231,33 @@ static cudaError_t launch_tma_variant(const WarpArgs& a, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(Cfg::CAP) * 5 + 128;  // + alignment slack
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(warp3d_tma_kernel<Cfg, kLabels, kNearest>,
+    const cudaError_t e = cudaFuncSetAttribute(warp3d_tma_kernel<Cfg, kBulk, kLabels, kNearest>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  warp3d_tma_kernel<Cfg, kLabels, kNearest><<<grid, S::THREADS, smem, s>>>(a, tiles_z);
+  warp3d_tma_kernel<Cfg, kBulk, kLabels, kNearest><<<grid, S::THREADS, smem, s>>>(a, tiles_z);
   return cudaGetLastError();
 }
 
-static cudaError_t launch_tma(const WarpArgs& a, cudaStream_t s) {
+template <bool kBulk>
+static cudaError_t launch_tma_kind(const WarpArgs& a, cudaStream_t s) {
   const bool labels = a.in_lbl != nullptr;
   const bool nearest = a.interp == W3D_INTERP_NEAREST;
   cudaError_t e;
   if (labels)
-    e = nearest ? launch_tma_variant<CfgC, true, true>(a, s)
-                : launch_tma_variant<CfgC, true, false>(a, s);
+    e = nearest ? launch_tma_variant<CfgC, kBulk, true, true>(a, s)
+                : launch_tma_variant<CfgC, kBulk, true, false>(a, s);
   else
-    e = nearest ? launch_tma_variant<CfgC, false, true>(a, s)
-                : launch_tma_variant<CfgC, false, false>(a, s);
+    e = nearest ? launch_tma_variant<CfgC, kBulk, false, true>(a, s)
+                : launch_tma_variant<CfgC, kBulk, false, false>(a, s);
   note_launch();
   return e;
 }
+
+cudaError_t launch_tma(const WarpArgs& a, cudaStream_t s) { return launch_tma_kind<false>(a, s); }
+cudaError_t launch_bulk(const WarpArgs& a, cudaStream_t s) { return launch_tma_kind<true>(a, s); }
 
 bool tma_supported(const WarpArgs& a) {
   const bool img_ok = (a.nx % 4 == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0);
@@ -1187,13 +1284,13 @@ cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s) {
   return launch_tiles(a, staged_supported(a), s);
 }
 
-// AUTO: the TMA-staged tile kernel when the tensor maps could be encoded, else
-// the cp.async-staged tile kernel; W3D_PERSISTENT=1 selects the persistent
+// AUTO: the bulk-copy-staged tile kernel when the layout allows 16 B row
+// copies, else the cp.async-staged tile kernel; W3D_PERSISTENT=1 selects the persistent
 // double-buffered kernel (experiment knob).
 cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s) {
   const char* e = getenv("W3D_PERSISTENT");
   if (e && e[0] == '1' && staged_supported(a)) return launch_persistent(a, s);
-  if (a.use_tma) return launch_tma(a, s);
+  if (tma_supported(a)) return launch_bulk(a, s);
   if (!staged_supported(a)) return launch_tiles(a, false, s);
   return launch_tiles(a, true, s);
 }
