@@ -59,12 +59,12 @@ typedef enum {
 
 /* Kernel variant selector for warp3d_affine_batched_ex (tests / benchmarks). */
 typedef enum {
-  W3D_KERNEL_AUTO = 0,     /* library choice: BULK when possible, else STAGED,
-                              else GATHER                                         */
+  W3D_KERNEL_AUTO = 0,     /* library choice: STAGED when the layout allows 16 B
+                              chunks (nx % 4 == 0, aligned input), else GATHER   */
   W3D_KERNEL_GATHER = 1,   /* every corner gathered through L1/L2 (__ldg)        */
   W3D_KERNEL_STAGED = 2,   /* per-tile source footprint staged in shared memory
-                              by cp.async (tiles whose footprint exceeds the
-                              buffer gather instead)                              */
+                              by cp.async; footprints larger than the buffer are
+                              split into 2 / 4 y-parts (gathers beyond that)      */
   W3D_KERNEL_TMA = 3,      /* footprint staged by cp.async.bulk.tensor (TMA
                               tensor boxes), large footprints split into 2 / 4
                               y-parts; needs nx % 4 == 0 (with labels

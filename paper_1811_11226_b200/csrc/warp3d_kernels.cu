@@ -462,18 +462,18 @@ __device__ __forceinline__ void tile_box(const WarpArgs& a, const Params& P, int
   }
 }
 
-// Issue the staging of one box into the buffer at byte offsets (img_off,
-// lbl_off) of g_smem: 16 B chunks (4 voxels); in-volume chunks by cp.async
-// (image 16 B + label 4 B), out-of-volume chunks set to fill / label_fill.
-// nx % 4 == 0 and x0 % 4 == 0, so a chunk is entirely inside or outside in x.
-// Thread t owns chunk column c = t % CW of rows r = t / CW + k (THREADS / CW);
-// rows advance in (y, z) without division.  Completion: cp.async.wait_*.
+// Issue the staging of one box {x0, y0, z0, W, H, D} into the buffer at byte
+// offsets (img_off, lbl_off) of g_smem: 16 B chunks (4 voxels); in-volume
+// chunks by cp.async (image 16 B + label 4 B), out-of-volume chunks set to fill
+// / label_fill.  nx % 4 == 0 and x0 % 4 == 0, so a chunk is entirely inside or
+// outside in x.  Thread t owns chunk column c = t % CW of rows r = t / CW +
+// k (THREADS / CW); rows advance in (y, z) without division; sources are one
+// mad.wide off hoisted 64-bit column bases.  Completion: cp.async.wait_*.
 template <class S, bool kLabels>
 __device__ __forceinline__ void stage_box(const WarpArgs& a, const float* __restrict__ vin,
                                           const uint8_t* __restrict__ lin, const int* box,
                                           uint32_t img_off, uint32_t lbl_off) {
   const int bx = box[0], by = box[1], bz = box[2], W = box[3], H = box[4], D = box[5];
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
   const int CW = W >> 2;
   const int rows_per_pass = S::THREADS / CW;
   const int tid = static_cast<int>(threadIdx.x);
@@ -481,34 +481,36 @@ __device__ __forceinline__ void stage_box(const WarpArgs& a, const float* __rest
   int r = tid / CW;
   if (r >= rows_per_pass) return;
   const int rows = H * D;
-  const int nx = a.nx, ny = a.ny, nz = a.nz;
+  const int nx = a.nx, ny = a.ny, nz = a.nz, plane = nx * ny;
   int rz = r / H, ry = r - rz * H;
   int gy = by + ry, gz = bz + rz;
   const int gx = bx + 4 * c;
   const bool x_in = static_cast<unsigned>(gx) < static_cast<unsigned>(nx);
-  const float* gcol = vin + gx;
-  const uint8_t* lcol = kLabels ? lin + gx : nullptr;
-  int goff = gz * (nx * ny) + gy * nx;
+  float* gcol = const_cast<float*>(vin) + gx;
+  uint8_t* lcol = kLabels ? const_cast<uint8_t*>(lin) + gx : nullptr;
+  uint32_t goff = static_cast<uint32_t>(gz * plane + gy * nx);
   const int step_y = rows_per_pass % H, step_z = rows_per_pass / H;
-  const int goff_step = step_z * (nx * ny) + step_y * nx;
-  const int goff_wrap = nx * ny - H * nx;
-  uint32_t li = static_cast<uint32_t>(r * W + 4 * c);
-  const uint32_t li_step = static_cast<uint32_t>(rows_per_pass * W);
-  const uint32_t simg = sbase + img_off, slbl = sbase + lbl_off;
+  const uint32_t goff_step = static_cast<uint32_t>(step_z * plane + step_y * nx);
+  const uint32_t goff_wrap = static_cast<uint32_t>(plane - H * nx);
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
+  uint32_t si = sbase + img_off + 4u * static_cast<uint32_t>(r * W + 4 * c);
+  uint32_t sl = sbase + lbl_off + static_cast<uint32_t>(r * W + 4 * c);
+  const uint32_t sstep = static_cast<uint32_t>(rows_per_pass * W);
   const float f = a.fill;
   const uint32_t lf4 = a.label_fill * 0x01010101u;
+#pragma unroll 2
   for (; r < rows; r += rows_per_pass) {
     const bool in = x_in & (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
                     (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
     if (in) {
-      cp_async16(simg + 4u * li, gcol + goff);
-      if (kLabels) cp_async4(slbl + li, lcol + goff);
+      cp_async16(si, addr_f32(gcol, goff));
+      if (kLabels) cp_async4(sl, addr_u8(lcol, goff));
     } else {
-      asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};\n" ::"r"(simg + 4u * li), "f"(f)
-                   : "memory");
-      if (kLabels) asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(slbl + li), "r"(lf4) : "memory");
+      asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};\n" ::"r"(si), "f"(f) : "memory");
+      if (kLabels) asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(sl), "r"(lf4) : "memory");
     }
-    li += li_step;
+    si += 4u * sstep;
+    sl += sstep;
     ry += step_y;
     gy += step_y;
     gz += step_z;
@@ -561,13 +563,175 @@ __device__ __forceinline__ void compute_staged(const WarpArgs& a, const Params& 
 // kStage: stage the tile's footprint box; tiles whose box exceeds cap_vox (or
 // kStage = false: the W3D_KERNEL_GATHER variant) gather through L1/L2.
 // ----------------------------------------------------------------------------
+// Box record: image origin x (multiple of 4: TMA needs 16 B aligned inner
+// coordinates), label origin x (multiple of 16), y, z, image / label widths
+// from those origins, H, D, classes, flags, byte sizes, first output row.
+enum { kBx, kBxl, kBy, kBz, kBW, kBWl, kBH, kBD, kBCi, kBCl, kBClamp, kBFix, kBImgBytes,
+       kBLblBytes, kBPart, kBPI, kBRI, kBPL, kBRL, kBNF };  // pitches / rows per plane
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+// Bounded wait: a TMA that never completes traps (a launch error) instead of
+// hanging the device.
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  for (uint32_t tries = 0;; ++tries) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (tries > (1u << 24)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            int z, int v, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(v), "r"(mbar)
+      : "memory");
+}
+
+// Warp 0: boxes of the tile split into nsub y-parts (nsub = 1, 2, 4: the
+// first that fits).  Lanes 8g .. 8g+7 evaluate part g's 8 corners.  Layout
+// modes: kPlanCp (cp.async: image and labels share origin x0 % 4 and pitch),
+// kPlanBulk (1D bulk rows: label origin x0 % 16, own pitch), kPlanTensor
+// (tensor boxes: width classes, 4 / 8-row groups).  Labels follow the image.
+enum { kPlanCp = 0, kPlanBulk = 1, kPlanTensor = 2 };
+template <class S, int kMode>
+__device__ __forceinline__ void tma_plan(const WarpArgs& a, const float* __restrict__ A, int ox,
+                                         int oy, int oz, int capb, bool labels,
+                                         int (*box)[kBNF], int* nsub_out) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
+  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                      static_cast<float>(a.nz)};
+  const bool fill_nz = a.fill != 0.0f, lfill_nz = labels && a.label_fill != 0u;
+  constexpr int kMaxSub = S::TY / 4 < 4 ? S::TY / 4 : 4;  // parts keep whole Philox blocks
+  for (int nsub = 1; nsub <= kMaxSub; nsub <<= 1) {
+    const int rows = S::TY / nsub;
+    const int y0 = oy + min(g, nsub - 1) * rows;
+    const bool empty = y0 >= a.my;
+    const float X = static_cast<float>((c & 1) ? min(ox + S::TX, a.mx) - 1 : ox);
+    const float Y = static_cast<float>((c & 2) ? min(y0 + rows, a.my) - 1 : min(y0, a.my - 1));
+    const float Z = static_cast<float>((c & 4) ? min(oz + S::TZ, a.mz) - 1 : oz);
+    float mn[3], mxv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float p = __fmaf_rn(A[4 * k], X, __fmaf_rn(A[4 * k + 1], Y,
+                                                       __fmaf_rn(A[4 * k + 2], Z, A[4 * k + 3])));
+      mn[k] = p;
+      mxv[k] = p;
+    }
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+        mxv[k] = fmaxf(mxv[k], __shfl_xor_sync(0xffffffffu, mxv[k], off));
+      }
+    int lo[3], hi[3];
+    bool inside = true, touches = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = static_cast<int>(floorf(fminf(fmaxf(mn[k], -1.0f), n[k])));
+      hi[k] = static_cast<int>(floorf(fminf(fmaxf(mxv[k], -1.0f), n[k]))) + 1;
+      inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
+      touches |= (lo[k] < 0) | (hi[k] >= static_cast<int>(n[k]));
+    }
+    const int bxi = lo[0] & ~3, bxl = lo[0] & ~15;  // floor to 4 / 16 (lo >= -1)
+    const int W = hi[0] - bxi + 1, Wl = hi[0] - bxl + 1;
+    const int H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
+    int ci = -1, cl = -1, PI, RI, PL, RL;
+    if (kMode == kPlanCp) {  // cp.async chunks: one index space for image and labels
+      ci = cl = 0;
+      PI = (W + 3) & ~3; RI = H;
+      PL = PI; RL = H;
+    } else if (kMode == kPlanBulk) {  // 1D bulk row copies: 16 B granularity only
+      ci = cl = 0;
+      PI = (W + 3) & ~3; RI = H;
+      PL = (Wl + 15) & ~15; RL = H;
+    } else {      // tensor boxes: width classes, 4 / 8-row groups
+#pragma unroll
+      for (int q = kNumImgCls - 1; q >= 0; --q)
+        if (img_cls_width(q) >= W) ci = q;
+#pragma unroll
+      for (int q = kNumLblCls - 1; q >= 0; --q)
+        if (lbl_cls_width(q) >= Wl) cl = q;
+      PI = ci < 0 ? 0 : img_cls_width(ci); RI = (H + 3) & ~3;
+      PL = cl < 0 ? 0 : lbl_cls_width(cl); RL = (H + 7) & ~7;
+    }
+    const int64_t bimg = static_cast<int64_t>(D) * RI * PI * 4;
+    const int64_t blbl = labels ? static_cast<int64_t>(D) * RL * PL : 0;
+    const bool fits = empty || (ci >= 0 && (!labels || cl >= 0) && bimg + blbl <= capb);
+    const bool all_fit = __all_sync(0xffffffffu, (g >= nsub) || fits);
+    if (all_fit) {
+      if (c == 0 && g < nsub) {
+        int* b = box[g];
+        b[kBx] = bxi; b[kBxl] = kMode == kPlanCp ? bxi : bxl; b[kBy] = lo[1]; b[kBz] = lo[2];
+        b[kBW] = W; b[kBWl] = Wl; b[kBH] = H; b[kBD] = empty ? 0 : D;
+        b[kBCi] = ci; b[kBCl] = cl;
+        b[kBClamp] = inside ? 0 : 1;
+        b[kBFix] = touches ? ((fill_nz ? 1 : 0) | (lfill_nz ? 2 : 0)) : 0;
+        b[kBImgBytes] = static_cast<int>(bimg);
+        b[kBLblBytes] = static_cast<int>(blbl);
+        b[kBPart] = y0;
+        b[kBPI] = PI; b[kBRI] = RI; b[kBPL] = PL; b[kBRL] = RL;
+      }
+      if (lane == 0) *nsub_out = nsub;
+      return;
+    }
+  }
+  if (lane == 0) *nsub_out = 0;
+}
+
+template <class Cfg, bool kStage, bool kLabels, bool kNearest>
+__global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
+    warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap_vox);
+
+// cp.async-staged part of a tile: stage the part's box, wait, compute its rows.
+template <int NR, bool kLabels, bool kNearest>
+__device__ __forceinline__ void cp_part_compute(const WarpArgs& a, const Params& P, float* vout,
+                                                uint8_t* lout, const int* box6, int lbl_off,
+                                                bool clamp, int X, int Z, int ybeg) {
+  const Stage sv = make_stage(a, box6, 0, lbl_off);
+  if (clamp)
+    column_rows<NR, true, kLabels, kNearest, true, false>(a, P, nullptr, nullptr, vout, lout, sv,
+                                                          X, Z, ybeg);
+  else
+    column_rows<NR, true, kLabels, kNearest, false, false>(a, P, nullptr, nullptr, vout, lout,
+                                                           sv, X, Z, ybeg);
+}
+
 template <class Cfg, bool kStage, bool kLabels, bool kNearest>
 __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
     warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap_vox) {
   using S = typename Cfg::S;
-  __shared__ int s_box[8];
+  __shared__ int s_box[4][kBNF];
+  __shared__ int s_nsub;
   const int vi = static_cast<int>(blockIdx.z) / tiles_z;
-  const Params P = load_params(a.vol[vi]);
   const int ox = static_cast<int>(blockIdx.x) * S::TX;
   const int oy = static_cast<int>(blockIdx.y) * S::TY;
   const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * S::TZ;
@@ -575,27 +739,47 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
   const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
   float* __restrict__ vout = a.out + vi * a.out_stride;
   uint8_t* __restrict__ lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
-  Stage sv;
-  if (!kStage) {
+  if (kStage) {
+    // plan (warp 0): whole-tile box, or 2 / 4 y-parts when it exceeds the buffer
+    if (threadIdx.x < 32)
+      tma_plan<S, kPlanCp>(a, a.vol[vi].A, ox, oy, oz, cap_vox * 5, kLabels, s_box, &s_nsub);
+    __syncthreads();
+  }
+  const int nsub = kStage ? s_nsub : 0;
+  if (nsub == 0 || (S::WARPS != S::TZ)) {  // gather variant, or nothing fits
     count_tile(false);
+    const Params P = load_params(a.vol[vi]);
+    Stage sv;
     tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
     return;
   }
-  if (threadIdx.x < 32) tile_box<S>(a, P, ox, oy, oz, cap_vox, s_box);
-  __syncthreads();
-  int box[8];
+  count_tile(true);
+  const int X = ox + static_cast<int>(threadIdx.x & 31);
+  const int Z = oz + static_cast<int>(threadIdx.x >> 5);
+  for (int k = 0; k < nsub; ++k) {
+    int b[kBNF];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) box[i] = s_box[i];
-  count_tile(box[6] != 0);
-  if (!box[6]) {
-    tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
-    return;
+    for (int i = 0; i < kBNF; ++i) b[i] = s_box[k][i];
+    if (b[kBD] == 0) continue;  // part entirely beyond the volume's last row
+    const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
+    stage_box<S, kLabels>(a, vin, lin, box6, 0u, static_cast<uint32_t>(b[kBImgBytes]));
+    cp_async_wait_all();
+    __syncthreads();
+    const Params P = load_params(a.vol[vi]);  // after staging: keeps the loop's registers free
+    if (nsub == 1) {
+      cp_part_compute<S::TY, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
+                                                b[kBClamp] != 0, X, Z, b[kBPart]);
+    } else if (nsub == 2) {
+      if constexpr (S::TY / 2 >= 4)
+        cp_part_compute<S::TY / 2, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
+                                                      b[kBClamp] != 0, X, Z, b[kBPart]);
+    } else {
+      if constexpr (S::TY / 4 >= 4)
+        cp_part_compute<S::TY / 4, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
+                                                      b[kBClamp] != 0, X, Z, b[kBPart]);
+    }
+    if (k + 1 < nsub) __syncthreads();  // buffer reuse by the next part
   }
-  stage_box<S, kLabels>(a, vin, lin, box, 0u, static_cast<uint32_t>(cap_vox) * 4u);
-  cp_async_wait_all();
-  __syncthreads();
-  compute_staged<S, kLabels, kNearest>(a, P, vin, lin, vout, lout, box, 0, cap_vox * 4, ox, oy,
-                                       oz);
 }
 
 // ----------------------------------------------------------------------------
@@ -827,141 +1011,6 @@ static cudaError_t launch_persistent(const WarpArgs& a, cudaStream_t s) {
 // Boundary boxes with a nonzero fill / label_fill get their out-of-volume
 // elements overwritten before compute (R6, R8).
 // ----------------------------------------------------------------------------
-// Box record: image origin x (multiple of 4: TMA needs 16 B aligned inner
-// coordinates), label origin x (multiple of 16), y, z, image / label widths
-// from those origins, H, D, classes, flags, byte sizes, first output row.
-enum { kBx, kBxl, kBy, kBz, kBW, kBWl, kBH, kBD, kBCi, kBCl, kBClamp, kBFix, kBImgBytes,
-       kBLblBytes, kBPart, kBPI, kBRI, kBPL, kBRL, kBNF };  // pitches / rows per plane
-
-__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes)
-               : "memory");
-}
-// Bounded wait: a TMA that never completes traps (a launch error) instead of
-// hanging the device.
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
-  for (uint32_t tries = 0;; ++tries) {
-    uint32_t done;
-    asm volatile(
-        "{\n .reg .pred P1;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, P1;\n}\n"
-        : "=r"(done)
-        : "r"(mbar), "r"(phase)
-        : "memory");
-    if (done) return;
-    if (tries > (1u << 24)) __trap();
-  }
-}
-__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mbar) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t mbar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-      ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int x, int y,
-                                            int z, int v, uint32_t mbar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(v), "r"(mbar)
-      : "memory");
-}
-
-// Warp 0: boxes of the tile split into nsub y-parts (nsub = 1, 2, 4: the
-// first that fits).  Lanes 8g .. 8g+7 evaluate part g's 8 corners.
-template <class S, bool kBulk>
-__device__ __forceinline__ void tma_plan(const WarpArgs& a, const Params& P, int ox, int oy,
-                                         int oz, int capb, bool labels, int (*box)[kBNF],
-                                         int* nsub_out) {
-  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
-  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
-                      static_cast<float>(a.nz)};
-  const bool fill_nz = a.fill != 0.0f, lfill_nz = labels && a.label_fill != 0u;
-  for (int nsub = 1; nsub <= 4; nsub <<= 1) {
-    const int rows = S::TY / nsub;
-    const int y0 = oy + min(g, nsub - 1) * rows;
-    const bool empty = y0 >= a.my;
-    const float X = static_cast<float>((c & 1) ? min(ox + S::TX, a.mx) - 1 : ox);
-    const float Y = static_cast<float>((c & 2) ? min(y0 + rows, a.my) - 1 : min(y0, a.my - 1));
-    const float Z = static_cast<float>((c & 4) ? min(oz + S::TZ, a.mz) - 1 : oz);
-    float mn[3], mxv[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float p = __fmaf_rn(P.A[4 * k], X, __fmaf_rn(P.A[4 * k + 1], Y,
-                                                         __fmaf_rn(P.A[4 * k + 2], Z, P.A[4 * k + 3])));
-      mn[k] = p;
-      mxv[k] = p;
-    }
-#pragma unroll
-    for (int off = 1; off < 8; off <<= 1)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
-        mxv[k] = fmaxf(mxv[k], __shfl_xor_sync(0xffffffffu, mxv[k], off));
-      }
-    int lo[3], hi[3];
-    bool inside = true, touches = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      lo[k] = static_cast<int>(floorf(fminf(fmaxf(mn[k], -1.0f), n[k])));
-      hi[k] = static_cast<int>(floorf(fminf(fmaxf(mxv[k], -1.0f), n[k]))) + 1;
-      inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
-      touches |= (lo[k] < 0) | (hi[k] >= static_cast<int>(n[k]));
-    }
-    const int bxi = lo[0] & ~3, bxl = lo[0] & ~15;  // floor to 4 / 16 (lo >= -1)
-    const int W = hi[0] - bxi + 1, Wl = hi[0] - bxl + 1;
-    const int H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
-    int ci = -1, cl = -1, PI, RI, PL, RL;
-    if (kBulk) {  // 1D bulk row copies: 16 B granularity only
-      ci = cl = 0;
-      PI = (W + 3) & ~3; RI = H;
-      PL = (Wl + 15) & ~15; RL = H;
-    } else {      // tensor boxes: width classes, 4 / 8-row groups
-#pragma unroll
-      for (int q = kNumImgCls - 1; q >= 0; --q)
-        if (img_cls_width(q) >= W) ci = q;
-#pragma unroll
-      for (int q = kNumLblCls - 1; q >= 0; --q)
-        if (lbl_cls_width(q) >= Wl) cl = q;
-      PI = ci < 0 ? 0 : img_cls_width(ci); RI = (H + 3) & ~3;
-      PL = cl < 0 ? 0 : lbl_cls_width(cl); RL = (H + 7) & ~7;
-    }
-    const int64_t bimg = static_cast<int64_t>(D) * RI * PI * 4;
-    const int64_t blbl = labels ? static_cast<int64_t>(D) * RL * PL : 0;
-    const bool fits = empty || (ci >= 0 && (!labels || cl >= 0) && bimg + blbl <= capb);
-    const bool all_fit = __all_sync(0xffffffffu, (g >= nsub) || fits);
-    if (all_fit) {
-      if (c == 0 && g < nsub) {
-        int* b = box[g];
-        b[kBx] = bxi; b[kBxl] = bxl; b[kBy] = lo[1]; b[kBz] = lo[2];
-        b[kBW] = W; b[kBWl] = Wl; b[kBH] = H; b[kBD] = empty ? 0 : D;
-        b[kBCi] = ci; b[kBCl] = cl;
-        b[kBClamp] = inside ? 0 : 1;
-        b[kBFix] = touches ? ((fill_nz ? 1 : 0) | (lfill_nz ? 2 : 0)) : 0;
-        b[kBImgBytes] = static_cast<int>(bimg);
-        b[kBLblBytes] = static_cast<int>(blbl);
-        b[kBPart] = y0;
-        b[kBPI] = PI; b[kBRI] = RI; b[kBPL] = PL; b[kBRL] = RL;
-      }
-      if (lane == 0) *nsub_out = nsub;
-      return;
-    }
-  }
-  if (lane == 0) *nsub_out = 0;
-}
-
 template <bool kLabels>
 __device__ __forceinline__ void tma_issue(const WarpArgs& a, const int* b, int vi, uint32_t sbase,
                                           uint32_t mbar) {
@@ -1173,7 +1222,8 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
       mbar_init(mbar, kBulk ? S::THREADS : 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    tma_plan<S, kBulk>(a, P, ox, oy, oz, Cfg::CAP * 5, kLabels, s_box, &s_nsub);
+    tma_plan<S, kBulk ? kPlanBulk : kPlanTensor>(a, a.vol[vi].A, ox, oy, oz, Cfg::CAP * 5,
+                                                 kLabels, s_box, &s_nsub);
   }
   __syncthreads();
   const int nsub = s_nsub;
@@ -1284,15 +1334,14 @@ cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s) {
   return launch_tiles(a, staged_supported(a), s);
 }
 
-// AUTO: the bulk-copy-staged tile kernel when the layout allows 16 B row
-// copies, else the cp.async-staged tile kernel; W3D_PERSISTENT=1 selects the persistent
+// AUTO: the cp.async-staged tile kernel (measured faster than the bulk / tensor
+// TMA variants on ~200 B footprint rows), else gathers when the
+// layout does not allow 16 B chunks.  W3D_PERSISTENT=1 selects the persistent
 // double-buffered kernel (experiment knob).
 cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s) {
   const char* e = getenv("W3D_PERSISTENT");
   if (e && e[0] == '1' && staged_supported(a)) return launch_persistent(a, s);
-  if (tma_supported(a)) return launch_bulk(a, s);
-  if (!staged_supported(a)) return launch_tiles(a, false, s);
-  return launch_tiles(a, true, s);
+  return launch_tiles(a, staged_supported(a), s);
 }
 
 // ----------------------------------------------------------------------------
