@@ -362,37 +362,47 @@ __device__ __forceinline__ void column_occluded(const WarpArgs& a, const Params&
 // y-pairs with FFMA2/FADD2.  The coordinate keeps the R4 nesting
 // p = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b))).
 // ----------------------------------------------------------------------------
+// Standard normals of NR rows (NR/4 Philox blocks, independent chains).
+template <int NR>
+__device__ __forceinline__ void column_noise(const WarpArgs& a, const Params& P, int X, int Z,
+                                             int ybeg, float* n) {
+#pragma unroll
+  for (int i = 0; i < NR; ++i) n[i] = 0.0f;
+  if (!(P.flags & kNoise)) return;
+  const int Gy = (a.my + 3) >> 2;
+  const uint32_t q0 = static_cast<uint32_t>(X) +
+                      static_cast<uint32_t>(a.mx) * static_cast<uint32_t>(Gy * Z + (ybeg >> 2));
+  uint4 r[NR / 4];
+#pragma unroll
+  for (int g = 0; g < NR / 4; ++g)
+    r[g] = philox4x32_10_rk(make_uint4(q0 + static_cast<uint32_t>(g * a.mx), 0u, P.vid0, P.vid1),
+                            P.rk0, P.rk1);
+#pragma unroll
+  for (int g = 0; g < NR / 4; ++g) {
+    const float2 u = box_muller(r[g].x, r[g].y), v = box_muller(r[g].z, r[g].w);
+    n[4 * g] = u.x; n[4 * g + 1] = u.y; n[4 * g + 2] = v.x; n[4 * g + 3] = v.y;
+  }
+}
+
+__device__ __forceinline__ bool column_occluded_z(const Params& P, int Z) {
+  return (P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;  // warp-uniform
+}
+
+// NR rows of one column whose noise n[] is already computed.
 template <int NR, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp, bool kSepLbl>
-__device__ __forceinline__ void column_rows(const WarpArgs& a, const Params& P,
-                                            const float* __restrict__ vin,
-                                            const uint8_t* __restrict__ lin,
-                                            float* __restrict__ vout, uint8_t* __restrict__ lout,
-                                            const Stage& sv, int X, int Z, int ybeg) {
-  const int mx = a.mx, my = a.my;
-  if (X >= mx || Z >= a.mz || ybeg >= my) return;
+__device__ __forceinline__ void column_rows_n(const WarpArgs& a, const Params& P,
+                                              const float* __restrict__ vin,
+                                              const uint8_t* __restrict__ lin,
+                                              float* __restrict__ vout,
+                                              uint8_t* __restrict__ lout, const Stage& sv, int X,
+                                              int Z, int ybeg, const float* n) {
+  const int my = a.my;
+  if (X >= a.mx || Z >= a.mz || ybeg >= my) return;
   const int yend = min(ybeg + NR, my);
-  if ((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi) {  // warp-uniform
+  if (column_occluded_z(P, Z)) {
     column_occluded<kStagedPath, kLabels, kClamp, kSepLbl>(a, P, lin, vout, lout, sv, X, Z, ybeg,
                                                            yend);
     return;
-  }
-  float n[NR];
-#pragma unroll
-  for (int i = 0; i < NR; ++i) n[i] = 0.0f;
-  if (P.flags & kNoise) {
-    const int Gy = (my + 3) >> 2;
-    const uint32_t q0 = static_cast<uint32_t>(X) +
-                        static_cast<uint32_t>(mx) * static_cast<uint32_t>(Gy * Z + (ybeg >> 2));
-    uint4 r[NR / 4];
-#pragma unroll
-    for (int g = 0; g < NR / 4; ++g)
-      r[g] = philox4x32_10_rk(make_uint4(q0 + static_cast<uint32_t>(g * mx), 0u, P.vid0, P.vid1),
-                              P.rk0, P.rk1);
-#pragma unroll
-    for (int g = 0; g < NR / 4; ++g) {
-      const float2 u = box_muller(r[g].x, r[g].y), v = box_muller(r[g].z, r[g].w);
-      n[4 * g] = u.x; n[4 * g + 1] = u.y; n[4 * g + 2] = v.x; n[4 * g + 3] = v.y;
-    }
   }
   if (yend - ybeg == NR)
     column_pairs<NR, kStagedPath, kLabels, kNearest, kClamp, kSepLbl, true>(
@@ -400,6 +410,27 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const Params& P,
   else
     column_pairs<NR, kStagedPath, kLabels, kNearest, kClamp, kSepLbl, false>(
         a, P, vin, lin, vout, lout, sv, X, Z, ybeg, yend, n);
+}
+
+// NR rows [ybeg, ybeg + NR) of one output column, in groups of 8 rows (two
+// interleaved Philox chains per group; the group loop is not unrolled to keep
+// the hot code inside the instruction cache).
+template <int NR, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp, bool kSepLbl>
+__device__ __forceinline__ void column_rows(const WarpArgs& a, const Params& P,
+                                            const float* __restrict__ vin,
+                                            const uint8_t* __restrict__ lin,
+                                            float* __restrict__ vout, uint8_t* __restrict__ lout,
+                                            const Stage& sv, int X, int Z, int ybeg) {
+  constexpr int G = NR < 8 ? NR : 8;
+  const bool occl = column_occluded_z(P, Z);
+#pragma unroll 1
+  for (int y = ybeg; y < ybeg + NR; y += G) {
+    float n[G];
+    if (!occl && X < a.mx && Z < a.mz && y < a.my)
+      column_noise<G>(a, P, X, Z, y, n);
+    column_rows_n<G, kStagedPath, kLabels, kNearest, kClamp, kSepLbl>(a, P, vin, lin, vout, lout,
+                                                                      sv, X, Z, y, n);
+  }
 }
 
 template <class S, bool kStagedPath, bool kLabels, bool kNearest, bool kClamp>
@@ -756,6 +787,29 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
   count_tile(true);
   const int X = ox + static_cast<int>(threadIdx.x & 31);
   const int Z = oz + static_cast<int>(threadIdx.x >> 5);
+  if (nsub == 1) {
+    // whole tile: issue the staging, compute the column's noise (independent of
+    // the box) while the copies are in flight, then wait and sample
+    int b[kBNF];
+#pragma unroll
+    for (int i = 0; i < kBNF; ++i) b[i] = s_box[0][i];
+    const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
+    stage_box<S, kLabels>(a, vin, lin, box6, 0u, static_cast<uint32_t>(b[kBImgBytes]));
+    const Params P = load_params(a.vol[vi]);
+    const bool live = X < a.mx && Z < a.mz && oy < a.my && !column_occluded_z(P, Z);
+    float n[S::TY];
+    if (live) column_noise<S::TY>(a, P, X, Z, oy, n);
+    cp_async_wait_all();
+    __syncthreads();
+    const Stage sv = make_stage(a, box6, 0, b[kBImgBytes]);
+    if (b[kBClamp])
+      column_rows_n<S::TY, true, kLabels, kNearest, true, false>(a, P, nullptr, nullptr, vout,
+                                                                 lout, sv, X, Z, oy, n);
+    else
+      column_rows_n<S::TY, true, kLabels, kNearest, false, false>(a, P, nullptr, nullptr, vout,
+                                                                  lout, sv, X, Z, oy, n);
+    return;
+  }
   for (int k = 0; k < nsub; ++k) {
     int b[kBNF];
 #pragma unroll
