@@ -500,27 +500,35 @@ __device__ __forceinline__ void tile_box(const WarpArgs& a, const Params& P, int
 // outside in x.  Thread t owns chunk column c = t % CW of rows r = t / CW +
 // k (THREADS / CW); rows advance in (y, z) without division; sources are one
 // mad.wide off hoisted 64-bit column bases.  Completion: cp.async.wait_*.
-template <class S, bool kLabels>
-__device__ __forceinline__ void stage_box(const WarpArgs& a, const float* __restrict__ vin,
-                                          const uint8_t* __restrict__ lin, const int* box,
-                                          uint32_t img_off, uint32_t lbl_off) {
+// q = floor(i / d) for 0 <= i < 2^20, 1 <= d < 2^12: the rounded reciprocal
+// quotient is within 2^-21 relative of (i + 0.5) / d, whose distance to an
+// integer is >= 0.5 / d, so truncation is exact.
+__device__ __forceinline__ int div_small(int i, float inv_d) {
+  return __float2int_rz((static_cast<float>(i) + 0.5f) * inv_d);
+}
+
+template <class S, bool kLabels, bool kInside>
+__device__ __forceinline__ void stage_box_impl(const WarpArgs& a, const float* __restrict__ vin,
+                                               const uint8_t* __restrict__ lin, const int* box,
+                                               uint32_t img_off, uint32_t lbl_off) {
   const int bx = box[0], by = box[1], bz = box[2], W = box[3], H = box[4], D = box[5];
   const int CW = W >> 2;
   const int rows_per_pass = S::THREADS / CW;
   const int tid = static_cast<int>(threadIdx.x);
-  const int c = tid % CW;
-  int r = tid / CW;
+  int r = div_small(tid, __frcp_rn(static_cast<float>(CW)));
+  const int c = tid - r * CW;
   if (r >= rows_per_pass) return;
   const int rows = H * D;
   const int nx = a.nx, ny = a.ny, nz = a.nz, plane = nx * ny;
-  int rz = r / H, ry = r - rz * H;
+  const float inv_h = __frcp_rn(static_cast<float>(H));
+  int rz = div_small(r, inv_h), ry = r - rz * H;
   int gy = by + ry, gz = bz + rz;
   const int gx = bx + 4 * c;
   const bool x_in = static_cast<unsigned>(gx) < static_cast<unsigned>(nx);
   float* gcol = const_cast<float*>(vin) + gx;
   uint8_t* lcol = kLabels ? const_cast<uint8_t*>(lin) + gx : nullptr;
   uint32_t goff = static_cast<uint32_t>(gz * plane + gy * nx);
-  const int step_y = rows_per_pass % H, step_z = rows_per_pass / H;
+  const int step_z = div_small(rows_per_pass, inv_h), step_y = rows_per_pass - step_z * H;
   const uint32_t goff_step = static_cast<uint32_t>(step_z * plane + step_y * nx);
   const uint32_t goff_wrap = static_cast<uint32_t>(plane - H * nx);
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(g_smem));
@@ -531,28 +539,55 @@ __device__ __forceinline__ void stage_box(const WarpArgs& a, const float* __rest
   const uint32_t lf4 = a.label_fill * 0x01010101u;
 #pragma unroll 2
   for (; r < rows; r += rows_per_pass) {
-    const bool in = x_in & (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
-                    (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
-    if (in) {
+    if (kInside) {
       cp_async16(si, addr_f32(gcol, goff));
       if (kLabels) cp_async4(sl, addr_u8(lcol, goff));
     } else {
-      asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};\n" ::"r"(si), "f"(f) : "memory");
-      if (kLabels) asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(sl), "r"(lf4) : "memory");
+      const bool in = x_in & (static_cast<unsigned>(gy) < static_cast<unsigned>(ny)) &
+                      (static_cast<unsigned>(gz) < static_cast<unsigned>(nz));
+      if (in) {
+        cp_async16(si, addr_f32(gcol, goff));
+        if (kLabels) cp_async4(sl, addr_u8(lcol, goff));
+      } else {
+        asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};\n" ::"r"(si), "f"(f) : "memory");
+        if (kLabels) asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(sl), "r"(lf4) : "memory");
+      }
+      gy += step_y;
+      gz += step_z;
     }
     si += 4u * sstep;
     sl += sstep;
     ry += step_y;
-    gy += step_y;
-    gz += step_z;
     goff += goff_step;
     if (ry >= H) {
       ry -= H;
-      gy -= H;
-      ++gz;
       goff += goff_wrap;
+      if (!kInside) {
+        gy -= H;
+        ++gz;
+      }
     }
   }
+}
+
+// Issue the staging of one box {x0, y0, z0, W, H, D} into the buffer at byte
+// offsets (img_off, lbl_off) of g_smem: 16 B chunks (4 voxels); in-volume
+// chunks by cp.async (image 16 B + label 4 B), out-of-volume chunks set to fill
+// / label_fill.  nx % 4 == 0 and x0 % 4 == 0, so a chunk is entirely inside or
+// outside in x.  Thread t owns chunk column c = t % CW of rows r = t / CW +
+// k (THREADS / CW); rows advance in (y, z) without division; sources are one
+// mad.wide off hoisted 64-bit column bases.  Boxes inside the volume skip the
+// per-chunk bounds test.  Completion: cp.async.wait_*.
+template <class S, bool kLabels>
+__device__ __forceinline__ void stage_box(const WarpArgs& a, const float* __restrict__ vin,
+                                          const uint8_t* __restrict__ lin, const int* box,
+                                          uint32_t img_off, uint32_t lbl_off) {
+  const bool inside = box[0] >= 0 && box[1] >= 0 && box[2] >= 0 && box[0] + box[3] <= a.nx &&
+                      box[1] + box[4] <= a.ny && box[2] + box[5] <= a.nz;
+  if (inside)
+    stage_box_impl<S, kLabels, true>(a, vin, lin, box, img_off, lbl_off);
+  else
+    stage_box_impl<S, kLabels, false>(a, vin, lin, box, img_off, lbl_off);
 }
 
 __device__ __forceinline__ Stage make_stage(const WarpArgs& a, const int* box, int img_off,
