@@ -74,10 +74,8 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // (absolute error ~2^-20.5; the angle itself is rounded once).  Worst case |n_gpu - n| < 1e-5, i.e. < 2e-4 HU
 // at sigma = 20 HU, inside the 1e-3 HU image tolerance.
 __device__ __forceinline__ float2 box_muller(uint32_t ua, uint32_t ub) {
-  // u1 = k 2^-23 + 2^-24 (exact): the float with mantissa k is 1 + k 2^-23, and
-  // subtracting 1 - 2^-24 is exact (no int->float conversion on the XU pipe).
-  // angle = pi s = j (pi 2^-23) - pi (one rounding)
-  const float u1 = __int_as_float(0x3F800000 | (ua >> 9)) - 0.99999994039535522f;
+  // u1 = k 2^-23 + 2^-24 (exact), angle = pi s = j (pi 2^-23) - pi (one rounding)
+  const float u1 = __fmaf_rn(__uint2float_rn(ua >> 9), 0x1.0p-23f, 0x1.0p-24f);
   const float angle = __fmaf_rn(__uint2float_rn(ub >> 8), 3.14159265358979f * 0x1.0p-23f,
                                 -3.14159274f);
   const float t = 1.0f - u1;  // exact wherever the series is used (u1 > 1/2)

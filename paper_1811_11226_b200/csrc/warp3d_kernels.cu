@@ -173,18 +173,14 @@ __device__ __forceinline__ void sample_staged2(const Stage& v, float2 px, float2
     py = make_float2(fminf(fmaxf(py.x, -1.0f), v.ny), fminf(fmaxf(py.y, -1.0f), v.ny));
     pz = make_float2(fminf(fmaxf(pz.x, -1.0f), v.nz), fminf(fmaxf(pz.y, -1.0f), v.nz));
   }
-  // floor on the FMA pipe (no FRND / F2I on the quarter-rate XU pipe): for
-  // |p| < 2^22, p + M with M = 1.5 * 2^23 rounded toward -inf is floor(p) + M
-  // exactly, and every later index term stays an exact integer below 2^24, so
-  // the index is read back from the float's bits.
-  const float2 M = f2(12582912.0f);
-  const float2 fxm = __fadd2_rd(px, M), fym = __fadd2_rd(py, M), fzm = __fadd2_rd(pz, M);
-  const float2 fx = sub2(fxm, M), fy = sub2(fym, M), fz = sub2(fzm, M);
+  const float2 fx = make_float2(floorf(px.x), floorf(px.y));
+  const float2 fy = make_float2(floorf(py.x), floorf(py.y));
+  const float2 fz = make_float2(floorf(pz.x), floorf(pz.y));
   const float2 tx = sub2(px, fx), ty = sub2(py, fy), tz = sub2(pz, fz);
-  // local element index + M: all terms are exact small integers
-  const float2 rx = sub2(fxm, f2(v.bx)), ry = sub2(fy, f2(v.by)), rz = sub2(fz, f2(v.bz));
+  // local element index: all terms are small integers, exact in fp32
+  const float2 rx = sub2(fx, f2(v.bx)), ry = sub2(fy, f2(v.by)), rz = sub2(fz, f2(v.bz));
   const float2 lf = __ffma2_rn(rz, f2(v.HWf), __ffma2_rn(ry, f2(v.Wf), rx));
-  const int li0 = __float_as_int(lf.x) - 0x4B400000, li1 = __float_as_int(lf.y) - 0x4B400000;
+  const int li0 = __float2int_rz(lf.x), li1 = __float2int_rz(lf.y);
   int ln0 = 0, ln1 = 0;
   if (kNearest || (kLabels && !kSepLbl)) {
     ln0 = li0 + (tx.x >= 0.5f ? 1 : 0) + (ty.x >= 0.5f ? v.W : 0) + (tz.x >= 0.5f ? v.HW : 0);
@@ -193,7 +189,7 @@ __device__ __forceinline__ void sample_staged2(const Stage& v, float2 px, float2
   if (kLabels) {
     if (kSepLbl) {  // label box with its own pitches (TMA layout)
       const float2 lfl = __ffma2_rn(rz, f2(v.HWLf), __ffma2_rn(ry, f2(v.WLf), rx));
-      const int m0 = __float_as_int(lfl.x) - 0x4B400000, m1 = __float_as_int(lfl.y) - 0x4B400000;
+      const int m0 = __float2int_rz(lfl.x), m1 = __float2int_rz(lfl.y);
       l0 = slbl[m0 + (tx.x >= 0.5f ? 1 : 0) + (ty.x >= 0.5f ? v.WL : 0) +
                 (tz.x >= 0.5f ? v.HWL : 0)];
       l1 = slbl[m1 + (tx.y >= 0.5f ? 1 : 0) + (ty.y >= 0.5f ? v.WL : 0) +
@@ -293,7 +289,6 @@ __device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
   const float2 cz2 = f2(__fmaf_rn(P.A[10], fZ, P.A[11]));
   // output offsets are 32-bit within a volume (< 2^31 voxels)
   const uint32_t o0 = static_cast<uint32_t>((Z * a.my + ybeg) * mx + X);
-  const float fY0 = static_cast<float>(ybeg);
 #pragma unroll
   for (int j = 0; j < NR / 2; ++j) {
     const int Ya = ybeg + 2 * j;
@@ -302,9 +297,7 @@ __device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
       if (Ya >= yend) break;
       second = Ya + 1 < yend;
     }
-    // row coordinates from one conversion per column (exact small integers)
-    const float fa = fY0 + static_cast<float>(2 * j);
-    const float2 fY = make_float2(fa, second ? fa + 1.0f : fa);
+    const float2 fY = make_float2(static_cast<float>(Ya), static_cast<float>(second ? Ya + 1 : Ya));
     const float2 px = __ffma2_rn(f2(P.A[0]), f2(fX), __ffma2_rn(f2(P.A[1]), fY, cz0));
     const float2 py = __ffma2_rn(f2(P.A[4]), f2(fX), __ffma2_rn(f2(P.A[5]), fY, cz1));
     const float2 pz = __ffma2_rn(f2(P.A[8]), f2(fX), __ffma2_rn(f2(P.A[9]), fY, cz2));
