@@ -399,23 +399,19 @@ def main():
 
 
 def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch, nvox_out):
+    """End to end through the library's FIFO host pipeline (warp3d_pipeline_run,
+    PAPER.md:379-387): pinned host inputs -> H2D -> warp -> D2H into pinned host
+    outputs, every step inside the timed region."""
     import torch.distributed as dist
     B = imgs.shape[0]
     h_img = torch.from_numpy(imgs).pin_memory()
     h_lbl = torch.from_numpy(lbls).pin_memory()
     h_out = torch.empty((B, *shape), dtype=torch.float32).pin_memory()
     h_out_l = torch.empty((B, *shape), dtype=torch.uint8).pin_memory()
-    d_img = torch.empty_like(h_img, device=dev)
-    d_lbl = torch.empty_like(h_lbl, device=dev)
-    d_out = torch.empty((B, *shape), dtype=torch.float32, device=dev)
-    d_out_l = torch.empty((B, *shape), dtype=torch.uint8, device=dev)
+    pipe = W.Pipeline(shape, shape, depth=3, labels=True)
 
     def step():
-        d_img.copy_(h_img, non_blocking=True)
-        d_lbl.copy_(h_lbl, non_blocking=True)
-        W.warp3d_affine_batched(d_img, d_lbl, params, fill=-1000.0, out=d_out, out_labels=d_out_l)
-        h_out.copy_(d_out, non_blocking=True)
-        h_out_l.copy_(d_out_l, non_blocking=True)
+        pipe.run(h_img, h_lbl, params, h_out, h_out_l, fill=-1000.0)
 
     for _ in range(2):
         step()
@@ -429,11 +425,12 @@ def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch
     e.record()
     torch.cuda.synchronize(dev)
     ms = reduce_max_ms(s.elapsed_time(e), dist if world > 1 else None, dev)
+    pipe.close()
     value = global_batch * nvox_out * steps / (ms * 1e-3) / 1e9
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(B * nvox_out * 5),
             "d2h_bytes_per_step": int(B * nvox_out * 5), "steps": steps,
-            "path": "pinned host -> cudaMemcpyAsync -> warp3d_affine_batched -> pinned host, "
-                    "one stream (sequential)"}
+            "path": "warp3d_pipeline_run (FIFO, depth 3): pinned host -> H2D stream -> "
+                    "warp stream -> D2H stream -> pinned host"}
 
 
 if __name__ == "__main__":

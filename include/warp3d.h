@@ -195,6 +195,35 @@ w3d_status warp3d_footprint_batched(int32_t batch, w3d_dims in_dims,
                                     const w3d_volume_params* params, w3d_dims out_dims,
                                     uint8_t* marks, unsigned long long* counts, void* stream);
 
+/*
+ * FIFO pipeline ("a first-in first-out (FIFO) queue to
+ * pipeline jobs ... while one image is being processed, the next has already
+ * begun transferring"): augments a batch held in HOST memory.  Volume i is job
+ * i; it uses device slot i % depth: copy-in stream (H2D image + labels) ->
+ * compute stream (warp3d_affine_batched on the slot) -> copy-out stream (D2H),
+ * each ordered by events, so H2D of job i+1, the warp of job i and the D2H of
+ * job i-1 overlap.  Host buffers should be pinned (cudaHostAlloc /
+ * cudaHostRegister) for the copies to be asynchronous.
+ *
+ * warp3d_pipeline_create allocates the slots' device buffers, streams and
+ * events (not on the hot path); warp3d_pipeline_run performs no allocation: it
+ * enqueues all jobs, makes them start after the work already queued on
+ * `stream` and makes `stream` wait for the last copy-out, and returns without
+ * synchronising (the outputs are valid after `stream` completes).
+ *   in_host          float [batch][in]   (read)
+ *   in_labels_host   uint8 [batch][in] or NULL (requires with_labels)
+ *   out_host         float [batch][out]  (written)
+ *   out_labels_host  uint8 [batch][out]; NULL iff in_labels_host is NULL
+ */
+typedef struct w3d_pipeline w3d_pipeline;
+w3d_status warp3d_pipeline_create(int32_t depth, w3d_dims in_dims, w3d_dims out_dims,
+                                  int32_t with_labels, w3d_pipeline** out);
+w3d_status warp3d_pipeline_run(w3d_pipeline* p, int32_t batch, const float* in_host,
+                               const uint8_t* in_labels_host, const w3d_volume_params* params,
+                               w3d_interp interp, float fill, uint8_t label_fill,
+                               float* out_host, uint8_t* out_labels_host, void* stream);
+w3d_status warp3d_pipeline_destroy(w3d_pipeline* p);
+
 /* Number of kernels this library has launched in this process (evidence for
  * bench.py's gpu_launches). */
 uint64_t warp3d_launch_count(void);

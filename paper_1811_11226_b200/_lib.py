@@ -25,7 +25,8 @@ EXPORTS = (
     "warp3d_affine", "warp3d_affine_batched", "warp3d_affine_batched_ex",
     "warp3d_compose_affine", "warp3d_noise", "warp3d_philox4x32_10",
     "warp3d_footprint_batched", "warp3d_launch_count", "warp3d_last_error",
-    "warp3d_abi_version", "warp3d_tile_stats",
+    "warp3d_abi_version", "warp3d_tile_stats", "warp3d_pipeline_create", "warp3d_pipeline_run",
+    "warp3d_pipeline_destroy",
 )
 
 
@@ -93,6 +94,11 @@ def load():
     L.warp3d_noise.argtypes = [P, Dims, F, U64, U64, P]
     L.warp3d_philox4x32_10.argtypes = [P, U64, P, I64, P]
     L.warp3d_footprint_batched.argtypes = [I32, Dims, P, Dims, P, P, P]
+    L.warp3d_pipeline_create.argtypes = [I32, Dims, Dims, I32, ctypes.POINTER(ctypes.c_void_p)]
+    L.warp3d_pipeline_run.argtypes = [P, I32, P, P, P, I32, F, ctypes.c_uint8, P, P, P]
+    L.warp3d_pipeline_destroy.argtypes = [P]
+    for name in ("warp3d_pipeline_create", "warp3d_pipeline_run", "warp3d_pipeline_destroy"):
+        getattr(L, name).restype = ctypes.c_int
     L.warp3d_tile_stats.argtypes = [P]
     L.warp3d_tile_stats.restype = ctypes.c_int
     L.warp3d_launch_count.restype = U64

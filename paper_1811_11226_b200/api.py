@@ -20,7 +20,7 @@ from ._lib import (INTERP_LINEAR, INTERP_NEAREST, KERNEL_AUTO, KERNEL_GATHER, KE
 __all__ = [
     "warp3d_affine", "warp3d_affine_batched", "warp3d_compose_affine", "warp3d_noise",
     "warp3d_philox4x32_10", "warp3d_footprint_batched", "warp3d_launch_count",
-    "warp3d_tile_stats",
+    "warp3d_tile_stats", "Pipeline",
     "warp3d_abi_version", "photometric", "volume_params", "make_geom", "Warp3DError",
     "INTERP_LINEAR", "INTERP_NEAREST", "KERNEL_AUTO", "KERNEL_GATHER", "KERNEL_STAGED",
     "KERNEL_TMA", "KERNEL_BULK",
@@ -154,6 +154,47 @@ def warp3d_footprint_batched(params, in_shape_zyx, out_shape_zyx=None, device="c
                                               ctypes.c_void_p(counts.data_ptr()), _stream()))
     c = counts.cpu().tolist()
     return int(c[0]), int(c[1])
+
+
+class Pipeline:
+    """FIFO host pipeline (include/warp3d.h warp3d_pipeline_*):
+    H2D of volume i+1, the warp of volume i and the D2H of volume i-1 overlap.
+    Host tensors should be pinned (tensor.pin_memory())."""
+
+    def __init__(self, in_shape_zyx, out_shape_zyx=None, depth=3, labels=True):
+        self.in_shape = tuple(in_shape_zyx)
+        self.out_shape = self.in_shape if out_shape_zyx is None else tuple(out_shape_zyx)
+        self._h = ctypes.c_void_p()
+        L.check(L.load().warp3d_pipeline_create(int(depth), L.dims(self.in_shape),
+                                                L.dims(self.out_shape), int(bool(labels)),
+                                                ctypes.byref(self._h)))
+
+    def run(self, inp: torch.Tensor, labels, params, out: torch.Tensor, out_labels=None,
+            interp=INTERP_LINEAR, fill=0.0, label_fill=0):
+        """inp/out (and labels) are CPU tensors [B, nz, ny, nx]; returns immediately,
+        results valid after torch.cuda.current_stream() completes."""
+        for t, name in ((inp, "inp"), (out, "out")):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous host tensor")
+        B = inp.shape[0]
+        arr = params if isinstance(params, ctypes.Array) else (VolumeParams * B)(*params)
+        L.check(L.load().warp3d_pipeline_run(
+            self._h, B, ctypes.c_void_p(inp.data_ptr()),
+            None if labels is None else ctypes.c_void_p(labels.data_ptr()), arr, int(interp),
+            float(fill), int(label_fill), ctypes.c_void_p(out.data_ptr()),
+            None if out_labels is None else ctypes.c_void_p(out_labels.data_ptr()), _stream()))
+        return out, out_labels
+
+    def close(self):
+        if self._h:
+            L.load().warp3d_pipeline_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def warp3d_launch_count() -> int:

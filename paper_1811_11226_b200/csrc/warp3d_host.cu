@@ -496,4 +496,149 @@ w3d_status warp3d_footprint_batched(int32_t batch, w3d_dims in_dims,
   return ok();
 }
 
+// ---------------------------------------------------------------------------
+// FIFO pipeline
+// ---------------------------------------------------------------------------
+struct w3d_pipeline {
+  int32_t depth = 0;
+  w3d_dims in_dims{}, out_dims{};
+  bool labels = false;
+  void* mem = nullptr;                    // all slots, one allocation
+  float* in_img[8] = {};
+  uint8_t* in_lbl[8] = {};
+  float* out_img[8] = {};
+  uint8_t* out_lbl[8] = {};
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[8] = {}, ev_comp[8] = {}, ev_out[8] = {};
+  cudaEvent_t ev_start = nullptr;
+};
+
+static void pipeline_free(w3d_pipeline* p) {
+  if (!p) return;
+  for (int i = 0; i < 8; ++i) {
+    if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
+    if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
+    if (p->ev_out[i]) cudaEventDestroy(p->ev_out[i]);
+  }
+  if (p->ev_start) cudaEventDestroy(p->ev_start);
+  if (p->s_in) cudaStreamDestroy(p->s_in);
+  if (p->s_comp) cudaStreamDestroy(p->s_comp);
+  if (p->s_out) cudaStreamDestroy(p->s_out);
+  if (p->mem) cudaFree(p->mem);
+  delete p;
+}
+
+w3d_status warp3d_pipeline_create(int32_t depth, w3d_dims in_dims, w3d_dims out_dims,
+                                  int32_t with_labels, w3d_pipeline** out) {
+  if (!out) return fail(W3D_ERR_INVALID_ARG, "out must be non-NULL");
+  *out = nullptr;
+  if (depth < 1 || depth > 8) return fail(W3D_ERR_INVALID_ARG, "depth = %d must be in [1, 8]", depth);
+  w3d_status st = check_dims(in_dims, "in_dims");
+  if (st != W3D_OK) return st;
+  if ((st = check_dims(out_dims, "out_dims")) != W3D_OK) return st;
+  w3d_pipeline* p = new w3d_pipeline;
+  p->depth = depth;
+  p->in_dims = in_dims;
+  p->out_dims = out_dims;
+  p->labels = with_labels != 0;
+  auto round256 = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t bi = round256(size_t(nvox(in_dims)) * 4), bo = round256(size_t(nvox(out_dims)) * 4);
+  const size_t bli = p->labels ? round256(size_t(nvox(in_dims))) : 0;
+  const size_t blo = p->labels ? round256(size_t(nvox(out_dims))) : 0;
+  const size_t per = bi + bo + bli + blo;
+  cudaError_t e = cudaMalloc(&p->mem, per * size_t(depth));
+  if (e == cudaSuccess) {
+    char* base = static_cast<char*>(p->mem);
+    for (int i = 0; i < depth; ++i) {
+      char* q = base + per * size_t(i);
+      p->in_img[i] = reinterpret_cast<float*>(q);
+      p->out_img[i] = reinterpret_cast<float*>(q + bi);
+      if (p->labels) {
+        p->in_lbl[i] = reinterpret_cast<uint8_t*>(q + bi + bo);
+        p->out_lbl[i] = reinterpret_cast<uint8_t*>(q + bi + bo + bli);
+      }
+    }
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming);
+  for (int i = 0; i < depth && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_out[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    pipeline_free(p);
+    return cuda_fail(e, "warp3d_pipeline_create");
+  }
+  *out = p;
+  return ok();
+}
+
+w3d_status warp3d_pipeline_run(w3d_pipeline* p, int32_t batch, const float* in_host,
+                               const uint8_t* in_labels_host, const w3d_volume_params* params,
+                               w3d_interp interp, float fill, uint8_t label_fill,
+                               float* out_host, uint8_t* out_labels_host, void* stream) {
+  if (!p) return fail(W3D_ERR_INVALID_ARG, "pipeline must be non-NULL");
+  if (batch < 1) return fail(W3D_ERR_INVALID_ARG, "batch = %d must be >= 1", batch);
+  if (!in_host || !out_host || !params)
+    return fail(W3D_ERR_INVALID_ARG, "in_host, out_host and params must be non-NULL");
+  if ((in_labels_host == nullptr) != (out_labels_host == nullptr))
+    return fail(W3D_ERR_INVALID_ARG, "out_labels_host must be NULL iff in_labels_host is NULL");
+  if (in_labels_host && !p->labels)
+    return fail(W3D_ERR_INVALID_ARG, "pipeline created without label buffers");
+  if (interp != W3D_INTERP_LINEAR && interp != W3D_INTERP_NEAREST)
+    return fail(W3D_ERR_INVALID_ARG, "interp = %d is not a w3d_interp", int(interp));
+  if (!std::isfinite(fill)) return fail(W3D_ERR_INVALID_ARG, "fill must be finite");
+  w3d_status st;
+  for (int32_t i = 0; i < batch; ++i) {
+    if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;
+    if ((st = check_ph(params[i].ph, i)) != W3D_OK) return st;
+  }
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  const size_t ni = size_t(nvox(p->in_dims)), no = size_t(nvox(p->out_dims));
+  const bool lab = in_labels_host != nullptr;
+  cudaError_t e = cudaEventRecord(p->ev_start, user);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_in, p->ev_start, 0);
+  for (int32_t i = 0; i < batch && e == cudaSuccess; ++i) {
+    const int s = i % p->depth;
+    if (i >= p->depth) e = cudaStreamWaitEvent(p->s_in, p->ev_out[s], 0);  // slot free again
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->in_img[s], in_host + ni * size_t(i), ni * 4, cudaMemcpyHostToDevice,
+                          p->s_in);
+    if (e == cudaSuccess && lab)
+      e = cudaMemcpyAsync(p->in_lbl[s], in_labels_host + ni * size_t(i), ni,
+                          cudaMemcpyHostToDevice, p->s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev_in[s], p->s_in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_comp, p->ev_in[s], 0);
+    if (e != cudaSuccess) break;
+    st = warp3d_affine_batched(1, p->in_img[s], lab ? p->in_lbl[s] : nullptr, p->in_dims,
+                               params + i, interp, fill, label_fill, p->out_img[s],
+                               lab ? p->out_lbl[s] : nullptr, p->out_dims, p->s_comp);
+    if (st != W3D_OK) return st;
+    e = cudaEventRecord(p->ev_comp[s], p->s_comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_out, p->ev_comp[s], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out_host + no * size_t(i), p->out_img[s], no * 4,
+                          cudaMemcpyDeviceToHost, p->s_out);
+    if (e == cudaSuccess && lab)
+      e = cudaMemcpyAsync(out_labels_host + no * size_t(i), p->out_lbl[s], no,
+                          cudaMemcpyDeviceToHost, p->s_out);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev_out[s], p->s_out);
+  }
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(user, p->ev_out[(batch - 1) % p->depth], 0);
+  if (e != cudaSuccess) return cuda_fail(e, "warp3d_pipeline_run");
+  return ok();
+}
+
+w3d_status warp3d_pipeline_destroy(w3d_pipeline* p) {
+  if (!p) return ok();
+  cudaStreamSynchronize(p->s_in);
+  cudaStreamSynchronize(p->s_comp);
+  cudaStreamSynchronize(p->s_out);
+  pipeline_free(p);
+  return ok();
+}
+
 }  // extern "C"

@@ -170,3 +170,14 @@ def test_no_gpu_means_cuda_error_not_fallback(W):
         pytest.skip("GPU present")
     st, msg = _call_batched(W)
     assert st == 3, msg
+
+
+def test_pipeline_create_validates(W):
+    from paper_1811_11226_b200 import _lib
+    L = _lib.load()
+    h = ctypes.c_void_p()
+    assert L.warp3d_pipeline_create(0, _lib.Dims(4, 4, 4), _lib.Dims(4, 4, 4), 1, ctypes.byref(h)) == 1
+    assert L.warp3d_pipeline_create(9, _lib.Dims(4, 4, 4), _lib.Dims(4, 4, 4), 1, ctypes.byref(h)) == 1
+    assert L.warp3d_pipeline_create(2, _lib.Dims(0, 4, 4), _lib.Dims(4, 4, 4), 1, ctypes.byref(h)) == 1
+    assert L.warp3d_pipeline_run(None, 1, None, None, None, 0, 0.0, 0, None, None, None) == 1
+    assert L.warp3d_pipeline_destroy(None) == 0

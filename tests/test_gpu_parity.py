@@ -408,3 +408,33 @@ def test_footprint_counts_match_oracle_marking(W):
         tot_l += len(np.unique(nimg[nimg >= 0]))
     assert f_lbl == tot_l
     assert f_img >= f_lbl
+
+
+# ----------------------------------------------------------------------------- FIFO pipeline
+@pytest.mark.parametrize("depth,B", [(1, 3), (2, 5), (3, 3), (3, 7)])
+def test_pipeline_matches_device_batched(W, depth, B):
+    """The host FIFO pipeline gives the device path's bits."""
+    shape = (24, 32, 48)
+    imgs, lbls, ds, As = _batch_inputs(shape, B, synth.TRAIN)
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B)]
+    ref, ref_l = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(),
+                                         torch.from_numpy(lbls).cuda(), params, fill=-1000.0,
+                                         label_fill=3)
+    pipe = W.Pipeline(shape, shape, depth=depth, labels=True)
+    h_img = torch.from_numpy(imgs).pin_memory()
+    h_lbl = torch.from_numpy(lbls).pin_memory()
+    out = torch.empty(imgs.shape, dtype=torch.float32).pin_memory()
+    out_l = torch.empty(lbls.shape, dtype=torch.uint8).pin_memory()
+    for _ in range(2):  # reuse across runs
+        out.fill_(7.0)
+        pipe.run(h_img, h_lbl, params, out, out_l, fill=-1000.0, label_fill=3)
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(out, ref.cpu()) and torch.equal(out_l, ref_l.cpu())
+    # images only
+    pipe2 = W.Pipeline(shape, shape, depth=depth, labels=False)
+    out2 = torch.empty(imgs.shape, dtype=torch.float32).pin_memory()
+    pipe2.run(h_img, None, params, out2, None, fill=-1000.0)
+    torch.cuda.current_stream().synchronize()
+    assert torch.equal(out2, ref.cpu())
+    pipe.close()
+    pipe2.close()
