@@ -70,9 +70,13 @@ typedef enum {
                               y-parts; needs nx % 4 == 0 (with labels
                               nx % 16 == 0) and 16 B aligned inputs, else
                               W3D_ERR_UNSUPPORTED                                 */
-  W3D_KERNEL_BULK = 4      /* as TMA, but each footprint row is one 1D
+  W3D_KERNEL_BULK = 4,     /* as TMA, but each footprint row is one 1D
                               cp.async.bulk copy (tight shared-memory layout);
                               same requirements                                   */
+  W3D_KERNEL_PERSISTENT = 5 /* persistent CTAs (2 per SM) staging the next
+                              tile's footprint by cp.async while computing the
+                              current one; same layout requirements as STAGED
+                              (falls back to GATHER otherwise)                    */
 } w3d_kernel;
 
 typedef struct {

@@ -276,6 +276,7 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
                           : (variant == W3D_KERNEL_STAGED) ? launch_staged(args, stream)
                           : (variant == W3D_KERNEL_TMA)    ? launch_tma(args, stream)
                           : (variant == W3D_KERNEL_BULK)   ? launch_bulk(args, stream)
+                          : (variant == W3D_KERNEL_PERSISTENT) ? launch_persistent_api(args, stream)
                                                            : launch_auto(args, stream);
     if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");
   }
@@ -346,7 +347,7 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
   if ((in_labels == nullptr) != (out_labels == nullptr))
     return fail(W3D_ERR_INVALID_ARG, "out_labels must be NULL iff in_labels is NULL");
   if (variant != W3D_KERNEL_AUTO && variant != W3D_KERNEL_GATHER && variant != W3D_KERNEL_STAGED &&
-      variant != W3D_KERNEL_TMA && variant != W3D_KERNEL_BULK)
+      variant != W3D_KERNEL_TMA && variant != W3D_KERNEL_BULK && variant != W3D_KERNEL_PERSISTENT)
     return fail(W3D_ERR_INVALID_ARG, "variant = %d is not a w3d_kernel", int(variant));
   for (int32_t i = 0; i < batch; ++i) {
     if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;

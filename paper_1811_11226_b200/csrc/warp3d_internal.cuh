@@ -57,7 +57,7 @@ __host__ __device__ constexpr int img_cls_width(int c) {
 __host__ __device__ constexpr int lbl_cls_width(int c) { return c < 6 ? 16 * (c + 1) : 128; }
 
 // Persistent kernel: two buffers of kPersCapVox voxels (5 B each) per SM.
-constexpr int kPersCapVox = 22528;
+constexpr int kPersCapVox = 11008;  // 2 CTAs/SM x 2 buffers x (55 KB + 1 KB reserve)
 
 struct alignas(64) WarpArgs {
   CUtensorMap tm_img[kNumImgCls];  // 4D (nx, ny, nz, nvol) float32, box (w, 4, 1, 1)
@@ -85,6 +85,7 @@ cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_tma(const WarpArgs& a, cudaStream_t s);
 cudaError_t launch_bulk(const WarpArgs& a, cudaStream_t s);
+cudaError_t launch_persistent_api(const WarpArgs& a, cudaStream_t s);
 bool tma_supported(const WarpArgs& a);
 cudaError_t encode_tensor_maps(WarpArgs& a);
 cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,

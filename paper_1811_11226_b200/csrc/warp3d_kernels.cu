@@ -251,8 +251,7 @@ using CfgB = TileCfg<Shape<32, 8, 8, 256>, 4, 11008>;   //  8 rows / thread, 32 
 using CfgC = TileCfg<Shape<32, 16, 8, 256>, 3, 14592>;  // 16 rows / thread, 24 warps / SM
 using CfgD = TileCfg<Shape<32, 8, 16, 512>, 2, 16384>;  //  8 rows / thread, 32 warps / SM
 using CfgE = TileCfg<Shape<32, 16, 8, 512>, 2, 16384>;  //  8 rows / thread, 32 warps / SM
-using PersShape = Shape<32, 16, 16, 1024>;           // persistent, double-buffered
-using PersShapeS = Shape<32, 16, 8, 512>;            // persistent, 2 CTAs / SM
+using PersShape = Shape<32, 8, 8, 256>;              // persistent, double-buffered, 2 CTAs/SM
 
 // 64-bit address base + 32-bit element offset in one IMAD.WIDE.U32
 __device__ __forceinline__ float* addr_f32(float* base, uint32_t off) {
@@ -872,82 +871,125 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
 }
 
 // ----------------------------------------------------------------------------
-// Kernel B (persistent): one 1024-thread CTA per SM walks the tiles t =
+// Kernel B (persistent, cp.async pipeline): each CTA walks the tiles t =
 // blockIdx.x + k * gridDim.x (volume-major order, so concurrently processed
-// tiles share the L2-resident part of one volume).  Two shared-memory buffers:
-// while tile k computes from buffer k & 1, the cp.async staging of tile k+1
-// fills buffer (k+1) & 1.  Box metadata uses 3 slots (k % 3) so warp 0 can
-// publish tile k+1's box while slow warps still read tile k-1's.
+// tiles share the L2-resident slab of one volume).  Two staging buffers: the
+// cp.async copies of tile k+1 are issued before tile k is computed, and each
+// thread computes tile k's noise while its copies are in flight.  Plans use 3
+// metadata slots (k % 3) so warp 0 can publish tile k+1's plan while slower
+// warps still read tile k-1's.  Tiles whose footprint exceeds a buffer are
+// split into y-parts and staged serially (no prefetch); if even those do not
+// fit, gathered.
 // ----------------------------------------------------------------------------
+template <class S>
+__device__ __forceinline__ void tile_coords(int t, int tiles_x, int tiles_y, int per_vol,
+                                            int& vi, int& ox, int& oy, int& oz) {
+  vi = t / per_vol;
+  int r = t - vi * per_vol;
+  const int txy = tiles_x * tiles_y;
+  const int tzi = r / txy;
+  r -= tzi * txy;
+  const int tyi = r / tiles_x;
+  ox = (r - tyi * tiles_x) * S::TX;
+  oy = tyi * S::TY;
+  oz = tzi * S::TZ;
+}
+
 template <class S, bool kLabels, bool kNearest>
-__global__ void __launch_bounds__(S::THREADS, 1024 / S::THREADS)
+__global__ void __launch_bounds__(S::THREADS, 2)
     warp3d_persistent_kernel(const __grid_constant__ WarpArgs a, const int tiles_x,
                              const int tiles_y, const int tiles_z, const int total,
                              const int cap_vox) {
-  __shared__ int s_box[3][8];
+  static_assert(S::WARPS == S::TZ && S::RPT == S::TY && S::TY == 8, "persistent shape");
+  __shared__ int s_box[3][2][kBNF];
+  __shared__ int s_nsub[3];
   const int per_vol = tiles_x * tiles_y * tiles_z;
   const uint32_t buf_bytes = static_cast<uint32_t>(cap_vox) * 5u;
   int t = static_cast<int>(blockIdx.x);
   if (t >= total) return;
-  auto coords = [&](int tt, int& vi, int& ox, int& oy, int& oz) {
-    vi = tt / per_vol;
-    int r = tt - vi * per_vol;
-    const int tzi = r / (tiles_x * tiles_y);
-    r -= tzi * tiles_x * tiles_y;
-    const int tyi = r / tiles_x;
-    ox = (r - tyi * tiles_x) * S::TX;
-    oy = tyi * S::TY;
-    oz = tzi * S::TZ;
-  };
-  // prologue: box + staging of the first tile into buffer 0
-  {
+  const int lane_x = static_cast<int>(threadIdx.x & 31), wz = static_cast<int>(threadIdx.x >> 5);
+  auto plan = [&](int tt, int slot) {
     int vi, ox, oy, oz;
-    coords(t, vi, ox, oy, oz);
-    if (threadIdx.x < 32) tile_box<S>(a, load_params(a.vol[vi]), ox, oy, oz, cap_vox, s_box[0]);
-    __syncthreads();
-    if (s_box[0][6])
+    tile_coords<S>(tt, tiles_x, tiles_y, per_vol, vi, ox, oy, oz);
+    tma_plan<S, kPlanCp>(a, a.vol[vi].A, ox, oy, oz, cap_vox * 5, kLabels, s_box[slot],
+                         &s_nsub[slot]);
+  };
+  auto stage_tile = [&](int tt, int slot, uint32_t buf) {
+    int vi, ox, oy, oz;
+    tile_coords<S>(tt, tiles_x, tiles_y, per_vol, vi, ox, oy, oz);
+    const int* b = s_box[slot][0];
+    const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
+    if (box6[5] > 0)
       stage_box<S, kLabels>(a, a.in + vi * a.in_stride,
-                            kLabels ? a.in_lbl + vi * a.in_stride : nullptr, s_box[0], 0u,
-                            static_cast<uint32_t>(cap_vox) * 4u);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
+                            kLabels ? a.in_lbl + vi * a.in_stride : nullptr, box6, buf,
+                            buf + static_cast<uint32_t>(b[kBImgBytes]));
+  };
+  if (threadIdx.x < 32) plan(t, 0);
+  __syncthreads();
+  if (s_nsub[0] == 1) stage_tile(t, 0, 0u);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   for (int k = 0;; ++k) {
     const int tn = t + static_cast<int>(gridDim.x);
     const int slot = k % 3, nslot = (k + 1) % 3;
     const uint32_t buf = (k & 1) ? buf_bytes : 0u, nbuf = (k & 1) ? 0u : buf_bytes;
-    int nvi = 0, nox = 0, noy = 0, noz = 0;
-    if (tn < total) {
-      coords(tn, nvi, nox, noy, noz);
-      if (threadIdx.x < 32) tile_box<S>(a, load_params(a.vol[nvi]), nox, noy, noz, cap_vox,
-                                        s_box[nslot]);
-    }
-    __syncthreads();  // (1) next box visible; every warp is done with tile k-1's buffer
-    if (tn < total && s_box[nslot][6])
-      stage_box<S, kLabels>(a, a.in + nvi * a.in_stride,
-                            kLabels ? a.in_lbl + nvi * a.in_stride : nullptr, s_box[nslot],
-                            nbuf, nbuf + static_cast<uint32_t>(cap_vox) * 4u);
+    if (tn < total && threadIdx.x < 32) plan(tn, nslot);
+    __syncthreads();  // (1) next plan visible; every warp is done with tile k-1's buffer
+    if (tn < total && s_nsub[nslot] == 1) stage_tile(tn, nslot, nbuf);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // tile k's group is complete
-    __syncthreads();  // (2) tile k's staged box visible to all
-    int box[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) box[i] = s_box[slot][i];
     int vi, ox, oy, oz;
-    coords(t, vi, ox, oy, oz);
+    tile_coords<S>(t, tiles_x, tiles_y, per_vol, vi, ox, oy, oz);
     const Params P = load_params(a.vol[vi]);
-    const float* vin = a.in + vi * a.in_stride;
-    const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
     float* vout = a.out + vi * a.out_stride;
     uint8_t* lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
-    count_tile(box[6] != 0);
-    if (box[6]) {
-      compute_staged<S, kLabels, kNearest>(a, P, vin, lin, vout, lout, box,
-                                           static_cast<int>(buf),
-                                           static_cast<int>(buf) + cap_vox * 4, ox, oy, oz);
-    } else {
+    const int X = ox + lane_x, Z = oz + wz;
+    const int nsub = s_nsub[slot];
+    const bool live = X < a.mx && Z < a.mz && oy < a.my && !column_occluded_z(P, Z);
+    float n[S::TY];
+    if (live) column_noise<S::TY>(a, P, X, Z, oy, n);  // overlaps the copies in flight
+    if (nsub == 1) {
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // tile k's group is complete
+      __syncthreads();  // (2) tile k's staged box visible to all
+      count_tile(true);
+      const int* b = s_box[slot][0];
+      const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
+      const Stage sv = make_stage(a, box6, static_cast<int>(buf),
+                                  static_cast<int>(buf) + b[kBImgBytes]);
+      if (b[kBClamp])
+        column_rows_n<S::TY, true, kLabels, kNearest, true, false>(a, P, nullptr, nullptr, vout,
+                                                                   lout, sv, X, Z, oy, n);
+      else
+        column_rows_n<S::TY, true, kLabels, kNearest, false, false>(a, P, nullptr, nullptr, vout,
+                                                                    lout, sv, X, Z, oy, n);
+    } else if (nsub == 2) {  // two y-parts staged serially into this tile's buffer
+      count_tile(true);
+      for (int part = 0; part < 2; ++part) {
+        const int* b = s_box[slot][part];
+        const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
+        if (box6[5] > 0)
+          stage_box<S, kLabels>(a, a.in + vi * a.in_stride,
+                                kLabels ? a.in_lbl + vi * a.in_stride : nullptr, box6, buf,
+                                buf + static_cast<uint32_t>(b[kBImgBytes]));
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        if (box6[5] > 0) {
+          const Stage sv = make_stage(a, box6, static_cast<int>(buf),
+                                      static_cast<int>(buf) + b[kBImgBytes]);
+          if (part == 0)
+            column_rows_n<S::TY / 2, true, kLabels, kNearest, true, false>(
+                a, P, nullptr, nullptr, vout, lout, sv, X, Z, b[kBPart], n);
+          else
+            column_rows_n<S::TY / 2, true, kLabels, kNearest, true, false>(
+                a, P, nullptr, nullptr, vout, lout, sv, X, Z, b[kBPart], n + S::TY / 2);
+        }
+        __syncthreads();
+      }
+    } else {  // footprint too large even in parts: gathers
+      count_tile(false);
       Stage sv;
-      tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy,
-                                                        oz);
+      const float* vin = a.in + vi * a.in_stride;
+      const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+      column_rows_n<S::TY, false, kLabels, kNearest, false, false>(a, P, vin, lin, vout, lout,
+                                                                    sv, X, Z, oy, n);
     }
     if (tn >= total) break;
     t = tn;
@@ -956,6 +998,7 @@ __global__ void __launch_bounds__(S::THREADS, 1024 / S::THREADS)
 }
 
 static int g_pers_cap_vox = kPersCapVox;
+static int g_num_sms = 0;
 
 template <class Cfg, bool kStage, bool kLabels, bool kNearest>
 static cudaError_t launch_variant(const WarpArgs& a, cudaStream_t s) {
@@ -1013,7 +1056,7 @@ static char tile_cfg() {
   return v;
 }
 
-static int g_num_sms = 0;
+
 
 template <class S, bool kLabels, bool kNearest>
 static cudaError_t launch_persistent_variant(const WarpArgs& a, int cap, cudaStream_t s) {
@@ -1022,13 +1065,13 @@ static cudaError_t launch_persistent_variant(const WarpArgs& a, int cap, cudaStr
   const int64_t total = static_cast<int64_t>(tiles_x) * tiles_y * tiles_z * a.nvol;
   if (total >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
   const size_t smem = static_cast<size_t>(cap) * 10;  // two buffers of cap * (4 + 1) B
-  static size_t configured = 0;
-  if (configured != smem) {
+  static bool configured = false;
+  if (!configured) {
     const cudaError_t e = cudaFuncSetAttribute(warp3d_persistent_kernel<S, kLabels, kNearest>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured = true;
   }
   if (g_num_sms == 0) {
     int dev = 0;
@@ -1036,28 +1079,15 @@ static cudaError_t launch_persistent_variant(const WarpArgs& a, int cap, cudaStr
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  const int64_t ctas = static_cast<int64_t>(g_num_sms) * (1024 / S::THREADS);
+  const int64_t ctas = static_cast<int64_t>(g_num_sms) * 2;
   const int grid = static_cast<int>(total < ctas ? total : ctas);
   warp3d_persistent_kernel<S, kLabels, kNearest><<<grid, S::THREADS, smem, s>>>(
       a, tiles_x, tiles_y, tiles_z, static_cast<int>(total), cap);
   return cudaGetLastError();
 }
 
-// Tuning knob for experiments (not part of the ABI): W3D_PERSISTENT_SHAPE=512
-// selects the 512-thread 32x16x8 persistent variant (2 CTAs / SM).
-static int pers_shape() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("W3D_PERSISTENT_SHAPE");
-    v = (e && atoi(e) == 512) ? 512 : 1024;
-  }
-  return v;
-}
-
 template <bool kLabels, bool kNearest>
 static cudaError_t launch_persistent_variant(const WarpArgs& a, cudaStream_t s) {
-  if (pers_shape() == 512)
-    return launch_persistent_variant<PersShapeS, kLabels, kNearest>(a, g_pers_cap_vox / 2, s);
   return launch_persistent_variant<PersShape, kLabels, kNearest>(a, g_pers_cap_vox, s);
 }
 
@@ -1418,6 +1448,10 @@ bool staged_supported(const WarpArgs& a) {
 }
 
 cudaError_t launch_gather(const WarpArgs& a, cudaStream_t s) { return launch_tiles(a, false, s); }
+
+cudaError_t launch_persistent_api(const WarpArgs& a, cudaStream_t s) {
+  return staged_supported(a) ? launch_persistent(a, s) : launch_tiles(a, false, s);
+}
 
 cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s) {
   return launch_tiles(a, staged_supported(a), s);

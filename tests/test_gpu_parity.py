@@ -117,7 +117,7 @@ def test_noise_hook_matches_oracle(W, shape):
 
 
 # ----------------------------------------------------------------------------- configs[0] (C1)
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_c1_fixed_affine_noise(W, variant):
     """32^3 float32 + uint8 labels, one fixed affine, trilinear + nearest, sigma = 10 HU."""
     img, lbl = synth.phantom((32, 32, 32))
@@ -142,7 +142,7 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 5])
 @pytest.mark.parametrize("case", range(len(SMALL)))
 def test_small_cases(W, case, variant):
     in_shape, out_shape, rname, flags, interp, B = SMALL[case]
@@ -176,7 +176,7 @@ def test_exact_permutations_on_gpu(W):
         A = np.zeros((3, 4), np.float32)
         A[:, :3] = M
         A[:, 3] = b
-        for variant in (1, 2, 3, 4):
+        for variant in (1, 2, 3, 4, 5):
             g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], 0, [0],
                                          variant=variant, fill=-5.0, label_fill=9)
             assert np.array_equal(g_img[0], ref[0][0]), name
@@ -189,7 +189,7 @@ def test_fully_out_of_bounds_and_occlusion(W):
     d = synth.draw(synth.TRAIN, 3)
     A = np.zeros((3, 4), np.float32)
     A[:, 3] = (-40, 3, 3)
-    for variant in (1, 2, 3, 4):
+    for variant in (1, 2, 3, 4, 5):
         g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], 0, [0], variant=variant,
                                      fill=-1000.0, label_fill=6)
         assert np.all(g_img == np.float32(-1000.0)) and np.all(g_lbl == 6)
@@ -201,7 +201,7 @@ def test_fully_out_of_bounds_and_occlusion(W):
     oph = O.photometric(FULL | O.OCCLUDE, window=d.window, gamma=d.gamma, sigma=d.sigma, seed=1,
                         volume_id=0, occ_z0=2.5, occ_height=4.0)
     r_img, r_lbl = O.warp_volume(img, lbl, A, None, 0, -1000.0, 0, oph)
-    for variant in (1, 2, 3, 4):
+    for variant in (1, 2, 3, 4, 5):
         out, out_l = W.warp3d_affine_batched(torch.from_numpy(img[None]).cuda(),
                                              torch.from_numpy(lbl[None]).cuda(), params,
                                              fill=-1000.0, variant=variant)
@@ -245,6 +245,10 @@ def test_tma_subtiling_and_fixup_paths(W):
     b_img, b_lbl, _ = run_case(W, imgs, lbls, As, ds, FULL, [0, 1, 2], variant=4, fill=-1000.0,
                                label_fill=5, oracle_volumes=[])
     assert np.array_equal(b_img, g_img) and np.array_equal(b_lbl, g_lbl)
+    for v in (0, 2, 5):  # cp.async kernels: sub-tiled / persistent paths, same bits
+        c_img, c_lbl, _ = run_case(W, imgs, lbls, As, ds, FULL, [0, 1, 2], variant=v,
+                                   fill=-1000.0, label_fill=5, oracle_volumes=[])
+        assert np.array_equal(c_img, g_img) and np.array_equal(c_lbl, g_lbl), v
     params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(3)]
     o1, l1 = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda(),
                                      params, fill=-1000.0, label_fill=5, variant=1)
@@ -274,7 +278,7 @@ def _batch_inputs(shape, B, ranges, first_vid=0, n_distinct=4):
     return imgs, lbls, ds, As
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 5])
 def test_c2_single_ct_volume(W, variant):
     imgs, lbls, ds, As = _batch_inputs((160, 128, 128), 1, synth.TRAIN)
     g_img, g_lbl, ref = run_case(W, imgs, lbls, As, ds, FULL, [0], variant=variant)
@@ -320,7 +324,7 @@ def test_c4_512cubed_large_rotations_sampled(W):
     img, lbl = synth.phantom(shape)
     ds = [synth.draw(synth.LARGE, 7)]
     As = [_oracle_affine(ds[0], shape, shape)]
-    for variant in (0, 1, 2):
+    for variant in (0, 1, 2, 5):
         out, out_l = _sampled_check(W, img[None], lbl[None], As, ds, FULL, [0], 200_000,
                                     variant=variant)
         # full z-slices (several thousand contiguous rows) through the oracle
@@ -359,7 +363,7 @@ def test_variants_batch_splits_and_determinism_bitwise(W):
     ti, tl = torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda()
     params = [W.volume_params(As[i], _wph(W, ds[i], FULL, 100 + i)) for i in range(6)]
     ref, ref_l = W.warp3d_affine_batched(ti, tl, params, fill=-1000.0, variant=1)
-    for variant in (0, 1, 2, 3, 4):
+    for variant in (0, 1, 2, 3, 4, 5):
         o, ol = W.warp3d_affine_batched(ti, tl, params, fill=-1000.0, variant=variant)
         assert torch.equal(o, ref) and torch.equal(ol, ref_l), variant
     for i in range(6):  # single calls
