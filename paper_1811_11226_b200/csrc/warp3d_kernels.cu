@@ -323,12 +323,13 @@ __device__ __forceinline__ void column_pairs(const WarpArgs& a, const Params& P,
 }
 
 // Occluded output z (R15): image 0, every later step skipped;
-// labels are still warped.
+// labels are still warped.  Rare: kept out of line (instruction-cache
+// footprint of the hot loop); P and the stage view are passed by value.
 template <bool kStagedPath, bool kLabels, bool kClamp, bool kSepLbl>
-__device__ __forceinline__ void column_occluded(const WarpArgs& a, const Params& P,
-                                                const uint8_t* __restrict__ lin, float* vout,
-                                                uint8_t* lout, const Stage& sv, int X, int Z,
-                                                int ybeg, int yend) {
+__device__ __noinline__ void column_occluded(const WarpArgs& a, const Params P,
+                                             const uint8_t* __restrict__ lin, float* vout,
+                                             uint8_t* lout, const Stage sv, int X, int Z,
+                                             int ybeg, int yend) {
   const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
   const float cz0 = __fmaf_rn(P.A[2], fZ, P.A[3]), cz1 = __fmaf_rn(P.A[6], fZ, P.A[7]);
   const float cz2 = __fmaf_rn(P.A[10], fZ, P.A[11]);
@@ -790,6 +791,49 @@ __device__ __forceinline__ void cp_part_compute(const WarpArgs& a, const Params&
                                                            sv, X, Z, ybeg);
 }
 
+// Out-of-line rare paths of the tile kernel (keep the hot loop's code small).
+template <class S, bool kLabels, bool kNearest>
+__device__ __noinline__ void gather_tile(const WarpArgs& a, int vi, int ox, int oy, int oz) {
+  const Params P = load_params(a.vol[vi]);
+  Stage sv;
+  tile_compute<S, false, kLabels, kNearest, false>(
+      a, P, a.in + vi * a.in_stride, kLabels ? a.in_lbl + vi * a.in_stride : nullptr,
+      a.out + vi * a.out_stride, kLabels ? a.out_lbl + vi * a.out_stride : nullptr, sv, ox, oy,
+      oz);
+}
+
+template <class S, bool kLabels, bool kNearest>
+__device__ __noinline__ void subtile_path(const WarpArgs& a, const int* boxes, int vi, int ox,
+                                          int oy, int oz, int nsub) {
+  const float* vin = a.in + vi * a.in_stride;
+  const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+  float* vout = a.out + vi * a.out_stride;
+  uint8_t* lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
+  const int X = ox + static_cast<int>(threadIdx.x & 31);
+  const int Z = oz + static_cast<int>(threadIdx.x >> 5);
+  for (int k = 0; k < nsub; ++k) {
+    int b[kBNF];
+#pragma unroll
+    for (int i = 0; i < kBNF; ++i) b[i] = boxes[k * kBNF + i];
+    if (b[kBD] == 0) continue;  // part entirely beyond the volume's last row
+    const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
+    stage_box<S, kLabels>(a, vin, lin, box6, 0u, static_cast<uint32_t>(b[kBImgBytes]));
+    cp_async_wait_all();
+    __syncthreads();
+    const Params P = load_params(a.vol[vi]);
+    if (nsub == 2) {
+      if constexpr (S::TY / 2 >= 4)
+        cp_part_compute<S::TY / 2, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
+                                                      b[kBClamp] != 0, X, Z, b[kBPart]);
+    } else {
+      if constexpr (S::TY / 4 >= 4)
+        cp_part_compute<S::TY / 4, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
+                                                      b[kBClamp] != 0, X, Z, b[kBPart]);
+    }
+    __syncthreads();  // buffer reuse by the next part
+  }
+}
+
 template <class Cfg, bool kStage, bool kLabels, bool kNearest>
 __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
     warp3d_tile_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap_vox) {
@@ -813,61 +857,36 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
   const int nsub = kStage ? s_nsub : 0;
   if (nsub == 0 || (S::WARPS != S::TZ)) {  // gather variant, or nothing fits
     count_tile(false);
-    const Params P = load_params(a.vol[vi]);
-    Stage sv;
-    tile_compute<S, false, kLabels, kNearest, false>(a, P, vin, lin, vout, lout, sv, ox, oy, oz);
+    gather_tile<S, kLabels, kNearest>(a, vi, ox, oy, oz);
     return;
   }
   count_tile(true);
-  const int X = ox + static_cast<int>(threadIdx.x & 31);
-  const int Z = oz + static_cast<int>(threadIdx.x >> 5);
-  if (nsub == 1) {
-    // whole tile: issue the staging, compute the column's noise (independent of
-    // the box) while the copies are in flight, then wait and sample
-    int b[kBNF];
-#pragma unroll
-    for (int i = 0; i < kBNF; ++i) b[i] = s_box[0][i];
-    const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
-    stage_box<S, kLabels>(a, vin, lin, box6, 0u, static_cast<uint32_t>(b[kBImgBytes]));
-    const Params P = load_params(a.vol[vi]);
-    const bool live = X < a.mx && Z < a.mz && oy < a.my && !column_occluded_z(P, Z);
-    float n[S::TY];
-    if (live) column_noise<S::TY>(a, P, X, Z, oy, n);
-    cp_async_wait_all();
-    __syncthreads();
-    const Stage sv = make_stage(a, box6, 0, b[kBImgBytes]);
-    if (b[kBClamp])
-      column_rows_n<S::TY, true, kLabels, kNearest, true, false>(a, P, nullptr, nullptr, vout,
-                                                                 lout, sv, X, Z, oy, n);
-    else
-      column_rows_n<S::TY, true, kLabels, kNearest, false, false>(a, P, nullptr, nullptr, vout,
-                                                                  lout, sv, X, Z, oy, n);
+  if (nsub > 1) {  // rare: the footprint needs 2 or 4 y-parts
+    subtile_path<S, kLabels, kNearest>(a, &s_box[0][0], vi, ox, oy, oz, nsub);
     return;
   }
-  for (int k = 0; k < nsub; ++k) {
-    int b[kBNF];
+  const int X = ox + static_cast<int>(threadIdx.x & 31);
+  const int Z = oz + static_cast<int>(threadIdx.x >> 5);
+  // whole tile: issue the staging, compute the column's noise (independent of
+  // the box) while the copies are in flight, then wait and sample
+  int b[kBNF];
 #pragma unroll
-    for (int i = 0; i < kBNF; ++i) b[i] = s_box[k][i];
-    if (b[kBD] == 0) continue;  // part entirely beyond the volume's last row
-    const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
-    stage_box<S, kLabels>(a, vin, lin, box6, 0u, static_cast<uint32_t>(b[kBImgBytes]));
-    cp_async_wait_all();
-    __syncthreads();
-    const Params P = load_params(a.vol[vi]);  // after staging: keeps the loop's registers free
-    if (nsub == 1) {
-      cp_part_compute<S::TY, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
-                                                b[kBClamp] != 0, X, Z, b[kBPart]);
-    } else if (nsub == 2) {
-      if constexpr (S::TY / 2 >= 4)
-        cp_part_compute<S::TY / 2, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
-                                                      b[kBClamp] != 0, X, Z, b[kBPart]);
-    } else {
-      if constexpr (S::TY / 4 >= 4)
-        cp_part_compute<S::TY / 4, kLabels, kNearest>(a, P, vout, lout, box6, b[kBImgBytes],
-                                                      b[kBClamp] != 0, X, Z, b[kBPart]);
-    }
-    if (k + 1 < nsub) __syncthreads();  // buffer reuse by the next part
-  }
+  for (int i = 0; i < kBNF; ++i) b[i] = s_box[0][i];
+  const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
+  stage_box<S, kLabels>(a, vin, lin, box6, 0u, static_cast<uint32_t>(b[kBImgBytes]));
+  const Params P = load_params(a.vol[vi]);
+  const bool live = X < a.mx && Z < a.mz && oy < a.my && !column_occluded_z(P, Z);
+  float n[S::TY];
+  if (live) column_noise<S::TY>(a, P, X, Z, oy, n);
+  cp_async_wait_all();
+  __syncthreads();
+  const Stage sv = make_stage(a, box6, 0, b[kBImgBytes]);
+  if (b[kBClamp])
+    column_rows_n<S::TY, true, kLabels, kNearest, true, false>(a, P, nullptr, nullptr, vout, lout,
+                                                               sv, X, Z, oy, n);
+  else
+    column_rows_n<S::TY, true, kLabels, kNearest, false, false>(a, P, nullptr, nullptr, vout,
+                                                                lout, sv, X, Z, oy, n);
 }
 
 // ----------------------------------------------------------------------------
