@@ -681,6 +681,52 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// Every warp computes the whole tile's cp.async box itself (identical in all
+// lanes: lanes 8g..8g+7 evaluate the 8 corners, reduced within 8-lane groups),
+// so the common case needs no barrier before staging.  Returns whether the box
+// fits cap_vox; b receives the kPlanCp record for nsub = 1.
+template <class S>
+__device__ __forceinline__ bool warp_box_cp(const WarpArgs& a, const float* __restrict__ A, int ox,
+                                            int oy, int oz, int cap_vox, int* b) {
+  const int c = threadIdx.x & 7;
+  const float X = static_cast<float>((c & 1) ? min(ox + S::TX, a.mx) - 1 : ox);
+  const float Y = static_cast<float>((c & 2) ? min(oy + S::TY, a.my) - 1 : oy);
+  const float Z = static_cast<float>((c & 4) ? min(oz + S::TZ, a.mz) - 1 : oz);
+  float mn[3], mxv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float p = __fmaf_rn(A[4 * k], X, __fmaf_rn(A[4 * k + 1], Y,
+                                                     __fmaf_rn(A[4 * k + 2], Z, A[4 * k + 3])));
+    mn[k] = p;
+    mxv[k] = p;
+  }
+#pragma unroll
+  for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+      mxv[k] = fmaxf(mxv[k], __shfl_xor_sync(0xffffffffu, mxv[k], off));
+    }
+  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                      static_cast<float>(a.nz)};
+  int lo[3], hi[3];
+  bool inside = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = static_cast<int>(floorf(fminf(fmaxf(mn[k], -1.0f), n[k])));
+    hi[k] = static_cast<int>(floorf(fminf(fmaxf(mxv[k], -1.0f), n[k]))) + 1;
+    inside &= (mn[k] >= -1.0f) & (mxv[k] <= n[k]);
+  }
+  const int bx = lo[0] & ~3;
+  const int W = (hi[0] - bx + 1 + 3) & ~3, H = hi[1] - lo[1] + 1, D = hi[2] - lo[2] + 1;
+  b[kBx] = bx; b[kBy] = lo[1]; b[kBz] = lo[2];
+  b[kBPI] = W; b[kBH] = H; b[kBD] = D;
+  b[kBClamp] = inside ? 0 : 1;
+  b[kBImgBytes] = D * H * W * 4;
+  b[kBPart] = oy;
+  return static_cast<int64_t>(W) * H * D <= cap_vox;
+}
+
 // Warp 0: boxes of the tile split into nsub y-parts (nsub = 1, 2, 4: the
 // first that fits).  Lanes 8g .. 8g+7 evaluate part g's 8 corners.  Layout
 // modes: kPlanCp (cp.async: image and labels share origin x0 % 4 and pitch),
@@ -848,30 +894,30 @@ __global__ void __launch_bounds__(Cfg::S::THREADS, Cfg::MINB)
   const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
   float* __restrict__ vout = a.out + vi * a.out_stride;
   uint8_t* __restrict__ lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
-  if (kStage) {
-    // plan (warp 0): whole-tile box, or 2 / 4 y-parts when it exceeds the buffer
-    if (threadIdx.x < 32)
-      tma_plan<S, kPlanCp>(a, a.vol[vi].A, ox, oy, oz, cap_vox * 5, kLabels, s_box, &s_nsub);
-    __syncthreads();
-  }
-  const int nsub = kStage ? s_nsub : 0;
-  if (nsub == 0 || (S::WARPS != S::TZ)) {  // gather variant, or nothing fits
+  if (!kStage || S::WARPS != S::TZ) {  // gather variant
     count_tile(false);
     gather_tile<S, kLabels, kNearest>(a, vi, ox, oy, oz);
     return;
   }
-  count_tile(true);
-  if (nsub > 1) {  // rare: the footprint needs 2 or 4 y-parts
-    subtile_path<S, kLabels, kNearest>(a, &s_box[0][0], vi, ox, oy, oz, nsub);
+  int b[kBNF];
+  if (!warp_box_cp<S>(a, a.vol[vi].A, ox, oy, oz, cap_vox, b)) {
+    // rare: the footprint exceeds the buffer -> y-parts (or gathers)
+    if (threadIdx.x < 32)
+      tma_plan<S, kPlanCp>(a, a.vol[vi].A, ox, oy, oz, cap_vox * 5, kLabels, s_box, &s_nsub);
+    __syncthreads();
+    const int nsub = s_nsub;
+    count_tile(nsub != 0);
+    if (nsub == 0)
+      gather_tile<S, kLabels, kNearest>(a, vi, ox, oy, oz);
+    else
+      subtile_path<S, kLabels, kNearest>(a, &s_box[0][0], vi, ox, oy, oz, nsub);
     return;
   }
+  count_tile(true);
   const int X = ox + static_cast<int>(threadIdx.x & 31);
   const int Z = oz + static_cast<int>(threadIdx.x >> 5);
   // whole tile: issue the staging, compute the column's noise (independent of
   // the box) while the copies are in flight, then wait and sample
-  int b[kBNF];
-#pragma unroll
-  for (int i = 0; i < kBNF; ++i) b[i] = s_box[0][i];
   const int box6[6] = {b[kBx], b[kBy], b[kBz], b[kBPI], b[kBH], b[kBD]};
   stage_box<S, kLabels>(a, vin, lin, box6, 0u, static_cast<uint32_t>(b[kBImgBytes]));
   const Params P = load_params(a.vol[vi]);
