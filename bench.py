@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
-    ap.add_argument("--variant", choices=["auto", "gather", "staged", "tma", "bulk", "persistent"], default="auto")
+    ap.add_argument("--variant", choices=["auto", "gather", "staged"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -297,9 +297,8 @@ def main():
     import paper_1811_11226_b200 as W
     from paper_1811_11226_b200.augment import FULL, build_params
 
-    variant = {"auto": W.KERNEL_AUTO, "gather": W.KERNEL_GATHER, "staged": W.KERNEL_STAGED,
-               "tma": W.KERNEL_TMA, "bulk": W.KERNEL_BULK,
-               "persistent": W.KERNEL_PERSISTENT}[args.variant]
+    variant = {"auto": W.KERNEL_AUTO, "gather": W.KERNEL_GATHER,
+               "staged": W.KERNEL_STAGED}[args.variant]
     wl = WORKLOADS[args.workload]
     shape = wl["shape"]
     vids, global_batch = shard(args.workload, world, rank)

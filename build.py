@@ -41,7 +41,8 @@ def build_oracle(force=False):
 
 CUDA_SOURCES = [
     "paper_1811_11226_b200/csrc/warp3d_host.cu",
-    "paper_1811_11226_b200/csrc/warp3d_kernels.cu",
+    "paper_1811_11226_b200/csrc/warp3d_cube.cu",
+    "paper_1811_11226_b200/csrc/warp3d_aux.cu",
 ]
 CUDA_HEADERS = [
     "include/warp3d.h",
@@ -57,8 +58,9 @@ def build_cuda(force=False):
     if force or _stale(out, srcs + hdrs):
         # No --use_fast_math and -fmad=false: the coordinate contract (R4)
         # and the trilinear lerp nesting use explicit __fmaf_rn, never contraction.
+        extra = os.environ.get("W3D_NVCC_EXTRA", "").split()  # experiment knobs (-DW3D_TZ=16)
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-              "-fmad=false", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"),
+              "-fmad=false", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), *extra,
               "-o", out, *srcs])
     return out
 

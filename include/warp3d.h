@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define WARP3D_ABI_VERSION 1
+#define WARP3D_ABI_VERSION 2
 
 typedef enum {
   W3D_OK = 0,
@@ -57,26 +57,20 @@ typedef enum {
   W3D_INTERP_NEAREST = 1   /* nearest, round half up (R7)                        */
 } w3d_interp;
 
-/* Kernel variant selector for warp3d_affine_batched_ex (tests / benchmarks). */
+/* Kernel variant selector for warp3d_affine_batched_ex (tests / benchmarks).
+   Both variants compute bit-identical results (same arithmetic, R4-R14).     */
 typedef enum {
-  W3D_KERNEL_AUTO = 0,     /* library choice: STAGED when the layout allows 16 B
-                              chunks (nx % 4 == 0, aligned input), else GATHER   */
-  W3D_KERNEL_GATHER = 1,   /* every corner gathered through L1/L2 (__ldg)        */
-  W3D_KERNEL_STAGED = 2,   /* per-tile source footprint staged in shared memory
-                              by cp.async; footprints larger than the buffer are
-                              split into 2 / 4 y-parts (gathers beyond that)      */
-  W3D_KERNEL_TMA = 3,      /* footprint staged by cp.async.bulk.tensor (TMA
-                              tensor boxes), large footprints split into 2 / 4
-                              y-parts; needs nx % 4 == 0 (with labels
-                              nx % 16 == 0) and 16 B aligned inputs, else
-                              W3D_ERR_UNSUPPORTED                                 */
-  W3D_KERNEL_BULK = 4,     /* as TMA, but each footprint row is one 1D
-                              cp.async.bulk copy (tight shared-memory layout);
-                              same requirements                                   */
-  W3D_KERNEL_PERSISTENT = 5 /* persistent CTAs (2 per SM) staging the next
-                              tile's footprint by cp.async while computing the
-                              current one; same layout requirements as STAGED
-                              (falls back to GATHER otherwise)                    */
+  W3D_KERNEL_AUTO = 0,     /* library choice = STAGED                            */
+  W3D_KERNEL_GATHER = 1,   /* every corner gathered through L1/L2 (__ldg) with
+                              per-corner bounds                                  */
+  W3D_KERNEL_STAGED = 2    /* per-tile source footprint staged in shared memory
+                              by cp.async (16 x 16 x 16 output tiles); a footprint
+                              larger than the buffer is split into 2 / 4 y-parts,
+                              gathered beyond that.  Layouts without 16 B chunks
+                              (nx % 4 != 0, unaligned input) and dims >= 2^21
+                              gather.  (Values 3-5 named TMA / bulk / persistent
+                              staging variants until ABI 1; removed after
+                              measuring slower.)               */
 } w3d_kernel;
 
 typedef struct {
@@ -108,7 +102,7 @@ typedef struct {
 
 typedef struct {
   float affine[12];    /* row-major [A | b]: OUTPUT voxel coords -> INPUT coords,
-                          p_k = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b_k))) in
+                          p_k = fma(A_k1, y, fma(A_k0, x, fma(A_k2, z, b_k))) in
                           fp32 (R4).  Finite, |A_kj| <= 2^20, |b_k| <= 2^30.      */
   w3d_photometric ph;
 } w3d_volume_params;   /* 96 bytes */

@@ -171,11 +171,11 @@ static voxel_result one_voxel(const float* in, const uint8_t* in_lbl, const int3
   uint32_t flags = ph ? ph->flags : 0u;
 
   /* Step 1 -- coordinate map p = A x + b, evaluated
-   * as fmaf(A_k0, x, fmaf(A_k1, y, fmaf(A_k2, z, b_k))) in fp32 (R4). */
+   * as fmaf(A_k1, y, fmaf(A_k0, x, fmaf(A_k2, z, b_k))) in fp32 (R4). */
   float X = (float)x, Y = (float)y, Z = (float)z;
   float p[3];
   for (int k = 0; k < 3; ++k)
-    p[k] = fmaf(A[4 * k + 0], X, fmaf(A[4 * k + 1], Y, fmaf(A[4 * k + 2], Z, A[4 * k + 3])));
+    p[k] = fmaf(A[4 * k + 1], Y, fmaf(A[4 * k + 0], X, fmaf(A[4 * k + 2], Z, A[4 * k + 3])));
 
   /* Label: nearest neighbour, round half up (R7),
    * label_fill when the nearest voxel is outside the volume (R8). */

@@ -17,7 +17,7 @@ W3D_OK, W3D_ERR_INVALID_ARG, W3D_ERR_UNSUPPORTED, W3D_ERR_CUDA, W3D_ERR_INTERNAL
 STATUS_NAMES = {0: "W3D_OK", 1: "W3D_ERR_INVALID_ARG", 2: "W3D_ERR_UNSUPPORTED",
                 3: "W3D_ERR_CUDA", 4: "W3D_ERR_INTERNAL"}
 INTERP_LINEAR, INTERP_NEAREST = 0, 1
-KERNEL_AUTO, KERNEL_GATHER, KERNEL_STAGED, KERNEL_TMA, KERNEL_BULK, KERNEL_PERSISTENT = range(6)
+KERNEL_AUTO, KERNEL_GATHER, KERNEL_STAGED = range(3)
 PH_NOISE, PH_WINDOW, PH_CLAMP, PH_GAMMA, PH_OCCLUDE = 1, 2, 4, 8, 16
 
 # every symbol include/warp3d.h declares (checked by tests/test_abi.py)

@@ -13,7 +13,6 @@ import torch
 
 from . import _lib as L
 from ._lib import (INTERP_LINEAR, INTERP_NEAREST, KERNEL_AUTO, KERNEL_GATHER, KERNEL_STAGED,
-                   KERNEL_TMA, KERNEL_BULK, KERNEL_PERSISTENT,
                    PH_CLAMP, PH_GAMMA, PH_NOISE, PH_OCCLUDE, PH_WINDOW, Geom, Photometric,
                    VolumeParams, Warp3DError)
 
@@ -23,7 +22,6 @@ __all__ = [
     "warp3d_tile_stats", "Pipeline",
     "warp3d_abi_version", "photometric", "volume_params", "make_geom", "Warp3DError",
     "INTERP_LINEAR", "INTERP_NEAREST", "KERNEL_AUTO", "KERNEL_GATHER", "KERNEL_STAGED",
-    "KERNEL_TMA", "KERNEL_BULK", "KERNEL_PERSISTENT",
     "PH_NOISE", "PH_WINDOW", "PH_CLAMP", "PH_GAMMA", "PH_OCCLUDE",
 ]
 

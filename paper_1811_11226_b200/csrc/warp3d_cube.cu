@@ -1,0 +1,969 @@
+// warp3d_cube.cu -- the default sm_100a kernel of the Sec. IV augmentation path
+// (Rister et al., arXiv 1811.11226).
+//
+// One CTA per 16 x TY x 16 output tile of one volume:
+//   1. every warp transforms the tile's 8 corners (p is monotone in each output
+//      coordinate, so their min/max bound every p of the tile exactly) and
+//      derives the tile's source footprint box -- no barrier needed;
+//   2. all threads stage the box into shared memory with cp.async (16 B image
+//      + 4 B label chunks; out-of-volume chunks are written with fill /
+//      label_fill, so the gathers need no per-corner predicate: R6, R8) while
+//      computing their first Philox block;
+//   3. thread = output column (x, z) (lane = 16 x by 2 z, half-warps on two
+//      z-planes: fewest bank conflicts, tools/model_tiles.py), rows y in groups
+//      of 4 (one Philox block each, R10), as y-pairs in packed fp32x2.
+// Per voxel, in the paper's order:
+//   p = A x + b (R4) -> floor / frac on the FMA pipe (magic-number add with
+//   round-down; indices read back from the float bits, no XU conversions) ->
+//   8 LDS + 7 lerps (R5) | nearest label (R7) -> noise (R9-R11) -> window /
+//   clamp (R12, R14) -> gamma (R13) -> store.
+// Tiles whose box exceeds the buffer are split into y-parts (whole Philox
+// blocks); a part that still does not fit is gathered through L1/L2.
+// Compiled without fast-math and with -fmad=false: every FMA is explicit.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdint>
+
+#include "philox.cuh"
+#include "warp3d_internal.cuh"
+
+namespace w3d {
+namespace cube {
+
+// Tile 16 x kTY x TZ output voxels; a warp = 16 x by 2 z, so TZ / 2 warps.
+#ifndef W3D_TZ
+#define W3D_TZ 16
+#endif
+constexpr int TX = 16, TZ = W3D_TZ, THREADS = 16 * TZ;
+constexpr float kM = 12582912.0f;       // 1.5 * 2^23: rm(p + kM) = kM + floor(p), |p| < 2^22
+constexpr int32_t kMbits = 0x4B400000;  // bit pattern of kM
+constexpr int kPlaneRes = 20;           // plane pitch = 20 (mod 32) words (bank spread)
+constexpr float kSane = 2097152.0f;     // 2^21: unclamped boxes only for |p| below this
+
+extern __shared__ __align__(16) unsigned char cube_smem[];
+
+__device__ unsigned long long g_cube_tiles[2];  // [staged, gathered] (warp3d_tile_stats)
+
+// dynamic shared memory, rounded up to 128 B (TMA destinations); the launch
+// reserves the slack
+__device__ __forceinline__ uint32_t smem_base() {
+  return (static_cast<uint32_t>(__cvta_generic_to_shared(cube_smem)) + 127u) & ~127u;
+}
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float2 add2_rm(float2 a, float2 b) {
+  float2 r;
+  asm("add.rm.ftz.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ float fset_ge_half(float t) {  // 1.0f if t >= 0.5 else 0.0f
+  float r;
+  asm("set.ge.f32.f32 %0, %1, 0f3F000000;" : "=f"(r) : "f"(t));
+  return r;
+}
+// lerp(a, b, t) = a + t (b - a): one rounding for the difference, one FMA (R5)
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) {
+  return __ffma2_rn(t, sub2(b, a), a);
+}
+__device__ __forceinline__ float lerp1(float a, float b, float t) {
+  return __fmaf_rn(t, __fsub_rn(b, a), a);
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ const float* gaddr_f32(const float* base, uint32_t off) {
+  const float* p;
+  asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(p) : "r"(off), "l"(base));
+  return p;
+}
+__device__ __forceinline__ const uint8_t* gaddr_u8(const uint8_t* base, uint32_t off) {
+  const uint8_t* p;
+  asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(p) : "r"(off), "l"(base));
+  return p;
+}
+
+// Pull-back coordinate (R4): p_k = fma(A_k1, y, fma(A_k0, x, fma(A_k2, z, b_k))).
+__device__ __forceinline__ float coord(const float* A, int k, float X, float Y, float Z) {
+  return __fmaf_rn(A[4 * k + 1], Y, __fmaf_rn(A[4 * k + 0], X, __fmaf_rn(A[4 * k + 2], Z,
+                                                                         A[4 * k + 3])));
+}
+
+// ---------------------------------------------------------------------------
+// Footprint box of output rows [y0, y1] of the tile (every lane returns the
+// same box).  Unclamped when it fits (then no clamp in the inner loop: the box
+// holds every corner, its out-of-volume part staged as fill); else from p
+// clamped to [-1, n] (the clamped coordinate reads only fill or gets weight 0
+// on in-volume voxels, which reproduces R6 / R8 exactly).
+// ---------------------------------------------------------------------------
+struct Box {
+  int bx, by, bz;  // element 0 = input voxel (bx, by, bz); cp.async boxes: bx % 4 == 0
+  int W, H, D, P;  // row pitch (W % 4 == 0), rows, planes, plane pitch (elements)
+  int Wl, Pl;      // label row / plane pitch (= W, P for cp.async boxes)
+  int bxl;         // label box origin x (TMA: bx rounded down to 16; cp.async: = bx)
+  bool clamp;
+};
+
+__device__ __forceinline__ void make_box(const float* mn, const float* mx, Box& b) {
+  const int lx = __float2int_rd(mn[0]), hx = __float2int_rd(mx[0]) + 1;
+  const int ly = __float2int_rd(mn[1]), hy = __float2int_rd(mx[1]) + 1;
+  const int lz = __float2int_rd(mn[2]), hz = __float2int_rd(mx[2]) + 1;
+  b.bx = lx & ~3;
+  b.by = ly;
+  b.bz = lz;
+  b.W = (hx - b.bx + 1 + 3) & ~3;
+  b.H = hy - ly + 1;
+  b.D = hz - lz + 1;
+  const int wh = b.W * b.H;
+  b.P = wh + ((kPlaneRes - wh) & 31);
+  b.Wl = b.W;
+  b.Pl = b.P;
+  b.bxl = b.bx;
+}
+
+__device__ __forceinline__ bool tile_box(const WarpArgs& a, const float* A, int ox, int y0,
+                                         int y1, int oz, int cap, Box& b) {
+  const int c = threadIdx.x & 7;
+  const float X = static_cast<float>((c & 1) ? min(ox + TX, a.mx) - 1 : ox);
+  const float Y = static_cast<float>((c & 2) ? y1 : y0);
+  const float Z = static_cast<float>((c & 4) ? min(oz + TZ, a.mz) - 1 : oz);
+  float mn[3], mx[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) mn[k] = mx[k] = coord(A, k, X, Y, Z);
+#pragma unroll
+  for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+      mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], off));
+    }
+  bool sane = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sane &= (mn[k] > -kSane) & (mx[k] < kSane);
+  if (sane) {
+    make_box(mn, mx, b);
+    if (b.P * b.D <= cap && b.W <= 4 * THREADS) {
+      b.clamp = false;
+      return true;
+    }
+  }
+  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                      static_cast<float>(a.nz)};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    mn[k] = fminf(fmaxf(mn[k], -1.0f), n[k]);
+    mx[k] = fminf(fmaxf(mx[k], -1.0f), n[k]);
+  }
+  make_box(mn, mx, b);
+  b.clamp = true;
+  return b.P * b.D <= cap && b.W <= 4 * THREADS;
+}
+
+// ---------------------------------------------------------------------------
+// Staging: thread t owns chunk column c = t % CW (4 voxels) of plane row
+// r = t / CW (+ 256 k when a plane has more than 256 chunks) and copies it in
+// every plane; in-volume chunks by cp.async (16 B image + 4 B label),
+// out-of-volume chunks set to fill / label_fill.  nx % 4 == 0 and bx % 4 == 0,
+// so a chunk is entirely inside or outside in x.
+// ---------------------------------------------------------------------------
+template <bool kLabels, bool kInside>
+__device__ __forceinline__ void stage_impl(const WarpArgs& a, const float* __restrict__ vin,
+                                           const uint8_t* __restrict__ lin, const Box& b,
+                                           uint32_t simg, uint32_t slbl) {
+  const int CW = b.W >> 2;
+  const int slots = CW * b.H;
+  const uint32_t plane = static_cast<uint32_t>(a.nx) * static_cast<uint32_t>(a.ny);
+  const float f = a.fill;
+  const uint32_t lf4 = a.label_fill * 0x01010101u;
+  for (int s = threadIdx.x; s < slots; s += THREADS) {
+    const int r = s / CW, c = s - r * CW;
+    const int gx = b.bx + 4 * c, gy = b.by + r;
+    const uint32_t e = static_cast<uint32_t>(r * b.W + 4 * c);
+    uint32_t si = simg + 4u * e, sl = slbl + e;
+    uint32_t goff = static_cast<uint32_t>(b.bz) * plane + static_cast<uint32_t>(gy * a.nx + gx);
+    const uint32_t sstep = static_cast<uint32_t>(b.P);
+    if (kInside) {
+#pragma unroll 4
+      for (int z = 0; z < b.D; ++z) {
+        cp_async16(si, gaddr_f32(vin, goff));
+        if (kLabels) cp_async4(sl, gaddr_u8(lin, goff));
+        si += 4u * sstep;
+        sl += sstep;
+        goff += plane;
+      }
+    } else {
+      const bool row_in = (static_cast<unsigned>(gx) < static_cast<unsigned>(a.nx)) &
+                          (static_cast<unsigned>(gy) < static_cast<unsigned>(a.ny));
+      for (int z = 0; z < b.D; ++z) {
+        const int gz = b.bz + z;
+        if (row_in & (static_cast<unsigned>(gz) < static_cast<unsigned>(a.nz))) {
+          cp_async16(si, gaddr_f32(vin, goff));
+          if (kLabels) cp_async4(sl, gaddr_u8(lin, goff));
+        } else {
+          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(si), "f"(f) : "memory");
+          if (kLabels) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl), "r"(lf4) : "memory");
+        }
+        si += 4u * sstep;
+        sl += sstep;
+        goff += plane;
+      }
+    }
+  }
+}
+
+template <bool kLabels>
+__device__ __forceinline__ void stage(const WarpArgs& a, const float* vin, const uint8_t* lin,
+                                      const Box& b, uint32_t simg, uint32_t slbl) {
+  const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
+                      b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
+  if (inside)
+    stage_impl<kLabels, true>(a, vin, lin, b, simg, slbl);
+  else
+    stage_impl<kLabels, false>(a, vin, lin, b, simg, slbl);
+}
+
+// ---------------------------------------------------------------------------
+// Per-thread constants of one staged part
+// ---------------------------------------------------------------------------
+// Values pinned in registers: ptxas would otherwise re-load loop invariants
+// from the (dynamically indexed) parameter bank inside the hot loop, one LDC
+// issue slot each.
+__device__ __forceinline__ float pin(float x) {
+  float y;
+  asm volatile("mov.b32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pin(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+// A warp-uniform value ptxas cannot see through (a shuffle from lane 0), so it
+// does not split constant parts off address bases into extra adds.  Every
+// lane of the warp must execute it.
+__device__ __forceinline__ uint32_t opaque(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
+
+struct View {
+  float Wf, Pf;           // pitches as floats
+  float Wlf, Plf;         // label pitches as floats
+  float Mby, Mbz;         // kM + by, kM + bz
+  uint32_t W4, P4;        // byte pitches of the image buffer
+  uint32_t cimg, clbl;    // image / label byte address = bits(L) * (4 | 1) + c
+  float nx, ny, nz;       // clamp bounds
+};
+
+__device__ __forceinline__ View make_view(const WarpArgs& a, const Box& b, uint32_t simg,
+                                          uint32_t slbl) {
+  View v;
+  v.Wf = pin(static_cast<float>(b.W));
+  v.Pf = pin(static_cast<float>(b.P));
+  v.Wlf = pin(static_cast<float>(b.Wl));
+  v.Plf = pin(static_cast<float>(b.Pl));
+  v.Mby = pin(kM + static_cast<float>(b.by));
+  v.Mbz = pin(kM + static_cast<float>(b.bz));
+  v.W4 = pin(4u * static_cast<uint32_t>(b.W));
+  v.P4 = pin(4u * static_cast<uint32_t>(b.P));
+  // bits(L) - kMbits = fx + W ry + P rz; element index = that - bx
+  v.cimg = opaque(simg - 4u * static_cast<uint32_t>(b.bx) - 4u * static_cast<uint32_t>(kMbits));
+  v.clbl = opaque(slbl - static_cast<uint32_t>(b.bxl) - static_cast<uint32_t>(kMbits));
+  v.nx = static_cast<float>(a.nx);
+  v.ny = static_cast<float>(a.ny);
+  v.nz = static_cast<float>(a.nz);
+  return v;
+}
+
+// Per-volume constants held by every thread.
+struct Vol {
+  float A1[3];            // y column of A
+  float sigma, ws, wo, lo, hi, gamma;
+  uint32_t flags;
+};
+
+enum { kPhGeneric = 0, kPhFull = 1 };
+
+// Photometric tail for a y-pair (PAPER.md:440-467 + gamma, R9-R14).
+// kPhFull: noise + window + clamp + gamma all on (host-checked), straight line.
+template <int kPh>
+__device__ __forceinline__ float2 photometric2(float2 img, float2 n, const Vol& V) {
+  const float2 v = __ffma2_rn(f2(V.sigma), n, img);  // I + sigma n (sigma = 0 without noise)
+  float2 w;
+  if (kPh == kPhFull) {
+    w.x = __saturatef(__fmaf_rn(v.x, V.ws, V.wo));    // min(max((I - a)/(b - a), 0), 1)
+    w.y = __saturatef(__fmaf_rn(v.y, V.ws, V.wo));
+    const float2 l = __fmul2_rn(make_float2(lg2_approx(w.x), lg2_approx(w.y)), f2(V.gamma));
+    return make_float2(ex2_approx(l.x), ex2_approx(l.y));
+  }
+  w = __ffma2_rn(v, f2(V.ws), f2(V.wo));
+  w.x = fminf(fmaxf(w.x, V.lo), V.hi);
+  w.y = fminf(fmaxf(w.y, V.lo), V.hi);
+  if (V.flags & kGamma) {
+    const float2 l = __fmul2_rn(make_float2(lg2_approx(w.x), lg2_approx(w.y)), f2(V.gamma));
+    w = make_float2(ex2_approx(l.x), ex2_approx(l.y));
+  }
+  return w;
+}
+
+// byte address bits * 4 + c  /  bits + c  (one IMAD / IADD, no re-association)
+__device__ __forceinline__ uint32_t addr4(float L, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(r) : "r"(__float_as_uint(L)), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t addr1(float L, uint32_t c) {
+  uint32_t r;
+  asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(__float_as_uint(L)), "r"(c));
+  return r;
+}
+// the two x-neighbours at addr and addr + 4
+__device__ __forceinline__ void lds_pair(uint32_t a, float& v0, float& v1) {
+  asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];"
+               : "=f"(v0), "=f"(v1)
+               : "r"(a));
+}
+
+// Staged sampling of a y-pair: image (trilinear or nearest) and label.
+template <bool kLabels, bool kNearest, bool kClamp>
+__device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, float2 pz,
+                                        float2& img, uint32_t& l0, uint32_t& l1) {
+  if (kClamp) {
+    px = make_float2(fminf(fmaxf(px.x, -1.0f), v.nx), fminf(fmaxf(px.y, -1.0f), v.nx));
+    py = make_float2(fminf(fmaxf(py.x, -1.0f), v.ny), fminf(fmaxf(py.y, -1.0f), v.ny));
+    pz = make_float2(fminf(fmaxf(pz.x, -1.0f), v.nz), fminf(fmaxf(pz.y, -1.0f), v.nz));
+  }
+  // floor on the FMA pipe: rm(p + kM) = kM + floor(p) exactly (|p| < 2^22)
+  const float2 sx = add2_rm(px, f2(kM)), sy = add2_rm(py, f2(kM)), sz = add2_rm(pz, f2(kM));
+  const float2 tx = sub2(px, sub2(sx, f2(kM)));
+  const float2 ty = sub2(py, sub2(sy, f2(kM)));
+  const float2 tz = sub2(pz, sub2(sz, f2(kM)));
+  const float2 ry = sub2(sy, f2(v.Mby)), rz = sub2(sz, f2(v.Mbz));
+  // kM + fx + W ry + P rz: exact integers below 2^24
+  const float2 L = __ffma2_rn(rz, f2(v.Pf), __ffma2_rn(ry, f2(v.Wf), sx));
+  float2 Ln = L;
+  if (kLabels || kNearest) {  // nearest voxel (R7): + (t >= 0.5) per axis
+    const float2 hx = make_float2(fset_ge_half(tx.x), fset_ge_half(tx.y));
+    const float2 hy = make_float2(fset_ge_half(ty.x), fset_ge_half(ty.y));
+    const float2 hz = make_float2(fset_ge_half(tz.x), fset_ge_half(tz.y));
+    if (kNearest) Ln = __ffma2_rn(hz, f2(v.Pf), __ffma2_rn(hy, f2(v.Wf), __fadd2_rn(L, hx)));
+    if (kLabels) {  // label buffer: own pitches (kM + fx + hx - bx + Wl (ry + hy) + Pl (rz + hz))
+      const float2 Ll = __ffma2_rn(__fadd2_rn(rz, hz), f2(v.Plf),
+                                   __ffma2_rn(__fadd2_rn(ry, hy), f2(v.Wlf), __fadd2_rn(sx, hx)));
+      l0 = lds_u8(addr1(Ll.x, v.clbl));
+      l1 = lds_u8(addr1(Ll.y, v.clbl));
+    }
+  }
+  if (kNearest) {
+    img = make_float2(lds_f32(addr4(Ln.x, v.cimg)), lds_f32(addr4(Ln.y, v.cimg)));
+    return;
+  }
+  const uint32_t a0 = addr4(L.x, v.cimg), b0 = addr4(L.y, v.cimg);
+  const uint32_t a1 = a0 + v.W4, b1 = b0 + v.W4, a2 = a0 + v.P4, b2 = b0 + v.P4;
+  const uint32_t a3 = a2 + v.W4, b3 = b2 + v.W4;
+  float2 c000, c100, c010, c110, c001, c101, c011, c111;
+  lds_pair(a0, c000.x, c100.x);
+  lds_pair(b0, c000.y, c100.y);
+  lds_pair(a1, c010.x, c110.x);
+  lds_pair(b1, c010.y, c110.y);
+  lds_pair(a2, c001.x, c101.x);
+  lds_pair(b2, c001.y, c101.y);
+  lds_pair(a3, c011.x, c111.x);
+  lds_pair(b3, c011.y, c111.y);
+  const float2 c00 = lerp2(c000, c100, tx), c10 = lerp2(c010, c110, tx);
+  const float2 c01 = lerp2(c001, c101, tx), c11 = lerp2(c011, c111, tx);
+  img = lerp2(lerp2(c00, c10, ty), lerp2(c01, c11, ty), tz);
+}
+
+// ---------------------------------------------------------------------------
+// Gather sampling of one voxel through L1/L2 with per-corner bounds (R6-R8,
+// NaN-safe float compares first).  Used for parts whose box does not fit.
+// ---------------------------------------------------------------------------
+template <bool kLabels, bool kNearest>
+__device__ __forceinline__ void sample_gather(const WarpArgs& a, const float* __restrict__ vin,
+                                              const uint8_t* __restrict__ lin, float px,
+                                              float py, float pz, float& img, uint32_t& lbl) {
+  img = a.fill;
+  lbl = a.label_fill;
+  const float fnx = static_cast<float>(a.nx), fny = static_cast<float>(a.ny),
+              fnz = static_cast<float>(a.nz);
+  const bool near_in = (px >= -0.5f) & (px < fnx - 0.5f) & (py >= -0.5f) & (py < fny - 0.5f) &
+                       (pz >= -0.5f) & (pz < fnz - 0.5f);
+  const bool any_in = (px > -1.0f) & (px < fnx) & (py > -1.0f) & (py < fny) & (pz > -1.0f) &
+                      (pz < fnz);
+  if (!any_in) return;  // then also !near_in
+  const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
+  const float tx = __fsub_rn(px, fx), ty = __fsub_rn(py, fy), tz = __fsub_rn(pz, fz);
+  const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+  const int64_t sy = a.nx, sz = static_cast<int64_t>(a.nx) * a.ny;
+  if (near_in && (kLabels || kNearest)) {
+    const int64_t r = (iz + (tz >= 0.5f)) * sz + (iy + (ty >= 0.5f)) * sy + (ix + (tx >= 0.5f));
+    if (kLabels) lbl = __ldg(lin + r);
+    if (kNearest) img = __ldg(vin + r);
+  }
+  if (kNearest) return;
+  const bool x0 = ix >= 0, x1 = ix + 1 < a.nx, y0 = iy >= 0, y1 = iy + 1 < a.ny;
+  const bool z0 = iz >= 0, z1 = iz + 1 < a.nz;
+  const float* b = vin + (iz * sz + iy * sy + ix);
+  const float f = a.fill;
+  const float c000 = (x0 & y0 & z0) ? __ldg(b) : f;
+  const float c100 = (x1 & y0 & z0) ? __ldg(b + 1) : f;
+  const float c010 = (x0 & y1 & z0) ? __ldg(b + sy) : f;
+  const float c110 = (x1 & y1 & z0) ? __ldg(b + sy + 1) : f;
+  const float c001 = (x0 & y0 & z1) ? __ldg(b + sz) : f;
+  const float c101 = (x1 & y0 & z1) ? __ldg(b + sz + 1) : f;
+  const float c011 = (x0 & y1 & z1) ? __ldg(b + sz + sy) : f;
+  const float c111 = (x1 & y1 & z1) ? __ldg(b + sz + sy + 1) : f;
+  const float c00 = lerp1(c000, c100, tx), c10 = lerp1(c010, c110, tx);
+  const float c01 = lerp1(c001, c101, tx), c11 = lerp1(c011, c111, tx);
+  img = lerp1(lerp1(c00, c10, ty), lerp1(c01, c11, ty), tz);
+}
+
+__device__ __forceinline__ void st_f32(float* p, float v) {
+  asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_u8(uint8_t* p, uint32_t v) {
+  asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// base + element offset in one IMAD.WIDE.U32
+__device__ __forceinline__ float* at(float* base, uint32_t off) {
+  float* r;
+  asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(r) : "r"(off), "l"(base));
+  return r;
+}
+__device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
+  uint8_t* r;
+  asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(r) : "r"(off), "l"(base));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Rows [y0, y0 + 4 ng) of the thread's output column (X, Z), 4-row groups.
+// kStaged: sample from the staged view v, else gather.  `n` holds the first
+// group's normals (computed while the staging copies were in flight); the next
+// group's Philox block is computed inside each iteration (independent chain).
+// ---------------------------------------------------------------------------
+template <bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp>
+__device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V0,
+                                            const View& v, int vi, int X, int Z, int y0, int ng,
+                                            float4 n) {
+  const float* __restrict__ vin = a.in + vi * a.in_stride;
+  const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+  Vol V = V0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) V.A1[k] = pin(V0.A1[k]);
+  V.sigma = pin(V0.sigma);
+  V.ws = pin(V0.ws);
+  V.wo = pin(V0.wo);
+  V.gamma = pin(V0.gamma);
+  const float fX = static_cast<float>(X), fZ = static_cast<float>(Z);
+  // x/z part of the coordinate, hoisted (R4 nesting)
+  const float t0 = __fmaf_rn(P.A[0], fX, __fmaf_rn(P.A[2], fZ, P.A[3]));
+  const float t1 = __fmaf_rn(P.A[4], fX, __fmaf_rn(P.A[6], fZ, P.A[7]));
+  const float t2 = __fmaf_rn(P.A[8], fX, __fmaf_rn(P.A[10], fZ, P.A[11]));
+  const int mx = a.mx, my = a.my;
+  const uint32_t mxu = pin(static_cast<uint32_t>(mx));
+  const uint32_t row1 = pin(mxu);
+  const uint32_t gyn = static_cast<uint32_t>((my + 3) >> 2);
+  const bool noise = kPh == kPhFull || (V.flags & kNoise);
+  const bool occl = kPh != kPhFull && (V.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;
+  const PhiloxPrefix pp{pin(P.ph_K0), pin(P.ph_K1), pin(P.ph_K2), pin(P.ph_U3)};
+  uint32_t rk0[10], rk1[10];
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {  // kPhFull: launch-wide keys at fixed parameter offsets
+    rk0[r] = kPh == kPhFull ? a.rk0[r] : pin(P.rk0[r]);
+    rk1[r] = kPh == kPhFull ? a.rk1[r] : pin(P.rk1[r]);
+  }
+  // output element offset of row y within the volume (< 2^31)
+  uint32_t o = static_cast<uint32_t>((Z * my + y0) * mx + X);
+  float* const vout = a.out + vi * a.out_stride;
+  uint8_t* const lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
+  uint32_t q = static_cast<uint32_t>(X) +
+               mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(y0 >> 2));
+  float2 Y2 = make_float2(static_cast<float>(y0), static_cast<float>(y0 + 1));
+#pragma unroll 1
+  for (int g = 0; g < ng; ++g) {
+    const int y = y0 + 4 * g;
+    if (y >= my) break;
+    float4 nn = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (noise && g + 1 < ng) nn = box_muller4(philox_block(q + mxu, pp, rk0, rk1));
+    const float ns[4] = {n.x, n.y, n.z, n.w};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ya = y + 2 * h;
+      if (ya >= my) break;
+      const float2 px = __ffma2_rn(f2(V.A1[0]), Y2, f2(t0));
+      const float2 py = __ffma2_rn(f2(V.A1[1]), Y2, f2(t1));
+      const float2 pz = __ffma2_rn(f2(V.A1[2]), Y2, f2(t2));
+      Y2 = __fadd2_rn(Y2, make_float2(2.0f, 2.0f));
+      float2 img;
+      uint32_t l0 = 0, l1 = 0;
+      if (kStaged) {
+        sample2<kLabels, kNearest, kClamp>(v, px, py, pz, img, l0, l1);
+      } else {
+        sample_gather<kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
+        sample_gather<kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
+      }
+      float2 out = photometric2<kPh>(img, make_float2(ns[2 * h], ns[2 * h + 1]), V);
+      if (occl) out = make_float2(0.0f, 0.0f);  // PAPER.md:437-438, R15
+      const bool second = ya + 1 < my;
+      const uint32_t o1 = o + row1;
+      st_f32(at(vout, o), out.x);
+      if (second) st_f32(at(vout, o1), out.y);
+      if (kLabels) {
+        st_u8(at(lout, o), l0);
+        if (second) st_u8(at(lout, o1), l1);
+      }
+      o = o1 + row1;
+    }
+    n = nn;
+    q += mxu;
+  }
+}
+
+__device__ __forceinline__ Vol load_vol(const VolDev& P) {
+  Vol V;
+  V.A1[0] = P.A[1];
+  V.A1[1] = P.A[5];
+  V.A1[2] = P.A[9];
+  V.sigma = P.sigma;
+  V.ws = P.win_s;
+  V.wo = P.win_off;
+  V.lo = P.clamp_lo;
+  V.hi = P.clamp_hi;
+  V.gamma = P.gamma;
+  V.flags = P.flags;
+  return V;
+}
+
+template <int kPh>
+__device__ __forceinline__ float4 first_normals(const WarpArgs& a, const VolDev& P, const Vol& V,
+                                                int X, int Z, int y0) {
+  if (!(kPh == kPhFull || (V.flags & kNoise))) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t gyn = static_cast<uint32_t>((a.my + 3) >> 2);
+  const uint32_t q = static_cast<uint32_t>(X) +
+                     static_cast<uint32_t>(a.mx) * (gyn * static_cast<uint32_t>(Z) +
+                                                    static_cast<uint32_t>(y0 >> 2));
+  const PhiloxPrefix pp{P.ph_K0, P.ph_K1, P.ph_K2, P.ph_U3};
+  return box_muller4(philox_block(q, pp, kPh == kPhFull ? a.rk0 : P.rk0,
+                                  kPh == kPhFull ? a.rk1 : P.rk1));
+}
+
+// Rare path (out of line): the tile in y-parts of TY/2, TY/4, ... rows, each
+// staged on its own, or gathered when even a 4-row part does not fit (or
+// always, for the W3D_KERNEL_GATHER variant).
+template <int TY, bool kLabels, bool kNearest, int kPh>
+__device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_x, int tiles_y, int cap,
+                                        bool gather_only) {
+  const int vi = static_cast<int>(blockIdx.y);
+  const int t = static_cast<int>(blockIdx.x);
+  const int txy = tiles_x * tiles_y;
+  const int tz = t / txy, r = t - tz * txy, ty = r / tiles_x, tx = r - ty * tiles_x;
+  const int ox = tx * TX, oy = ty * TY, oz = tz * TZ;
+  const uint32_t simg = smem_base();
+  const VolDev& P = a.vol[vi];
+  const Vol V = load_vol(P);
+  const float* vin = a.in + vi * a.in_stride;
+  const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+  const int lane = threadIdx.x & 31;
+  const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
+  const bool live = X < a.mx && Z < a.mz;
+  const int ylast = min(oy + TY, a.my) - 1;
+  int rows = gather_only ? 0 : TY / 2;
+  Box b;
+  // largest part size whose every part fits
+  for (; rows >= 4; rows >>= 1) {
+    bool all = true;
+    for (int y = oy; y <= ylast; y += rows)
+      all &= tile_box(a, P.A, ox, y, min(y + rows - 1, ylast), oz, cap, b);
+    if (all) break;
+  }
+  if (rows < 4) {  // gathers
+    if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[1], 1ull);
+    if (!live) return;
+    View v;
+    column_rows<kLabels, kNearest, kPh, false, false>(a, P, V, v, vi, X, Z, oy, TY / 4,
+                                                      first_normals<kPh>(a, P, V, X, Z, oy));
+    return;
+  }
+  if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[0], 1ull);
+  for (int y = oy; y <= ylast; y += rows) {
+    tile_box(a, P.A, ox, y, min(y + rows - 1, ylast), oz, cap, b);
+    const uint32_t slbl = simg + 4u * static_cast<uint32_t>(b.P * b.D);
+    __syncthreads();  // previous part's buffer no longer read
+    stage<kLabels>(a, vin, lin, b, simg, slbl);
+    const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, y) : make_float4(0, 0, 0, 0);
+    const View v = make_view(a, b, simg, slbl);
+    cp_async_wait_all();
+    __syncthreads();
+    if (!live) continue;
+    if (b.clamp)
+      column_rows<kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, y, rows / 4, n);
+    else
+      column_rows<kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, y, rows / 4, n);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// TMA staging (the default): the tile's footprint box is ONE 3D tensor box of
+// the volume (dims fixed per volume: every full tile of an affine warp has the
+// same footprint extent, host-computed by cube_tma_box), loaded by one thread
+// with cp.async.bulk.tensor into shared memory, completion on an mbarrier.
+// Out-of-volume elements arrive as 0; boxes that leave the volume get fill /
+// label_fill written over them before the compute (R6, R8).  Image and label
+// boxes share the origin; the label rows have their own pitch (16 B rows).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+// Bounded wait: a TMA that never completes traps (a launch error) instead of
+// hanging the device.
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  for (uint32_t tries = 0;; ++tries) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (tries > (1u << 22)) {
+#ifdef W3D_DEBUG_TMA
+      if ((threadIdx.x & 31) == 0) printf("mbar timeout blk %d %d thr %d\n", blockIdx.x, blockIdx.y, threadIdx.x);
+      return;
+#else
+      __trap();
+#endif
+    }
+  }
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            int z, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(mbar)
+      : "memory");
+}
+
+// The tile's box in the volume's fixed TMA dims; false if the footprint does
+// not fit them (then the cp.async path takes the tile).
+__device__ __forceinline__ bool tma_box(const WarpArgs& a, const VolDev& P, int ox, int y0, int y1,
+                                        int oz, Box& b) {
+  const int c = threadIdx.x & 7;
+  const float X = static_cast<float>((c & 1) ? min(ox + TX, a.mx) - 1 : ox);
+  const float Y = static_cast<float>((c & 2) ? y1 : y0);
+  const float Z = static_cast<float>((c & 4) ? min(oz + TZ, a.mz) - 1 : oz);
+  float mn[3], mx[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) mn[k] = mx[k] = coord(P.A, k, X, Y, Z);
+#pragma unroll
+  for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+      mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], off));
+    }
+  bool sane = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sane &= (mn[k] > -kSane) & (mx[k] < kSane);
+  if (!sane) return false;
+  // TMA box inner origins must be 16 B aligned: image x0 % 4, label x0 % 16
+  const int lx = __float2int_rd(mn[0]);
+  b.bx = lx & ~3;
+  b.bxl = lx & ~15;
+  b.by = __float2int_rd(mn[1]);
+  b.bz = __float2int_rd(mn[2]);
+  b.W = P.box_w;
+  b.H = P.box_h;
+  b.D = P.box_d;
+  b.P = b.W * b.H;
+  b.Wl = P.box_wl;
+  b.Pl = b.Wl * b.H;
+  b.clamp = false;
+  const int hx = __float2int_rd(mx[0]) + 1;
+  return hx - b.bx < b.W && hx - b.bxl < b.Wl && __float2int_rd(mx[1]) + 1 - b.by < b.H &&
+         __float2int_rd(mx[2]) + 1 - b.bz < b.D;
+}
+
+// fill / label_fill over the out-of-volume elements of a TMA box (TMA wrote 0);
+// rows [0, W) of the image box and [0, Wl) of the label box.
+template <bool kLabels>
+__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint32_t simg,
+                                          uint32_t slbl, bool fi, bool fl) {
+  const float f = a.fill;
+  const uint32_t lf4 = a.label_fill * 0x01010101u;
+  const int head = min(b.W, max(0, -b.bx)), tail = max(0, min(b.W, a.nx - b.bx));
+  const int headl = min(b.Wl, max(0, -b.bxl)), taill = max(0, min(b.Wl, a.nx - b.bxl));
+  for (int r = threadIdx.x; r < b.H * b.D; r += THREADS) {
+    const int z = r / b.H, y = r - z * b.H;
+    const bool row_out = static_cast<unsigned>(b.bz + z) >= static_cast<unsigned>(a.nz) ||
+                         static_cast<unsigned>(b.by + y) >= static_cast<unsigned>(a.ny);
+    const uint32_t irow = simg + 4u * static_cast<uint32_t>(z * b.P + y * b.W);
+    const uint32_t lrow = slbl + static_cast<uint32_t>(z * b.Pl + y * b.Wl);
+    if (row_out) {
+      if (fi)
+        for (int x = 0; x < b.W; x += 4)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(irow + 4u * x), "f"(f)
+                       : "memory");
+      if (kLabels && fl)
+        for (int x = 0; x < b.Wl; x += 16)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(lrow + x), "r"(lf4)
+                       : "memory");
+      continue;
+    }
+    if (fi) {
+      for (int x = 0; x < head; ++x)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(irow + 4u * x), "f"(f) : "memory");
+      for (int x = tail; x < b.W; ++x)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(irow + 4u * x), "f"(f) : "memory");
+    }
+    if (kLabels && fl) {
+      for (int x = 0; x < headl; ++x)
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
+      for (int x = taill; x < b.Wl; ++x)
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
+    }
+  }
+}
+
+// grid = (tiles per volume, volumes); tiles x-fastest, then y, then z.
+template <int TY, int MINB, bool kLabels, bool kNearest, int kPh, bool kGather>
+__global__ void __launch_bounds__(THREADS, MINB)
+    warp3d_cube_kernel(const __grid_constant__ WarpArgs a, const int tiles_x, const int tiles_y,
+                       const int cap) {
+  __shared__ __align__(8) unsigned long long s_mbar;
+  const int vi = static_cast<int>(blockIdx.y);
+  const int t = static_cast<int>(blockIdx.x);
+  const int txy = tiles_x * tiles_y;
+  const int tz = t / txy, r = t - tz * txy, ty = r / tiles_x, tx = r - ty * tiles_x;
+  const int ox = tx * TX, oy = ty * TY, oz = tz * TZ;
+  const uint32_t simg = smem_base();
+  const VolDev& P = a.vol[vi];
+  const int ylast = min(oy + TY, a.my) - 1;
+  Box b;
+  const bool use_tma = !kGather && a.use_tma && vi < kTmaVolPerLaunch && P.box_w != 0;
+  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
+  if (use_tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  const bool tma = use_tma && tma_box(a, P, ox, oy, ylast, oz, b);
+  if (!tma) {
+    if (kGather || !tile_box(a, P.A, ox, oy, ylast, oz, cap, b)) {
+      tile_parts<TY, kLabels, kNearest, kPh>(a, tiles_x, tiles_y, cap, kGather);
+      return;
+    }
+  }
+  if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[0], 1ull);
+  uint32_t slbl;
+  if (tma) {
+    slbl = simg + ((4u * static_cast<uint32_t>(b.P * b.D) + 127u) & ~127u);
+#ifdef W3D_DEBUG_TMA
+    if (threadIdx.x == 0 && blockIdx.x < 3)
+      printf("blk %d vol %d box o=(%d %d %d) WHD=(%d %d %d) Wl=%d P=%d Pl=%d simg=%u slbl=%u\n",
+             blockIdx.x, vi, b.bx, b.by, b.bz, b.W, b.H, b.D, b.Wl, b.P, b.Pl, simg, slbl);
+#endif
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(mbar, 4u * static_cast<uint32_t>(b.P * b.D) +
+                               (kLabels ? static_cast<uint32_t>(b.Pl * b.D) : 0u));
+      tma_load_3d(simg, &a.tm[2 * vi], b.bx, b.by, b.bz, mbar);
+      if (kLabels) tma_load_3d(slbl, &a.tm[2 * vi + 1], b.bxl, b.by, b.bz, mbar);
+    }
+  } else {
+    slbl = simg + 4u * static_cast<uint32_t>(b.P * b.D);
+    stage<kLabels>(a, a.in + vi * a.in_stride, kLabels ? a.in_lbl + vi * a.in_stride : nullptr,
+                   b, simg, slbl);
+  }
+  const Vol V = load_vol(P);
+  const int lane = threadIdx.x & 31;
+  const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
+  const bool live = X < a.mx && Z < a.mz;
+  // the first Philox block overlaps the copies in flight
+  const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, oy) : make_float4(0, 0, 0, 0);
+  const View v = make_view(a, b, simg, slbl);
+  if (tma) {
+    mbar_wait(mbar, 0);
+    const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
+                        b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
+    const bool fi = a.fill != 0.0f, fl = kLabels && a.label_fill != 0u;
+    if (!inside && (fi || fl)) {
+      tma_fixup<kLabels>(a, b, simg, slbl, fi, fl);
+      __syncthreads();
+    }
+  } else {
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  if (!live) return;
+  if (b.clamp)
+    column_rows<kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
+  else
+    column_rows<kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
+}
+
+// ---------------------------------------------------------------------------
+// Launch
+// ---------------------------------------------------------------------------
+#ifndef W3D_MINB
+#define W3D_MINB (TZ > 16 ? 2 : 4)
+#endif
+constexpr int kTY = 16, kMinB = W3D_MINB;
+// staging buffer (voxels of 5 B): kMinB * (kCapVox * 5 B + 256 + 1 KB) <= 228 KB
+constexpr int kCapVox = (233472 / kMinB - 1024 - 272) / 5;
+
+template <bool kLabels, bool kNearest, int kPh, bool kGather = false>
+static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
+  const int tiles_x = (a.mx + TX - 1) / TX, tiles_y = (a.my + kTY - 1) / kTY;
+  const int tiles_z = (a.mz + TZ - 1) / TZ;
+  const int64_t per_vol = static_cast<int64_t>(tiles_x) * tiles_y * tiles_z;
+  if (per_vol >= (int64_t(1) << 31) || a.nvol > 65535) return cudaErrorInvalidConfiguration;
+  const size_t smem = kGather ? 0 : static_cast<size_t>(kCapVox) * 5 + 256;
+  static bool configured = false;
+  if (!configured && !kGather) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        warp3d_cube_kernel<kTY, kMinB, kLabels, kNearest, kPh, kGather>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const dim3 grid(static_cast<unsigned>(per_vol), static_cast<unsigned>(a.nvol));
+  warp3d_cube_kernel<kTY, kMinB, kLabels, kNearest, kPh, kGather>
+      <<<grid, THREADS, smem, s>>>(a, tiles_x, tiles_y, kCapVox);
+  return cudaGetLastError();
+}
+
+// The full photometric chain on every volume of the launch (the training
+// configuration): noise, window + clamp to [0, 1], gamma != 1, no occlusion.
+// ... and one seed for every volume (the round keys are launch constants, a.rk*).
+static bool all_full(const WarpArgs& a) {
+  for (int i = 0; i < a.nvol; ++i) {
+    const VolDev& P = a.vol[i];
+    if (P.flags != (kNoise | kGamma) || P.clamp_lo != 0.0f || P.clamp_hi != 1.0f) return false;
+    if (P.key0 != a.vol[0].key0 || P.key1 != a.vol[0].key1) return false;
+  }
+  return true;
+}
+
+}  // namespace cube
+
+// Coordinates must stay below 2^21 for the magic-number floor, pitches below
+// the float-exact range; dims up to 2^21 per axis qualify.
+bool cube_supported(const WarpArgs& a) {
+  return (a.nx % 4 == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) &&
+         (a.in_stride % 4 == 0) &&
+         (a.in_lbl == nullptr || reinterpret_cast<uintptr_t>(a.in_lbl) % 4 == 0) &&
+         a.nx < (1 << 21) && a.ny < (1 << 21) && a.nz < (1 << 21);
+}
+
+// gather_only (W3D_KERNEL_GATHER, or layouts cube_supported() rejects): every
+// tile through L1/L2 gathers.
+cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s) {
+  using namespace cube;
+  const bool labels = a.in_lbl != nullptr;
+  const bool nearest = a.interp == W3D_INTERP_NEAREST;
+  cudaError_t e;
+  if (gather_only || !cube_supported(a)) {
+    if (nearest)
+      e = labels ? launch_v<true, true, kPhGeneric, true>(a, s)
+                 : launch_v<false, true, kPhGeneric, true>(a, s);
+    else
+      e = labels ? launch_v<true, false, kPhGeneric, true>(a, s)
+                 : launch_v<false, false, kPhGeneric, true>(a, s);
+  } else if (nearest)
+    e = labels ? launch_v<true, true, kPhGeneric>(a, s) : launch_v<false, true, kPhGeneric>(a, s);
+  else if (all_full(a))
+    e = labels ? launch_v<true, false, kPhFull>(a, s) : launch_v<false, false, kPhFull>(a, s);
+  else
+    e = labels ? launch_v<true, false, kPhGeneric>(a, s) : launch_v<false, false, kPhGeneric>(a, s);
+  note_launch();
+  return e;
+}
+
+bool cube_tma_supported(const WarpArgs& a) {
+  // 16 B aligned global strides and volume bases for the image (and labels)
+  const bool img = cube_supported(a) && a.nx % 4 == 0 && a.in_stride % 4 == 0;
+  const bool lbl = a.in_lbl == nullptr ||
+                   (a.nx % 16 == 0 && a.in_stride % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(a.in_lbl) % 16 == 0);
+  return img && lbl && a.interp == W3D_INTERP_LINEAR;
+}
+
+// TMA box dims of one volume: the footprint extent of a full tile, ext_k =
+// sum_j |A_kj| (T_j - 1) input voxels, plus the trilinear +1 corner, the floor
+// offsets and a rounding margin; rows padded to 16 B (labels: 16 elements);
+// rows per plane padded so the plane pitch spreads the two half-warps over the
+// banks (tools/model_tiles.py).  box_w = 0 when the box exceeds the buffer.
+void cube_tma_box(const float A[12], VolDev& P, bool labels) {
+  using namespace cube;
+  const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
+  int d[3];
+  for (int k = 0; k < 3; ++k) {
+    double ext = 0.0, mag = std::fabs(double(A[4 * k + 3]));
+    for (int j = 0; j < 3; ++j) {
+      ext += std::fabs(double(A[4 * k + j])) * span[j];
+      mag += std::fabs(double(A[4 * k + j])) * 2097152.0;
+    }
+    // fp32 evaluation of p (3 roundings each) moves max - min by < 6 ulp(|p|)
+    const double margin = 6.0 * mag * 0x1.0p-24 + 1e-6;
+    d[k] = static_cast<int>(std::floor(ext + margin)) + 3;
+  }
+  P.box_w = P.box_h = P.box_d = P.box_wl = 0;
+  // + alignment slack of the 16 B aligned inner origins (image x0 % 4, labels % 16)
+  int W = (d[0] + 3 + 3) & ~3, H = d[1], D = d[2];
+  const int Wl = (d[0] + 15 + 15) & ~15;
+  for (int h = H; h < H + 8; ++h) {
+    const int res = (W * h) & 31;
+    if (res == 20 || res == 24 || res == 16 || res == 12) {
+      H = h;
+      break;
+    }
+  }
+  if (W > 256 || H > 256 || D > 256) return;
+  const int64_t bytes = ((int64_t(4) * W * H * D + 127) & ~int64_t(127)) +
+                        (labels ? int64_t(Wl) * H * D : 0);
+  if (bytes > int64_t(kCapVox) * 5) return;
+  P.box_w = static_cast<uint16_t>(W);
+  P.box_h = static_cast<uint16_t>(H);
+  P.box_d = static_cast<uint16_t>(D);
+  P.box_wl = static_cast<uint16_t>(Wl);
+}
+
+cudaError_t read_cube_stats(unsigned long long out[2]) {
+  return cudaMemcpyFromSymbol(out, cube::g_cube_tiles, 2 * sizeof(unsigned long long));
+}
+
+}  // namespace w3d

@@ -11,9 +11,11 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
+#include "philox.cuh"
 #include "warp3d.h"
 #include "warp3d_internal.cuh"
 
@@ -154,13 +156,19 @@ static VolDev derive(const float* A, const w3d_photometric* ph) {
     P.rk0[r] = P.key0 + static_cast<uint32_t>(r) * 0x9E3779B9u;
     P.rk1[r] = P.key1 + static_cast<uint32_t>(r) * 0xBB67AE85u;
   }
+  const PhiloxPrefix pp = philox_prefix(P.vid0, P.vid1, P.key0, P.key1);
+  P.ph_K0 = pp.K0;
+  P.ph_K1 = pp.K1;
+  P.ph_K2 = pp.K2;
+  P.ph_U3 = pp.U3;
   return P;
 }
 
 // ---------------------------------------------------------------------------
-// TMA tensor maps (one per width class) for the launch chunk's input volumes.
+// TMA tensor maps: one 3D map per volume for the image (float32) and one for
+// the labels (uint8), box dims = the volume's tile footprint (cube_tma_box).
 // Encoded with the driver's cuTensorMapEncodeTiled (fetched through the
-// runtime), cached per (pointers, dims, volumes).
+// runtime); a per-slot cache skips re-encoding identical maps.
 // ---------------------------------------------------------------------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -184,47 +192,63 @@ static EncodeFn get_encode() {
   return fn;
 }
 
-cudaError_t encode_tensor_maps(WarpArgs& a) {
+static bool encode_3d(CUtensorMap* m, bool u8, const void* base, const WarpArgs& a, uint32_t bw,
+                      uint32_t bh, uint32_t bd) {
   EncodeFn enc = get_encode();
-  if (!enc) return cudaErrorNotSupported;
-  const cuuint64_t dims[4] = {cuuint64_t(a.nx), cuuint64_t(a.ny), cuuint64_t(a.nz),
-                              cuuint64_t(a.nvol)};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  {
-    const cuuint64_t strides[3] = {cuuint64_t(a.nx) * 4, cuuint64_t(a.nx) * a.ny * 4,
-                                   cuuint64_t(a.in_stride) * 4};
-    for (int c = 0; c < kNumImgCls; ++c) {
-      const cuuint32_t box[4] = {cuuint32_t(img_cls_width(c)), cuuint32_t(kTmaRowsImg), 1, 1};
-      if (enc(&a.tm_img[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a.in), dims,
-              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
-    }
-  }
-  if (a.in_lbl) {
-    const cuuint64_t strides[3] = {cuuint64_t(a.nx), cuuint64_t(a.nx) * a.ny,
-                                   cuuint64_t(a.in_stride)};
-    for (int c = 0; c < kNumLblCls; ++c) {
-      const cuuint32_t box[4] = {cuuint32_t(lbl_cls_width(c)), cuuint32_t(kTmaRowsLbl), 1, 1};
-      if (enc(&a.tm_lbl[c], CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(a.in_lbl), dims,
-              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
-    }
-  }
-  return cudaSuccess;
+  if (!enc) return false;
+  const cuuint64_t es = u8 ? 1 : 4;
+  const cuuint64_t dims[3] = {cuuint64_t(a.nx), cuuint64_t(a.ny), cuuint64_t(a.nz)};
+  const cuuint64_t strides[2] = {cuuint64_t(a.nx) * es, cuuint64_t(a.nx) * a.ny * es};
+  const cuuint32_t box[3] = {bw, bh, bd};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-struct TmaKey {
-  const void* in = nullptr;
-  const void* lbl = nullptr;
-  int32_t nx = 0, ny = 0, nz = 0, nvol = 0;
-  bool valid = false;
-  bool operator==(const TmaKey& o) const {
-    return in == o.in && lbl == o.lbl && nx == o.nx && ny == o.ny && nz == o.nz &&
-           nvol == o.nvol && valid == o.valid;
+struct MapKey {
+  const void* base = nullptr;
+  int32_t nx = 0, ny = 0, nz = 0;
+  uint32_t bw = 0, bh = 0, bd = 0;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && nx == o.nx && ny == o.ny && nz == o.nz && bw == o.bw &&
+           bh == o.bh && bd == o.bd;
   }
 };
+
+// Tensor maps of the launch chunk in `args` (volumes whose box fits); returns
+// false (and clears every box) when encoding is unavailable.
+static bool prepare_tma(WarpArgs& args, const float* const* affines) {
+  static thread_local MapKey key_img[kTmaVolPerLaunch], key_lbl[kTmaVolPerLaunch];
+  const bool labels = args.in_lbl != nullptr;
+  bool ok = get_encode() != nullptr;
+  for (int32_t i = 0; i < args.nvol && ok; ++i) {
+    VolDev& P = args.vol[i];
+    if (i >= kTmaVolPerLaunch) break;
+    cube_tma_box(affines[i], P, labels);
+    if (!P.box_w) continue;
+    MapKey ki{args.in + i * args.in_stride, args.nx, args.ny, args.nz, P.box_w, P.box_h,
+              P.box_d};
+    if (!(ki == key_img[i])) {
+      key_img[i] = MapKey();
+      ok = encode_3d(&args.tm[2 * i], false, ki.base, args, ki.bw, ki.bh, ki.bd);
+      if (ok) key_img[i] = ki;
+    }
+    if (ok && labels) {
+      MapKey kl{args.in_lbl + i * args.in_stride, args.nx, args.ny, args.nz, P.box_wl, P.box_h,
+                P.box_d};
+      if (!(kl == key_lbl[i])) {
+        key_lbl[i] = MapKey();
+        ok = encode_3d(&args.tm[2 * i + 1], true, kl.base, args, kl.bw, kl.bh, kl.bd);
+        if (ok) key_lbl[i] = kl;
+      }
+    }
+  }
+  if (!ok)
+    for (int32_t i = 0; i < args.nvol; ++i) args.vol[i].box_w = 0;
+  return ok;
+}
 
 // One batch, already validated; chunks of kMaxVolPerLaunch volumes.
 static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_labels,
@@ -232,11 +256,13 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
                               const w3d_photometric* const* phs, w3d_interp interp, float fill,
                               uint8_t label_fill, float* out, uint8_t* out_labels,
                               w3d_dims out_dims, w3d_kernel variant, cudaStream_t stream) {
-  static thread_local WarpArgs args;  // ~26 KB: keep off the stack
-  static thread_local TmaKey tma_key;  // tensor maps currently encoded in args
+  static thread_local WarpArgs args;  // ~31 KB: keep off the stack
   const int64_t in_n = nvox(in_dims), out_n = nvox(out_dims);
-  for (int32_t v0 = 0; v0 < batch; v0 += kMaxVolPerLaunch) {
-    const int32_t nv = (batch - v0 < kMaxVolPerLaunch) ? batch - v0 : kMaxVolPerLaunch;
+  static const bool no_tma = getenv("W3D_NO_TMA") && getenv("W3D_NO_TMA")[0] == '1';
+  const bool want_tma = variant != W3D_KERNEL_GATHER && !no_tma;
+  const int32_t chunk = want_tma ? kTmaVolPerLaunch : kMaxVolPerLaunch;
+  for (int32_t v0 = 0; v0 < batch; v0 += chunk) {
+    const int32_t nv = (batch - v0 < chunk) ? batch - v0 : chunk;
     args.in = in + v0 * in_n;
     args.in_lbl = in_labels ? in_labels + v0 * in_n : nullptr;
     args.out = out + v0 * out_n;
@@ -250,34 +276,16 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
     args.interp = interp;
     args.nvol = nv;
     for (int32_t i = 0; i < nv; ++i) args.vol[i] = derive(affines[v0 + i], phs[v0 + i]);
-    args.use_tma = 0;
-    if (variant == W3D_KERNEL_TMA && tma_supported(args)) {
-      TmaKey k;
-      k.in = args.in; k.lbl = args.in_lbl;
-      k.nx = args.nx; k.ny = args.ny; k.nz = args.nz; k.nvol = nv; k.valid = true;
-      if (k == tma_key) {
-        args.use_tma = 1;
-      } else if (encode_tensor_maps(args) == cudaSuccess) {
-        tma_key = k;
-        args.use_tma = 1;
-      } else {
-        tma_key = TmaKey();
-      }
+    for (int r = 0; r < 10; ++r) {  // volume 0's key schedule (used when all seeds agree)
+      args.rk0[r] = args.vol[0].rk0[r];
+      args.rk1[r] = args.vol[0].rk1[r];
     }
-    if (variant == W3D_KERNEL_TMA && !args.use_tma)
-      return fail(W3D_ERR_UNSUPPORTED,
-                  "W3D_KERNEL_TMA needs nx %% 4 == 0 (labels: nx %% 16 == 0), 16 B aligned "
-                  "inputs and cuTensorMapEncodeTiled");
-    if (variant == W3D_KERNEL_BULK && !tma_supported(args))
-      return fail(W3D_ERR_UNSUPPORTED,
-                  "W3D_KERNEL_BULK needs nx %% 4 == 0 (labels: nx %% 16 == 0) and 16 B aligned "
-                  "inputs");
-    const cudaError_t e = (variant == W3D_KERNEL_GATHER)   ? launch_gather(args, stream)
-                          : (variant == W3D_KERNEL_STAGED) ? launch_staged(args, stream)
-                          : (variant == W3D_KERNEL_TMA)    ? launch_tma(args, stream)
-                          : (variant == W3D_KERNEL_BULK)   ? launch_bulk(args, stream)
-                          : (variant == W3D_KERNEL_PERSISTENT) ? launch_persistent_api(args, stream)
-                                                           : launch_auto(args, stream);
+    args.use_tma = 0;
+    if (want_tma && cube_tma_supported(args))
+      args.use_tma = prepare_tma(args, affines + v0) ? 1 : 0;
+    // AUTO / STAGED: the staged cube kernel (it gathers by itself when the
+    // layout does not allow 16 B chunks); GATHER: every tile gathered.
+    const cudaError_t e = launch_cube(args, variant == W3D_KERNEL_GATHER, stream);
     if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");
   }
   return ok();
@@ -313,7 +321,7 @@ uint64_t warp3d_launch_count(void) { return g_launches.load(); }
 w3d_status warp3d_tile_stats(uint64_t out[2]) {
   if (!out) return fail(W3D_ERR_INVALID_ARG, "out must be non-NULL");
   unsigned long long v[2] = {0, 0};
-  const cudaError_t e = read_tile_stats(v);
+  const cudaError_t e = read_cube_stats(v);
   if (e != cudaSuccess) return cuda_fail(e, "warp3d_tile_stats");
   out[0] = v[0];
   out[1] = v[1];
@@ -346,8 +354,7 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
   if (!params) return fail(W3D_ERR_INVALID_ARG, "params must be a non-NULL host array");
   if ((in_labels == nullptr) != (out_labels == nullptr))
     return fail(W3D_ERR_INVALID_ARG, "out_labels must be NULL iff in_labels is NULL");
-  if (variant != W3D_KERNEL_AUTO && variant != W3D_KERNEL_GATHER && variant != W3D_KERNEL_STAGED &&
-      variant != W3D_KERNEL_TMA && variant != W3D_KERNEL_BULK && variant != W3D_KERNEL_PERSISTENT)
+  if (variant != W3D_KERNEL_AUTO && variant != W3D_KERNEL_GATHER && variant != W3D_KERNEL_STAGED)
     return fail(W3D_ERR_INVALID_ARG, "variant = %d is not a w3d_kernel", int(variant));
   for (int32_t i = 0; i < batch; ++i) {
     if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;

@@ -1,5 +1,5 @@
 // warp3d_internal.cuh -- launch-argument structs shared by the host entry
-// points (warp3d_host.cu) and the kernels (warp3d_kernels.cu).
+// points (warp3d_host.cu) and the kernels (warp3d_cube.cu, warp3d_aux.cu).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -36,34 +36,25 @@ struct alignas(16) VolDev {
   uint32_t key0, key1;  // Philox key = seed
   uint32_t vid0, vid1;  // Philox counter words 2,3 = volume_id
   int32_t occ_lo, occ_hi;  // occluded output z in [occ_lo, occ_hi]
-  uint32_t _pad[2];
+  // TMA box of this volume's tiles (host-computed from A, warp3d_cube.cu): image
+  // box (box_w, box_h, box_d) floats, label box (box_wl, box_h, box_d) bytes;
+  // box_w == 0: no TMA for this volume (cp.async staging)
+  uint16_t box_w, box_h, box_d, box_wl;
   uint32_t rk0[10], rk1[10];  // Philox round keys k + r * (W0, W1), host-precomputed
-  uint32_t _pad2[4];
+  uint32_t ph_K0, ph_K1, ph_K2, ph_U3;  // PhiloxPrefix (philox.cuh), host-precomputed
 };
 static_assert(sizeof(VolDev) == 208, "VolDev layout");
 
-constexpr int kMaxVolPerLaunch = 112;
-
-// TMA staging: the box is loaded with
-// cp.async.bulk.tensor boxes of kTmaRowsImg image rows x WI floats and
-// kTmaRowsLbl label rows x WL bytes; WI / WL come from these width classes
-// (one tensor map per class; WI*kTmaRowsImg*4 and WL*kTmaRowsLbl must be
-// multiples of 128 B so consecutive boxes stay 128 B aligned in smem).
-constexpr int kTmaRowsImg = 4, kTmaRowsLbl = 8;
-constexpr int kNumImgCls = 10, kNumLblCls = 7;
-__host__ __device__ constexpr int img_cls_width(int c) {
-  return c < 7 ? 16 + 8 * c : (c == 7 ? 80 : (c == 8 ? 96 : 128));
-}
-__host__ __device__ constexpr int lbl_cls_width(int c) { return c < 6 ? 16 * (c + 1) : 128; }
-
-// Persistent kernel: two buffers of kPersCapVox voxels (5 B each) per SM.
-constexpr int kPersCapVox = 11008;  // 2 CTAs/SM x 2 buffers x (55 KB + 1 KB reserve)
+constexpr int kMaxVolPerLaunch = 128;  // sizeof(WarpArgs) < 32764 B of kernel parameters
+// Volumes per launch when TMA staging is used: the tensor maps must lie in the
+// first 4 KB of the kernel parameters (measured: TMA on a __grid_constant__
+// map at a larger parameter offset faults).
+constexpr int kTmaVolPerLaunch = 16;
 
 struct alignas(64) WarpArgs {
-  CUtensorMap tm_img[kNumImgCls];  // 4D (nx, ny, nz, nvol) float32, box (w, 4, 1, 1)
-  CUtensorMap tm_lbl[kNumLblCls];  // 4D uint8, box (w, 8, 1, 1)
-  int32_t use_tma;                 // tensor maps valid
-  int32_t _pad_tma[15];
+  // per volume i: tm[2i] 3D (nx, ny, nz) float32 box (box_w, box_h, box_d),
+  //               tm[2i+1] 3D uint8 box (box_wl, box_h, box_d)
+  CUtensorMap tm[2 * kTmaVolPerLaunch];
   const float* in;
   const uint8_t* in_lbl;  // may be null
   float* out;
@@ -76,22 +67,27 @@ struct alignas(64) WarpArgs {
   uint32_t label_fill;
   int32_t interp;         // W3D_INTERP_*
   int32_t nvol;           // volumes in this launch
+  int32_t use_tma;        // tensor maps valid for the volumes with box_w > 0
+  int32_t _pad[3];
+  // Philox round keys shared by every volume of the launch (all seeds equal;
+  // required by the kPhFull kernels: fixed parameter offsets, so the round
+  // function reads them as constant-bank operands)
+  uint32_t rk0[10], rk1[10];
   VolDev vol[kMaxVolPerLaunch];
 };
+static_assert(sizeof(WarpArgs) <= 32764, "kernel parameter space");
 
-// Launchers (warp3d_kernels.cu).  All return cudaGetLastError() of the launch.
-cudaError_t launch_gather(const WarpArgs& a, cudaStream_t s);
-cudaError_t launch_staged(const WarpArgs& a, cudaStream_t s);
-cudaError_t launch_auto(const WarpArgs& a, cudaStream_t s);
-cudaError_t launch_tma(const WarpArgs& a, cudaStream_t s);
-cudaError_t launch_bulk(const WarpArgs& a, cudaStream_t s);
-cudaError_t launch_persistent_api(const WarpArgs& a, cudaStream_t s);
-bool tma_supported(const WarpArgs& a);
-cudaError_t encode_tensor_maps(WarpArgs& a);
+// Launchers.  All return cudaGetLastError() of the launch.
+// warp3d_cube.cu (the warp): cube_supported() = the staged layout requirements.
+bool cube_supported(const WarpArgs& a);
+bool cube_tma_supported(const WarpArgs& a);
+// TMA box dims for one volume's tiles (0 when the box exceeds the buffer)
+void cube_tma_box(const float A[12], VolDev& P, bool labels);
+cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s);
+cudaError_t read_cube_stats(unsigned long long out[2]);
+// warp3d_aux.cu (test hooks, measurement)
 cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,
                          uint32_t k1, uint32_t v0, uint32_t v1, cudaStream_t s);
-bool staged_supported(const WarpArgs& a);
-cudaError_t read_tile_stats(unsigned long long out[2]);
 cudaError_t launch_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                           int64_t n, cudaStream_t s);
 cudaError_t launch_footprint(const WarpArgs& a, uint8_t* marks, cudaStream_t s);

@@ -298,8 +298,8 @@ def _fma32(a, x, c):
 
 
 def _p_fp32(A, x, y, z):
-    """p_k = fma(A_k0, x, fma(A_k1, y, fma(A_k2, z, b_k))) in fp32 (R4)."""
-    return [float(_fma32(A[k, 0], x, _fma32(A[k, 1], y, _fma32(A[k, 2], z, A[k, 3]))))
+    """p_k = fma(A_k1, y, fma(A_k0, x, fma(A_k2, z, b_k))) in fp32 (R4)."""
+    return [float(_fma32(A[k, 1], y, _fma32(A[k, 0], x, _fma32(A[k, 2], z, A[k, 3]))))
             for k in range(3)]
 
 

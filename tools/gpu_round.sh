@@ -16,6 +16,6 @@ if [ "${NCU:-0}" == "1" ]; then
   CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline ${NCU_BENCH_ARGS}"
   $CMD > gpurun_out/ncu_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launches.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"warp3d_t(ile|ma)" -s 3 -c 1 -o gpurun_out/prof_${TAG} -f $CMD > gpurun_out/ncu_full.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:warp3d_cube -s 3 -c 1 -o gpurun_out/prof_${TAG} -f $CMD > gpurun_out/ncu_full.log 2>&1
   echo "ncu rc=$?"; tail -3 gpurun_out/ncu_full.log
 fi
