@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--variant", choices=["auto", "gather", "staged"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-labels", action="store_true",
+                    help="image-only warp (diagnostic; the headline includes labels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded oracle sample")
@@ -309,7 +311,7 @@ def main():
     B = len(vids)
     nvox_out = int(np.prod(shape))
     t_img = torch.from_numpy(imgs).to(dev)
-    t_lbl = torch.from_numpy(lbls).to(dev)
+    t_lbl = None if args.no_labels else torch.from_numpy(lbls).to(dev)
     batch = W.AugmentBatch(t_img, t_lbl, params, fill=-1000.0, label_fill=0, variant=variant)
 
     # algorithmic bytes: 5 B written per output voxel

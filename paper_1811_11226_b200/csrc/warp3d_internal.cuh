@@ -42,10 +42,14 @@ struct alignas(16) VolDev {
   uint16_t box_w, box_h, box_d, box_wl;
   uint32_t rk0[10], rk1[10];  // Philox round keys k + r * (W0, W1), host-precomputed
   uint32_t ph_K0, ph_K1, ph_K2, ph_U3;  // PhiloxPrefix (philox.cuh), host-precomputed
+  // TMA box origin of a tile: floor(p(tile origin voxel) + box_mlo[k]) with
+  // box_mlo[k] = sum_j min(0, A_kj span_j) - rounding margin (cube_tma_box)
+  float box_mlo[3];
+  uint32_t _pad2;
 };
-static_assert(sizeof(VolDev) == 208, "VolDev layout");
+static_assert(sizeof(VolDev) == 224, "VolDev layout");
 
-constexpr int kMaxVolPerLaunch = 128;  // sizeof(WarpArgs) < 32764 B of kernel parameters
+constexpr int kMaxVolPerLaunch = 120;  // sizeof(WarpArgs) < 32764 B of kernel parameters
 // Volumes per launch when TMA staging is used: the tensor maps must lie in the
 // first 4 KB of the kernel parameters (measured: TMA on a __grid_constant__
 // map at a larger parameter offset faults).
