@@ -32,6 +32,9 @@
 namespace w3d {
 namespace cube {
 
+#ifndef W3D_IMG_ALIGN_MASK
+#define W3D_IMG_ALIGN_MASK ~3
+#endif
 // Tile 16 x kTY x TZ output voxels; a warp = 16 x by 2 z, so TZ / 2 warps.
 #ifndef W3D_TZ
 #define W3D_TZ 16
@@ -263,6 +266,12 @@ __device__ __forceinline__ uint32_t pin(uint32_t x) {
   uint32_t y;
   asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
   return y;
+}
+template <class T>
+__device__ __forceinline__ T* pin_ptr(T* p) {
+  unsigned long long y;
+  asm volatile("mov.b64 %0, %1;" : "=l"(y) : "l"(reinterpret_cast<unsigned long long>(p)));
+  return reinterpret_cast<T*>(y);
 }
 // A warp-uniform value ptxas cannot see through (a shuffle from lane 0), so it
 // does not split constant parts off address bases into extra adds.  Every
@@ -502,9 +511,10 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
     rk1[r] = kPh == kPhFull ? a.rk1[r] : pin(P.rk1[r]);
   }
   // output element offset of row y within the volume (< 2^31)
-  uint32_t o = static_cast<uint32_t>((Z * my + y0) * mx + X);
-  float* const vout = a.out + vi * a.out_stride;
-  uint8_t* const lout = kLabels ? a.out_lbl + vi * a.out_stride : nullptr;
+  // output row pointers, pinned (else re-derived from the parameters every row)
+  const size_t o = static_cast<size_t>((Z * my + y0) * mx + X);
+  float* po = pin_ptr(a.out + vi * a.out_stride + o);
+  uint8_t* pl = kLabels ? pin_ptr(a.out_lbl + vi * a.out_stride + o) : nullptr;
   uint32_t q = static_cast<uint32_t>(X) +
                mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(y0 >> 2));
   float2 Y2 = make_float2(static_cast<float>(y0), static_cast<float>(y0 + 1));
@@ -534,14 +544,16 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
       float2 out = photometric2<kPh>(img, make_float2(ns[2 * h], ns[2 * h + 1]), V);
       if (occl) out = make_float2(0.0f, 0.0f);  // PAPER.md:437-438, R15
       const bool second = ya + 1 < my;
-      const uint32_t o1 = o + row1;
-      st_f32(at(vout, o), out.x);
-      if (second) st_f32(at(vout, o1), out.y);
+      float* po1 = po + row1;
+      st_f32(po, out.x);
+      if (second) st_f32(po1, out.y);
+      po = po1 + row1;
       if (kLabels) {
-        st_u8(at(lout, o), l0);
-        if (second) st_u8(at(lout, o1), l1);
+        uint8_t* pl1 = pl + row1;
+        st_u8(pl, l0);
+        if (second) st_u8(pl1, l1);
+        pl = pl1 + row1;
       }
-      o = o1 + row1;
     }
     n = nn;
     q += mxu;
@@ -696,7 +708,7 @@ __device__ __forceinline__ bool tma_box(const VolDev& P, int ox, int oy, int oz,
     lo[k] = __float2int_rd(__fadd_rd(p0, P.box_mlo[k]));
   }
   // TMA box inner origins must be 16 B aligned: image x0 % 4, label x0 % 16
-  b.bx = lo[0] & ~3;
+  b.bx = lo[0] & W3D_IMG_ALIGN_MASK;
   b.bxl = lo[0] & ~15;
   b.by = lo[1];
   b.bz = lo[2];
@@ -817,7 +829,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, oy) : make_float4(0, 0, 0, 0);
   const View v = make_view(a, b, simg, slbl);
 #ifdef W3D_DBG_NOSTAGE
+#ifndef W3D_DBG_NOBAR
   __syncthreads();
+#endif
   if (false) {
 #else
   if (tma) {
@@ -851,7 +865,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
 #ifndef W3D_MINB
 #define W3D_MINB (TZ > 16 ? 2 : 4)
 #endif
-constexpr int kTY = 16, kMinB = W3D_MINB;
+#ifndef W3D_TY
+#define W3D_TY 16
+#endif
+constexpr int kTY = W3D_TY, kMinB = W3D_MINB;
 // staging buffer (voxels of 5 B): kMinB * (kCapVox * 5 B + 256 + 1 KB) <= 228 KB
 constexpr int kCapVox = (233472 / kMinB - 1024 - 272) / 5;
 
@@ -958,20 +975,22 @@ void cube_tma_box(const float A[12], VolDev& P, bool labels) {
     // origin >= p_min - margin - 1, needed up to floor(p_max) + 1 <= p_min + ext + margin + 1
     d[k] = static_cast<int>(std::floor(ext + 2.0 * margin)) + 4;
   }
-  // + alignment slack of the 16 B aligned inner origins (image x0 % 4, labels % 16)
+  // + alignment slack of the 16 B aligned inner origins (image x0 % 4, labels
+  // x0 % 16; an unaligned origin faults: measured)
   int W = (d[0] + 3 + 3) & ~3, H = d[1], D = d[2];
   const int Wl = (d[0] + 15 + 15) & ~15;
-  for (int h = H; h < H + 8; ++h) {
+  auto bytes = [&](int h) {
+    return ((int64_t(4) * W * h * D + 127) & ~int64_t(127)) + (labels ? int64_t(Wl) * h * D : 0);
+  };
+  for (int h = H; h < H + 8; ++h) {  // bank-spreading plane pitch, if it still fits
     const int res = (W * h) & 31;
-    if (res == 20 || res == 24 || res == 16 || res == 12) {
+    if ((res == 20 || res == 24 || res == 16 || res == 12) && bytes(h) <= int64_t(kCapVox) * 5) {
       H = h;
       break;
     }
   }
   if (W > 256 || H > 256 || D > 256) return;
-  const int64_t bytes = ((int64_t(4) * W * H * D + 127) & ~int64_t(127)) +
-                        (labels ? int64_t(Wl) * H * D : 0);
-  if (bytes > int64_t(kCapVox) * 5) return;
+  if (bytes(H) > int64_t(kCapVox) * 5) return;
   P.box_w = static_cast<uint16_t>(W);
   P.box_h = static_cast<uint16_t>(H);
   P.box_d = static_cast<uint16_t>(D);

@@ -7,7 +7,7 @@ subprocess.run([build.NVCC, *build.ARCH, "-O3", "-std=c++17", "-shared", "-Xcomp
                 *build.CUDA_SOURCES], check=True)
 import paper_1811_11226_b200 as W, synth, oracle as O
 shape=(160,128,128)
-for B in (1, 2, 16):
+for B in (1,):
     imgs=[]; lbls=[]; params=[]
     for i in range(B):
         im, lb = synth.phantom(shape, seed=100+i)
