@@ -133,7 +133,7 @@ struct Box {
   bool clamp;
 };
 
-__device__ __forceinline__ void make_box(const float* mn, const float* mx, Box& b) {
+__device__ __forceinline__ void make_box(const float* mn, const float* mx, int cap, Box& b) {
   const int lx = __float2int_rd(mn[0]), hx = __float2int_rd(mx[0]) + 1;
   const int ly = __float2int_rd(mn[1]), hy = __float2int_rd(mx[1]) + 1;
   const int lz = __float2int_rd(mn[2]), hz = __float2int_rd(mx[2]) + 1;
@@ -144,7 +144,8 @@ __device__ __forceinline__ void make_box(const float* mn, const float* mx, Box& 
   b.H = hy - ly + 1;
   b.D = hz - lz + 1;
   const int wh = b.W * b.H;
-  b.P = wh + ((kPlaneRes - wh) & 31);
+  b.P = wh + ((kPlaneRes - wh) & 31);  // bank-spreading plane pitch, if it fits
+  if (b.P * b.D > cap) b.P = wh;
   b.Wl = b.W;
   b.Pl = b.P;
   b.bxl = b.bx;
@@ -170,7 +171,7 @@ __device__ __forceinline__ bool tile_box(const WarpArgs& a, const float* A, int 
 #pragma unroll
   for (int k = 0; k < 3; ++k) sane &= (mn[k] > -kSane) & (mx[k] < kSane);
   if (sane) {
-    make_box(mn, mx, b);
+    make_box(mn, mx, cap, b);
     if (b.P * b.D <= cap && b.W <= 4 * THREADS) {
       b.clamp = false;
       return true;
@@ -183,7 +184,7 @@ __device__ __forceinline__ bool tile_box(const WarpArgs& a, const float* A, int 
     mn[k] = fminf(fmaxf(mn[k], -1.0f), n[k]);
     mx[k] = fminf(fmaxf(mx[k], -1.0f), n[k]);
   }
-  make_box(mn, mx, b);
+  make_box(mn, mx, cap, b);
   b.clamp = true;
   return b.P * b.D <= cap && b.W <= 4 * THREADS;
 }
