@@ -30,12 +30,12 @@ def _stale(target, sources):
 
 
 def build_oracle(force=False):
-    src = os.path.join(ROOT, "oracle", "oracle_warp3d.c")
+    srcs = [os.path.join(ROOT, "oracle", f) for f in ("oracle_warp3d.c", "oracle_resample.c")]
     hdr = os.path.join(ROOT, "oracle", "oracle_warp3d.h")
     out = os.path.join(ROOT, "oracle", "liboracle_warp3d.so")
-    if force or _stale(out, [src, hdr]):
+    if force or _stale(out, srcs + [hdr]):
         _run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-              "-shared", "-Wall", "-Wextra", "-D_GNU_SOURCE", "-o", out, src, "-lm"])
+              "-shared", "-Wall", "-Wextra", "-D_GNU_SOURCE", "-o", out, *srcs, "-lm"])
     return out
 
 

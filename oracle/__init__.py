@@ -12,6 +12,12 @@ Parity status per function:
   compose_affine   pinned: Ac+b=c+d, hand-derived factor products
   warp_volume      pinned: identity, permutations, constant/ramp closed forms,
                    OOB fill, tent-kernel brute force, window worked value, gamma
+  resample_sigma   pinned: PAPER.md:488-490 worked values (u=1 -> 2/3, u=3 -> 0)
+  resample_dims    pinned: SPEC.md example (240,240,480) at 1.5 mm -> (120,120,240)
+  smooth3d         pinned: constant invariance, sigma=0 identity, interior impulse
+                   response = outer product of the normalised 1D kernels, linear ramp
+                   preserved in the interior (symmetric kernel)
+  resample         composition of the above with warp_volume (scale-only affine)
 """
 from __future__ import annotations
 
@@ -76,6 +82,13 @@ def lib():
         L.oracle_warp_points.argtypes = [P, P, P, P, ctypes.c_int32, ctypes.c_float,
                                          ctypes.c_uint8, P, P, P, ctypes.c_int64, P, P]
         L.oracle_noise_field.argtypes = [P, P, ctypes.c_float, ctypes.c_uint64, ctypes.c_uint64]
+        D = ctypes.c_double
+        L.oracle_resample_sigma.argtypes = [P, D, P]
+        L.oracle_resample_dims.argtypes = [P, P, D, P]
+        L.oracle_gauss_radius.argtypes = [D]
+        L.oracle_gauss_radius.restype = ctypes.c_int32
+        L.oracle_smooth3d.argtypes = [P, P, P, P]
+        L.oracle_resample_affine.argtypes = [P, P, P, D, P]
         _lib = L
     return _lib
 
@@ -175,3 +188,54 @@ def warp_points(image, labels, affine, xyz, out_shape_zyx=None, interp=LINEAR, f
                              None if ph is None else ctypes.byref(ph),
                              _ptr(_dims(out_shape_zyx)), _ptr(xyz), n, _ptr(vals), _ptr(lbls))
     return vals, lbls
+
+
+# ----------------------------------------------------------------------------- resampling
+def resample_sigma(spacing_mm, target_mm=3.0):
+    """sigma_k = max(r/u_k - 1, 0)/3 (PAPER.md:488-490), as (x, y, z)."""
+    u = np.ascontiguousarray(spacing_mm, dtype=np.float64)
+    out = np.zeros(3, dtype=np.float64)
+    lib().oracle_resample_sigma(_ptr(u), float(target_mm), _ptr(out))
+    return out
+
+
+def resample_dims(in_shape_zyx, spacing_mm, target_mm=3.0):
+    """Output numpy shape (nz, ny, nx) of the resampling; spacing_mm is (x, y, z)."""
+    u = np.ascontiguousarray(spacing_mm, dtype=np.float64)
+    out = np.zeros(3, dtype=np.int32)
+    lib().oracle_resample_dims(_ptr(_dims(in_shape_zyx)), _ptr(u), float(target_mm), _ptr(out))
+    return (int(out[2]), int(out[1]), int(out[0]))
+
+
+def gauss_radius(sigma):
+    return int(lib().oracle_gauss_radius(float(sigma)))
+
+
+def smooth3d(volume, sigma_xyz):
+    """Direct 3D Gaussian smoothing (float64 result) of a float32 [nz,ny,nx] volume."""
+    v = np.ascontiguousarray(volume, dtype=np.float32)
+    s = np.ascontiguousarray(sigma_xyz, dtype=np.float64)
+    out = np.empty(v.shape, dtype=np.float64)
+    lib().oracle_smooth3d(_ptr(v), _ptr(_dims(v.shape)), _ptr(s), _ptr(out))
+    return out
+
+
+def resample_affine(in_shape_zyx, out_shape_zyx, spacing_mm, target_mm=3.0):
+    u = np.ascontiguousarray(spacing_mm, dtype=np.float64)
+    A = np.zeros(12, dtype=np.float32)
+    lib().oracle_resample_affine(_ptr(_dims(in_shape_zyx)), _ptr(_dims(out_shape_zyx)), _ptr(u),
+                                 float(target_mm), _ptr(A))
+    return A.reshape(3, 4)
+
+
+def resample(image, labels, spacing_mm, target_mm=3.0, fill=-1000.0, label_fill=0):
+    """Smooth the image (never the labels), round the smoothed volume to float32,
+    then trilinear (image) / nearest (labels) at spacing target_mm, centre-aligned."""
+    out_shape = resample_dims(image.shape, spacing_mm, target_mm)
+    sm = smooth3d(image, resample_sigma(spacing_mm, target_mm)).astype(np.float32)
+    A = resample_affine(image.shape, out_shape, spacing_mm, target_mm)
+    img, _ = warp_volume(sm, None, A, out_shape, LINEAR, fill, 0, None)
+    lbl = None
+    if labels is not None:
+        _, lbl = warp_volume(image, labels, A, out_shape, LINEAR, fill, label_fill, None)
+    return img, lbl

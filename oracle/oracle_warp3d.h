@@ -90,7 +90,17 @@ void oracle_warp_points(const float* in, const uint8_t* in_lbl, const int32_t in
 void oracle_noise_field(float* out, const int32_t dims[3], float sigma, uint64_t seed,
                         uint64_t volume_id);
 
+/* Resampling to r mm (oracle_resample.c). */
+void oracle_resample_sigma(const double u[3], double r, double sigma[3]);
+void oracle_resample_dims(const int32_t in_dims[3], const double u[3], double r,
+                          int32_t out_dims[3]);
+int32_t oracle_gauss_radius(double sigma);
+void oracle_smooth3d(const float* in, const int32_t dims[3], const double sigma[3], double* out);
+void oracle_resample_affine(const int32_t in_dims[3], const int32_t out_dims[3], const double u[3],
+                            double r, float A[12]);
+
 #ifdef __cplusplus
 }
 #endif
+
 #endif
