@@ -43,6 +43,7 @@ CUDA_SOURCES = [
     "paper_1811_11226_b200/csrc/warp3d_host.cu",
     "paper_1811_11226_b200/csrc/warp3d_cube.cu",
     "paper_1811_11226_b200/csrc/warp3d_aux.cu",
+    "paper_1811_11226_b200/csrc/warp3d_resample.cu",
 ]
 CUDA_HEADERS = [
     "include/warp3d.h",

@@ -194,6 +194,51 @@ w3d_status warp3d_footprint_batched(int32_t batch, w3d_dims in_dims,
                                     uint8_t* marks, unsigned long long* counts, void* stream);
 
 /*
+ * Resampling to r mm before the network ("Resampling consists
+ * of Gaussian smoothing, which serves as a lowpass filter to avoid aliasing
+ * artifacts, followed by interpolation at the new resolution").
+ * spacing_mm = (u_x, u_y, u_z) of the input voxels, target_mm = r (the paper's 3).
+ * Readings (R22-R25):
+ *   sigma_k = max(r / u_k - 1, 0) / 3
+ *   g(x) ~ exp(-sum_k x_k^2 / sigma_k^2), x in input voxels,
+ *   sampled at |i_k| <= ceil(3 sigma_k), normalised to sum 1 per axis; voxels
+ *   beyond the volume replicate the nearest edge voxel (a constant stays constant)
+ *   out dims_k = max(1, floor(n_k u_k / r + 1/2))
+ *   output voxel j samples input c_in + (j - c_out) r / u_k (centre-aligned, R3):
+ *   trilinear for the image, nearest for the labels (never smoothed), border fill
+ *   (R6, R8) for the rare samples beyond the edge.
+ */
+/* sigma_out[3] (host only). */
+w3d_status warp3d_resample_sigma(const double spacing_mm[3], double target_mm,
+                                 double sigma_out[3]);
+/* Output dims (host only). */
+w3d_status warp3d_resample_dims(w3d_dims in_dims, const double spacing_mm[3], double target_mm,
+                                w3d_dims* out_dims);
+/* The centre-aligned scale map [A|b] (host only; R4 contract of warp3d_affine). */
+w3d_status warp3d_resample_affine(w3d_dims in_dims, w3d_dims out_dims, const double spacing_mm[3],
+                                  double target_mm, float affine_out[12]);
+/*
+ * warp3d_smooth3d -- the separable Gaussian lowpass alone.  in, out, tmp: device
+ * float32 [nz][ny][nx], caller-owned, pairwise disjoint (tmp = scratch).
+ * sigma: host double[3] per axis (x, y, z), >= 0; at most 63 taps per axis
+ * (sigma <= 10.33, else W3D_ERR_UNSUPPORTED); ny, nz <= 65535.  Passes x, y, z
+ * (axes with sigma 0 skipped), fp32 accumulation in tap order.  Async on stream.
+ */
+w3d_status warp3d_smooth3d(const float* in, w3d_dims dims, const double sigma[3], float* out,
+                           float* tmp, void* stream);
+/*
+ * warp3d_resample -- smoothing + interpolation of one volume (and its labels).
+ * in / in_labels: device [in_dims] (labels nullable); out / out_labels: device
+ * [out_dims], out_dims must equal warp3d_resample_dims(); tmp: device float32
+ * scratch of 2 * in_dims voxels; all disjoint.  fill / label_fill: values beyond
+ * the input (R6, R8).  Async on stream.
+ */
+w3d_status warp3d_resample(const float* in, const uint8_t* in_labels, w3d_dims in_dims,
+                           const double spacing_mm[3], double target_mm, float fill,
+                           uint8_t label_fill, float* out, uint8_t* out_labels,
+                           w3d_dims out_dims, float* tmp, void* stream);
+
+/*
  * FIFO pipeline ("a first-in first-out (FIFO) queue to
  * pipeline jobs ... while one image is being processed, the next has already
  * begun transferring"): augments a batch held in HOST memory.  Volume i is job

@@ -26,7 +26,8 @@ EXPORTS = (
     "warp3d_compose_affine", "warp3d_noise", "warp3d_philox4x32_10",
     "warp3d_footprint_batched", "warp3d_launch_count", "warp3d_last_error",
     "warp3d_abi_version", "warp3d_tile_stats", "warp3d_pipeline_create", "warp3d_pipeline_run",
-    "warp3d_pipeline_destroy",
+    "warp3d_pipeline_destroy", "warp3d_resample_sigma", "warp3d_resample_dims",
+    "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample",
 )
 
 
@@ -98,6 +99,15 @@ def load():
     L.warp3d_pipeline_run.argtypes = [P, I32, P, P, P, I32, F, ctypes.c_uint8, P, P, P]
     L.warp3d_pipeline_destroy.argtypes = [P]
     for name in ("warp3d_pipeline_create", "warp3d_pipeline_run", "warp3d_pipeline_destroy"):
+        getattr(L, name).restype = ctypes.c_int
+    D = ctypes.c_double
+    L.warp3d_resample_sigma.argtypes = [P, D, P]
+    L.warp3d_resample_dims.argtypes = [Dims, P, D, ctypes.POINTER(Dims)]
+    L.warp3d_resample_affine.argtypes = [Dims, Dims, P, D, P]
+    L.warp3d_smooth3d.argtypes = [P, Dims, P, P, P, P]
+    L.warp3d_resample.argtypes = [P, P, Dims, P, D, F, ctypes.c_uint8, P, P, Dims, P, P]
+    for name in ("warp3d_resample_sigma", "warp3d_resample_dims", "warp3d_resample_affine",
+                 "warp3d_smooth3d", "warp3d_resample"):
         getattr(L, name).restype = ctypes.c_int
     L.warp3d_tile_stats.argtypes = [P]
     L.warp3d_tile_stats.restype = ctypes.c_int

@@ -19,7 +19,8 @@ from ._lib import (INTERP_LINEAR, INTERP_NEAREST, KERNEL_AUTO, KERNEL_GATHER, KE
 __all__ = [
     "warp3d_affine", "warp3d_affine_batched", "warp3d_compose_affine", "warp3d_noise",
     "warp3d_philox4x32_10", "warp3d_footprint_batched", "warp3d_launch_count",
-    "warp3d_tile_stats", "Pipeline",
+    "warp3d_tile_stats", "Pipeline", "warp3d_resample_sigma", "warp3d_resample_dims",
+    "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample",
     "warp3d_abi_version", "photometric", "volume_params", "make_geom", "Warp3DError",
     "INTERP_LINEAR", "INTERP_NEAREST", "KERNEL_AUTO", "KERNEL_GATHER", "KERNEL_STAGED",
     "PH_NOISE", "PH_WINDOW", "PH_CLAMP", "PH_GAMMA", "PH_OCCLUDE",
@@ -193,6 +194,64 @@ class Pipeline:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+# ----------------------------------------------------------------------------- resampling
+def _u(spacing_mm):
+    u = (ctypes.c_double * 3)(*[float(v) for v in spacing_mm])
+    return u
+
+
+def warp3d_resample_sigma(spacing_mm, target_mm=3.0):
+    """sigma_k = max(r/u_k - 1, 0)/3 (PAPER.md:488-490); spacing_mm = (u_x, u_y, u_z)."""
+    out = (ctypes.c_double * 3)()
+    L.check(L.load().warp3d_resample_sigma(_u(spacing_mm), float(target_mm), out))
+    return tuple(out)
+
+
+def warp3d_resample_dims(in_shape_zyx, spacing_mm, target_mm=3.0):
+    """numpy-order output shape (nz, ny, nx) of warp3d_resample."""
+    d = L.Dims()
+    L.check(L.load().warp3d_resample_dims(L.dims(in_shape_zyx), _u(spacing_mm), float(target_mm),
+                                          ctypes.byref(d)))
+    return (d.nz, d.ny, d.nx)
+
+
+def warp3d_resample_affine(in_shape_zyx, out_shape_zyx, spacing_mm, target_mm=3.0):
+    A = (ctypes.c_float * 12)()
+    L.check(L.load().warp3d_resample_affine(L.dims(in_shape_zyx), L.dims(out_shape_zyx),
+                                            _u(spacing_mm), float(target_mm), A))
+    return np.array(A, dtype=np.float32).reshape(3, 4)
+
+
+def warp3d_smooth3d(inp: torch.Tensor, sigma_xyz) -> torch.Tensor:
+    """Separable Gaussian lowpass of a float32 [nz, ny, nx] CUDA tensor."""
+    out = torch.empty_like(inp)
+    tmp = torch.empty_like(inp)
+    s = (ctypes.c_double * 3)(*[float(v) for v in sigma_xyz])
+    L.check(L.load().warp3d_smooth3d(_dev(inp, torch.float32, "inp"), L.dims(inp.shape), s,
+                                     _dev(out, torch.float32, "out"),
+                                     _dev(tmp, torch.float32, "tmp"), _stream()))
+    return out
+
+
+def warp3d_resample(inp: torch.Tensor, labels, spacing_mm, target_mm=3.0, fill=-1000.0,
+                    label_fill=0):
+    """Resample one volume (float32 [nz, ny, nx]) and its labels (uint8 or None) to
+    target_mm spacing: Gaussian lowpass then trilinear / nearest."""
+    out_shape = warp3d_resample_dims(inp.shape, spacing_mm, target_mm)
+    out = torch.empty(out_shape, dtype=torch.float32, device=inp.device)
+    out_l = None if labels is None else torch.empty(out_shape, dtype=torch.uint8,
+                                                    device=inp.device)
+    tmp = torch.empty(2 * inp.numel(), dtype=torch.float32, device=inp.device)
+    L.check(L.load().warp3d_resample(
+        _dev(inp, torch.float32, "inp"), None if labels is None else _dev(labels, torch.uint8,
+                                                                             "labels"),
+        L.dims(inp.shape), _u(spacing_mm), float(target_mm), float(fill), int(label_fill),
+        _dev(out, torch.float32, "out"), None if out_l is None else _dev(out_l, torch.uint8,
+                                                                         "out_labels"),
+        L.dims(out_shape), _dev(tmp, torch.float32, "tmp"), _stream()))
+    return out, out_l
 
 
 def warp3d_launch_count() -> int:

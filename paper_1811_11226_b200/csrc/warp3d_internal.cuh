@@ -89,6 +89,11 @@ bool cube_tma_supported(const WarpArgs& a);
 void cube_tma_box(const float A[12], VolDev& P, bool labels);
 cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s);
 cudaError_t read_cube_stats(unsigned long long out[2]);
+// warp3d_resample.cu (NEXT-3): one separable Gaussian pass along `axis` (0 x, 1 y, 2 z)
+constexpr int kMaxTaps = 63;  // radius ceil(3 sigma) <= 31
+int gauss_radius(double sigma);
+cudaError_t launch_smooth_axis(int axis, const float* in, float* out, int nx, int ny, int nz,
+                               double sigma, cudaStream_t s);
 // warp3d_aux.cu (test hooks, measurement)
 cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,
                          uint32_t k1, uint32_t v0, uint32_t v1, cudaStream_t s);

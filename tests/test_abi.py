@@ -181,3 +181,22 @@ def test_pipeline_create_validates(W):
     assert L.warp3d_pipeline_create(2, _lib.Dims(0, 4, 4), _lib.Dims(4, 4, 4), 1, ctypes.byref(h)) == 1
     assert L.warp3d_pipeline_run(None, 1, None, None, None, 0, 0.0, 0, None, None, None) == 1
     assert L.warp3d_pipeline_destroy(None) == 0
+
+
+def test_resample_host_functions_match_oracle(W):
+    """NEXT-3 host side (no GPU): sigma, dims and the centre-aligned scale map agree
+    with the oracle's independent implementations (dims / affine bit for bit)."""
+    import oracle as O
+    rng = np.random.default_rng(11)
+    for _ in range(40):
+        shape = tuple(int(v) for v in rng.integers(1, 600, size=3))
+        u = tuple(float(v) for v in rng.uniform(0.3, 6.0, size=3))
+        r = float(rng.choice([3.0, 2.0, 1.5]))
+        assert np.allclose(W.warp3d_resample_sigma(u, r), O.resample_sigma(u, r), rtol=0,
+                           atol=1e-15)
+        out_shape = W.warp3d_resample_dims(shape, u, r)
+        assert out_shape == O.resample_dims(shape, u, r)
+        assert np.array_equal(W.warp3d_resample_affine(shape, out_shape, u, r),
+                              O.resample_affine(shape, out_shape, u, r))
+    with pytest.raises(W.Warp3DError):
+        W.warp3d_resample_sigma((1.0, 0.0, 1.0), 3.0)
