@@ -514,6 +514,11 @@ static w3d_status smooth_passes(const float* in, w3d_dims d, const double sigma[
     const cudaError_t e = cudaMemcpyAsync(out, in, size_t(nvox(d)) * 4, cudaMemcpyDeviceToDevice, s);
     return e == cudaSuccess ? ok() : cuda_fail(e, "warp3d_smooth3d copy");
   }
+  static const bool no_fuse = getenv("W3D_SMOOTH_PASSES") && getenv("W3D_SMOOTH_PASSES")[0] == '1';
+  if (smooth_fusable(sigma) && !no_fuse) {
+    const cudaError_t e = launch_smooth_fused(in, out, d.nx, d.ny, d.nz, sigma, s);
+    return e == cudaSuccess ? ok() : cuda_fail(e, "warp3d_smooth3d launch");
+  }
   const float* src = in;
   float* dst = (na % 2 == 1) ? out : tmp;
   for (int i = 0; i < na; ++i) {

@@ -94,6 +94,10 @@ constexpr int kMaxTaps = 63;  // radius ceil(3 sigma) <= 31
 int gauss_radius(double sigma);
 cudaError_t launch_smooth_axis(int axis, const float* in, float* out, int nx, int ny, int nz,
                                double sigma, cudaStream_t s);
+// all three passes in one kernel (radius <= 8 per axis), bit-identical to the passes
+bool smooth_fusable(const double sigma[3]);
+cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int nz,
+                                const double sigma[3], cudaStream_t s);
 // warp3d_aux.cu (test hooks, measurement)
 cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,
                          uint32_t k1, uint32_t v0, uint32_t v1, cudaStream_t s);

@@ -47,6 +47,100 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
   out[(static_cast<int64_t>(z) * ny + y) * nx + x] = acc;
 }
 
+// Fused separable smoothing of one 32 x 8 x 8 output tile (radius <= kFuseR per
+// axis): the input tile + halo (edge voxels replicated) is read once into shared
+// memory, then the x, y and z passes run out of shared memory in the same
+// order and fp32 arithmetic as smooth_axis_kernel (bit-identical results), and
+// only the output tile is written back: one HBM read + one write per voxel
+// instead of three of each.
+constexpr int kFuseR = 8, FX = 32, FY = 8, FZ = 8;
+struct Taps3 {
+  float wx[2 * kFuseR + 1], wy[2 * kFuseR + 1], wz[2 * kFuseR + 1];
+  int32_t rx, ry, rz;
+};
+
+extern __shared__ float fuse_smem[];
+
+// RM: compile-time tap radius >= every axis' radius; an axis with a smaller
+// radius has its weights centred and zero-padded (fma(0, v, acc) = acc exactly,
+// so the result equals the per-axis passes bit for bit).
+template <int RM>
+__global__ void __launch_bounds__(256) smooth_fused_kernel(const float* __restrict__ in,
+                                                           float* __restrict__ out, int nx, int ny,
+                                                           int nz, const __grid_constant__ Taps3 t) {
+  const int ox = static_cast<int>(blockIdx.x) * FX, oy = static_cast<int>(blockIdx.y) * FY,
+            oz = static_cast<int>(blockIdx.z) * FZ;
+  // halo RM on every axis (zero-weight taps read real, finite, edge-replicated data)
+  constexpr int AX = FX + 2 * RM, AY = FY + 2 * RM, AZ = FZ + 2 * RM;
+  float* A = fuse_smem;            // [AZ][AY][AX]  input + halo; later the y-pass result
+  float* B = fuse_smem + AX * AY * AZ;  // [AZ][AY][FX] x-pass result
+  // taps centred in 2 RM + 1 slots, zero-padded (registers)
+  float wx[2 * RM + 1], wy[2 * RM + 1], wz[2 * RM + 1];
+#pragma unroll
+  for (int k = 0; k <= 2 * RM; ++k) {
+    wx[k] = (k >= RM - t.rx && k <= RM + t.rx) ? t.wx[k - (RM - t.rx)] : 0.0f;
+    wy[k] = (k >= RM - t.ry && k <= RM + t.ry) ? t.wy[k - (RM - t.ry)] : 0.0f;
+    wz[k] = (k >= RM - t.rz && k <= RM + t.rz) ? t.wz[k - (RM - t.rz)] : 0.0f;
+  }
+  // lane = x (32 = FX), warp w walks rows (y, z) w, w + 8, ...: no per-element division
+  const int lx = static_cast<int>(threadIdx.x & 31), w = static_cast<int>(threadIdx.x >> 5);
+  const int gx0 = min(max(ox + lx - RM, 0), nx - 1);
+  const int gx1 = min(max(ox + lx + 32 - RM, 0), nx - 1);
+  const bool x1 = lx + 32 < AX;
+  {
+    int y = w, z = 0;
+    while (y >= AY) { y -= AY; ++z; }
+    for (int r = w; r < AY * AZ; r += 8) {
+      const int gy = min(max(oy + y - RM, 0), ny - 1), gz = min(max(oz + z - RM, 0), nz - 1);
+      const float* row = in + (static_cast<int64_t>(gz) * ny + gy) * nx;
+      float* arow = A + r * AX;
+      arow[lx] = __ldg(row + gx0);
+      if (x1) arow[lx + 32] = __ldg(row + gx1);
+      y += 8;
+      while (y >= AY) { y -= AY; ++z; }
+    }
+  }
+  __syncthreads();
+  for (int r = w; r < AY * AZ; r += 8) {  // x pass: B[z][y][x], rows of A
+    const float* a = A + r * AX + lx;
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], a[k], acc);
+    B[r * FX + lx] = acc;
+  }
+  __syncthreads();
+  float* C = A;  // [AZ][FY][FX] y-pass result
+  for (int r = w; r < FY * AZ; r += 8) {
+    const int z = r / FY, y = r - z * FY;
+    const float* b = B + (z * AY + y) * FX + lx;
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wy[k], b[k * FX], acc);
+    C[r * FX + lx] = acc;
+  }
+  __syncthreads();
+  const int gx = ox + lx;
+  for (int r = w; r < FY * FZ; r += 8) {  // z pass + store
+    const int z = r / FY, y = r - z * FY;
+    const int gy = oy + y, gz = oz + z;
+    if (gx >= nx || gy >= ny || gz >= nz) continue;
+    const float* c = C + r * FX + lx;
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wz[k], c[k * FX * FY], acc);
+    out[(static_cast<int64_t>(gz) * ny + gy) * nx + gx] = acc;
+  }
+}
+
+void make_taps(double sigma, int R, float* w) {
+  double d[kMaxTaps], sum = 0.0;
+  for (int i = -R; i <= R; ++i) {
+    d[i + R] = sigma > 0.0 ? std::exp(-double(i) * double(i) / (sigma * sigma)) : 1.0;
+    sum += d[i + R];
+  }
+  for (int i = 0; i <= 2 * R; ++i) w[i] = static_cast<float>(d[i] / sum);
+}
+
 }  // namespace
 
 int gauss_radius(double sigma) { return sigma > 0.0 ? static_cast<int>(std::ceil(3.0 * sigma)) : 0; }
@@ -55,12 +149,7 @@ cudaError_t launch_smooth_axis(int axis, const float* in, float* out, int nx, in
                                double sigma, cudaStream_t s) {
   Taps t;
   t.R = gauss_radius(sigma);
-  double w[kMaxTaps], sum = 0.0;
-  for (int i = -t.R; i <= t.R; ++i) {
-    w[i + t.R] = std::exp(-double(i) * double(i) / (sigma * sigma));
-    sum += w[i + t.R];
-  }
-  for (int i = 0; i <= 2 * t.R; ++i) t.w[i] = static_cast<float>(w[i] / sum);
+  make_taps(sigma, t.R, t.w);
   const dim3 grid(static_cast<unsigned>((nx + 255) / 256), static_cast<unsigned>(ny),
                   static_cast<unsigned>(nz));
   if (axis == 0)
@@ -71,6 +160,44 @@ cudaError_t launch_smooth_axis(int axis, const float* in, float* out, int nx, in
     smooth_axis_kernel<2><<<grid, 256, 0, s>>>(in, out, nx, ny, nz, t);
   note_launch();
   return cudaGetLastError();
+}
+
+bool smooth_fusable(const double sigma[3]) {
+  for (int k = 0; k < 3; ++k)
+    if (gauss_radius(sigma[k]) > kFuseR) return false;
+  return true;
+}
+
+cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int nz,
+                                const double sigma[3], cudaStream_t s) {
+  Taps3 t;
+  t.rx = gauss_radius(sigma[0]);
+  t.ry = gauss_radius(sigma[1]);
+  t.rz = gauss_radius(sigma[2]);
+  make_taps(sigma[0], t.rx, t.wx);
+  make_taps(sigma[1], t.ry, t.wy);
+  make_taps(sigma[2], t.rz, t.wz);
+  const dim3 grid(static_cast<unsigned>((nx + FX - 1) / FX), static_cast<unsigned>((ny + FY - 1) / FY),
+                  static_cast<unsigned>((nz + FZ - 1) / FZ));
+  const int rmax = max(t.rx, max(t.ry, t.rz));
+  const int RM = rmax <= 4 ? (rmax < 1 ? 1 : rmax) : (rmax <= 6 ? 6 : 8);
+  const int AX = FX + 2 * RM, AY = FY + 2 * RM, AZ = FZ + 2 * RM;
+  const size_t smem = sizeof(float) * (size_t(AX) * AY * AZ + size_t(FX) * AY * AZ);
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto kernel) {
+    if (smem > 48 * 1024)
+      e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem));
+    if (e == cudaSuccess) kernel<<<grid, 256, smem, s>>>(in, out, nx, ny, nz, t);
+  };
+  if (rmax <= 1) go(smooth_fused_kernel<1>);
+  else if (rmax <= 2) go(smooth_fused_kernel<2>);
+  else if (rmax <= 3) go(smooth_fused_kernel<3>);
+  else if (rmax <= 4) go(smooth_fused_kernel<4>);
+  else if (rmax <= 6) go(smooth_fused_kernel<6>);
+  else go(smooth_fused_kernel<8>);
+  note_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace w3d
