@@ -396,13 +396,13 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
   const uint32_t a3 = a2 + v.W4, b3 = b2 + v.W4;
   float2 c000, c100, c010, c110, c001, c101, c011, c111;
   lds_pair(a0, c000.x, c100.x);
-  lds_pair(a1, c010.x, c110.x);
-  lds_pair(a2, c001.x, c101.x);
-  lds_pair(a3, c011.x, c111.x);
-  lds_pair(b1, c010.y, c110.y);
-  lds_pair(b3, c011.y, c111.y);
   lds_pair(b0, c000.y, c100.y);
+  lds_pair(a1, c010.x, c110.x);
+  lds_pair(b1, c010.y, c110.y);
+  lds_pair(a2, c001.x, c101.x);
   lds_pair(b2, c001.y, c101.y);
+  lds_pair(a3, c011.x, c111.x);
+  lds_pair(b3, c011.y, c111.y);
   const float2 c00 = lerp2(c000, c100, tx), c10 = lerp2(c010, c110, tx);
   const float2 c01 = lerp2(c001, c101, tx), c11 = lerp2(c011, c111, tx);
   img = lerp2(lerp2(c00, c10, ty), lerp2(c01, c11, ty), tz);
