@@ -159,6 +159,26 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
                                     w3d_kernel variant, void* stream);
 
 /*
+ * warp3d_affine_batched_i16[_ex] -- the batched warp with an int16 image input
+ * (CT is 12-bit HU; 2 B per input voxel instead
+ * of 4).  Identical to warp3d_affine_batched[_ex] except that `in` is int16
+ * [batch][nz][ny][nx] (2-byte aligned); every input voxel converts to float
+ * exactly (R17b) and the rest of the chain is unchanged, so the result equals
+ * warp3d_affine_batched on the same volume stored as float32, bit for bit.
+ * Staged paths need nx % 8 == 0, a 16 B aligned input and an integral `fill` in
+ * int16 range (others gather).
+ */
+w3d_status warp3d_affine_batched_i16(int32_t batch, const int16_t* in, const uint8_t* in_labels,
+                                     w3d_dims in_dims, const w3d_volume_params* params,
+                                     w3d_interp interp, float fill, uint8_t label_fill, float* out,
+                                     uint8_t* out_labels, w3d_dims out_dims, void* stream);
+w3d_status warp3d_affine_batched_i16_ex(int32_t batch, const int16_t* in, const uint8_t* in_labels,
+                                        w3d_dims in_dims, const w3d_volume_params* params,
+                                        w3d_interp interp, float fill, uint8_t label_fill,
+                                        float* out, uint8_t* out_labels, w3d_dims out_dims,
+                                        w3d_kernel variant, void* stream);
+
+/*
  * warp3d_compose_affine -- host only (no GPU needed).  A = F Rz Ry Rx Sh S G
  * (R16), b = c_in + d - A c_out with c = (n - 1)/2 per axis (PAPER.md:411-413,
  * R3), evaluated in double and rounded once to fp32 into affine_out[12].

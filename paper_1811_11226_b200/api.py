@@ -97,8 +97,8 @@ def warp3d_affine_batched(inp: torch.Tensor, labels: torch.Tensor | None, params
                           interp=INTERP_LINEAR, fill=0.0, label_fill=0, out_shape=None,
                           out: torch.Tensor | None = None, out_labels: torch.Tensor | None = None,
                           variant=KERNEL_AUTO):
-    """Batch: inp float32 [B,nz,ny,nx], labels uint8 [B,nz,ny,nx] or None,
-    params: sequence of B VolumeParams (or a ctypes array of them)."""
+    """Batch: inp float32 or int16 (HU) [B,nz,ny,nx], labels uint8 [B,nz,ny,nx] or None,
+    params: sequence of B VolumeParams (or a ctypes array of them).  Output float32."""
     if inp.dim() != 4:
         raise ValueError("inp must be [batch, nz, ny, nx]")
     B = inp.shape[0]
@@ -113,8 +113,12 @@ def warp3d_affine_batched(inp: torch.Tensor, labels: torch.Tensor | None, params
         arr = (VolumeParams * B)(*params)
     if len(arr) != B:
         raise ValueError(f"{len(arr)} params for a batch of {B}")
-    L.check(L.load().warp3d_affine_batched_ex(
-        B, _dev(inp, torch.float32, "inp"),
+    if inp.dtype == torch.int16:  # NEXT-4: int16 HU input, float32 output
+        fn, src = L.load().warp3d_affine_batched_i16_ex, _dev(inp, torch.int16, "inp")
+    else:
+        fn, src = L.load().warp3d_affine_batched_ex, _dev(inp, torch.float32, "inp")
+    L.check(fn(
+        B, src,
         None if labels is None else _dev(labels, torch.uint8, "labels"),
         L.dims(inp.shape[1:]), arr, int(interp), float(fill), int(label_fill),
         _dev(out, torch.float32, "out"),

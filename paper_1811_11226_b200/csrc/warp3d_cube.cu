@@ -32,9 +32,6 @@
 namespace w3d {
 namespace cube {
 
-#ifndef W3D_IMG_ALIGN_MASK
-#define W3D_IMG_ALIGN_MASK ~3
-#endif
 // Tile 16 x kTY x TZ output voxels; a warp = 16 x by 2 z, so TZ / 2 warps.
 #ifndef W3D_TZ
 #define W3D_TZ 16
@@ -112,6 +109,24 @@ __device__ __forceinline__ const uint8_t* gaddr_u8(const uint8_t* base, uint32_t
   return p;
 }
 
+// Input image element types: float32 (the headline) and int16 HU (NEXT-4: the
+// 12-bit CT range; converted to float exactly at the gather).
+// kChunk = elements per 16 B chunk (cp.async granularity, TMA row alignment).
+template <class T> struct InT;
+template <> struct InT<float> {
+  static constexpr int kBytes = 4, kChunk = 4;
+  __device__ static float load(const float* p) { return __ldg(p); }
+};
+template <> struct InT<int16_t> {
+  static constexpr int kBytes = 2, kChunk = 8;
+  __device__ static float load(const int16_t* p) { return static_cast<float>(__ldg(p)); }
+};
+template <class T> __device__ __forceinline__ const T* in_ptr(const WarpArgs& a);
+template <> __device__ __forceinline__ const float* in_ptr<float>(const WarpArgs& a) { return a.in; }
+template <> __device__ __forceinline__ const int16_t* in_ptr<int16_t>(const WarpArgs& a) {
+  return a.in16;
+}
+
 // Pull-back coordinate (R4): p_k = fma(A_k1, y, fma(A_k0, x, fma(A_k2, z, b_k))).
 __device__ __forceinline__ float coord(const float* A, int k, float X, float Y, float Z) {
   return __fmaf_rn(A[4 * k + 1], Y, __fmaf_rn(A[4 * k + 0], X, __fmaf_rn(A[4 * k + 2], Z,
@@ -133,24 +148,29 @@ struct Box {
   bool clamp;
 };
 
+template <class T>
 __device__ __forceinline__ void make_box(const float* mn, const float* mx, int cap, Box& b) {
+  constexpr int kC = InT<T>::kChunk;
   const int lx = __float2int_rd(mn[0]), hx = __float2int_rd(mx[0]) + 1;
   const int ly = __float2int_rd(mn[1]), hy = __float2int_rd(mx[1]) + 1;
   const int lz = __float2int_rd(mn[2]), hz = __float2int_rd(mx[2]) + 1;
-  b.bx = lx & ~3;
+  b.bx = lx & ~(kC - 1);
   b.by = ly;
   b.bz = lz;
-  b.W = (hx - b.bx + 1 + 3) & ~3;
+  b.W = (hx - b.bx + 1 + kC - 1) & ~(kC - 1);
   b.H = hy - ly + 1;
   b.D = hz - lz + 1;
   const int wh = b.W * b.H;
-  b.P = wh + ((kPlaneRes - wh) & 31);  // bank-spreading plane pitch, if it fits
+  // bank-spreading plane pitch (a whole number of 16 B chunks), if it fits
+  constexpr int kRes = kC == 4 ? kPlaneRes : 16;
+  b.P = wh + ((kRes - wh) & 31);
   if (b.P * b.D > cap) b.P = wh;
   b.Wl = b.W;
   b.Pl = b.P;
   b.bxl = b.bx;
 }
 
+template <class T>
 __device__ __forceinline__ bool tile_box(const WarpArgs& a, const float* A, int ox, int y0,
                                          int y1, int oz, int cap, Box& b) {
   const int c = threadIdx.x & 7;
@@ -171,7 +191,7 @@ __device__ __forceinline__ bool tile_box(const WarpArgs& a, const float* A, int 
 #pragma unroll
   for (int k = 0; k < 3; ++k) sane &= (mn[k] > -kSane) & (mx[k] < kSane);
   if (sane) {
-    make_box(mn, mx, cap, b);
+    make_box<T>(mn, mx, cap, b);
     if (b.P * b.D <= cap && b.W <= 4 * THREADS) {
       b.clamp = false;
       return true;
@@ -184,7 +204,7 @@ __device__ __forceinline__ bool tile_box(const WarpArgs& a, const float* A, int 
     mn[k] = fminf(fmaxf(mn[k], -1.0f), n[k]);
     mx[k] = fminf(fmaxf(mx[k], -1.0f), n[k]);
   }
-  make_box(mn, mx, cap, b);
+  make_box<T>(mn, mx, cap, b);
   b.clamp = true;
   return b.P * b.D <= cap && b.W <= 4 * THREADS;
 }
@@ -196,28 +216,55 @@ __device__ __forceinline__ bool tile_box(const WarpArgs& a, const float* A, int 
 // out-of-volume chunks set to fill / label_fill.  nx % 4 == 0 and bx % 4 == 0,
 // so a chunk is entirely inside or outside in x.
 // ---------------------------------------------------------------------------
-template <bool kLabels, bool kInside>
-__device__ __forceinline__ void stage_impl(const WarpArgs& a, const float* __restrict__ vin,
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
+}
+template <int kBytes>
+__device__ __forceinline__ const void* gaddr(const void* base, uint32_t off) {
+  const void* p;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(off), "n"(kBytes), "l"(base));
+  return p;
+}
+// the image fill as a 32-bit smem word: float bits, or two int16 copies
+template <class T> __device__ __forceinline__ uint32_t fill_word(const WarpArgs& a);
+template <> __device__ __forceinline__ uint32_t fill_word<float>(const WarpArgs& a) {
+  return __float_as_uint(a.fill);
+}
+template <> __device__ __forceinline__ uint32_t fill_word<int16_t>(const WarpArgs& a) {
+  return a.fill16_pair;
+}
+
+template <class T, bool kLabels, bool kInside>
+__device__ __forceinline__ void stage_impl(const WarpArgs& a, const T* __restrict__ vin,
                                            const uint8_t* __restrict__ lin, const Box& b,
                                            uint32_t simg, uint32_t slbl) {
-  const int CW = b.W >> 2;
+  constexpr int kC = InT<T>::kChunk, kB = InT<T>::kBytes;
+  const int CW = b.W / kC;
   const int slots = CW * b.H;
   const uint32_t plane = static_cast<uint32_t>(a.nx) * static_cast<uint32_t>(a.ny);
-  const float f = a.fill;
+  const uint32_t fw = fill_word<T>(a);
   const uint32_t lf4 = a.label_fill * 0x01010101u;
   for (int s = threadIdx.x; s < slots; s += THREADS) {
     const int r = s / CW, c = s - r * CW;
-    const int gx = b.bx + 4 * c, gy = b.by + r;
-    const uint32_t e = static_cast<uint32_t>(r * b.W + 4 * c);
-    uint32_t si = simg + 4u * e, sl = slbl + e;
+    const int gx = b.bx + kC * c, gy = b.by + r;
+    const uint32_t e = static_cast<uint32_t>(r * b.W + kC * c);
+    uint32_t si = simg + kB * e, sl = slbl + e;
     uint32_t goff = static_cast<uint32_t>(b.bz) * plane + static_cast<uint32_t>(gy * a.nx + gx);
     const uint32_t sstep = static_cast<uint32_t>(b.P);
+    auto copy = [&]() {
+      cp_async16(si, gaddr<kB>(vin, goff));
+      if (kLabels) {
+        if (kC == 4)
+          cp_async4(sl, gaddr<1>(lin, goff));
+        else
+          cp_async8(sl, gaddr<1>(lin, goff));
+      }
+    };
     if (kInside) {
 #pragma unroll 4
       for (int z = 0; z < b.D; ++z) {
-        cp_async16(si, gaddr_f32(vin, goff));
-        if (kLabels) cp_async4(sl, gaddr_u8(lin, goff));
-        si += 4u * sstep;
+        copy();
+        si += kB * sstep;
         sl += sstep;
         goff += plane;
       }
@@ -227,13 +274,17 @@ __device__ __forceinline__ void stage_impl(const WarpArgs& a, const float* __res
       for (int z = 0; z < b.D; ++z) {
         const int gz = b.bz + z;
         if (row_in & (static_cast<unsigned>(gz) < static_cast<unsigned>(a.nz))) {
-          cp_async16(si, gaddr_f32(vin, goff));
-          if (kLabels) cp_async4(sl, gaddr_u8(lin, goff));
+          copy();
         } else {
-          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(si), "f"(f) : "memory");
-          if (kLabels) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl), "r"(lf4) : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(si), "r"(fw) : "memory");
+          if (kLabels) {
+            if (kC == 4)
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl), "r"(lf4) : "memory");
+            else
+              asm volatile("st.shared.v2.b32 [%0], {%1, %1};" ::"r"(sl), "r"(lf4) : "memory");
+          }
         }
-        si += 4u * sstep;
+        si += kB * sstep;
         sl += sstep;
         goff += plane;
       }
@@ -241,15 +292,15 @@ __device__ __forceinline__ void stage_impl(const WarpArgs& a, const float* __res
   }
 }
 
-template <bool kLabels>
-__device__ __forceinline__ void stage(const WarpArgs& a, const float* vin, const uint8_t* lin,
+template <class T, bool kLabels>
+__device__ __forceinline__ void stage(const WarpArgs& a, const T* vin, const uint8_t* lin,
                                       const Box& b, uint32_t simg, uint32_t slbl) {
   const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
                       b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
   if (inside)
-    stage_impl<kLabels, true>(a, vin, lin, b, simg, slbl);
+    stage_impl<T, kLabels, true>(a, vin, lin, b, simg, slbl);
   else
-    stage_impl<kLabels, false>(a, vin, lin, b, simg, slbl);
+    stage_impl<T, kLabels, false>(a, vin, lin, b, simg, slbl);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,8 +339,10 @@ struct View {
   float nx, ny, nz;       // clamp bounds
 };
 
+template <class T>
 __device__ __forceinline__ View make_view(const WarpArgs& a, const Box& b, uint32_t simg,
                                           uint32_t slbl) {
+  constexpr uint32_t kB = InT<T>::kBytes;
   View v;
   v.Wf = pin(static_cast<float>(b.W));
   v.Pf = pin(static_cast<float>(b.P));
@@ -297,10 +350,10 @@ __device__ __forceinline__ View make_view(const WarpArgs& a, const Box& b, uint3
   v.Plf = pin(static_cast<float>(b.Pl));
   v.Mby = pin(kM + static_cast<float>(b.by));
   v.Mbz = pin(kM + static_cast<float>(b.bz));
-  v.W4 = pin(4u * static_cast<uint32_t>(b.W));
-  v.P4 = pin(4u * static_cast<uint32_t>(b.P));
+  v.W4 = pin(kB * static_cast<uint32_t>(b.W));
+  v.P4 = pin(kB * static_cast<uint32_t>(b.P));
   // bits(L) - kMbits = fx + W ry + P rz; element index = that - bx
-  v.cimg = opaque(simg - 4u * static_cast<uint32_t>(b.bx) - 4u * static_cast<uint32_t>(kMbits));
+  v.cimg = opaque(simg - kB * static_cast<uint32_t>(b.bx) - kB * static_cast<uint32_t>(kMbits));
   v.clbl = opaque(slbl - static_cast<uint32_t>(b.bxl) - static_cast<uint32_t>(kMbits));
   v.nx = static_cast<float>(a.nx);
   v.ny = static_cast<float>(a.ny);
@@ -350,15 +403,40 @@ __device__ __forceinline__ uint32_t addr1(float L, uint32_t c) {
   asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(__float_as_uint(L)), "r"(c));
   return r;
 }
-// the two x-neighbours at addr and addr + 4
-__device__ __forceinline__ void lds_pair(uint32_t a, float& v0, float& v1) {
+__device__ __forceinline__ uint32_t addr2(float L, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(r) : "r"(__float_as_uint(L)), "r"(c));
+  return r;
+}
+template <class T> __device__ __forceinline__ uint32_t addrT(float L, uint32_t c) {
+  return InT<T>::kBytes == 4 ? addr4(L, c) : addr2(L, c);
+}
+// the two x-neighbours at addr and addr + element size, as floats
+template <class T> __device__ __forceinline__ void lds_pair(uint32_t a, float& v0, float& v1);
+template <> __device__ __forceinline__ void lds_pair<float>(uint32_t a, float& v0, float& v1) {
   asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];"
                : "=f"(v0), "=f"(v1)
                : "r"(a));
 }
+template <> __device__ __forceinline__ void lds_pair<int16_t>(uint32_t a, float& v0, float& v1) {
+  asm volatile(
+      "{\n\t.reg .s16 h0, h1;\n\tld.shared.s16 h0, [%2];\n\tld.shared.s16 h1, [%2+2];\n\t"
+      "cvt.rn.f32.s16 %0, h0;\n\tcvt.rn.f32.s16 %1, h1;\n\t}"
+      : "=f"(v0), "=f"(v1)
+      : "r"(a));
+}
+template <class T> __device__ __forceinline__ float lds_one(uint32_t a) {
+  float v0, v1;
+  if (InT<T>::kBytes == 4) return lds_f32(a);
+  asm volatile("{\n\t.reg .s16 h0;\n\tld.shared.s16 h0, [%1];\n\tcvt.rn.f32.s16 %0, h0;\n\t}"
+               : "=f"(v0)
+               : "r"(a));
+  (void)v1;
+  return v0;
+}
 
 // Staged sampling of a y-pair: image (trilinear or nearest) and label.
-template <bool kLabels, bool kNearest, bool kClamp>
+template <class T, bool kLabels, bool kNearest, bool kClamp>
 __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, float2 pz,
                                         float2& img, uint32_t& l0, uint32_t& l1) {
   if (kClamp) {
@@ -388,21 +466,21 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
     }
   }
   if (kNearest) {
-    img = make_float2(lds_f32(addr4(Ln.x, v.cimg)), lds_f32(addr4(Ln.y, v.cimg)));
+    img = make_float2(lds_one<T>(addrT<T>(Ln.x, v.cimg)), lds_one<T>(addrT<T>(Ln.y, v.cimg)));
     return;
   }
-  const uint32_t a0 = addr4(L.x, v.cimg), b0 = addr4(L.y, v.cimg);
+  const uint32_t a0 = addrT<T>(L.x, v.cimg), b0 = addrT<T>(L.y, v.cimg);
   const uint32_t a1 = a0 + v.W4, b1 = b0 + v.W4, a2 = a0 + v.P4, b2 = b0 + v.P4;
   const uint32_t a3 = a2 + v.W4, b3 = b2 + v.W4;
   float2 c000, c100, c010, c110, c001, c101, c011, c111;
-  lds_pair(a0, c000.x, c100.x);
-  lds_pair(b0, c000.y, c100.y);
-  lds_pair(a1, c010.x, c110.x);
-  lds_pair(b1, c010.y, c110.y);
-  lds_pair(a2, c001.x, c101.x);
-  lds_pair(b2, c001.y, c101.y);
-  lds_pair(a3, c011.x, c111.x);
-  lds_pair(b3, c011.y, c111.y);
+  lds_pair<T>(a0, c000.x, c100.x);
+  lds_pair<T>(b0, c000.y, c100.y);
+  lds_pair<T>(a1, c010.x, c110.x);
+  lds_pair<T>(b1, c010.y, c110.y);
+  lds_pair<T>(a2, c001.x, c101.x);
+  lds_pair<T>(b2, c001.y, c101.y);
+  lds_pair<T>(a3, c011.x, c111.x);
+  lds_pair<T>(b3, c011.y, c111.y);
   const float2 c00 = lerp2(c000, c100, tx), c10 = lerp2(c010, c110, tx);
   const float2 c01 = lerp2(c001, c101, tx), c11 = lerp2(c011, c111, tx);
   img = lerp2(lerp2(c00, c10, ty), lerp2(c01, c11, ty), tz);
@@ -412,8 +490,8 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
 // Gather sampling of one voxel through L1/L2 with per-corner bounds (R6-R8,
 // NaN-safe float compares first).  Used for parts whose box does not fit.
 // ---------------------------------------------------------------------------
-template <bool kLabels, bool kNearest>
-__device__ __forceinline__ void sample_gather(const WarpArgs& a, const float* __restrict__ vin,
+template <class T, bool kLabels, bool kNearest>
+__device__ __forceinline__ void sample_gather(const WarpArgs& a, const T* __restrict__ vin,
                                               const uint8_t* __restrict__ lin, float px,
                                               float py, float pz, float& img, uint32_t& lbl) {
   img = a.fill;
@@ -432,21 +510,21 @@ __device__ __forceinline__ void sample_gather(const WarpArgs& a, const float* __
   if (near_in && (kLabels || kNearest)) {
     const int64_t r = (iz + (tz >= 0.5f)) * sz + (iy + (ty >= 0.5f)) * sy + (ix + (tx >= 0.5f));
     if (kLabels) lbl = __ldg(lin + r);
-    if (kNearest) img = __ldg(vin + r);
+    if (kNearest) img = InT<T>::load(vin + r);
   }
   if (kNearest) return;
   const bool x0 = ix >= 0, x1 = ix + 1 < a.nx, y0 = iy >= 0, y1 = iy + 1 < a.ny;
   const bool z0 = iz >= 0, z1 = iz + 1 < a.nz;
-  const float* b = vin + (iz * sz + iy * sy + ix);
+  const T* b = vin + (iz * sz + iy * sy + ix);
   const float f = a.fill;
-  const float c000 = (x0 & y0 & z0) ? __ldg(b) : f;
-  const float c100 = (x1 & y0 & z0) ? __ldg(b + 1) : f;
-  const float c010 = (x0 & y1 & z0) ? __ldg(b + sy) : f;
-  const float c110 = (x1 & y1 & z0) ? __ldg(b + sy + 1) : f;
-  const float c001 = (x0 & y0 & z1) ? __ldg(b + sz) : f;
-  const float c101 = (x1 & y0 & z1) ? __ldg(b + sz + 1) : f;
-  const float c011 = (x0 & y1 & z1) ? __ldg(b + sz + sy) : f;
-  const float c111 = (x1 & y1 & z1) ? __ldg(b + sz + sy + 1) : f;
+  const float c000 = (x0 & y0 & z0) ? InT<T>::load(b) : f;
+  const float c100 = (x1 & y0 & z0) ? InT<T>::load(b + 1) : f;
+  const float c010 = (x0 & y1 & z0) ? InT<T>::load(b + sy) : f;
+  const float c110 = (x1 & y1 & z0) ? InT<T>::load(b + sy + 1) : f;
+  const float c001 = (x0 & y0 & z1) ? InT<T>::load(b + sz) : f;
+  const float c101 = (x1 & y0 & z1) ? InT<T>::load(b + sz + 1) : f;
+  const float c011 = (x0 & y1 & z1) ? InT<T>::load(b + sz + sy) : f;
+  const float c111 = (x1 & y1 & z1) ? InT<T>::load(b + sz + sy + 1) : f;
   const float c00 = lerp1(c000, c100, tx), c10 = lerp1(c010, c110, tx);
   const float c01 = lerp1(c001, c101, tx), c11 = lerp1(c011, c111, tx);
   img = lerp1(lerp1(c00, c10, ty), lerp1(c01, c11, ty), tz);
@@ -476,11 +554,11 @@ __device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
 // group's normals (computed while the staging copies were in flight); the next
 // group's Philox block is computed inside each iteration (independent chain).
 // ---------------------------------------------------------------------------
-template <bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp>
+template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp>
 __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n) {
-  const float* __restrict__ vin = a.in + vi * a.in_stride;
+  const T* __restrict__ vin = in_ptr<T>(a) + vi * a.in_stride;
   const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
   Vol V = V0;
 #pragma unroll
@@ -537,10 +615,10 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
       float2 img;
       uint32_t l0 = 0, l1 = 0;
       if (kStaged) {
-        sample2<kLabels, kNearest, kClamp>(v, px, py, pz, img, l0, l1);
+        sample2<T, kLabels, kNearest, kClamp>(v, px, py, pz, img, l0, l1);
       } else {
-        sample_gather<kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
-        sample_gather<kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
+        sample_gather<T, kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
+        sample_gather<T, kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
       }
       float2 out = photometric2<kPh>(img, make_float2(ns[2 * h], ns[2 * h + 1]), V);
       if (occl) out = make_float2(0.0f, 0.0f);  // PAPER.md:437-438, R15
@@ -595,7 +673,7 @@ __device__ __forceinline__ float4 first_normals(const WarpArgs& a, const VolDev&
 // Rare path (out of line): the tile in y-parts of TY/2, TY/4, ... rows, each
 // staged on its own, or gathered when even a 4-row part does not fit (or
 // always, for the W3D_KERNEL_GATHER variant).
-template <int TY, bool kLabels, bool kNearest, int kPh>
+template <class T, int TY, bool kLabels, bool kNearest, int kPh>
 __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int cap,
                                         bool gather_only) {
   const int vi = static_cast<int>(blockIdx.z) / tiles_z;
@@ -604,7 +682,7 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
   const uint32_t simg = smem_base();
   const VolDev& P = a.vol[vi];
   const Vol V = load_vol(P);
-  const float* vin = a.in + vi * a.in_stride;
+  const T* vin = in_ptr<T>(a) + vi * a.in_stride;
   const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
   const int lane = threadIdx.x & 31;
   const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
@@ -616,32 +694,32 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
   for (; rows >= 4; rows >>= 1) {
     bool all = true;
     for (int y = oy; y <= ylast; y += rows)
-      all &= tile_box(a, P.A, ox, y, min(y + rows - 1, ylast), oz, cap, b);
+      all &= tile_box<T>(a, P.A, ox, y, min(y + rows - 1, ylast), oz, cap, b);
     if (all) break;
   }
   if (rows < 4) {  // gathers
     if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[1], 1ull);
     if (!live) return;
     View v;
-    column_rows<kLabels, kNearest, kPh, false, false>(a, P, V, v, vi, X, Z, oy, TY / 4,
+    column_rows<T, kLabels, kNearest, kPh, false, false>(a, P, V, v, vi, X, Z, oy, TY / 4,
                                                       first_normals<kPh>(a, P, V, X, Z, oy));
     return;
   }
   if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[0], 1ull);
   for (int y = oy; y <= ylast; y += rows) {
-    tile_box(a, P.A, ox, y, min(y + rows - 1, ylast), oz, cap, b);
-    const uint32_t slbl = simg + 4u * static_cast<uint32_t>(b.P * b.D);
+    tile_box<T>(a, P.A, ox, y, min(y + rows - 1, ylast), oz, cap, b);
+    const uint32_t slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
     __syncthreads();  // previous part's buffer no longer read
-    stage<kLabels>(a, vin, lin, b, simg, slbl);
+    stage<T, kLabels>(a, vin, lin, b, simg, slbl);
     const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, y) : make_float4(0, 0, 0, 0);
-    const View v = make_view(a, b, simg, slbl);
+    const View v = make_view<T>(a, b, simg, slbl);
     cp_async_wait_all();
     __syncthreads();
     if (!live) continue;
     if (b.clamp)
-      column_rows<kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, y, rows / 4, n);
+      column_rows<T, kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, y, rows / 4, n);
     else
-      column_rows<kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, y, rows / 4, n);
+      column_rows<T, kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, y, rows / 4, n);
   }
 }
 
@@ -698,6 +776,7 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 // alone: every p of the tile is >= p(origin) + sum_j min(0, A_kj span_j) (up to
 // fp32 rounding, inside the host's margin), so the box needs no per-tile
 // reduction over corners.  False for coordinates beyond 2^20 (cp.async path).
+template <class T>
 __device__ __forceinline__ bool tma_box(const VolDev& P, int ox, int oy, int oz, Box& b) {
   const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
   int lo[3];
@@ -709,7 +788,7 @@ __device__ __forceinline__ bool tma_box(const VolDev& P, int ox, int oy, int oz,
     lo[k] = __float2int_rd(__fadd_rd(p0, P.box_mlo[k]));
   }
   // TMA box inner origins must be 16 B aligned: image x0 % 4, label x0 % 16
-  b.bx = lo[0] & W3D_IMG_ALIGN_MASK;
+  b.bx = lo[0] & ~(InT<T>::kChunk - 1);
   b.bxl = lo[0] & ~15;
   b.by = lo[1];
   b.bz = lo[2];
@@ -725,10 +804,11 @@ __device__ __forceinline__ bool tma_box(const VolDev& P, int ox, int oy, int oz,
 
 // fill / label_fill over the out-of-volume elements of a TMA box (TMA wrote 0);
 // rows [0, W) of the image box and [0, Wl) of the label box.
-template <bool kLabels>
+template <class T, bool kLabels>
 __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint32_t simg,
                                           uint32_t slbl, bool fi, bool fl) {
-  const float f = a.fill;
+  constexpr uint32_t kB = InT<T>::kBytes;
+  const uint32_t fw = fill_word<T>(a);
   const uint32_t lf4 = a.label_fill * 0x01010101u;
   const int head = min(b.W, max(0, -b.bx)), tail = max(0, min(b.W, a.nx - b.bx));
   const int headl = min(b.Wl, max(0, -b.bxl)), taill = max(0, min(b.Wl, a.nx - b.bxl));
@@ -736,12 +816,12 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint3
     const int z = r / b.H, y = r - z * b.H;
     const bool row_out = static_cast<unsigned>(b.bz + z) >= static_cast<unsigned>(a.nz) ||
                          static_cast<unsigned>(b.by + y) >= static_cast<unsigned>(a.ny);
-    const uint32_t irow = simg + 4u * static_cast<uint32_t>(z * b.P + y * b.W);
+    const uint32_t irow = simg + kB * static_cast<uint32_t>(z * b.P + y * b.W);
     const uint32_t lrow = slbl + static_cast<uint32_t>(z * b.Pl + y * b.Wl);
     if (row_out) {
       if (fi)
-        for (int x = 0; x < b.W; x += 4)
-          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(irow + 4u * x), "f"(f)
+        for (int x = 0; x < b.W; x += 16 / kB)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(irow + kB * x), "r"(fw)
                        : "memory");
       if (kLabels && fl)
         for (int x = 0; x < b.Wl; x += 16)
@@ -750,10 +830,18 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint3
       continue;
     }
     if (fi) {
-      for (int x = 0; x < head; ++x)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(irow + 4u * x), "f"(f) : "memory");
-      for (int x = tail; x < b.W; ++x)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(irow + 4u * x), "f"(f) : "memory");
+      for (int x = 0; x < head; ++x) {
+        if (kB == 4)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
+        else
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
+      }
+      for (int x = tail; x < b.W; ++x) {
+        if (kB == 4)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
+        else
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
+      }
     }
     if (kLabels && fl) {
       for (int x = 0; x < headl; ++x)
@@ -765,7 +853,7 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint3
 }
 
 // grid = (tiles per volume, volumes); tiles x-fastest, then y, then z.
-template <int TY, int MINB, bool kLabels, bool kNearest, int kPh, bool kGather>
+template <class T, int TY, int MINB, bool kLabels, bool kNearest, int kPh, bool kGather>
 __global__ void __launch_bounds__(THREADS, MINB)
     warp3d_cube_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap) {
   __shared__ __align__(8) unsigned long long s_mbar;
@@ -786,10 +874,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
     __syncthreads();
   }
-  const bool tma = use_tma && tma_box(P, ox, oy, oz, b);
+  const bool tma = use_tma && tma_box<T>(P, ox, oy, oz, b);
   if (!tma) {
-    if (kGather || !tile_box(a, P.A, ox, oy, ylast, oz, cap, b)) {
-      tile_parts<TY, kLabels, kNearest, kPh>(a, tiles_z, cap, kGather);
+    if (kGather || !tile_box<T>(a, P.A, ox, oy, ylast, oz, cap, b)) {
+      tile_parts<T, TY, kLabels, kNearest, kPh>(a, tiles_z, cap, kGather);
       return;
     }
   }
@@ -797,30 +885,30 @@ __global__ void __launch_bounds__(THREADS, MINB)
   uint32_t slbl;
 #ifdef W3D_DBG_NOSTAGE
   if (tma) {
-    slbl = simg + ((4u * static_cast<uint32_t>(b.P * b.D) + 127u) & ~127u);
+    slbl = simg + ((InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D) + 127u) & ~127u);
   } else {
-    slbl = simg + 4u * static_cast<uint32_t>(b.P * b.D);
+    slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
   }
   if (false) {
 #else
   if (tma) {
 #endif
-    slbl = simg + ((4u * static_cast<uint32_t>(b.P * b.D) + 127u) & ~127u);
+    slbl = simg + ((InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D) + 127u) & ~127u);
 #ifdef W3D_DEBUG_TMA
     if (threadIdx.x == 0 && blockIdx.x < 3)
       printf("blk %d vol %d box o=(%d %d %d) WHD=(%d %d %d) Wl=%d P=%d Pl=%d simg=%u slbl=%u\n",
              blockIdx.x, vi, b.bx, b.by, b.bz, b.W, b.H, b.D, b.Wl, b.P, b.Pl, simg, slbl);
 #endif
     if (threadIdx.x == 0) {
-      mbar_expect_tx(mbar, 4u * static_cast<uint32_t>(b.P * b.D) +
+      mbar_expect_tx(mbar, InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D) +
                                (kLabels ? static_cast<uint32_t>(b.Pl * b.D) : 0u));
       tma_load_3d(simg, &a.tm[2 * vi], b.bx, b.by, b.bz, mbar);
       if (kLabels) tma_load_3d(slbl, &a.tm[2 * vi + 1], b.bxl, b.by, b.bz, mbar);
     }
   } else {
-    slbl = simg + 4u * static_cast<uint32_t>(b.P * b.D);
-    stage<kLabels>(a, a.in + vi * a.in_stride, kLabels ? a.in_lbl + vi * a.in_stride : nullptr,
-                   b, simg, slbl);
+    slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
+    stage<T, kLabels>(a, in_ptr<T>(a) + vi * a.in_stride,
+                      kLabels ? a.in_lbl + vi * a.in_stride : nullptr, b, simg, slbl);
   }
   const Vol V = load_vol(P);
   const int lane = threadIdx.x & 31;
@@ -828,7 +916,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const bool live = X < a.mx && Z < a.mz;
   // the first Philox block overlaps the copies in flight
   const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, oy) : make_float4(0, 0, 0, 0);
-  const View v = make_view(a, b, simg, slbl);
+  const View v = make_view<T>(a, b, simg, slbl);
 #ifdef W3D_DBG_NOSTAGE
 #ifndef W3D_DBG_NOBAR
   __syncthreads();
@@ -840,9 +928,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
     mbar_wait(mbar, 0);
     const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
                         b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
-    const bool fi = a.fill != 0.0f, fl = kLabels && a.label_fill != 0u;
+    const bool fi = a.fill != 0.0f, fl = kLabels && a.label_fill != 0u;  // TMA fills 0
     if (!inside && (fi || fl)) {
-      tma_fixup<kLabels>(a, b, simg, slbl, fi, fl);
+      tma_fixup<T, kLabels>(a, b, simg, slbl, fi, fl);
       __syncthreads();
     }
   } else {
@@ -855,9 +943,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
   return;
 #endif
   if (b.clamp)
-    column_rows<kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
+    column_rows<T, kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
   else
-    column_rows<kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
+    column_rows<T, kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -873,24 +961,25 @@ constexpr int kTY = W3D_TY, kMinB = W3D_MINB;
 // staging buffer (voxels of 5 B): kMinB * (kCapVox * 5 B + 256 + 1 KB) <= 228 KB
 constexpr int kCapVox = (233472 / kMinB - 1024 - 272) / 5;
 
-template <bool kLabels, bool kNearest, int kPh, bool kGather = false>
+template <class T, bool kLabels, bool kNearest, int kPh, bool kGather = false>
 static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
   const int tiles_x = (a.mx + TX - 1) / TX, tiles_y = (a.my + kTY - 1) / kTY;
   const int tiles_z = (a.mz + TZ - 1) / TZ;
   if (tiles_y > 65535 || int64_t(tiles_z) * a.nvol > 65535) return cudaErrorInvalidConfiguration;
   const size_t smem = kGather ? 0 : static_cast<size_t>(kCapVox) * 5 + 256;
+  const int cap = kCapVox * 5 / (InT<T>::kBytes + 1);  // staged voxels (image + label bytes)
   static bool configured = false;
   if (!configured && !kGather) {
     const cudaError_t e = cudaFuncSetAttribute(
-        warp3d_cube_kernel<kTY, kMinB, kLabels, kNearest, kPh, kGather>,
+        warp3d_cube_kernel<T, kTY, kMinB, kLabels, kNearest, kPh, kGather>,
         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
                   static_cast<unsigned>(tiles_z * a.nvol));
-  warp3d_cube_kernel<kTY, kMinB, kLabels, kNearest, kPh, kGather>
-      <<<grid, THREADS, smem, s>>>(a, tiles_z, kCapVox);
+  warp3d_cube_kernel<T, kTY, kMinB, kLabels, kNearest, kPh, kGather>
+      <<<grid, THREADS, smem, s>>>(a, tiles_z, cap);
   return cudaGetLastError();
 }
 
@@ -906,56 +995,66 @@ static bool all_full(const WarpArgs& a) {
   return true;
 }
 
+template <class T>
+static cudaError_t launch_typed(const WarpArgs& a, bool gather_only, cudaStream_t s) {
+  const bool labels = a.in_lbl != nullptr;
+  const bool nearest = a.interp == W3D_INTERP_NEAREST;
+  if (gather_only || !cube_supported(a)) {
+    if (nearest)
+      return labels ? launch_v<T, true, true, kPhGeneric, true>(a, s)
+                    : launch_v<T, false, true, kPhGeneric, true>(a, s);
+    return labels ? launch_v<T, true, false, kPhGeneric, true>(a, s)
+                  : launch_v<T, false, false, kPhGeneric, true>(a, s);
+  }
+  if (nearest)
+    return labels ? launch_v<T, true, true, kPhGeneric>(a, s)
+                  : launch_v<T, false, true, kPhGeneric>(a, s);
+  if (all_full(a))
+    return labels ? launch_v<T, true, false, kPhFull>(a, s) : launch_v<T, false, false, kPhFull>(a, s);
+  return labels ? launch_v<T, true, false, kPhGeneric>(a, s)
+                : launch_v<T, false, false, kPhGeneric>(a, s);
+}
+
 }  // namespace cube
 
-// Coordinates must stay below 2^21 for the magic-number floor, pitches below
-// the float-exact range; dims up to 2^21 per axis qualify.
+// Staged layouts: 16 B chunks (nx and the volume stride multiples of the chunk,
+// 16 B aligned input), coordinates below 2^21 (magic-number floor), and for
+// int16 input a fill that int16 represents (the staged box holds fill).
 bool cube_supported(const WarpArgs& a) {
-  return (a.nx % 4 == 0) && (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) &&
-         (a.in_stride % 4 == 0) &&
-         (a.in_lbl == nullptr || reinterpret_cast<uintptr_t>(a.in_lbl) % 4 == 0) &&
+  const int chunk = a.in16 ? 8 : 4;
+  const void* in = a.in16 ? static_cast<const void*>(a.in16) : static_cast<const void*>(a.in);
+  const bool fill_ok = !a.in16 || (a.fill == std::nearbyint(a.fill) && a.fill >= -32768.0f &&
+                                   a.fill <= 32767.0f);
+  return (a.nx % chunk == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
+         (a.in_stride % chunk == 0) && fill_ok &&
+         (a.in_lbl == nullptr || reinterpret_cast<uintptr_t>(a.in_lbl) % 8 == 0) &&
          a.nx < (1 << 21) && a.ny < (1 << 21) && a.nz < (1 << 21);
 }
 
 // gather_only (W3D_KERNEL_GATHER, or layouts cube_supported() rejects): every
 // tile through L1/L2 gathers.
 cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s) {
-  using namespace cube;
-  const bool labels = a.in_lbl != nullptr;
-  const bool nearest = a.interp == W3D_INTERP_NEAREST;
-  cudaError_t e;
-  if (gather_only || !cube_supported(a)) {
-    if (nearest)
-      e = labels ? launch_v<true, true, kPhGeneric, true>(a, s)
-                 : launch_v<false, true, kPhGeneric, true>(a, s);
-    else
-      e = labels ? launch_v<true, false, kPhGeneric, true>(a, s)
-                 : launch_v<false, false, kPhGeneric, true>(a, s);
-  } else if (nearest)
-    e = labels ? launch_v<true, true, kPhGeneric>(a, s) : launch_v<false, true, kPhGeneric>(a, s);
-  else if (all_full(a))
-    e = labels ? launch_v<true, false, kPhFull>(a, s) : launch_v<false, false, kPhFull>(a, s);
-  else
-    e = labels ? launch_v<true, false, kPhGeneric>(a, s) : launch_v<false, false, kPhGeneric>(a, s);
+  const cudaError_t e = a.in16 ? cube::launch_typed<int16_t>(a, gather_only, s)
+                               : cube::launch_typed<float>(a, gather_only, s);
   note_launch();
   return e;
 }
 
 bool cube_tma_supported(const WarpArgs& a) {
   // 16 B aligned global strides and volume bases for the image (and labels)
-  const bool img = cube_supported(a) && a.nx % 4 == 0 && a.in_stride % 4 == 0;
   const bool lbl = a.in_lbl == nullptr ||
                    (a.nx % 16 == 0 && a.in_stride % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(a.in_lbl) % 16 == 0);
-  return img && lbl && a.interp == W3D_INTERP_LINEAR;
+  return cube_supported(a) && lbl && a.interp == W3D_INTERP_LINEAR;
 }
 
 // TMA box dims of one volume: the footprint extent of a full tile, ext_k =
 // sum_j |A_kj| (T_j - 1) input voxels, plus the trilinear +1 corner, the floor
-// offsets and a rounding margin; rows padded to 16 B (labels: 16 elements);
-// rows per plane padded so the plane pitch spreads the two half-warps over the
-// banks (tools/model_tiles.py).  box_w = 0 when the box exceeds the buffer.
-void cube_tma_box(const float A[12], VolDev& P, bool labels) {
+// offsets and a rounding margin; rows of 16 B multiples with 16 B aligned
+// origins (image: 4 float / 8 int16 elements, labels 16); rows per plane padded
+// so the plane pitch spreads the two half-warps over the banks
+// (tools/model_tiles.py).  box_w = 0 when the box exceeds the buffer.
+void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes) {
   using namespace cube;
   const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
   int d[3];
@@ -976,12 +1075,14 @@ void cube_tma_box(const float A[12], VolDev& P, bool labels) {
     // origin >= p_min - margin - 1, needed up to floor(p_max) + 1 <= p_min + ext + margin + 1
     d[k] = static_cast<int>(std::floor(ext + 2.0 * margin)) + 4;
   }
-  // + alignment slack of the 16 B aligned inner origins (image x0 % 4, labels
-  // x0 % 16; an unaligned origin faults: measured)
-  int W = (d[0] + 3 + 3) & ~3, H = d[1], D = d[2];
+  // + alignment slack of the 16 B aligned inner origins (an unaligned origin
+  // faults: measured)
+  const int al = 16 / elem_bytes;
+  int W = (d[0] + al - 1 + al - 1) & ~(al - 1), H = d[1], D = d[2];
   const int Wl = (d[0] + 15 + 15) & ~15;
   auto bytes = [&](int h) {
-    return ((int64_t(4) * W * h * D + 127) & ~int64_t(127)) + (labels ? int64_t(Wl) * h * D : 0);
+    return ((int64_t(elem_bytes) * W * h * D + 127) & ~int64_t(127)) +
+           (labels ? int64_t(Wl) * h * D : 0);
   };
   for (int h = H; h < H + 8; ++h) {  // bank-spreading plane pitch, if it still fits
     const int res = (W * h) & 31;

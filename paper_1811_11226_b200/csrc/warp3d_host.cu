@@ -193,16 +193,20 @@ static EncodeFn get_encode() {
   return fn;
 }
 
-static bool encode_3d(CUtensorMap* m, bool u8, const void* base, const WarpArgs& a, uint32_t bw,
+// elem: 1 = uint8 labels, 2 = int16 image, 4 = float32 image
+static bool encode_3d(CUtensorMap* m, int elem, const void* base, const WarpArgs& a, uint32_t bw,
                       uint32_t bh, uint32_t bd) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
-  const cuuint64_t es = u8 ? 1 : 4;
+  const cuuint64_t es = static_cast<cuuint64_t>(elem);
+  const CUtensorMapDataType dt = elem == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16  // raw int16 bits
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const cuuint64_t dims[3] = {cuuint64_t(a.nx), cuuint64_t(a.ny), cuuint64_t(a.nz)};
   const cuuint64_t strides[2] = {cuuint64_t(a.nx) * es, cuuint64_t(a.nx) * a.ny * es};
   const cuuint32_t box[3] = {bw, bh, bd};
   const cuuint32_t estr[3] = {1, 1, 1};
-  return enc(m, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+  return enc(m, dt, 3,
              const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -212,9 +216,10 @@ struct MapKey {
   const void* base = nullptr;
   int32_t nx = 0, ny = 0, nz = 0;
   uint32_t bw = 0, bh = 0, bd = 0;
+  int32_t elem = 0;
   bool operator==(const MapKey& o) const {
     return base == o.base && nx == o.nx && ny == o.ny && nz == o.nz && bw == o.bw &&
-           bh == o.bh && bd == o.bd;
+           bh == o.bh && bd == o.bd && elem == o.elem;
   }
 };
 
@@ -227,21 +232,23 @@ static bool prepare_tma(WarpArgs& args, const float* const* affines) {
   for (int32_t i = 0; i < args.nvol && ok; ++i) {
     VolDev& P = args.vol[i];
     if (i >= kTmaVolPerLaunch) break;
-    cube_tma_box(affines[i], P, labels);
+    const int eb = args.in16 ? 2 : 4;
+    cube_tma_box(affines[i], P, labels, eb);
     if (!P.box_w) continue;
-    MapKey ki{args.in + i * args.in_stride, args.nx, args.ny, args.nz, P.box_w, P.box_h,
-              P.box_d};
+    const void* base = args.in16 ? static_cast<const void*>(args.in16 + i * args.in_stride)
+                                 : static_cast<const void*>(args.in + i * args.in_stride);
+    MapKey ki{base, args.nx, args.ny, args.nz, P.box_w, P.box_h, P.box_d, eb};
     if (!(ki == key_img[i])) {
       key_img[i] = MapKey();
-      ok = encode_3d(&args.tm[2 * i], false, ki.base, args, ki.bw, ki.bh, ki.bd);
+      ok = encode_3d(&args.tm[2 * i], eb, ki.base, args, ki.bw, ki.bh, ki.bd);
       if (ok) key_img[i] = ki;
     }
     if (ok && labels) {
       MapKey kl{args.in_lbl + i * args.in_stride, args.nx, args.ny, args.nz, P.box_wl, P.box_h,
-                P.box_d};
+                P.box_d, 1};
       if (!(kl == key_lbl[i])) {
         key_lbl[i] = MapKey();
-        ok = encode_3d(&args.tm[2 * i + 1], true, kl.base, args, kl.bw, kl.bh, kl.bd);
+        ok = encode_3d(&args.tm[2 * i + 1], 1, kl.base, args, kl.bw, kl.bh, kl.bd);
         if (ok) key_lbl[i] = kl;
       }
     }
@@ -251,8 +258,10 @@ static bool prepare_tma(WarpArgs& args, const float* const* affines) {
   return ok;
 }
 
-// One batch, already validated; chunks of kMaxVolPerLaunch volumes.
-static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_labels,
+// One batch, already validated; chunks of kMaxVolPerLaunch volumes.  The image
+// input is float32 (in) or int16 (in16, NEXT-4), exactly one non-null.
+static w3d_status run_batched_t(int32_t batch, const float* in, const int16_t* in16,
+                                const uint8_t* in_labels,
                               w3d_dims in_dims, const float* const* affines,
                               const w3d_photometric* const* phs, w3d_interp interp, float fill,
                               uint8_t label_fill, float* out, uint8_t* out_labels,
@@ -264,7 +273,15 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
   const int32_t chunk = want_tma ? kTmaVolPerLaunch : kMaxVolPerLaunch;
   for (int32_t v0 = 0; v0 < batch; v0 += chunk) {
     const int32_t nv = (batch - v0 < chunk) ? batch - v0 : chunk;
-    args.in = in + v0 * in_n;
+    args.in = in ? in + v0 * in_n : nullptr;
+    args.in16 = in16 ? in16 + v0 * in_n : nullptr;
+    {
+      const float f = std::nearbyint(fill) == fill && fill >= -32768.0f && fill <= 32767.0f
+                          ? fill
+                          : 0.0f;
+      const uint32_t h = static_cast<uint16_t>(static_cast<int16_t>(f));
+      args.fill16_pair = h | (h << 16);
+    }
     args.in_lbl = in_labels ? in_labels + v0 * in_n : nullptr;
     args.out = out + v0 * out_n;
     args.out_lbl = out_labels ? out_labels + v0 * out_n : nullptr;
@@ -292,11 +309,20 @@ static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_
   return ok();
 }
 
-static w3d_status check_common(const float* in, w3d_dims in_dims, w3d_interp interp, float fill,
-                               float* out, w3d_dims out_dims) {
+static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_labels,
+                              w3d_dims in_dims, const float* const* affines,
+                              const w3d_photometric* const* phs, w3d_interp interp, float fill,
+                              uint8_t label_fill, float* out, uint8_t* out_labels,
+                              w3d_dims out_dims, w3d_kernel variant, cudaStream_t stream) {
+  return run_batched_t(batch, in, nullptr, in_labels, in_dims, affines, phs, interp, fill,
+                       label_fill, out, out_labels, out_dims, variant, stream);
+}
+
+static w3d_status check_common(const void* in, w3d_dims in_dims, w3d_interp interp, float fill,
+                               float* out, w3d_dims out_dims, int in_bytes = 4) {
   if (!in || !out) return fail(W3D_ERR_INVALID_ARG, "in/out must be non-NULL device pointers");
-  if (reinterpret_cast<uintptr_t>(in) % 4 || reinterpret_cast<uintptr_t>(out) % 4)
-    return fail(W3D_ERR_INVALID_ARG, "in/out must be 4-byte aligned float pointers");
+  if (reinterpret_cast<uintptr_t>(in) % in_bytes || reinterpret_cast<uintptr_t>(out) % 4)
+    return fail(W3D_ERR_INVALID_ARG, "in/out must be aligned to their element size");
   w3d_status st = check_dims(in_dims, "in_dims");
   if (st != W3D_OK) return st;
   st = check_dims(out_dims, "out_dims");
@@ -344,13 +370,15 @@ w3d_status warp3d_affine(const float* in, w3d_dims in_dims, const float affine[1
                      W3D_KERNEL_AUTO, static_cast<cudaStream_t>(stream));
 }
 
-w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_t* in_labels,
-                                    w3d_dims in_dims, const w3d_volume_params* params,
-                                    w3d_interp interp, float fill, uint8_t label_fill,
-                                    float* out, uint8_t* out_labels, w3d_dims out_dims,
-                                    w3d_kernel variant, void* stream) {
+static w3d_status batched_impl(int32_t batch, const float* in, const int16_t* in16,
+                               const uint8_t* in_labels, w3d_dims in_dims,
+                               const w3d_volume_params* params, w3d_interp interp, float fill,
+                               uint8_t label_fill, float* out, uint8_t* out_labels,
+                               w3d_dims out_dims, w3d_kernel variant, void* stream) {
   if (batch < 1) return fail(W3D_ERR_INVALID_ARG, "batch = %d must be >= 1", batch);
-  w3d_status st = check_common(in, in_dims, interp, fill, out, out_dims);
+  const int eb = in16 ? 2 : 4;
+  const void* inp = in16 ? static_cast<const void*>(in16) : static_cast<const void*>(in);
+  w3d_status st = check_common(inp, in_dims, interp, fill, out, out_dims, eb);
   if (st != W3D_OK) return st;
   if (!params) return fail(W3D_ERR_INVALID_ARG, "params must be a non-NULL host array");
   if ((in_labels == nullptr) != (out_labels == nullptr))
@@ -362,8 +390,8 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
     if ((st = check_ph(params[i].ph, i)) != W3D_OK) return st;
   }
   const int64_t in_b = int64_t(batch) * nvox(in_dims), out_b = int64_t(batch) * nvox(out_dims);
-  if (overlap(in, in_b * 4, out, out_b * 4) || overlap(in_labels, in_b, out_labels, out_b) ||
-      overlap(in, in_b * 4, out_labels, out_b) || overlap(in_labels, in_b, out, out_b * 4) ||
+  if (overlap(inp, in_b * eb, out, out_b * 4) || overlap(in_labels, in_b, out_labels, out_b) ||
+      overlap(inp, in_b * eb, out_labels, out_b) || overlap(in_labels, in_b, out, out_b * 4) ||
       overlap(out, out_b * 4, out_labels, out_b))
     return fail(W3D_ERR_INVALID_ARG, "output buffers overlap inputs or each other");
   const int n = batch;
@@ -375,14 +403,41 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
       A[i] = params[v0 + i].affine;
       P[i] = &params[v0 + i].ph;
     }
-    st = run_batched(nv, in + int64_t(v0) * nvox(in_dims),
-                     in_labels ? in_labels + int64_t(v0) * nvox(in_dims) : nullptr, in_dims, A, P,
-                     interp, fill, label_fill, out + int64_t(v0) * nvox(out_dims),
-                     out_labels ? out_labels + int64_t(v0) * nvox(out_dims) : nullptr, out_dims,
-                     variant, static_cast<cudaStream_t>(stream));
+    st = run_batched_t(nv, in ? in + int64_t(v0) * nvox(in_dims) : nullptr,
+                       in16 ? in16 + int64_t(v0) * nvox(in_dims) : nullptr,
+                       in_labels ? in_labels + int64_t(v0) * nvox(in_dims) : nullptr, in_dims, A,
+                       P, interp, fill, label_fill, out + int64_t(v0) * nvox(out_dims),
+                       out_labels ? out_labels + int64_t(v0) * nvox(out_dims) : nullptr, out_dims,
+                       variant, static_cast<cudaStream_t>(stream));
     if (st != W3D_OK) return st;
   }
   return ok();
+}
+
+w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_t* in_labels,
+                                    w3d_dims in_dims, const w3d_volume_params* params,
+                                    w3d_interp interp, float fill, uint8_t label_fill,
+                                    float* out, uint8_t* out_labels, w3d_dims out_dims,
+                                    w3d_kernel variant, void* stream) {
+  return batched_impl(batch, in, nullptr, in_labels, in_dims, params, interp, fill, label_fill,
+                      out, out_labels, out_dims, variant, stream);
+}
+
+w3d_status warp3d_affine_batched_i16_ex(int32_t batch, const int16_t* in, const uint8_t* in_labels,
+                                        w3d_dims in_dims, const w3d_volume_params* params,
+                                        w3d_interp interp, float fill, uint8_t label_fill,
+                                        float* out, uint8_t* out_labels, w3d_dims out_dims,
+                                        w3d_kernel variant, void* stream) {
+  return batched_impl(batch, nullptr, in, in_labels, in_dims, params, interp, fill, label_fill,
+                      out, out_labels, out_dims, variant, stream);
+}
+
+w3d_status warp3d_affine_batched_i16(int32_t batch, const int16_t* in, const uint8_t* in_labels,
+                                     w3d_dims in_dims, const w3d_volume_params* params,
+                                     w3d_interp interp, float fill, uint8_t label_fill, float* out,
+                                     uint8_t* out_labels, w3d_dims out_dims, void* stream) {
+  return batched_impl(batch, nullptr, in, in_labels, in_dims, params, interp, fill, label_fill,
+                      out, out_labels, out_dims, W3D_KERNEL_AUTO, stream);
 }
 
 w3d_status warp3d_affine_batched(int32_t batch, const float* in, const uint8_t* in_labels,

@@ -59,7 +59,8 @@ struct alignas(64) WarpArgs {
   // per volume i: tm[2i] 3D (nx, ny, nz) float32 box (box_w, box_h, box_d),
   //               tm[2i+1] 3D uint8 box (box_wl, box_h, box_d)
   CUtensorMap tm[2 * kTmaVolPerLaunch];
-  const float* in;
+  const float* in;        // float32 image input, or null with in16
+  const int16_t* in16;    // int16 HU image input (NEXT-4), or null
   const uint8_t* in_lbl;  // may be null
   float* out;
   uint8_t* out_lbl;       // null iff in_lbl null
@@ -69,6 +70,7 @@ struct alignas(64) WarpArgs {
   int64_t out_stride;     // voxels per output volume
   float fill;
   uint32_t label_fill;
+  uint32_t fill16_pair;   // int16 input: (int16)fill in both halves (staged boxes)
   int32_t interp;         // W3D_INTERP_*
   int32_t nvol;           // volumes in this launch
   int32_t use_tma;        // tensor maps valid for the volumes with box_w > 0
@@ -86,7 +88,7 @@ static_assert(sizeof(WarpArgs) <= 32764, "kernel parameter space");
 bool cube_supported(const WarpArgs& a);
 bool cube_tma_supported(const WarpArgs& a);
 // TMA box dims for one volume's tiles (0 when the box exceeds the buffer)
-void cube_tma_box(const float A[12], VolDev& P, bool labels);
+void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes);
 cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s);
 cudaError_t read_cube_stats(unsigned long long out[2]);
 // warp3d_resample.cu (NEXT-3): one separable Gaussian pass along `axis` (0 x, 1 y, 2 z)

@@ -496,3 +496,37 @@ def test_resample_constant_and_identity(W):
     g, gl = W.warp3d_resample(torch.from_numpy(img).cuda(), torch.from_numpy(lbl).cuda(),
                               (3.0, 3.0, 3.0), 3.0)
     assert np.array_equal(g.cpu().numpy(), img) and np.array_equal(gl.cpu().numpy(), lbl)
+
+
+# ----------------------------------------------------------------------------- NEXT-4 int16 input
+@pytest.mark.parametrize("shape,rname,fill", [
+    ((160, 128, 128), "train", -1000.0),   # C2 geometry, staged (TMA / cp.async)
+    ((48, 40, 64), "large", -1024.0),      # large rotations: parts and gathers
+    ((23, 29, 37), "train", -1000.0),      # nx % 8 != 0: gather path
+    ((40, 36, 48), "train", -1000.5),      # non-integral fill: gather path
+])
+def test_int16_input_equals_float_input_bitwise(W, shape, rname, fill):
+    """int16 HU input converts exactly, so the warp equals the float32 warp of the same
+    values bit for bit; and both match the oracle (labels exact)."""
+    ranges = synth.TRAIN if rname == "train" else synth.LARGE
+    B = 3
+    imgs, lbls, ds, As = [], [], [], []
+    for i in range(B):
+        im, lb = synth.phantom(shape, seed=300 + i)
+        imgs.append(np.round(im).astype(np.int16))
+        lbls.append(lb)
+        ds.append(synth.draw(ranges, 500 + i))
+        As.append(_oracle_affine(ds[i], shape, shape))
+    i16 = np.stack(imgs)
+    f32 = i16.astype(np.float32)
+    lb = np.stack(lbls)
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B)]
+    for variant in (0, 1):
+        o16, l16 = W.warp3d_affine_batched(torch.from_numpy(i16).cuda(), torch.from_numpy(lb).cuda(),
+                                           params, fill=fill, label_fill=2, variant=variant)
+        o32, l32 = W.warp3d_affine_batched(torch.from_numpy(f32).cuda(), torch.from_numpy(lb).cuda(),
+                                           params, fill=fill, label_fill=2, variant=variant)
+        assert torch.equal(o16, o32) and torch.equal(l16, l32), variant
+    r_img, r_lbl = O.warp_volume(f32[1], lb[1], As[1], None, 0, fill, 2, _oph(ds[1], FULL, 1))
+    assert_image_close(o16[1].cpu().numpy(), r_img, ds[1].window, ds[1].gamma, True, "int16")
+    assert np.array_equal(l16[1].cpu().numpy(), r_lbl)
