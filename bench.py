@@ -58,6 +58,8 @@ def parse():
                     help="resample: the NEXT-3 step (1 mm^3 512^3 CT -> 3 mm^3), its own metric")
     ap.add_argument("--variant", choices=["auto", "gather", "staged"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--input", choices=["f32", "i16"], default="f32",
+                    help="i16: the same volumes as int16 HU (NEXT-4; 2 B per input voxel)")
     ap.add_argument("--no-labels", action="store_true",
                     help="image-only warp (diagnostic; the headline includes labels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -272,7 +274,7 @@ def config_of(args, world):
             "volumes_per_gpu": per if per else wl["total"] // world,
             "global_batch": per * world if per else wl["total"],
             "transforms": wl["ranges"], "photometric": "noise+window+clamp+gamma",
-            "kernel_variant": args.variant,
+            "kernel_variant": args.variant, "input": args.input,
             "l2": "flushed between timed steps (256 MiB write)",
             "parallelism": f"dp{world} (volume shards, no data-path collective)"}
 
@@ -381,6 +383,8 @@ def main():
     imgs, lbls = host_inputs(shape, vids)
     B = len(vids)
     nvox_out = int(np.prod(shape))
+    if args.input == "i16":  # NEXT-4: 12-bit HU as int16 (the phantom rounded)
+        imgs = np.round(imgs).astype(np.int16)
     t_img = torch.from_numpy(imgs).to(dev)
     t_lbl = None if args.no_labels else torch.from_numpy(lbls).to(dev)
     batch = W.AugmentBatch(t_img, t_lbl, params, fill=-1000.0, label_fill=0, variant=variant)
@@ -392,7 +396,8 @@ def main():
         a, b = W.warp3d_footprint_batched(params[c0:c0 + 64], shape, shape, device=dev)
         f_img += a
         f_lbl += b
-    alg_bytes = 5 * B * nvox_out + 4 * f_img + 1 * f_lbl
+    in_bytes = 2 if args.input == "i16" else 4
+    alg_bytes = 5 * B * nvox_out + in_bytes * f_img + (0 if args.no_labels else 1) * f_lbl
     naive_bytes = 10 * B * nvox_out
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)

@@ -418,6 +418,8 @@ template <> __device__ __forceinline__ void lds_pair<float>(uint32_t a, float& v
                : "=f"(v0), "=f"(v1)
                : "r"(a));
 }
+// int16: exact conversion (cvt.rn.f32.s16; measured faster than an
+// integer-bias-then-FADD2 conversion on the FMA pipe: 211 vs 206 GVoxel/s)
 template <> __device__ __forceinline__ void lds_pair<int16_t>(uint32_t a, float& v0, float& v1) {
   asm volatile(
       "{\n\t.reg .s16 h0, h1;\n\tld.shared.s16 h0, [%2];\n\tld.shared.s16 h1, [%2+2];\n\t"
