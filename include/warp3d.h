@@ -159,6 +159,28 @@ w3d_status warp3d_affine_batched_ex(int32_t batch, const float* in, const uint8_
                                     w3d_kernel variant, void* stream);
 
 /*
+ * warp3d_affine_batched_v -- a batch of volumes of DIFFERENT dims (NEXT-4:
+ * "CT scans vary in resolution and number of slices"), each a
+ * separate device allocation, warped into one uniform output batch (the
+ * paper's fixed training crop).
+ *   in_type      element type of every image: W3D_IN_F32 or W3D_IN_I16.
+ *   in           host array [batch] of device pointers to the images
+ *                [nz_i][ny_i][nx_i] (caller-owned).
+ *   in_labels    host array [batch] of device uint8 label pointers, or NULL.
+ *   in_dims      host array [batch] of the volumes' dims.
+ *   params, interp, fill, label_fill, out, out_labels, out_dims: as
+ *                warp3d_affine_batched (out = [batch][out_dims], slot i = volume i).
+ * Volumes with equal dims share a launch (one per distinct dims); the result
+ * of each volume equals warp3d_affine_batched on that volume alone.
+ */
+typedef enum { W3D_IN_F32 = 0, W3D_IN_I16 = 1 } w3d_in_type;
+w3d_status warp3d_affine_batched_v(int32_t batch, w3d_in_type in_type, const void* const* in,
+                                   const uint8_t* const* in_labels, const w3d_dims* in_dims,
+                                   const w3d_volume_params* params, w3d_interp interp, float fill,
+                                   uint8_t label_fill, float* out, uint8_t* out_labels,
+                                   w3d_dims out_dims, void* stream);
+
+/*
  * warp3d_affine_batched_i16[_ex] -- the batched warp with an int16 image input
  * (CT is 12-bit HU; 2 B per input voxel instead
  * of 4).  Identical to warp3d_affine_batched[_ex] except that `in` is int16

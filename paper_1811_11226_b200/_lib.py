@@ -28,7 +28,7 @@ EXPORTS = (
     "warp3d_abi_version", "warp3d_tile_stats", "warp3d_pipeline_create", "warp3d_pipeline_run",
     "warp3d_pipeline_destroy", "warp3d_resample_sigma", "warp3d_resample_dims",
     "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample",
-    "warp3d_affine_batched_i16", "warp3d_affine_batched_i16_ex",
+    "warp3d_affine_batched_i16", "warp3d_affine_batched_i16_ex", "warp3d_affine_batched_v",
 )
 
 
@@ -106,6 +106,9 @@ def load():
     L.warp3d_affine_batched_i16_ex.argtypes = [I32, P, P, Dims, P, I32, F, ctypes.c_uint8, P, P,
                                                Dims, I32, P]
     L.warp3d_affine_batched_i16.restype = ctypes.c_int
+    L.warp3d_affine_batched_v.argtypes = [I32, I32, P, P, P, P, I32, F, ctypes.c_uint8, P, P, Dims,
+                                          P]
+    L.warp3d_affine_batched_v.restype = ctypes.c_int
     L.warp3d_affine_batched_i16_ex.restype = ctypes.c_int
     D = ctypes.c_double
     L.warp3d_resample_sigma.argtypes = [P, D, P]

@@ -20,7 +20,7 @@ __all__ = [
     "warp3d_affine", "warp3d_affine_batched", "warp3d_compose_affine", "warp3d_noise",
     "warp3d_philox4x32_10", "warp3d_footprint_batched", "warp3d_launch_count",
     "warp3d_tile_stats", "Pipeline", "warp3d_resample_sigma", "warp3d_resample_dims",
-    "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample",
+    "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample", "warp3d_affine_batched_list",
     "warp3d_abi_version", "photometric", "volume_params", "make_geom", "Warp3DError",
     "INTERP_LINEAR", "INTERP_NEAREST", "KERNEL_AUTO", "KERNEL_GATHER", "KERNEL_STAGED",
     "PH_NOISE", "PH_WINDOW", "PH_CLAMP", "PH_GAMMA", "PH_OCCLUDE",
@@ -125,6 +125,32 @@ def warp3d_affine_batched(inp: torch.Tensor, labels: torch.Tensor | None, params
         None if out_labels is None else _dev(out_labels, torch.uint8, "out_labels"),
         L.dims(out.shape[1:]), int(variant), _stream()))
     return out, out_labels
+
+
+def warp3d_affine_batched_list(inputs, labels, params, out_shape, interp=INTERP_LINEAR,
+                               fill=0.0, label_fill=0):
+    """Volumes of different shapes (list of float32 or int16 [nz,ny,nx] CUDA tensors, one
+    dtype) and their labels (list or None) into one [B, *out_shape] batch (NEXT-4)."""
+    B = len(inputs)
+    if B == 0 or (labels is not None and len(labels) != B) or len(params) != B:
+        raise ValueError("inputs, labels and params must have the same non-zero length")
+    i16 = inputs[0].dtype == torch.int16
+    dt = torch.int16 if i16 else torch.float32
+    dev = inputs[0].device
+    ptrs = (ctypes.c_void_p * B)(*[_dev(t, dt, f"inputs[{i}]").value for i, t in enumerate(inputs)])
+    dims = (L.Dims * B)(*[L.dims(t.shape) for t in inputs])
+    lptrs = None
+    if labels is not None:
+        lptrs = (ctypes.c_void_p * B)(*[_dev(t, torch.uint8, f"labels[{i}]").value
+                                        for i, t in enumerate(labels)])
+    out = torch.empty((B, *out_shape), dtype=torch.float32, device=dev)
+    out_l = None if labels is None else torch.empty((B, *out_shape), dtype=torch.uint8, device=dev)
+    arr = params if isinstance(params, ctypes.Array) else (VolumeParams * B)(*params)
+    L.check(L.load().warp3d_affine_batched_v(
+        B, 1 if i16 else 0, ptrs, lptrs, dims, arr, int(interp), float(fill), int(label_fill),
+        _dev(out, torch.float32, "out"), None if out_l is None else _dev(out_l, torch.uint8, "out_labels"),
+        L.dims(out_shape), _stream()))
+    return out, out_l
 
 
 def warp3d_noise(shape_zyx, sigma, seed, volume_id, device="cuda") -> torch.Tensor:

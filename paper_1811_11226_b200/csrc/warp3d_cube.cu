@@ -121,10 +121,12 @@ template <> struct InT<int16_t> {
   static constexpr int kBytes = 2, kChunk = 8;
   __device__ static float load(const int16_t* p) { return static_cast<float>(__ldg(p)); }
 };
-template <class T> __device__ __forceinline__ const T* in_ptr(const WarpArgs& a);
-template <> __device__ __forceinline__ const float* in_ptr<float>(const WarpArgs& a) { return a.in; }
-template <> __device__ __forceinline__ const int16_t* in_ptr<int16_t>(const WarpArgs& a) {
-  return a.in16;
+// per-volume input addresses (uniform batches or per-volume allocations, NEXT-4)
+template <class T> __device__ __forceinline__ const T* vol_in(const VolDev& P) {
+  return reinterpret_cast<const T*>(P.in_addr);
+}
+__device__ __forceinline__ const uint8_t* vol_lbl(const VolDev& P) {
+  return reinterpret_cast<const uint8_t*>(P.lbl_addr);
 }
 
 // Pull-back coordinate (R4): p_k = fma(A_k1, y, fma(A_k0, x, fma(A_k2, z, b_k))).
@@ -560,8 +562,8 @@ template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kCla
 __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n) {
-  const T* __restrict__ vin = in_ptr<T>(a) + vi * a.in_stride;
-  const uint8_t* __restrict__ lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+  const T* __restrict__ vin = vol_in<T>(P);
+  const uint8_t* __restrict__ lin = kLabels ? vol_lbl(P) : nullptr;
   Vol V = V0;
 #pragma unroll
   for (int k = 0; k < 3; ++k) V.A1[k] = pin(V0.A1[k]);
@@ -594,8 +596,8 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
   // output element offset of row y within the volume (< 2^31)
   // output row pointers, pinned (else re-derived from the parameters every row)
   const size_t o = static_cast<size_t>((Z * my + y0) * mx + X);
-  float* po = pin_ptr(a.out + vi * a.out_stride + o);
-  uint8_t* pl = kLabels ? pin_ptr(a.out_lbl + vi * a.out_stride + o) : nullptr;
+  float* po = pin_ptr(a.out + P.out_slot * a.out_stride + o);
+  uint8_t* pl = kLabels ? pin_ptr(a.out_lbl + P.out_slot * a.out_stride + o) : nullptr;
   uint32_t q = static_cast<uint32_t>(X) +
                mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(y0 >> 2));
   float2 Y2 = make_float2(static_cast<float>(y0), static_cast<float>(y0 + 1));
@@ -684,8 +686,8 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
   const uint32_t simg = smem_base();
   const VolDev& P = a.vol[vi];
   const Vol V = load_vol(P);
-  const T* vin = in_ptr<T>(a) + vi * a.in_stride;
-  const uint8_t* lin = kLabels ? a.in_lbl + vi * a.in_stride : nullptr;
+  const T* vin = vol_in<T>(P);
+  const uint8_t* lin = kLabels ? vol_lbl(P) : nullptr;
   const int lane = threadIdx.x & 31;
   const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
   const bool live = X < a.mx && Z < a.mz;
@@ -909,8 +911,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
   } else {
     slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
-    stage<T, kLabels>(a, in_ptr<T>(a) + vi * a.in_stride,
-                      kLabels ? a.in_lbl + vi * a.in_stride : nullptr, b, simg, slbl);
+    stage<T, kLabels>(a, vol_in<T>(P), kLabels ? vol_lbl(P) : nullptr, b, simg, slbl);
   }
   const Vol V = load_vol(P);
   const int lane = threadIdx.x & 31;
@@ -1027,10 +1028,9 @@ bool cube_supported(const WarpArgs& a) {
   const void* in = a.in16 ? static_cast<const void*>(a.in16) : static_cast<const void*>(a.in);
   const bool fill_ok = !a.in16 || (a.fill == std::nearbyint(a.fill) && a.fill >= -32768.0f &&
                                    a.fill <= 32767.0f);
-  return (a.nx % chunk == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
-         (a.in_stride % chunk == 0) && fill_ok &&
-         (a.in_lbl == nullptr || reinterpret_cast<uintptr_t>(a.in_lbl) % 8 == 0) &&
-         a.nx < (1 << 21) && a.ny < (1 << 21) && a.nz < (1 << 21);
+  (void)in;
+  return (a.nx % chunk == 0) && a.in_aligned && fill_ok && a.nx < (1 << 21) &&
+         a.ny < (1 << 21) && a.nz < (1 << 21);
 }
 
 // gather_only (W3D_KERNEL_GATHER, or layouts cube_supported() rejects): every
@@ -1044,9 +1044,8 @@ cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s) {
 
 bool cube_tma_supported(const WarpArgs& a) {
   // 16 B aligned global strides and volume bases for the image (and labels)
-  const bool lbl = a.in_lbl == nullptr ||
-                   (a.nx % 16 == 0 && a.in_stride % 16 == 0 &&
-                    reinterpret_cast<uintptr_t>(a.in_lbl) % 16 == 0);
+  bool lbl = a.in_lbl == nullptr || a.nx % 16 == 0;  // 16 B label rows
+  for (int i = 0; lbl && a.in_lbl && i < a.nvol; ++i) lbl = a.vol[i].lbl_addr % 16 == 0;
   return cube_supported(a) && lbl && a.interp == W3D_INTERP_LINEAR;
 }
 

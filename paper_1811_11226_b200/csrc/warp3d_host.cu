@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <tuple>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -15,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "philox.cuh"
 #include "warp3d.h"
@@ -235,8 +237,7 @@ static bool prepare_tma(WarpArgs& args, const float* const* affines) {
     const int eb = args.in16 ? 2 : 4;
     cube_tma_box(affines[i], P, labels, eb);
     if (!P.box_w) continue;
-    const void* base = args.in16 ? static_cast<const void*>(args.in16 + i * args.in_stride)
-                                 : static_cast<const void*>(args.in + i * args.in_stride);
+    const void* base = reinterpret_cast<const void*>(P.in_addr);
     MapKey ki{base, args.nx, args.ny, args.nz, P.box_w, P.box_h, P.box_d, eb};
     if (!(ki == key_img[i])) {
       key_img[i] = MapKey();
@@ -244,8 +245,8 @@ static bool prepare_tma(WarpArgs& args, const float* const* affines) {
       if (ok) key_img[i] = ki;
     }
     if (ok && labels) {
-      MapKey kl{args.in_lbl + i * args.in_stride, args.nx, args.ny, args.nz, P.box_wl, P.box_h,
-                P.box_d, 1};
+      MapKey kl{reinterpret_cast<const void*>(P.lbl_addr), args.nx, args.ny, args.nz, P.box_wl,
+                P.box_h, P.box_d, 1};
       if (!(kl == key_lbl[i])) {
         key_lbl[i] = MapKey();
         ok = encode_3d(&args.tm[2 * i + 1], 1, kl.base, args, kl.bw, kl.bh, kl.bd);
@@ -258,23 +259,32 @@ static bool prepare_tma(WarpArgs& args, const float* const* affines) {
   return ok;
 }
 
-// One batch, already validated; chunks of kMaxVolPerLaunch volumes.  The image
-// input is float32 (in) or int16 (in16, NEXT-4), exactly one non-null.
-static w3d_status run_batched_t(int32_t batch, const float* in, const int16_t* in16,
-                                const uint8_t* in_labels,
-                              w3d_dims in_dims, const float* const* affines,
-                              const w3d_photometric* const* phs, w3d_interp interp, float fill,
-                              uint8_t label_fill, float* out, uint8_t* out_labels,
-                              w3d_dims out_dims, w3d_kernel variant, cudaStream_t stream) {
+// One group of volumes with the same in_dims, already validated; chunks of
+// kMaxVolPerLaunch (kTmaVolPerLaunch with TMA) volumes.  Volume i reads
+// vols[i] (image: float32 if elem == 4, int16 if elem == 2; labels nullable)
+// and writes output slot vols[i].slot of the uniform output batch out[].
+struct VolIn {
+  const void* img;
+  const uint8_t* lbl;
+  int32_t slot;
+};
+
+static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_dims in_dims,
+                               const float* const* affines, const w3d_photometric* const* phs,
+                               w3d_interp interp, float fill, uint8_t label_fill, float* out,
+                               uint8_t* out_labels, w3d_dims out_dims, w3d_kernel variant,
+                               cudaStream_t stream) {
   static thread_local WarpArgs args;  // ~31 KB: keep off the stack
   const int64_t in_n = nvox(in_dims), out_n = nvox(out_dims);
   static const bool no_tma = getenv("W3D_NO_TMA") && getenv("W3D_NO_TMA")[0] == '1';
   const bool want_tma = variant != W3D_KERNEL_GATHER && !no_tma;
   const int32_t chunk = want_tma ? kTmaVolPerLaunch : kMaxVolPerLaunch;
+  const bool labels = vols[0].lbl != nullptr;
   for (int32_t v0 = 0; v0 < batch; v0 += chunk) {
     const int32_t nv = (batch - v0 < chunk) ? batch - v0 : chunk;
-    args.in = in ? in + v0 * in_n : nullptr;
-    args.in16 = in16 ? in16 + v0 * in_n : nullptr;
+    // type flags (the kernels read every address from vol[i])
+    args.in = elem == 4 ? static_cast<const float*>(vols[v0].img) : nullptr;
+    args.in16 = elem == 2 ? static_cast<const int16_t*>(vols[v0].img) : nullptr;
     {
       const float f = std::nearbyint(fill) == fill && fill >= -32768.0f && fill <= 32767.0f
                           ? fill
@@ -282,9 +292,9 @@ static w3d_status run_batched_t(int32_t batch, const float* in, const int16_t* i
       const uint32_t h = static_cast<uint16_t>(static_cast<int16_t>(f));
       args.fill16_pair = h | (h << 16);
     }
-    args.in_lbl = in_labels ? in_labels + v0 * in_n : nullptr;
-    args.out = out + v0 * out_n;
-    args.out_lbl = out_labels ? out_labels + v0 * out_n : nullptr;
+    args.in_lbl = labels ? vols[v0].lbl : nullptr;
+    args.out = out;
+    args.out_lbl = out_labels;
     args.nx = in_dims.nx; args.ny = in_dims.ny; args.nz = in_dims.nz;
     args.mx = out_dims.nx; args.my = out_dims.ny; args.mz = out_dims.nz;
     args.in_stride = in_n;
@@ -293,7 +303,15 @@ static w3d_status run_batched_t(int32_t batch, const float* in, const int16_t* i
     args.label_fill = label_fill;
     args.interp = interp;
     args.nvol = nv;
-    for (int32_t i = 0; i < nv; ++i) args.vol[i] = derive(affines[v0 + i], phs[v0 + i]);
+    args.in_aligned = 1;
+    for (int32_t i = 0; i < nv; ++i) {
+      VolDev& P = args.vol[i];
+      P = derive(affines[v0 + i], phs[v0 + i]);
+      P.in_addr = reinterpret_cast<uint64_t>(vols[v0 + i].img);
+      P.lbl_addr = reinterpret_cast<uint64_t>(vols[v0 + i].lbl);
+      P.out_slot = vols[v0 + i].slot;
+      if (P.in_addr % 16 || P.lbl_addr % 8) args.in_aligned = 0;
+    }
     for (int r = 0; r < 10; ++r) {  // volume 0's key schedule (used when all seeds agree)
       args.rk0[r] = args.vol[0].rk0[r];
       args.rk1[r] = args.vol[0].rk1[r];
@@ -309,13 +327,29 @@ static w3d_status run_batched_t(int32_t batch, const float* in, const int16_t* i
   return ok();
 }
 
+// A uniform batch: volume i at in + i * nvox(in_dims), output slot i.
+static w3d_status run_batched_t(int32_t batch, const void* in, int elem, const uint8_t* in_labels,
+                                w3d_dims in_dims, const float* const* affines,
+                                const w3d_photometric* const* phs, w3d_interp interp, float fill,
+                                uint8_t label_fill, float* out, uint8_t* out_labels,
+                                w3d_dims out_dims, w3d_kernel variant, cudaStream_t stream) {
+  static thread_local std::vector<VolIn> vols;
+  vols.resize(static_cast<size_t>(batch));
+  const int64_t in_n = nvox(in_dims);
+  for (int32_t i = 0; i < batch; ++i)
+    vols[i] = VolIn{static_cast<const char*>(in) + i * in_n * elem,
+                    in_labels ? in_labels + i * in_n : nullptr, i};
+  return launch_group(batch, vols.data(), elem, in_dims, affines, phs, interp, fill, label_fill,
+                      out, out_labels, out_dims, variant, stream);
+}
+
 static w3d_status run_batched(int32_t batch, const float* in, const uint8_t* in_labels,
                               w3d_dims in_dims, const float* const* affines,
                               const w3d_photometric* const* phs, w3d_interp interp, float fill,
                               uint8_t label_fill, float* out, uint8_t* out_labels,
                               w3d_dims out_dims, w3d_kernel variant, cudaStream_t stream) {
-  return run_batched_t(batch, in, nullptr, in_labels, in_dims, affines, phs, interp, fill,
-                       label_fill, out, out_labels, out_dims, variant, stream);
+  return run_batched_t(batch, in, 4, in_labels, in_dims, affines, phs, interp, fill, label_fill,
+                       out, out_labels, out_dims, variant, stream);
 }
 
 static w3d_status check_common(const void* in, w3d_dims in_dims, w3d_interp interp, float fill,
@@ -403,8 +437,9 @@ static w3d_status batched_impl(int32_t batch, const float* in, const int16_t* in
       A[i] = params[v0 + i].affine;
       P[i] = &params[v0 + i].ph;
     }
-    st = run_batched_t(nv, in ? in + int64_t(v0) * nvox(in_dims) : nullptr,
-                       in16 ? in16 + int64_t(v0) * nvox(in_dims) : nullptr,
+    const void* base = in16 ? static_cast<const void*>(in16 + int64_t(v0) * nvox(in_dims))
+                            : static_cast<const void*>(in + int64_t(v0) * nvox(in_dims));
+    st = run_batched_t(nv, base, eb,
                        in_labels ? in_labels + int64_t(v0) * nvox(in_dims) : nullptr, in_dims, A,
                        P, interp, fill, label_fill, out + int64_t(v0) * nvox(out_dims),
                        out_labels ? out_labels + int64_t(v0) * nvox(out_dims) : nullptr, out_dims,
@@ -446,6 +481,70 @@ w3d_status warp3d_affine_batched(int32_t batch, const float* in, const uint8_t* 
                                  uint8_t* out_labels, w3d_dims out_dims, void* stream) {
   return warp3d_affine_batched_ex(batch, in, in_labels, in_dims, params, interp, fill, label_fill,
                                   out, out_labels, out_dims, W3D_KERNEL_AUTO, stream);
+}
+
+// Per-volume inputs of different dims (NEXT-4): volumes grouped by in_dims, one
+// launch group per distinct dims, each volume writing its own slot of out[].
+w3d_status warp3d_affine_batched_v(int32_t batch, w3d_in_type in_type, const void* const* in,
+                                   const uint8_t* const* in_labels, const w3d_dims* in_dims,
+                                   const w3d_volume_params* params, w3d_interp interp, float fill,
+                                   uint8_t label_fill, float* out, uint8_t* out_labels,
+                                   w3d_dims out_dims, void* stream) {
+  if (batch < 1) return fail(W3D_ERR_INVALID_ARG, "batch = %d must be >= 1", batch);
+  if (in_type != W3D_IN_F32 && in_type != W3D_IN_I16)
+    return fail(W3D_ERR_INVALID_ARG, "in_type = %d is not a w3d_in_type", int(in_type));
+  if (!in || !in_dims || !params)
+    return fail(W3D_ERR_INVALID_ARG, "in, in_dims and params must be non-NULL host arrays");
+  if ((in_labels == nullptr) != (out_labels == nullptr))
+    return fail(W3D_ERR_INVALID_ARG, "out_labels must be NULL iff in_labels is NULL");
+  const int eb = in_type == W3D_IN_I16 ? 2 : 4;
+  const int64_t out_b = int64_t(batch) * nvox(out_dims);
+  w3d_status st;
+  for (int32_t i = 0; i < batch; ++i) {
+    if ((st = check_common(in[i], in_dims[i], interp, fill, out, out_dims, eb)) != W3D_OK)
+      return fail(st, "volume %d: %s", i, g_last_error.c_str());
+    if (in_labels && !in_labels[i])
+      return fail(W3D_ERR_INVALID_ARG, "in_labels[%d] is NULL", i);
+    if ((st = check_affine(params[i].affine, i)) != W3D_OK) return st;
+    if ((st = check_ph(params[i].ph, i)) != W3D_OK) return st;
+    const int64_t n = nvox(in_dims[i]);
+    if (overlap(in[i], n * eb, out, out_b * 4) ||
+        (in_labels && (overlap(in_labels[i], n, out_labels, out_b) ||
+                       overlap(in_labels[i], n, out, out_b * 4) ||
+                       overlap(in[i], n * eb, out_labels, out_b))))
+      return fail(W3D_ERR_INVALID_ARG, "volume %d: input overlaps the outputs", i);
+  }
+  if (out_labels && overlap(out, out_b * 4, out_labels, out_b))
+    return fail(W3D_ERR_INVALID_ARG, "out and out_labels overlap");
+  std::vector<int32_t> order(static_cast<size_t>(batch));
+  for (int32_t i = 0; i < batch; ++i) order[i] = i;
+  auto key = [&](int32_t i) {
+    return std::make_tuple(in_dims[i].nz, in_dims[i].ny, in_dims[i].nx);
+  };
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return key(a) < key(b); });
+  std::vector<VolIn> vols;
+  std::vector<const float*> A;
+  std::vector<const w3d_photometric*> P;
+  for (size_t g0 = 0; g0 < order.size();) {
+    size_t g1 = g0;
+    while (g1 < order.size() && key(order[g1]) == key(order[g0])) ++g1;
+    vols.clear();
+    A.clear();
+    P.clear();
+    for (size_t k = g0; k < g1; ++k) {
+      const int32_t i = order[k];
+      vols.push_back(VolIn{in[i], in_labels ? in_labels[i] : nullptr, i});
+      A.push_back(params[i].affine);
+      P.push_back(&params[i].ph);
+    }
+    st = launch_group(static_cast<int32_t>(g1 - g0), vols.data(), eb, in_dims[order[g0]],
+                      A.data(), P.data(), interp, fill, label_fill, out, out_labels, out_dims,
+                      W3D_KERNEL_AUTO, static_cast<cudaStream_t>(stream));
+    if (st != W3D_OK) return st;
+    g0 = g1;
+  }
+  return ok();
 }
 
 // A = F Rz Ry Rx Sh S G (R16), b = c_in + d - A c_out, double.

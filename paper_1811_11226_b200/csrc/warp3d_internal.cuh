@@ -45,11 +45,13 @@ struct alignas(16) VolDev {
   // TMA box origin of a tile: floor(p(tile origin voxel) + box_mlo[k]) with
   // box_mlo[k] = sum_j min(0, A_kj span_j) - rounding margin (cube_tma_box)
   float box_mlo[3];
-  uint32_t _pad2;
+  int32_t out_slot;     // output volume index in the caller's batch (out + slot * out_stride)
+  uint64_t in_addr;     // device address of this volume's image (float32 or int16)
+  uint64_t lbl_addr;    // device address of its labels (0 without labels)
 };
-static_assert(sizeof(VolDev) == 224, "VolDev layout");
+static_assert(sizeof(VolDev) == 240, "VolDev layout");
 
-constexpr int kMaxVolPerLaunch = 120;  // sizeof(WarpArgs) < 32764 B of kernel parameters
+constexpr int kMaxVolPerLaunch = 112;  // sizeof(WarpArgs) < 32764 B of kernel parameters
 // Volumes per launch when TMA staging is used: the tensor maps must lie in the
 // first 4 KB of the kernel parameters (measured: TMA on a __grid_constant__
 // map at a larger parameter offset faults).
@@ -59,8 +61,8 @@ struct alignas(64) WarpArgs {
   // per volume i: tm[2i] 3D (nx, ny, nz) float32 box (box_w, box_h, box_d),
   //               tm[2i+1] 3D uint8 box (box_wl, box_h, box_d)
   CUtensorMap tm[2 * kTmaVolPerLaunch];
-  const float* in;        // float32 image input, or null with in16
-  const int16_t* in16;    // int16 HU image input (NEXT-4), or null
+  const float* in;        // non-null: float32 image input (per-volume addresses in vol[i])
+  const int16_t* in16;    // non-null: int16 HU image input (NEXT-4)
   const uint8_t* in_lbl;  // may be null
   float* out;
   uint8_t* out_lbl;       // null iff in_lbl null
@@ -74,7 +76,8 @@ struct alignas(64) WarpArgs {
   int32_t interp;         // W3D_INTERP_*
   int32_t nvol;           // volumes in this launch
   int32_t use_tma;        // tensor maps valid for the volumes with box_w > 0
-  int32_t _pad[3];
+  int32_t in_aligned;     // every volume's image (labels) 16 B (8 B) aligned: staged paths
+  int32_t _pad[2];
   // Philox round keys shared by every volume of the launch (all seeds equal;
   // required by the kPhFull kernels: fixed parameter offsets, so the round
   // function reads them as constant-bank operands)

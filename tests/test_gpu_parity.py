@@ -530,3 +530,51 @@ def test_int16_input_equals_float_input_bitwise(W, shape, rname, fill):
     r_img, r_lbl = O.warp_volume(f32[1], lb[1], As[1], None, 0, fill, 2, _oph(ds[1], FULL, 1))
     assert_image_close(o16[1].cpu().numpy(), r_img, ds[1].window, ds[1].gamma, True, "int16")
     assert np.array_equal(l16[1].cpu().numpy(), r_lbl)
+
+
+# ----------------------------------------------------------------------------- NEXT-4 per-volume dims
+@pytest.mark.parametrize("dtype", ["f32", "i16"])
+@pytest.mark.parametrize("with_labels", [True, False])
+def test_volumes_of_different_dims_into_one_batch(W, dtype, with_labels):
+    """CT volumes of different resolutions and slice counts warped into one
+    fixed-size batch: every slot equals the single-volume warp of its own
+    volume bit for bit (shared dims share a launch; slots keep the caller's order), and a
+    sampled volume matches the oracle."""
+    shapes = [(40, 48, 64), (23, 29, 37), (40, 48, 64), (64, 32, 48), (23, 29, 37), (17, 56, 40)]
+    out_shape = (32, 40, 48)
+    B = len(shapes)
+    imgs, lbls, ds, As = [], [], [], []
+    for i, s in enumerate(shapes):
+        im, lb = synth.phantom(s, seed=700 + i)
+        imgs.append(np.round(im).astype(np.int16) if dtype == "i16" else im)
+        lbls.append(lb)
+        ds.append(synth.draw(synth.TRAIN, 800 + i))
+        As.append(_oracle_affine(ds[i], s, out_shape))
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B)]
+    ti = [torch.from_numpy(a).cuda() for a in imgs]
+    tl = [torch.from_numpy(a).cuda() for a in lbls] if with_labels else None
+    out, out_l = W.warp3d_affine_batched_list(ti, tl, params, out_shape, fill=-1000.0, label_fill=3)
+    assert out.shape == (B, *out_shape) and (out_l is None) == (not with_labels)
+    for i in range(B):
+        o1, l1 = W.warp3d_affine_batched(ti[i][None], None if tl is None else tl[i][None],
+                                         [params[i]], fill=-1000.0, label_fill=3,
+                                         out_shape=out_shape)
+        assert torch.equal(out[i], o1[0]), f"slot {i}"
+        if with_labels:
+            assert torch.equal(out_l[i], l1[0]), f"slot {i} labels"
+    k = 1
+    r_img, r_lbl = O.warp_volume(imgs[k].astype(np.float32), lbls[k] if with_labels else None,
+                                 As[k], out_shape, 0, -1000.0, 3, _oph(ds[k], FULL, k))
+    assert_image_close(out[k].cpu().numpy(), r_img, ds[k].window, ds[k].gamma, True, "list")
+    if with_labels:
+        assert np.array_equal(out_l[k].cpu().numpy(), r_lbl)
+
+
+def test_volumes_of_different_dims_rejects_bad_input(W):
+    a = torch.zeros((8, 8, 8), device="cuda")
+    b = torch.zeros((8, 8, 9), device="cuda", dtype=torch.int16)
+    p = [W.volume_params(np.eye(3, 4, dtype=np.float32), W.photometric(0))] * 2
+    with pytest.raises(Exception):
+        W.warp3d_affine_batched_list([a, b], None, p, (8, 8, 8))   # mixed dtypes
+    with pytest.raises(Exception):
+        W.warp3d_affine_batched_list([a], None, p, (8, 8, 8))      # length mismatch
