@@ -465,7 +465,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
-            "tiles": {"staged": st0[0] - tiles_before[0], "gather": st0[1] - tiles_before[1]},
+            "tiles": {"staged": st0[0] - tiles_before[0], "gather": st0[1] - tiles_before[1],
+                      "tma": st0[2] - tiles_before[2], "parts": st0[3] - tiles_before[3]},
             "clocks": clk.summary(),
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms),
                         "max": max(step_ms)},

@@ -315,9 +315,10 @@ uint64_t warp3d_launch_count(void);
 
 /* Diagnostics: out[0] = output tiles computed from a staged shared-memory box,
  * out[1] = tiles computed by gathers (variant GATHER, unaligned inputs, or a
- * footprint larger than the staging buffer), cumulative in this process.
- * Synchronises the device (not for the hot path). */
-w3d_status warp3d_tile_stats(uint64_t out[2]);
+ * footprint larger than the staging buffer), out[2] = the staged tiles whose box
+ * came by TMA, out[3] = the staged tiles split into y-parts; cumulative in this
+ * process.  Synchronises the device (not for the hot path). */
+w3d_status warp3d_tile_stats(uint64_t out[4]);
 
 /* Thread-local message for the last non-OK status of this thread ("" if none). */
 const char* warp3d_last_error(void);

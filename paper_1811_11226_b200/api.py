@@ -289,10 +289,11 @@ def warp3d_launch_count() -> int:
 
 
 def warp3d_tile_stats():
-    """(staged tiles, gather tiles) computed so far in this process (diagnostic)."""
-    out = (ctypes.c_uint64 * 2)()
+    """(staged tiles, gather tiles, staged by TMA, staged in y-parts) so far in this
+    process (diagnostic)."""
+    out = (ctypes.c_uint64 * 4)()
     L.check(L.load().warp3d_tile_stats(out))
-    return int(out[0]), int(out[1])
+    return tuple(int(v) for v in out)
 
 
 def warp3d_abi_version() -> int:

@@ -44,7 +44,7 @@ constexpr float kSane = 2097152.0f;     // 2^21: unclamped boxes only for |p| be
 
 extern __shared__ __align__(16) unsigned char cube_smem[];
 
-__device__ unsigned long long g_cube_tiles[2];  // [staged, gathered] (warp3d_tile_stats)
+__device__ unsigned long long g_cube_tiles[4];  // [staged, gathered, TMA, parts] (warp3d_tile_stats)
 
 // dynamic shared memory, rounded up to 128 B (TMA destinations); the launch
 // reserves the slack
@@ -246,8 +246,12 @@ __device__ __forceinline__ void stage_impl(const WarpArgs& a, const T* __restric
   const uint32_t plane = static_cast<uint32_t>(a.nx) * static_cast<uint32_t>(a.ny);
   const uint32_t fw = fill_word<T>(a);
   const uint32_t lf4 = a.label_fill * 0x01010101u;
+  // r = s / CW in fp32: (s + 1/2) / CW is >= 1/(2 CW) away from an integer and
+  // s < 2^16, CW <= 256, so the product's error (< 2^-7) cannot cross one
+  const float inv_cw = __frcp_rn(static_cast<float>(CW));
   for (int s = threadIdx.x; s < slots; s += THREADS) {
-    const int r = s / CW, c = s - r * CW;
+    const int r = __float2int_rz(__fmul_rn(static_cast<float>(s) + 0.5f, inv_cw));
+    const int c = s - r * CW;
     const int gx = b.bx + kC * c, gy = b.by + r;
     const uint32_t e = static_cast<uint32_t>(r * b.W + kC * c);
     uint32_t si = simg + kB * e, sl = slbl + e;
@@ -440,7 +444,8 @@ template <class T> __device__ __forceinline__ float lds_one(uint32_t a) {
 }
 
 // Staged sampling of a y-pair: image (trilinear or nearest) and label.
-template <class T, bool kLabels, bool kNearest, bool kClamp>
+// kSameLbl: the label box has the image box's pitches (cp.async boxes).
+template <class T, bool kLabels, bool kNearest, bool kClamp, bool kSameLbl>
 __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, float2 pz,
                                         float2& img, uint32_t& l0, uint32_t& l1) {
   if (kClamp) {
@@ -463,8 +468,11 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
     const float2 hz = make_float2(fset_ge_half(tz.x), fset_ge_half(tz.y));
     if (kNearest) Ln = __ffma2_rn(hz, f2(v.Pf), __ffma2_rn(hy, f2(v.Wf), __fadd2_rn(L, hx)));
     if (kLabels) {  // label buffer: own pitches (kM + fx + hx - bx + Wl (ry + hy) + Pl (rz + hz))
-      const float2 Ll = __ffma2_rn(__fadd2_rn(rz, hz), f2(v.Plf),
-                                   __ffma2_rn(__fadd2_rn(ry, hy), f2(v.Wlf), __fadd2_rn(sx, hx)));
+      const float2 Ll =
+          kSameLbl ? (kNearest ? Ln
+                               : __ffma2_rn(hz, f2(v.Pf), __ffma2_rn(hy, f2(v.Wf), __fadd2_rn(L, hx))))
+                   : __ffma2_rn(__fadd2_rn(rz, hz), f2(v.Plf),
+                                __ffma2_rn(__fadd2_rn(ry, hy), f2(v.Wlf), __fadd2_rn(sx, hx)));
       l0 = lds_u8(addr1(Ll.x, v.clbl));
       l1 = lds_u8(addr1(Ll.y, v.clbl));
     }
@@ -558,7 +566,8 @@ __device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
 // group's normals (computed while the staging copies were in flight); the next
 // group's Philox block is computed inside each iteration (independent chain).
 // ---------------------------------------------------------------------------
-template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp>
+template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
+          bool kSameLbl = false, bool kFull = false>
 __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n) {
@@ -604,14 +613,14 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
 #pragma unroll 1
   for (int g = 0; g < ng; ++g) {
     const int y = y0 + 4 * g;
-    if (y >= my) break;
+    if (!kFull && y >= my) break;
     float4 nn = make_float4(0.f, 0.f, 0.f, 0.f);
     if (noise && g + 1 < ng) nn = box_muller4(philox_block(q + mxu, pp, rk0, rk1));
     const float ns[4] = {n.x, n.y, n.z, n.w};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int ya = y + 2 * h;
-      if (ya >= my) break;
+      if (!kFull && ya >= my) break;
       const float2 px = __ffma2_rn(f2(V.A1[0]), Y2, f2(t0));
       const float2 py = __ffma2_rn(f2(V.A1[1]), Y2, f2(t1));
       const float2 pz = __ffma2_rn(f2(V.A1[2]), Y2, f2(t2));
@@ -619,14 +628,14 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
       float2 img;
       uint32_t l0 = 0, l1 = 0;
       if (kStaged) {
-        sample2<T, kLabels, kNearest, kClamp>(v, px, py, pz, img, l0, l1);
+        sample2<T, kLabels, kNearest, kClamp, kSameLbl>(v, px, py, pz, img, l0, l1);
       } else {
         sample_gather<T, kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
         sample_gather<T, kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
       }
       float2 out = photometric2<kPh>(img, make_float2(ns[2 * h], ns[2 * h + 1]), V);
       if (occl) out = make_float2(0.0f, 0.0f);  // PAPER.md:437-438, R15
-      const bool second = ya + 1 < my;
+      const bool second = kFull || ya + 1 < my;
       float* po1 = po + row1;
       st_f32(po, out.x);
       if (second) st_f32(po1, out.y);
@@ -680,7 +689,7 @@ __device__ __forceinline__ float4 first_normals(const WarpArgs& a, const VolDev&
 template <class T, int TY, bool kLabels, bool kNearest, int kPh>
 __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int cap,
                                         bool gather_only) {
-  const int vi = static_cast<int>(blockIdx.z) / tiles_z;
+  const int vi = static_cast<int>(blockIdx.z) / tiles_z;  // rare path: plain division
   const int ox = static_cast<int>(blockIdx.x) * TX, oy = static_cast<int>(blockIdx.y) * TY;
   const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * TZ;
   const uint32_t simg = smem_base();
@@ -709,7 +718,10 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
                                                       first_normals<kPh>(a, P, V, X, Z, oy));
     return;
   }
-  if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[0], 1ull);
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_cube_tiles[0], 1ull);
+    atomicAdd(&g_cube_tiles[3], 1ull);
+  }
   for (int y = oy; y <= ylast; y += rows) {
     tile_box<T>(a, P.A, ox, y, min(y + rows - 1, ylast), oz, cap, b);
     const uint32_t slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
@@ -721,9 +733,73 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
     __syncthreads();
     if (!live) continue;
     if (b.clamp)
-      column_rows<T, kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, y, rows / 4, n);
+      column_rows<T, kLabels, kNearest, kPh, true, true, true>(a, P, V, v, vi, X, Z, y, rows / 4, n);
     else
-      column_rows<T, kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, y, rows / 4, n);
+      column_rows<T, kLabels, kNearest, kPh, true, false, true>(a, P, V, v, vi, X, Z, y, rows / 4, n);
+  }
+}
+
+// The tile's coordinates stay below 2^21 (magic-number floor, float indices):
+// its origin voxel's p below 2^20 and the footprint extent below 200 (host).
+__device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz) {
+  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
+  bool sane = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sane &= fabsf(coord(P.A, k, X, Y, Z)) < 1048576.0f;
+  return sane;
+}
+
+// The common path: the tile in y-parts of P.cp_rows rows, each staged as ONE
+// box of the volume's fixed dims (cp_w, cp_h, cp_d; host-computed by
+// cube_cp_box to hold the footprint of any part) whose origin follows from the
+// part's origin voxel alone -- every value here is CTA-uniform (no per-tile
+// corner reduction; the view's pitches live in uniform registers).
+template <class T, int TY, bool kLabels, bool kNearest, int kPh>
+__device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int vi, int ox, int oy,
+                                        int oz, int ylast) {
+  constexpr int kC = InT<T>::kChunk;
+  const int rows = P.cp_rows;
+  const uint32_t simg = smem_base();
+  float mlo[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)  // a part of r rows: box_mlo - min(0, A_k1) (TY - r)
+    mlo[k] = __fmaf_rn(fminf(P.A[4 * k + 1], 0.0f), -static_cast<float>(TY - rows), P.box_mlo[k]);
+  Box b;
+  b.W = P.cp_w;
+  b.H = P.cp_h;
+  b.D = P.cp_d;
+  b.P = P.cp_p;
+  b.Wl = b.W;
+  b.Pl = b.P;
+  b.clamp = false;
+  const uint32_t slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
+  const Vol V = load_vol(P);
+  const T* vin = vol_in<T>(P);
+  const uint8_t* lin = kLabels ? vol_lbl(P) : nullptr;
+  const int lane = threadIdx.x & 31;
+  const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
+  const bool live = X < a.mx && Z < a.mz;
+  for (int y = oy; y <= ylast; y += rows) {
+    const float fx = static_cast<float>(ox), fy = static_cast<float>(y), fz = static_cast<float>(oz);
+    b.bx = __float2int_rd(__fadd_rd(coord(P.A, 0, fx, fy, fz), mlo[0])) & ~(kC - 1);
+    b.by = __float2int_rd(__fadd_rd(coord(P.A, 1, fx, fy, fz), mlo[1]));
+    b.bz = __float2int_rd(__fadd_rd(coord(P.A, 2, fx, fy, fz), mlo[2]));
+    b.bxl = b.bx;
+    if (y != oy) __syncthreads();  // previous part's buffer no longer read
+    stage<T, kLabels>(a, vin, lin, b, simg, slbl);
+    const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, y) : make_float4(0, 0, 0, 0);
+    View v = make_view<T>(a, b, simg, slbl);
+    v.W4 = P.cp_w_bytes;  // straight from the parameters: uniform registers, folded
+    v.P4 = P.cp_p_bytes;  // into the shared-memory addresses ([R + UR])
+    cp_async_wait_all();
+    __syncthreads();
+    if (!live) continue;
+    if (y + rows <= a.my)  // every row of the part is an output row
+      column_rows<T, kLabels, kNearest, kPh, true, false, true, true>(a, P, V, v, vi, X, Z, y,
+                                                                      rows / 4, n);
+    else
+      column_rows<T, kLabels, kNearest, kPh, true, false, true>(a, P, V, v, vi, X, Z, y, rows / 4,
+                                                               n);
   }
 }
 
@@ -859,10 +935,13 @@ __device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint3
 // grid = (tiles per volume, volumes); tiles x-fastest, then y, then z.
 template <class T, int TY, int MINB, bool kLabels, bool kNearest, int kPh, bool kGather>
 __global__ void __launch_bounds__(THREADS, MINB)
-    warp3d_cube_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap) {
+    warp3d_cube_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap,
+                       const uint32_t tz_magic) {
   __shared__ __align__(8) unsigned long long s_mbar;
-  // grid = (tiles_x, tiles_y, tiles_z * volumes)
-  const int vi = static_cast<int>(blockIdx.z) / tiles_z;
+  // grid = (tiles_x, tiles_y, tiles_z * volumes); vi = blockIdx.z / tiles_z by
+  // multiply-high with tz_magic = ceil(2^32 / tiles_z) (exact for operands < 2^16)
+  const int vi = tiles_z == 1 ? static_cast<int>(blockIdx.z)
+                              : static_cast<int>(__umulhi(blockIdx.z, tz_magic));
   const int ox = static_cast<int>(blockIdx.x) * TX, oy = static_cast<int>(blockIdx.y) * TY;
   const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * TZ;
   const uint32_t simg = smem_base();
@@ -880,12 +959,22 @@ __global__ void __launch_bounds__(THREADS, MINB)
   }
   const bool tma = use_tma && tma_box<T>(P, ox, oy, oz, b);
   if (!tma) {
+    // analytic boxes for whole tiles only: an exact per-tile box (tile_box) of a
+    // volume whose worst-case box does not fit usually still fits
+    if (!kGather && P.cp_rows == TY && cp_sane(P, ox, oy, oz)) {
+      if (threadIdx.x == 0) {
+        atomicAdd(&g_cube_tiles[0], 1ull);
+        if (P.cp_rows < TY) atomicAdd(&g_cube_tiles[3], 1ull);
+      }
+      cp_tile<T, TY, kLabels, kNearest, kPh>(a, P, vi, ox, oy, oz, ylast);
+      return;
+    }
     if (kGather || !tile_box<T>(a, P.A, ox, oy, ylast, oz, cap, b)) {
       tile_parts<T, TY, kLabels, kNearest, kPh>(a, tiles_z, cap, kGather);
       return;
     }
   }
-  if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[0], 1ull);
+  if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[tma ? 2 : 0], 1ull);
   uint32_t slbl;
 #ifdef W3D_DBG_NOSTAGE
   if (tma) {
@@ -981,8 +1070,10 @@ static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
   }
   const dim3 grid(static_cast<unsigned>(tiles_x), static_cast<unsigned>(tiles_y),
                   static_cast<unsigned>(tiles_z * a.nvol));
+  const uint32_t tz_magic =
+      tiles_z > 1 ? static_cast<uint32_t>(((uint64_t(1) << 32) + tiles_z - 1) / tiles_z) : 0u;
   warp3d_cube_kernel<T, kTY, kMinB, kLabels, kNearest, kPh, kGather>
-      <<<grid, THREADS, smem, s>>>(a, tiles_z, cap);
+      <<<grid, THREADS, smem, s>>>(a, tiles_z, cap, tz_magic);
   return cudaGetLastError();
 }
 
@@ -993,7 +1084,7 @@ static bool all_full(const WarpArgs& a) {
   for (int i = 0; i < a.nvol; ++i) {
     const VolDev& P = a.vol[i];
     if (P.flags != (kNoise | kGamma) || P.clamp_lo != 0.0f || P.clamp_hi != 1.0f) return false;
-    if (P.key0 != a.vol[0].key0 || P.key1 != a.vol[0].key1) return false;
+    if (P.rk0[0] != a.vol[0].rk0[0] || P.rk1[0] != a.vol[0].rk1[0]) return false;
   }
   return true;
 }
@@ -1055,7 +1146,7 @@ bool cube_tma_supported(const WarpArgs& a) {
 // origins (image: 4 float / 8 int16 elements, labels 16); rows per plane padded
 // so the plane pitch spreads the two half-warps over the banks
 // (tools/model_tiles.py).  box_w = 0 when the box exceeds the buffer.
-void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes) {
+void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes, const int out[3]) {
   using namespace cube;
   const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
   int d[3];
@@ -1066,7 +1157,7 @@ void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes) {
       const double a = double(A[4 * k + j]) * span[j];
       ext += std::fabs(a);
       mlo += a < 0.0 ? a : 0.0;
-      mag += std::fabs(double(A[4 * k + j])) * 1048576.0;  // |p| < 2^20 on this path
+      mag += std::fabs(double(A[4 * k + j])) * (out[j] + 16.0);  // any voxel of any tile
     }
     // fp32 evaluation of p (3 roundings each) and of the origin term: a few
     // ulp(|p|); the margin covers 16 ulp
@@ -1100,8 +1191,61 @@ void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes) {
   P.box_wl = static_cast<uint16_t>(Wl);
 }
 
-cudaError_t read_cube_stats(unsigned long long out[2]) {
-  return cudaMemcpyFromSymbol(out, cube::g_cube_tiles, 2 * sizeof(unsigned long long));
+// cp.async staging box of one volume (and box_mlo, shared with the TMA path):
+// the footprint of a 16 x r x 16 part has extent ext_k = sum_j |A_kj| span_j;
+// from the origin floor(p0 + box_mlo) the part needs at most
+// floor(ext_k + 2 margin) + 3 elements per axis (floor of the lower bound, the
+// +1 trilinear corner, rounding inside the margin), plus chunk - 1 in x for the
+// 16 B aligned row start.  r = kTY, kTY/2, kTY/4: the first that fits.
+void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3]) {
+  using namespace cube;
+  const int kC = 16 / elem_bytes;
+  const int cap = kCapVox * 5 / (elem_bytes + 1);
+  P.cp_w = P.cp_h = P.cp_d = P.cp_rows = 0;
+  P.cp_p = 0;
+  P.cp_w_bytes = P.cp_p_bytes = 0;
+  double margin[3], mlo[3], ext_xz[3], ay[3];
+  for (int k = 0; k < 3; ++k) {
+    double mag = std::fabs(double(A[4 * k + 3]));
+    for (int j = 0; j < 3; ++j) mag += std::fabs(double(A[4 * k + j])) * (out[j] + 16.0);
+    margin[k] = 16.0 * mag * 0x1.0p-24 + 1e-3;
+    const double ax = double(A[4 * k]) * (TX - 1.0), az = double(A[4 * k + 2]) * (TZ - 1.0);
+    ay[k] = double(A[4 * k + 1]);
+    ext_xz[k] = std::fabs(ax) + std::fabs(az);
+    mlo[k] = (ax < 0 ? ax : 0.0) + (az < 0 ? az : 0.0) + (ay[k] < 0 ? ay[k] * (kTY - 1.0) : 0.0);
+    P.box_mlo[k] = static_cast<float>(mlo[k] - margin[k]);
+  }
+  for (int rows = kTY; rows >= 4 && rows >= kTY / 4; rows /= 2) {
+    int d[3];
+    bool ok = true;
+    for (int k = 0; k < 3; ++k) {
+      const double ext = ext_xz[k] + std::fabs(ay[k]) * (rows - 1.0);
+      if (ext > 200.0) ok = false;
+      d[k] = ok ? static_cast<int>(std::floor(ext + 2.0 * margin[k])) + 3 : 0;
+    }
+    if (!ok) return;
+    const int W = (d[0] + kC - 1 + kC - 1) & ~(kC - 1), H = d[1], D = d[2];
+    const int wh = W * H;
+    const int res = kC == 4 ? kPlaneRes : 16;
+    int Pp = wh + ((res - wh) & 31);
+    if (int64_t(Pp) * D > cap) Pp = wh;
+    if (int64_t(Pp) * D <= cap && W <= 4 * THREADS) {
+      P.cp_w = static_cast<uint16_t>(W);
+      P.cp_h = static_cast<uint16_t>(H);
+      P.cp_d = static_cast<uint16_t>(D);
+      P.cp_p = Pp;
+      P.cp_rows = static_cast<uint16_t>(rows);
+      P.cp_w_bytes = static_cast<uint16_t>(W * elem_bytes);
+      P.cp_p_bytes = static_cast<uint16_t>(Pp * elem_bytes);
+      return;
+    }
+  }
+}
+
+cudaError_t read_cube_stats(unsigned long long out[4]) {
+  const cudaError_t e = cudaMemcpyFromSymbol(out, cube::g_cube_tiles, 4 * sizeof(unsigned long long));
+  out[0] += out[2];  // staged = cp.async + TMA
+  return e;
 }
 
 }  // namespace w3d

@@ -151,15 +151,15 @@ static VolDev derive(const float* A, const w3d_photometric* ph) {
     if (P.occ_lo <= P.occ_hi) f |= kOcclude;
   }
   P.flags = f;
-  P.key0 = static_cast<uint32_t>(ph->seed);
-  P.key1 = static_cast<uint32_t>(ph->seed >> 32);
-  P.vid0 = static_cast<uint32_t>(ph->volume_id);
-  P.vid1 = static_cast<uint32_t>(ph->volume_id >> 32);
-  for (int r = 0; r < 10; ++r) {  // Philox key schedule (philox.cuh)
-    P.rk0[r] = P.key0 + static_cast<uint32_t>(r) * 0x9E3779B9u;
-    P.rk1[r] = P.key1 + static_cast<uint32_t>(r) * 0xBB67AE85u;
+  const uint32_t key0 = static_cast<uint32_t>(ph->seed);
+  const uint32_t key1 = static_cast<uint32_t>(ph->seed >> 32);
+  const uint32_t vid0 = static_cast<uint32_t>(ph->volume_id);
+  const uint32_t vid1 = static_cast<uint32_t>(ph->volume_id >> 32);
+  for (int r = 0; r < 10; ++r) {  // Philox key schedule (philox.cuh); rk*[0] = the key
+    P.rk0[r] = key0 + static_cast<uint32_t>(r) * 0x9E3779B9u;
+    P.rk1[r] = key1 + static_cast<uint32_t>(r) * 0xBB67AE85u;
   }
-  const PhiloxPrefix pp = philox_prefix(P.vid0, P.vid1, P.key0, P.key1);
+  const PhiloxPrefix pp = philox_prefix(vid0, vid1, key0, key1);
   P.ph_K0 = pp.K0;
   P.ph_K1 = pp.K1;
   P.ph_K2 = pp.K2;
@@ -235,7 +235,8 @@ static bool prepare_tma(WarpArgs& args, const float* const* affines) {
     VolDev& P = args.vol[i];
     if (i >= kTmaVolPerLaunch) break;
     const int eb = args.in16 ? 2 : 4;
-    cube_tma_box(affines[i], P, labels, eb);
+    const int out[3] = {args.mx, args.my, args.mz};
+    cube_tma_box(affines[i], P, labels, eb, out);
     if (!P.box_w) continue;
     const void* base = reinterpret_cast<const void*>(P.in_addr);
     MapKey ki{base, args.nx, args.ny, args.nz, P.box_w, P.box_h, P.box_d, eb};
@@ -311,6 +312,8 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       P.lbl_addr = reinterpret_cast<uint64_t>(vols[v0 + i].lbl);
       P.out_slot = vols[v0 + i].slot;
       if (P.in_addr % 16 || P.lbl_addr % 8) args.in_aligned = 0;
+      const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
+      cube_cp_box(affines[v0 + i], P, elem, od);
     }
     for (int r = 0; r < 10; ++r) {  // volume 0's key schedule (used when all seeds agree)
       args.rk0[r] = args.vol[0].rk0[r];
@@ -379,13 +382,12 @@ const char* warp3d_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t warp3d_launch_count(void) { return g_launches.load(); }
 
-w3d_status warp3d_tile_stats(uint64_t out[2]) {
+w3d_status warp3d_tile_stats(uint64_t out[4]) {
   if (!out) return fail(W3D_ERR_INVALID_ARG, "out must be non-NULL");
-  unsigned long long v[2] = {0, 0};
+  unsigned long long v[4] = {0, 0, 0, 0};
   const cudaError_t e = read_cube_stats(v);
   if (e != cudaSuccess) return cuda_fail(e, "warp3d_tile_stats");
-  out[0] = v[0];
-  out[1] = v[1];
+  for (int k = 0; k < 4; ++k) out[k] = v[k];
   return ok();
 }
 

@@ -33,8 +33,13 @@ struct alignas(16) VolDev {
   float clamp_lo;     // 0 with CLAMP, else -inf
   float clamp_hi;     // 1 with CLAMP, else +inf
   float gamma;
-  uint32_t key0, key1;  // Philox key = seed
-  uint32_t vid0, vid1;  // Philox counter words 2,3 = volume_id
+  // cp.async staging box of this volume's tiles (host-computed from A,
+  // cube_cp_box): tiles in y-parts of cp_rows rows (kTY, kTY/2 or kTY/4; 0 =
+  // the footprint does not fit: per-tile boxes / gathers), box cp_w x cp_h x
+  // cp_d elements with plane pitch cp_p, origin as the TMA box (box_mlo)
+  uint16_t cp_w, cp_h, cp_d, cp_rows;
+  int32_t cp_p;
+  uint16_t cp_w_bytes, cp_p_bytes;  // cp_w, cp_p in bytes of the image element type
   int32_t occ_lo, occ_hi;  // occluded output z in [occ_lo, occ_hi]
   // TMA box of this volume's tiles (host-computed from A, warp3d_cube.cu): image
   // box (box_w, box_h, box_d) floats, label box (box_wl, box_h, box_d) bytes;
@@ -42,8 +47,9 @@ struct alignas(16) VolDev {
   uint16_t box_w, box_h, box_d, box_wl;
   uint32_t rk0[10], rk1[10];  // Philox round keys k + r * (W0, W1), host-precomputed
   uint32_t ph_K0, ph_K1, ph_K2, ph_U3;  // PhiloxPrefix (philox.cuh), host-precomputed
-  // TMA box origin of a tile: floor(p(tile origin voxel) + box_mlo[k]) with
-  // box_mlo[k] = sum_j min(0, A_kj span_j) - rounding margin (cube_tma_box)
+  // box origin of a full tile (TMA and cp.async): floor(p(tile origin voxel) +
+  // box_mlo[k]) with box_mlo[k] = sum_j min(0, A_kj span_j) - rounding margin
+  // (cube_box_mlo); a y-part of r rows adds -min(0, A_k1) (kTY - r)
   float box_mlo[3];
   int32_t out_slot;     // output volume index in the caller's batch (out + slot * out_stride)
   uint64_t in_addr;     // device address of this volume's image (float32 or int16)
@@ -91,9 +97,12 @@ static_assert(sizeof(WarpArgs) <= 32764, "kernel parameter space");
 bool cube_supported(const WarpArgs& a);
 bool cube_tma_supported(const WarpArgs& a);
 // TMA box dims for one volume's tiles (0 when the box exceeds the buffer)
-void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes);
+// (out = output dims x, y, z: the rounding margin scales with the largest |p|)
+void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes, const int out[3]);
+// box origin offsets and cp.async staging box of one volume's tiles
+void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3]);
 cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s);
-cudaError_t read_cube_stats(unsigned long long out[2]);
+cudaError_t read_cube_stats(unsigned long long out[4]);
 // warp3d_resample.cu (NEXT-3): one separable Gaussian pass along `axis` (0 x, 1 y, 2 z)
 constexpr int kMaxTaps = 63;  // radius ceil(3 sigma) <= 31
 int gauss_radius(double sigma);

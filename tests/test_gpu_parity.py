@@ -242,6 +242,7 @@ def test_large_footprints_subtiles_clamp_and_gathers(W):
     check(g_img, g_lbl, ref, ds, FULL, "large footprints")
     s1 = W.warp3d_tile_stats()
     assert s1[1] > s0[1], "expected some gathered tiles"
+    assert s1[3] > s0[3], "expected some tiles staged in y-parts"
     for v in (0, 1):
         c_img, c_lbl, _ = run_case(W, imgs, lbls, As, ds, FULL, [0, 1, 2, 3], variant=v,
                                    fill=-1000.0, label_fill=5, oracle_volumes=[])
