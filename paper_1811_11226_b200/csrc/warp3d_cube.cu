@@ -236,7 +236,7 @@ template <> __device__ __forceinline__ uint32_t fill_word<int16_t>(const WarpArg
   return a.fill16_pair;
 }
 
-template <class T, bool kLabels, bool kInside>
+template <class T, bool kLabels, bool kInside, bool kImg = true>
 __device__ __forceinline__ void stage_impl(const WarpArgs& a, const T* __restrict__ vin,
                                            const uint8_t* __restrict__ lin, const Box& b,
                                            uint32_t simg, uint32_t slbl) {
@@ -258,7 +258,7 @@ __device__ __forceinline__ void stage_impl(const WarpArgs& a, const T* __restric
     uint32_t goff = static_cast<uint32_t>(b.bz) * plane + static_cast<uint32_t>(gy * a.nx + gx);
     const uint32_t sstep = static_cast<uint32_t>(b.P);
     auto copy = [&]() {
-      cp_async16(si, gaddr<kB>(vin, goff));
+      if (kImg) cp_async16(si, gaddr<kB>(vin, goff));
       if (kLabels) {
         if (kC == 4)
           cp_async4(sl, gaddr<1>(lin, goff));
@@ -282,7 +282,8 @@ __device__ __forceinline__ void stage_impl(const WarpArgs& a, const T* __restric
         if (row_in & (static_cast<unsigned>(gz) < static_cast<unsigned>(a.nz))) {
           copy();
         } else {
-          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(si), "r"(fw) : "memory");
+          if (kImg)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(si), "r"(fw) : "memory");
           if (kLabels) {
             if (kC == 4)
               asm volatile("st.shared.u32 [%0], %1;" ::"r"(sl), "r"(lf4) : "memory");
@@ -307,6 +308,17 @@ __device__ __forceinline__ void stage(const WarpArgs& a, const T* vin, const uin
     stage_impl<T, kLabels, true>(a, vin, lin, b, simg, slbl);
   else
     stage_impl<T, kLabels, false>(a, vin, lin, b, simg, slbl);
+}
+// the label box alone (the image box comes by TMA)
+template <class T>
+__device__ __forceinline__ void stage_lbl(const WarpArgs& a, const uint8_t* lin, const Box& b,
+                                          uint32_t slbl) {
+  const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
+                      b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
+  if (inside)
+    stage_impl<T, true, true, false>(a, nullptr, lin, b, 0u, slbl);
+  else
+    stage_impl<T, true, false, false>(a, nullptr, lin, b, 0u, slbl);
 }
 
 // ---------------------------------------------------------------------------
@@ -739,79 +751,14 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
   }
 }
 
-// The tile's coordinates stay below 2^21 (magic-number floor, float indices):
-// its origin voxel's p below 2^20 and the footprint extent below 200 (host).
-__device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz) {
-  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
-  bool sane = true;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) sane &= fabsf(coord(P.A, k, X, Y, Z)) < 1048576.0f;
-  return sane;
-}
-
-// The common path: the tile in y-parts of P.cp_rows rows, each staged as ONE
-// box of the volume's fixed dims (cp_w, cp_h, cp_d; host-computed by
-// cube_cp_box to hold the footprint of any part) whose origin follows from the
-// part's origin voxel alone -- every value here is CTA-uniform (no per-tile
-// corner reduction; the view's pitches live in uniform registers).
-template <class T, int TY, bool kLabels, bool kNearest, int kPh>
-__device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int vi, int ox, int oy,
-                                        int oz, int ylast) {
-  constexpr int kC = InT<T>::kChunk;
-  const int rows = P.cp_rows;
-  const uint32_t simg = smem_base();
-  float mlo[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)  // a part of r rows: box_mlo - min(0, A_k1) (TY - r)
-    mlo[k] = __fmaf_rn(fminf(P.A[4 * k + 1], 0.0f), -static_cast<float>(TY - rows), P.box_mlo[k]);
-  Box b;
-  b.W = P.cp_w;
-  b.H = P.cp_h;
-  b.D = P.cp_d;
-  b.P = P.cp_p;
-  b.Wl = b.W;
-  b.Pl = b.P;
-  b.clamp = false;
-  const uint32_t slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
-  const Vol V = load_vol(P);
-  const T* vin = vol_in<T>(P);
-  const uint8_t* lin = kLabels ? vol_lbl(P) : nullptr;
-  const int lane = threadIdx.x & 31;
-  const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
-  const bool live = X < a.mx && Z < a.mz;
-  for (int y = oy; y <= ylast; y += rows) {
-    const float fx = static_cast<float>(ox), fy = static_cast<float>(y), fz = static_cast<float>(oz);
-    b.bx = __float2int_rd(__fadd_rd(coord(P.A, 0, fx, fy, fz), mlo[0])) & ~(kC - 1);
-    b.by = __float2int_rd(__fadd_rd(coord(P.A, 1, fx, fy, fz), mlo[1]));
-    b.bz = __float2int_rd(__fadd_rd(coord(P.A, 2, fx, fy, fz), mlo[2]));
-    b.bxl = b.bx;
-    if (y != oy) __syncthreads();  // previous part's buffer no longer read
-    stage<T, kLabels>(a, vin, lin, b, simg, slbl);
-    const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, y) : make_float4(0, 0, 0, 0);
-    View v = make_view<T>(a, b, simg, slbl);
-    v.W4 = P.cp_w_bytes;  // straight from the parameters: uniform registers, folded
-    v.P4 = P.cp_p_bytes;  // into the shared-memory addresses ([R + UR])
-    cp_async_wait_all();
-    __syncthreads();
-    if (!live) continue;
-    if (y + rows <= a.my)  // every row of the part is an output row
-      column_rows<T, kLabels, kNearest, kPh, true, false, true, true>(a, P, V, v, vi, X, Z, y,
-                                                                      rows / 4, n);
-    else
-      column_rows<T, kLabels, kNearest, kPh, true, false, true>(a, P, V, v, vi, X, Z, y, rows / 4,
-                                                               n);
-  }
-}
-
-
 // ---------------------------------------------------------------------------
-// TMA staging (the default): the tile's footprint box is ONE 3D tensor box of
-// the volume (dims fixed per volume: every full tile of an affine warp has the
-// same footprint extent, host-computed by cube_tma_box), loaded by one thread
-// with cp.async.bulk.tensor into shared memory, completion on an mbarrier.
-// Out-of-volume elements arrive as 0; boxes that leave the volume get fill /
-// label_fill written over them before the compute (R6, R8).  Image and label
-// boxes share the origin; the label rows have their own pitch (16 B rows).
+// TMA image staging: the tile's image footprint box is ONE 3D tensor box of the
+// volume (dims fixed per volume, cube_cp_box), loaded by one thread with
+// cp.async.bulk.tensor, completion on an mbarrier; out-of-volume elements
+// arrive as 0 and boxes that leave the volume get fill written over them before
+// the compute (R6).  The label box (1 B elements) goes by cp.async with the
+// same pitches: a TMA box row must start 16 B aligned (measured: an unaligned
+// inner origin faults), which for labels would cost a 16-element x slack.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
@@ -852,84 +799,115 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-// The tile's box in the volume's fixed TMA dims, from the tile's origin voxel
-// alone: every p of the tile is >= p(origin) + sum_j min(0, A_kj span_j) (up to
-// fp32 rounding, inside the host's margin), so the box needs no per-tile
-// reduction over corners.  False for coordinates beyond 2^20 (cp.async path).
+// fill over the out-of-volume elements of a TMA image box (TMA wrote 0).
 template <class T>
-__device__ __forceinline__ bool tma_box(const VolDev& P, int ox, int oy, int oz, Box& b) {
-  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
-  int lo[3];
-  bool sane = true;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const float p0 = coord(P.A, k, X, Y, Z);
-    sane &= fabsf(p0) < 1048576.0f;
-    lo[k] = __float2int_rd(__fadd_rd(p0, P.box_mlo[k]));
-  }
-  // TMA box inner origins must be 16 B aligned: image x0 % 4, label x0 % 16
-  b.bx = lo[0] & ~(InT<T>::kChunk - 1);
-  b.bxl = lo[0] & ~15;
-  b.by = lo[1];
-  b.bz = lo[2];
-  b.W = P.box_w;
-  b.H = P.box_h;
-  b.D = P.box_d;
-  b.P = b.W * b.H;
-  b.Wl = P.box_wl;
-  b.Pl = b.Wl * b.H;
-  b.clamp = false;
-  return sane;
-}
-
-// fill / label_fill over the out-of-volume elements of a TMA box (TMA wrote 0);
-// rows [0, W) of the image box and [0, Wl) of the label box.
-template <class T, bool kLabels>
-__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint32_t simg,
-                                          uint32_t slbl, bool fi, bool fl) {
+__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint32_t simg) {
   constexpr uint32_t kB = InT<T>::kBytes;
   const uint32_t fw = fill_word<T>(a);
-  const uint32_t lf4 = a.label_fill * 0x01010101u;
   const int head = min(b.W, max(0, -b.bx)), tail = max(0, min(b.W, a.nx - b.bx));
-  const int headl = min(b.Wl, max(0, -b.bxl)), taill = max(0, min(b.Wl, a.nx - b.bxl));
   for (int r = threadIdx.x; r < b.H * b.D; r += THREADS) {
     const int z = r / b.H, y = r - z * b.H;
     const bool row_out = static_cast<unsigned>(b.bz + z) >= static_cast<unsigned>(a.nz) ||
                          static_cast<unsigned>(b.by + y) >= static_cast<unsigned>(a.ny);
     const uint32_t irow = simg + kB * static_cast<uint32_t>(z * b.P + y * b.W);
-    const uint32_t lrow = slbl + static_cast<uint32_t>(z * b.Pl + y * b.Wl);
     if (row_out) {
-      if (fi)
-        for (int x = 0; x < b.W; x += 16 / kB)
-          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(irow + kB * x), "r"(fw)
-                       : "memory");
-      if (kLabels && fl)
-        for (int x = 0; x < b.Wl; x += 16)
-          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(lrow + x), "r"(lf4)
-                       : "memory");
+      for (int x = 0; x < b.W; x += 16 / kB)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(irow + kB * x), "r"(fw)
+                     : "memory");
       continue;
     }
-    if (fi) {
-      for (int x = 0; x < head; ++x) {
-        if (kB == 4)
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
-        else
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
-      }
-      for (int x = tail; x < b.W; ++x) {
-        if (kB == 4)
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
-        else
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
-      }
+    for (int x = 0; x < head; ++x) {
+      if (kB == 4)
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
+      else
+        asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
     }
-    if (kLabels && fl) {
-      for (int x = 0; x < headl; ++x)
-        asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
-      for (int x = taill; x < b.Wl; ++x)
-        asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
+    for (int x = tail; x < b.W; ++x) {
+      if (kB == 4)
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
+      else
+        asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
     }
   }
+}
+
+// The tile's coordinates stay below 2^21 (magic-number floor, float indices):
+// its origin voxel's p below 2^20 and the footprint extent below 200 (host).
+__device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz) {
+  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
+  bool sane = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sane &= fabsf(coord(P.A, k, X, Y, Z)) < 1048576.0f;
+  return sane;
+}
+
+// The common path: the whole tile staged as ONE box of the volume's fixed dims
+// (cp_w, cp_h, cp_d; host-computed by cube_cp_box to hold any tile's
+// footprint) whose origin follows from the tile's origin voxel alone -- every
+// value here is CTA-uniform (no per-tile corner reduction; the view's pitches
+// sit in uniform registers, folded into the shared-memory addresses).  The
+// image box comes by TMA when the volume has a tensor map (tma), else by
+// cp.async; the labels by cp.async.
+template <class T, int TY, bool kLabels, bool kNearest, int kPh>
+__device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int vi, int ox, int oy,
+                                        int oz, bool tma, uint32_t mbar) {
+  constexpr int kC = InT<T>::kChunk;
+  constexpr uint32_t kB = InT<T>::kBytes;
+  const uint32_t simg = smem_base();
+  Box b;
+  b.W = P.cp_w;
+  b.H = P.cp_h;
+  b.D = P.cp_d;
+  b.P = P.cp_p;
+  b.Wl = b.W;
+  b.Pl = b.P;
+  b.clamp = false;
+  {
+    const float fx = static_cast<float>(ox), fy = static_cast<float>(oy), fz = static_cast<float>(oz);
+    b.bx = __float2int_rd(__fadd_rd(coord(P.A, 0, fx, fy, fz), P.box_mlo[0])) & ~(kC - 1);
+    b.by = __float2int_rd(__fadd_rd(coord(P.A, 1, fx, fy, fz), P.box_mlo[1]));
+    b.bz = __float2int_rd(__fadd_rd(coord(P.A, 2, fx, fy, fz), P.box_mlo[2]));
+    b.bxl = b.bx;
+  }
+  const uint32_t slbl = simg + ((kB * static_cast<uint32_t>(b.P * b.D) + 15u) & ~15u);
+  const Vol V = load_vol(P);
+  const T* vin = vol_in<T>(P);
+  const uint8_t* lin = kLabels ? vol_lbl(P) : nullptr;
+  const int lane = threadIdx.x & 31;
+  const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
+  const bool live = X < a.mx && Z < a.mz;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(mbar, kB * static_cast<uint32_t>(b.P * b.D));
+      tma_load_3d(simg, &a.tm[vi], b.bx, b.by, b.bz, mbar);
+    }
+    if (kLabels) stage_lbl<T>(a, lin, b, slbl);
+  } else {
+    stage<T, kLabels>(a, vin, lin, b, simg, slbl);
+  }
+  const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, oy) : make_float4(0, 0, 0, 0);
+  View v = make_view<T>(a, b, simg, slbl);
+  v.W4 = P.cp_w_bytes;  // straight from the parameters: uniform registers, folded
+  v.P4 = P.cp_p_bytes;  // into the shared-memory addresses ([R + UR])
+  cp_async_wait_all();
+  __syncthreads();  // label copies (and the mbarrier init) visible to every thread
+  if (tma) {
+    mbar_wait(mbar, 0);
+    const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
+                        b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
+    if (!inside && a.fill != 0.0f) {  // uniform
+      tma_fixup<T>(a, b, simg);
+      __syncthreads();
+    }
+  }
+  if (!live) return;
+  if (oy + TY <= a.my)  // every row of the tile is an output row
+    column_rows<T, kLabels, kNearest, kPh, true, false, true, true>(a, P, V, v, vi, X, Z, oy,
+                                                                    TY / 4, n);
+  else
+    column_rows<T, kLabels, kNearest, kPh, true, false, true>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
 }
 
 // grid = (tiles per volume, volumes); tiles x-fastest, then y, then z.
@@ -947,61 +925,24 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const uint32_t simg = smem_base();
   const VolDev& P = a.vol[vi];
   const int ylast = min(oy + TY, a.my) - 1;
+  if (!kGather && P.cp_rows == TY && cp_sane(P, ox, oy, oz)) {
+    const bool tma = a.use_tma && vi < kTmaVolPerLaunch && P.box_w != 0;
+    if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[tma ? 2 : 0], 1ull);
+    cp_tile<T, TY, kLabels, kNearest, kPh>(a, P, vi, ox, oy, oz, tma,
+                                           static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar)));
+    return;
+  }
+  // per-tile exact boxes (volumes whose worst-case box does not fit)
   Box b;
-  const bool use_tma = !kGather && a.use_tma && vi < kTmaVolPerLaunch && P.box_w != 0;
-  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
-  if (use_tma) {
-    if (threadIdx.x == 0) {
-      mbar_init(mbar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
+  if (kGather || !tile_box<T>(a, P.A, ox, oy, ylast, oz, cap, b)) {
+    tile_parts<T, TY, kLabels, kNearest, kPh>(a, tiles_z, cap, kGather);
+    return;
   }
-  const bool tma = use_tma && tma_box<T>(P, ox, oy, oz, b);
-  if (!tma) {
-    // analytic boxes for whole tiles only: an exact per-tile box (tile_box) of a
-    // volume whose worst-case box does not fit usually still fits
-    if (!kGather && P.cp_rows == TY && cp_sane(P, ox, oy, oz)) {
-      if (threadIdx.x == 0) {
-        atomicAdd(&g_cube_tiles[0], 1ull);
-        if (P.cp_rows < TY) atomicAdd(&g_cube_tiles[3], 1ull);
-      }
-      cp_tile<T, TY, kLabels, kNearest, kPh>(a, P, vi, ox, oy, oz, ylast);
-      return;
-    }
-    if (kGather || !tile_box<T>(a, P.A, ox, oy, ylast, oz, cap, b)) {
-      tile_parts<T, TY, kLabels, kNearest, kPh>(a, tiles_z, cap, kGather);
-      return;
-    }
-  }
-  if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[tma ? 2 : 0], 1ull);
-  uint32_t slbl;
-#ifdef W3D_DBG_NOSTAGE
-  if (tma) {
-    slbl = simg + ((InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D) + 127u) & ~127u);
-  } else {
-    slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
-  }
-  if (false) {
-#else
-  if (tma) {
+  if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[0], 1ull);
+  const uint32_t slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
+#ifndef W3D_DBG_NOSTAGE
+  stage<T, kLabels>(a, vol_in<T>(P), kLabels ? vol_lbl(P) : nullptr, b, simg, slbl);
 #endif
-    slbl = simg + ((InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D) + 127u) & ~127u);
-#ifdef W3D_DEBUG_TMA
-    if (threadIdx.x == 0 && blockIdx.x < 3)
-      printf("blk %d vol %d box o=(%d %d %d) WHD=(%d %d %d) Wl=%d P=%d Pl=%d simg=%u slbl=%u\n",
-             blockIdx.x, vi, b.bx, b.by, b.bz, b.W, b.H, b.D, b.Wl, b.P, b.Pl, simg, slbl);
-#endif
-    if (threadIdx.x == 0) {
-      mbar_expect_tx(mbar, InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D) +
-                               (kLabels ? static_cast<uint32_t>(b.Pl * b.D) : 0u));
-      tma_load_3d(simg, &a.tm[2 * vi], b.bx, b.by, b.bz, mbar);
-      if (kLabels) tma_load_3d(slbl, &a.tm[2 * vi + 1], b.bxl, b.by, b.bz, mbar);
-    }
-  } else {
-    slbl = simg + InT<T>::kBytes * static_cast<uint32_t>(b.P * b.D);
-    stage<T, kLabels>(a, vol_in<T>(P), kLabels ? vol_lbl(P) : nullptr, b, simg, slbl);
-  }
   const Vol V = load_vol(P);
   const int lane = threadIdx.x & 31;
   const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
@@ -1009,35 +950,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
   // the first Philox block overlaps the copies in flight
   const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, oy) : make_float4(0, 0, 0, 0);
   const View v = make_view<T>(a, b, simg, slbl);
-#ifdef W3D_DBG_NOSTAGE
-#ifndef W3D_DBG_NOBAR
+  cp_async_wait_all();
   __syncthreads();
-#endif
-  if (false) {
-#else
-  if (tma) {
-#endif
-    mbar_wait(mbar, 0);
-    const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
-                        b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
-    const bool fi = a.fill != 0.0f, fl = kLabels && a.label_fill != 0u;  // TMA fills 0
-    if (!inside && (fi || fl)) {
-      tma_fixup<T, kLabels>(a, b, simg, slbl, fi, fl);
-      __syncthreads();
-    }
-  } else {
-    cp_async_wait_all();
-    __syncthreads();
-  }
   if (!live) return;
 #ifdef W3D_DBG_NOCOMPUTE
   if (n.x == 12345.0f) a.out[X] = n.y;  // keep the first Philox block alive
   return;
 #endif
   if (b.clamp)
-    column_rows<T, kLabels, kNearest, kPh, true, true>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
+    column_rows<T, kLabels, kNearest, kPh, true, true, true>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
   else
-    column_rows<T, kLabels, kNearest, kPh, true, false>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
+    column_rows<T, kLabels, kNearest, kPh, true, false, true>(a, P, V, v, vi, X, Z, oy, TY / 4, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -1116,10 +1039,8 @@ static cudaError_t launch_typed(const WarpArgs& a, bool gather_only, cudaStream_
 // int16 input a fill that int16 represents (the staged box holds fill).
 bool cube_supported(const WarpArgs& a) {
   const int chunk = a.in16 ? 8 : 4;
-  const void* in = a.in16 ? static_cast<const void*>(a.in16) : static_cast<const void*>(a.in);
   const bool fill_ok = !a.in16 || (a.fill == std::nearbyint(a.fill) && a.fill >= -32768.0f &&
                                    a.fill <= 32767.0f);
-  (void)in;
   return (a.nx % chunk == 0) && a.in_aligned && fill_ok && a.nx < (1 << 21) &&
          a.ny < (1 << 21) && a.nz < (1 << 21);
 }
@@ -1133,70 +1054,21 @@ cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s) {
   return e;
 }
 
-bool cube_tma_supported(const WarpArgs& a) {
-  // 16 B aligned global strides and volume bases for the image (and labels)
-  bool lbl = a.in_lbl == nullptr || a.nx % 16 == 0;  // 16 B label rows
-  for (int i = 0; lbl && a.in_lbl && i < a.nvol; ++i) lbl = a.vol[i].lbl_addr % 16 == 0;
-  return cube_supported(a) && lbl && a.interp == W3D_INTERP_LINEAR;
-}
+// TMA image boxes: 16 B aligned global strides and volume bases (the staged
+// layout), one tensor map per volume in the first kTmaVolPerLaunch volumes.
+bool cube_tma_supported(const WarpArgs& a) { return cube_supported(a); }
 
-// TMA box dims of one volume: the footprint extent of a full tile, ext_k =
-// sum_j |A_kj| (T_j - 1) input voxels, plus the trilinear +1 corner, the floor
-// offsets and a rounding margin; rows of 16 B multiples with 16 B aligned
-// origins (image: 4 float / 8 int16 elements, labels 16); rows per plane padded
-// so the plane pitch spreads the two half-warps over the banks
-// (tools/model_tiles.py).  box_w = 0 when the box exceeds the buffer.
-void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes, const int out[3]) {
-  using namespace cube;
-  const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
-  int d[3];
-  P.box_w = P.box_h = P.box_d = P.box_wl = 0;
-  for (int k = 0; k < 3; ++k) {
-    double ext = 0.0, mlo = 0.0, mag = std::fabs(double(A[4 * k + 3]));
-    for (int j = 0; j < 3; ++j) {
-      const double a = double(A[4 * k + j]) * span[j];
-      ext += std::fabs(a);
-      mlo += a < 0.0 ? a : 0.0;
-      mag += std::fabs(double(A[4 * k + j])) * (out[j] + 16.0);  // any voxel of any tile
-    }
-    // fp32 evaluation of p (3 roundings each) and of the origin term: a few
-    // ulp(|p|); the margin covers 16 ulp
-    const double margin = 16.0 * mag * 0x1.0p-24 + 1e-3;
-    if (ext > 200.0) return;
-    P.box_mlo[k] = static_cast<float>(mlo - margin);
-    // origin >= p_min - margin - 1, needed up to floor(p_max) + 1 <= p_min + ext + margin + 1
-    d[k] = static_cast<int>(std::floor(ext + 2.0 * margin)) + 4;
-  }
-  // + alignment slack of the 16 B aligned inner origins (an unaligned origin
-  // faults: measured)
-  const int al = 16 / elem_bytes;
-  int W = (d[0] + al - 1 + al - 1) & ~(al - 1), H = d[1], D = d[2];
-  const int Wl = (d[0] + 15 + 15) & ~15;
-  auto bytes = [&](int h) {
-    return ((int64_t(elem_bytes) * W * h * D + 127) & ~int64_t(127)) +
-           (labels ? int64_t(Wl) * h * D : 0);
-  };
-  for (int h = H; h < H + 8; ++h) {  // bank-spreading plane pitch, if it still fits
-    const int res = (W * h) & 31;
-    if ((res == 20 || res == 24 || res == 16 || res == 12) && bytes(h) <= int64_t(kCapVox) * 5) {
-      H = h;
-      break;
-    }
-  }
-  if (W > 256 || H > 256 || D > 256) return;
-  if (bytes(H) > int64_t(kCapVox) * 5) return;
-  P.box_w = static_cast<uint16_t>(W);
-  P.box_h = static_cast<uint16_t>(H);
-  P.box_d = static_cast<uint16_t>(D);
-  P.box_wl = static_cast<uint16_t>(Wl);
-}
-
-// cp.async staging box of one volume (and box_mlo, shared with the TMA path):
-// the footprint of a 16 x r x 16 part has extent ext_k = sum_j |A_kj| span_j;
-// from the origin floor(p0 + box_mlo) the part needs at most
-// floor(ext_k + 2 margin) + 3 elements per axis (floor of the lower bound, the
-// +1 trilinear corner, rounding inside the margin), plus chunk - 1 in x for the
-// 16 B aligned row start.  r = kTY, kTY/2, kTY/4: the first that fits.
+// Staging box of one volume's tiles (TMA image box and cp.async boxes) and its
+// origin offsets: the footprint of a 16 x kTY x 16 tile has extent
+// ext_k = sum_j |A_kj| span_j; from the origin floor(p0 + box_mlo) the tile
+// needs at most floor(ext_k + 2 margin) + 3 elements per axis (floor of the
+// lower bound, the +1 trilinear corner, rounding inside the margin; the margin
+// covers 16 ulp of the largest |p| of any tile voxel), plus chunk - 1 in x for
+// the 16 B aligned row start.  Rows per plane padded (and the row widened by
+// one chunk when no padding works) so the plane pitch spreads the two
+// half-warps over the banks (tools/model_tiles.py); cp_p = cp_w * cp_h, so the
+// TMA box (cp_w, cp_h, cp_d) lands with the same pitches.  cp_rows = kTY when
+// the box fits the buffer, else 0 (per-tile exact boxes, parts, gathers).
 void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3]) {
   using namespace cube;
   const int kC = 16 / elem_bytes;
@@ -1204,42 +1076,51 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3])
   P.cp_w = P.cp_h = P.cp_d = P.cp_rows = 0;
   P.cp_p = 0;
   P.cp_w_bytes = P.cp_p_bytes = 0;
-  double margin[3], mlo[3], ext_xz[3], ay[3];
+  P.box_w = P.box_h = P.box_d = 0;
+  int d[3];
+  const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
+  bool ok = true;
   for (int k = 0; k < 3; ++k) {
-    double mag = std::fabs(double(A[4 * k + 3]));
-    for (int j = 0; j < 3; ++j) mag += std::fabs(double(A[4 * k + j])) * (out[j] + 16.0);
-    margin[k] = 16.0 * mag * 0x1.0p-24 + 1e-3;
-    const double ax = double(A[4 * k]) * (TX - 1.0), az = double(A[4 * k + 2]) * (TZ - 1.0);
-    ay[k] = double(A[4 * k + 1]);
-    ext_xz[k] = std::fabs(ax) + std::fabs(az);
-    mlo[k] = (ax < 0 ? ax : 0.0) + (az < 0 ? az : 0.0) + (ay[k] < 0 ? ay[k] * (kTY - 1.0) : 0.0);
-    P.box_mlo[k] = static_cast<float>(mlo[k] - margin[k]);
-  }
-  for (int rows = kTY; rows >= 4 && rows >= kTY / 4; rows /= 2) {
-    int d[3];
-    bool ok = true;
-    for (int k = 0; k < 3; ++k) {
-      const double ext = ext_xz[k] + std::fabs(ay[k]) * (rows - 1.0);
-      if (ext > 200.0) ok = false;
-      d[k] = ok ? static_cast<int>(std::floor(ext + 2.0 * margin[k])) + 3 : 0;
+    double mag = std::fabs(double(A[4 * k + 3])), ext = 0.0, mlo = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      const double a = double(A[4 * k + j]) * span[j];
+      ext += std::fabs(a);
+      mlo += a < 0.0 ? a : 0.0;
+      mag += std::fabs(double(A[4 * k + j])) * (out[j] + 16.0);  // any voxel of any tile
     }
-    if (!ok) return;
-    const int W = (d[0] + kC - 1 + kC - 1) & ~(kC - 1), H = d[1], D = d[2];
-    const int wh = W * H;
-    const int res = kC == 4 ? kPlaneRes : 16;
-    int Pp = wh + ((res - wh) & 31);
-    if (int64_t(Pp) * D > cap) Pp = wh;
-    if (int64_t(Pp) * D <= cap && W <= 4 * THREADS) {
-      P.cp_w = static_cast<uint16_t>(W);
-      P.cp_h = static_cast<uint16_t>(H);
-      P.cp_d = static_cast<uint16_t>(D);
-      P.cp_p = Pp;
-      P.cp_rows = static_cast<uint16_t>(rows);
-      P.cp_w_bytes = static_cast<uint16_t>(W * elem_bytes);
-      P.cp_p_bytes = static_cast<uint16_t>(Pp * elem_bytes);
-      return;
-    }
+    const double margin = 16.0 * mag * 0x1.0p-24 + 1e-3;
+    P.box_mlo[k] = static_cast<float>(mlo - margin);
+    if (ext > 200.0) ok = false;
+    d[k] = ok ? static_cast<int>(std::floor(ext + 2.0 * margin)) + 3 : 0;
   }
+  if (!ok) return;
+  const int W0 = (d[0] + kC - 1 + kC - 1) & ~(kC - 1), H0 = d[1], D = d[2];
+  int best_w = 0, best_h = 0;
+  int64_t best = INT64_MAX;
+  for (int W = W0; W <= W0 + kC; W += kC)
+    for (int h = H0; h < H0 + 8; ++h) {
+      const int res = (W * h) & 31;
+      const bool spread = elem_bytes == 4 ? (res == 12 || res == 16 || res == 20 || res == 24)
+                                          : res == 16;
+      if (spread && int64_t(W) * h < best) {
+        best = int64_t(W) * h;
+        best_w = W;
+        best_h = h;
+      }
+    }
+  if (best_w == 0 || int64_t(best_w) * best_h * D > cap) {  // unpadded, if that fits
+    best_w = W0;
+    best_h = H0;
+  }
+  const int64_t Pp = int64_t(best_w) * best_h;
+  if (Pp * D > cap || best_w > 4 * THREADS || best_w > 256 || best_h > 256 || D > 256) return;
+  P.cp_w = static_cast<uint16_t>(best_w);
+  P.cp_h = static_cast<uint16_t>(best_h);
+  P.cp_d = static_cast<uint16_t>(D);
+  P.cp_p = static_cast<int32_t>(Pp);
+  P.cp_rows = static_cast<uint16_t>(kTY);
+  P.cp_w_bytes = static_cast<uint16_t>(best_w * elem_bytes);
+  P.cp_p_bytes = static_cast<uint16_t>(Pp * elem_bytes);
 }
 
 cudaError_t read_cube_stats(unsigned long long out[4]) {

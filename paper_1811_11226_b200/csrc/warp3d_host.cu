@@ -225,34 +225,28 @@ struct MapKey {
   }
 };
 
-// Tensor maps of the launch chunk in `args` (volumes whose box fits); returns
-// false (and clears every box) when encoding is unavailable.
-static bool prepare_tma(WarpArgs& args, const float* const* affines) {
-  static thread_local MapKey key_img[kTmaVolPerLaunch], key_lbl[kTmaVolPerLaunch];
-  const bool labels = args.in_lbl != nullptr;
+// Image tensor maps of the launch chunk in `args` (volumes whose staging box
+// fits, cube_cp_box); returns false (and clears every box) when encoding is
+// unavailable.
+static bool prepare_tma(WarpArgs& args) {
+  static thread_local MapKey key_img[kTmaVolPerLaunch];
   bool ok = get_encode() != nullptr;
-  for (int32_t i = 0; i < args.nvol && ok; ++i) {
+  const int eb = args.in16 ? 2 : 4;
+  for (int32_t i = 0; i < args.nvol && i < kTmaVolPerLaunch && ok; ++i) {
     VolDev& P = args.vol[i];
-    if (i >= kTmaVolPerLaunch) break;
-    const int eb = args.in16 ? 2 : 4;
-    const int out[3] = {args.mx, args.my, args.mz};
-    cube_tma_box(affines[i], P, labels, eb, out);
-    if (!P.box_w) continue;
+    P.box_w = P.box_h = P.box_d = 0;
+    if (P.cp_rows == 0) continue;
     const void* base = reinterpret_cast<const void*>(P.in_addr);
-    MapKey ki{base, args.nx, args.ny, args.nz, P.box_w, P.box_h, P.box_d, eb};
+    MapKey ki{base, args.nx, args.ny, args.nz, P.cp_w, P.cp_h, P.cp_d, eb};
     if (!(ki == key_img[i])) {
       key_img[i] = MapKey();
-      ok = encode_3d(&args.tm[2 * i], eb, ki.base, args, ki.bw, ki.bh, ki.bd);
+      ok = encode_3d(&args.tm[i], eb, ki.base, args, ki.bw, ki.bh, ki.bd);
       if (ok) key_img[i] = ki;
     }
-    if (ok && labels) {
-      MapKey kl{reinterpret_cast<const void*>(P.lbl_addr), args.nx, args.ny, args.nz, P.box_wl,
-                P.box_h, P.box_d, 1};
-      if (!(kl == key_lbl[i])) {
-        key_lbl[i] = MapKey();
-        ok = encode_3d(&args.tm[2 * i + 1], 1, kl.base, args, kl.bw, kl.bh, kl.bd);
-        if (ok) key_lbl[i] = kl;
-      }
+    if (ok) {
+      P.box_w = P.cp_w;
+      P.box_h = P.cp_h;
+      P.box_d = P.cp_d;
     }
   }
   if (!ok)
@@ -321,7 +315,7 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
     }
     args.use_tma = 0;
     if (want_tma && cube_tma_supported(args))
-      args.use_tma = prepare_tma(args, affines + v0) ? 1 : 0;
+      args.use_tma = prepare_tma(args) ? 1 : 0;
     // AUTO / STAGED: the staged cube kernel (it gathers by itself when the
     // layout does not allow 16 B chunks); GATHER: every tile gathered.
     const cudaError_t e = launch_cube(args, variant == W3D_KERNEL_GATHER, stream);

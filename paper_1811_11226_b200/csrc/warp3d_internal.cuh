@@ -41,10 +41,9 @@ struct alignas(16) VolDev {
   int32_t cp_p;
   uint16_t cp_w_bytes, cp_p_bytes;  // cp_w, cp_p in bytes of the image element type
   int32_t occ_lo, occ_hi;  // occluded output z in [occ_lo, occ_hi]
-  // TMA box of this volume's tiles (host-computed from A, warp3d_cube.cu): image
-  // box (box_w, box_h, box_d) floats, label box (box_wl, box_h, box_d) bytes;
-  // box_w == 0: no TMA for this volume (cp.async staging)
-  uint16_t box_w, box_h, box_d, box_wl;
+  // TMA image box of this volume's tiles (= cp_w, cp_h, cp_d when tm[vi] holds
+  // its tensor map; box_w == 0: the image box goes by cp.async)
+  uint16_t box_w, box_h, box_d, _box_pad;
   uint32_t rk0[10], rk1[10];  // Philox round keys k + r * (W0, W1), host-precomputed
   uint32_t ph_K0, ph_K1, ph_K2, ph_U3;  // PhiloxPrefix (philox.cuh), host-precomputed
   // box origin of a full tile (TMA and cp.async): floor(p(tile origin voxel) +
@@ -61,12 +60,12 @@ constexpr int kMaxVolPerLaunch = 112;  // sizeof(WarpArgs) < 32764 B of kernel p
 // Volumes per launch when TMA staging is used: the tensor maps must lie in the
 // first 4 KB of the kernel parameters (measured: TMA on a __grid_constant__
 // map at a larger parameter offset faults).
-constexpr int kTmaVolPerLaunch = 16;
+constexpr int kTmaVolPerLaunch = 32;
 
 struct alignas(64) WarpArgs {
-  // per volume i: tm[2i] 3D (nx, ny, nz) float32 box (box_w, box_h, box_d),
-  //               tm[2i+1] 3D uint8 box (box_wl, box_h, box_d)
-  CUtensorMap tm[2 * kTmaVolPerLaunch];
+  // per volume i: tm[i] 3D (nx, ny, nz) image map (float32 or int16), box
+  // (box_w, box_h, box_d)
+  CUtensorMap tm[kTmaVolPerLaunch];
   const float* in;        // non-null: float32 image input (per-volume addresses in vol[i])
   const int16_t* in16;    // non-null: int16 HU image input (NEXT-4)
   const uint8_t* in_lbl;  // may be null
@@ -96,10 +95,9 @@ static_assert(sizeof(WarpArgs) <= 32764, "kernel parameter space");
 // warp3d_cube.cu (the warp): cube_supported() = the staged layout requirements.
 bool cube_supported(const WarpArgs& a);
 bool cube_tma_supported(const WarpArgs& a);
-// TMA box dims for one volume's tiles (0 when the box exceeds the buffer)
-// (out = output dims x, y, z: the rounding margin scales with the largest |p|)
-void cube_tma_box(const float A[12], VolDev& P, bool labels, int elem_bytes, const int out[3]);
-// box origin offsets and cp.async staging box of one volume's tiles
+// staging box (TMA image box and cp.async boxes) of one volume's tiles and its
+// origin offsets (out = output dims x, y, z: the rounding margin scales with
+// the largest |p|)
 void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3]);
 cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s);
 cudaError_t read_cube_stats(unsigned long long out[4]);
