@@ -47,13 +47,22 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
   out[(static_cast<int64_t>(z) * ny + y) * nx + x] = acc;
 }
 
-// Fused separable smoothing of one 32 x 8 x 8 output tile (radius <= kFuseR per
-// axis): the input tile + halo (edge voxels replicated) is read once into shared
-// memory, then the x, y and z passes run out of shared memory in the same
-// order and fp32 arithmetic as smooth_axis_kernel (bit-identical results), and
-// only the output tile is written back: one HBM read + one write per voxel
-// instead of three of each.
-constexpr int kFuseR = 8, FX = 32, FY = 8, FZ = 8;
+// Fused separable smoothing, z-marching (2.5D): a CTA owns a 32 x 8 NYT column of
+// outputs and walks MZ output planes along z.  Each input plane's tile
+// plus its x/y halo (edge voxels replicated by clamped coordinates) streams
+// into a ring of shared-memory stages by cp.async, kStages - 1 planes ahead of
+// the compute; per plane the x pass runs over the halo rows (shared memory ->
+// shared memory), the y pass gives each thread its (x, y) value, and the z pass
+// runs in registers over a window of the last 2 RM + 1 planes.  Same passes,
+// order and fp32 FMAs as smooth_axis_kernel (bit-identical results); HBM sees
+// one read (+ the z halo of 2 RM planes per MZ) and one write per voxel.
+#ifndef W3D_SM_STAGES
+#define W3D_SM_STAGES 6
+#endif
+#ifndef W3D_SM_MZ
+#define W3D_SM_MZ 64
+#endif
+constexpr int kFuseR = 8, MX = 32, MZ = W3D_SM_MZ, kStages = W3D_SM_STAGES;
 struct Taps3 {
   float wx[2 * kFuseR + 1], wy[2 * kFuseR + 1], wz[2 * kFuseR + 1];
   int32_t rx, ry, rz;
@@ -61,20 +70,34 @@ struct Taps3 {
 
 extern __shared__ float fuse_smem[];
 
+__device__ __forceinline__ void cp_async4(float* s, const float* g) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* s, const float* g) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // RM: compile-time tap radius >= every axis' radius; an axis with a smaller
 // radius has its weights centred and zero-padded (fma(0, v, acc) = acc exactly,
-// so the result equals the per-axis passes bit for bit).
-template <int RM>
+// so the result equals the per-axis passes bit for bit).  NYT: output rows per
+// thread (warp w owns rows NYT w .. NYT w + NYT - 1 of the MY = 8 NYT rows).
+template <int RM, int NYT>
 __global__ void __launch_bounds__(256) smooth_fused_kernel(const float* __restrict__ in,
                                                            float* __restrict__ out, int nx, int ny,
                                                            int nz, const __grid_constant__ Taps3 t) {
-  const int ox = static_cast<int>(blockIdx.x) * FX, oy = static_cast<int>(blockIdx.y) * FY,
-            oz = static_cast<int>(blockIdx.z) * FZ;
-  // halo RM on every axis (zero-weight taps read real, finite, edge-replicated data)
-  constexpr int AX = FX + 2 * RM, AY = FY + 2 * RM, AZ = FZ + 2 * RM;
-  float* A = fuse_smem;            // [AZ][AY][AX]  input + halo; later the y-pass result
-  float* B = fuse_smem + AX * AY * AZ;  // [AZ][AY][FX] x-pass result
-  // taps centred in 2 RM + 1 slots, zero-padded (registers)
+  constexpr int MYT = 8 * NYT;
+  // plane tile: x range [ox - XP, ox + 32 + XP) (16 B aligned chunks), y halo RM
+  constexpr int XP = RM <= 4 ? 4 : 8;
+  constexpr int AX = MX + 2 * XP, AY = MYT + 2 * RM, PL = AX * AY;
+  constexpr int CX = AX / 4, PC = CX * AY;   // 16 B chunks per row / plane
+  constexpr int kPer = (PL + 255) / 256;     // elements per thread (edge tiles)
+  constexpr int kPerC = (PC + 255) / 256;    // chunks per thread (interior tiles)
+  float* X = fuse_smem + kStages * PL;       // [AY][MX] x-pass result of the current plane
   float wx[2 * RM + 1], wy[2 * RM + 1], wz[2 * RM + 1];
 #pragma unroll
   for (int k = 0; k <= 2 * RM; ++k) {
@@ -82,53 +105,99 @@ __global__ void __launch_bounds__(256) smooth_fused_kernel(const float* __restri
     wy[k] = (k >= RM - t.ry && k <= RM + t.ry) ? t.wy[k - (RM - t.ry)] : 0.0f;
     wz[k] = (k >= RM - t.rz && k <= RM + t.rz) ? t.wz[k - (RM - t.rz)] : 0.0f;
   }
-  // lane = x (32 = FX), warp w walks rows (y, z) w, w + 8, ...: no per-element division
+  const int ox = static_cast<int>(blockIdx.x) * MX, oy = static_cast<int>(blockIdx.y) * MYT,
+            oz = static_cast<int>(blockIdx.z) * MZ;
   const int lx = static_cast<int>(threadIdx.x & 31), w = static_cast<int>(threadIdx.x >> 5);
-  const int gx0 = min(max(ox + lx - RM, 0), nx - 1);
-  const int gx1 = min(max(ox + lx + 32 - RM, 0), nx - 1);
-  const bool x1 = lx + 32 < AX;
-  {
-    int y = w, z = 0;
-    while (y >= AY) { y -= AY; ++z; }
-    for (int r = w; r < AY * AZ; r += 8) {
-      const int gy = min(max(oy + y - RM, 0), ny - 1), gz = min(max(oz + z - RM, 0), nz - 1);
-      const float* row = in + (static_cast<int64_t>(gz) * ny + gy) * nx;
-      float* arow = A + r * AX;
-      arow[lx] = __ldg(row + gx0);
-      if (x1) arow[lx + 32] = __ldg(row + gx1);
-      y += 8;
-      while (y >= AY) { y -= AY; ++z; }
+  const int nin = min(MZ, nz - oz) + 2 * RM;  // input planes oz - RM + i, i < nin
+  // interior in x (whole aligned chunks inside the rows): 16 B copies, else 4 B
+  // copies of clamped coordinates (edge replication)
+  const bool chunked = ox - XP >= 0 && ox + MX + XP <= nx && (nx & 3) == 0 &&
+                       (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  int soff[kPer];
+  uint32_t goff[kPer];
+  if (chunked) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int e = static_cast<int>(threadIdx.x) + 256 * j;  // chunk index
+      const int r = e / CX, c = e - r * CX;
+      const int gy = min(max(oy - RM + r, 0), ny - 1);
+      soff[j] = (j < kPerC && e < PC) ? r * AX + 4 * c : -1;
+      goff[j] = static_cast<uint32_t>(gy) * static_cast<uint32_t>(nx) +
+                static_cast<uint32_t>(ox - XP + 4 * c);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int e = static_cast<int>(threadIdx.x) + 256 * j;
+      const int r = e / AX, c = e - r * AX;
+      const int gx = min(max(ox - XP + c, 0), nx - 1), gy = min(max(oy - RM + r, 0), ny - 1);
+      soff[j] = e < PL ? e : -1;
+      goff[j] = static_cast<uint32_t>(gy) * static_cast<uint32_t>(nx) + static_cast<uint32_t>(gx);
     }
   }
-  __syncthreads();
-  for (int r = w; r < AY * AZ; r += 8) {  // x pass: B[z][y][x], rows of A
-    const float* a = A + r * AX + lx;
-    float acc = 0.0f;
+  const size_t plane = static_cast<size_t>(nx) * static_cast<size_t>(ny);
+  auto load_plane = [&](int i) {
+    const int zc = min(max(oz - RM + i, 0), nz - 1);
+    const float* src = in + static_cast<size_t>(zc) * plane;
+    float* dst = fuse_smem + (i % kStages) * PL;
+    if (chunked) {
 #pragma unroll
-    for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], a[k], acc);
-    B[r * FX + lx] = acc;
+      for (int j = 0; j < kPerC; ++j)
+        if (soff[j] >= 0) cp_async16(dst + soff[j], src + goff[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j)
+        if (soff[j] >= 0) cp_async4(dst + soff[j], src + goff[j]);
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < kStages - 1; ++i) {
+    if (i < nin) load_plane(i);
+    cp_async_commit();
   }
-  __syncthreads();
-  float* C = A;  // [AZ][FY][FX] y-pass result
-  for (int r = w; r < FY * AZ; r += 8) {
-    const int z = r / FY, y = r - z * FY;
-    const float* b = B + (z * AY + y) * FX + lx;
-    float acc = 0.0f;
+  const int gx = ox + lx, gy0 = oy + NYT * w;
+  float* po = out + (static_cast<size_t>(oz) * ny + gy0) * nx + gx;
+  float ring[NYT][2 * RM + 1];
 #pragma unroll
-    for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wy[k], b[k * FX], acc);
-    C[r * FX + lx] = acc;
-  }
-  __syncthreads();
-  const int gx = ox + lx;
-  for (int r = w; r < FY * FZ; r += 8) {  // z pass + store
-    const int z = r / FY, y = r - z * FY;
-    const int gy = oy + y, gz = oz + z;
-    if (gx >= nx || gy >= ny || gz >= nz) continue;
-    const float* c = C + r * FX + lx;
-    float acc = 0.0f;
+  for (int q = 0; q < NYT; ++q)
 #pragma unroll
-    for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wz[k], c[k * FX * FY], acc);
-    out[(static_cast<int64_t>(gz) * ny + gy) * nx + gx] = acc;
+    for (int k = 0; k <= 2 * RM; ++k) ring[q][k] = 0.0f;
+  for (int i = 0; i < nin; ++i) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // plane i landed; X free (previous y pass done)
+    const float* A = fuse_smem + (i % kStages) * PL;
+    for (int r = w; r < AY; r += 8) {  // x pass over the halo rows
+      const float* a = A + r * AX + lx + (XP - RM);
+      float acc = 0.0f;
+#pragma unroll
+      for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], a[k], acc);
+      X[r * MX + lx] = acc;
+    }
+    if (i + kStages - 1 < nin) load_plane(i + kStages - 1);  // into plane i-1's stage
+    cp_async_commit();
+    __syncthreads();
+    float xv[NYT + 2 * RM];  // y pass: the thread's rows share their x-pass inputs
+#pragma unroll
+    for (int k = 0; k < NYT + 2 * RM; ++k) xv[k] = X[(NYT * w + k) * MX + lx];
+#pragma unroll
+    for (int q = 0; q < NYT; ++q) {
+      float yv = 0.0f;
+#pragma unroll
+      for (int k = 0; k <= 2 * RM; ++k) yv = __fmaf_rn(wy[k], xv[q + k], yv);
+#pragma unroll
+      for (int k = 0; k < 2 * RM; ++k) ring[q][k] = ring[q][k + 1];
+      ring[q][2 * RM] = yv;
+    }
+    if (i >= 2 * RM) {  // z pass: output plane oz + i - 2 RM complete
+#pragma unroll
+      for (int q = 0; q < NYT; ++q) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wz[k], ring[q][k], acc);
+        if (gx < nx && gy0 + q < ny) po[static_cast<size_t>(q) * nx] = acc;
+      }
+      po += plane;
+    }
   }
 }
 
@@ -177,25 +246,25 @@ cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int
   make_taps(sigma[0], t.rx, t.wx);
   make_taps(sigma[1], t.ry, t.wy);
   make_taps(sigma[2], t.rz, t.wz);
-  const dim3 grid(static_cast<unsigned>((nx + FX - 1) / FX), static_cast<unsigned>((ny + FY - 1) / FY),
-                  static_cast<unsigned>((nz + FZ - 1) / FZ));
   const int rmax = max(t.rx, max(t.ry, t.rz));
-  const int RM = rmax <= 4 ? (rmax < 1 ? 1 : rmax) : (rmax <= 6 ? 6 : 8);
-  const int AX = FX + 2 * RM, AY = FY + 2 * RM, AZ = FZ + 2 * RM;
-  const size_t smem = sizeof(float) * (size_t(AX) * AY * AZ + size_t(FX) * AY * AZ);
   cudaError_t e = cudaSuccess;
-  auto go = [&](auto kernel) {
+  auto go = [&](auto kernel, int RM, int nyt) {
+    const int my = 8 * nyt, xp = RM <= 4 ? 4 : 8;
+    const size_t smem =
+        sizeof(float) * (size_t(kStages) * (MX + 2 * xp) * (my + 2 * RM) + size_t(my + 2 * RM) * MX);
     if (smem > 48 * 1024)
       e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem));
+    const dim3 grid(static_cast<unsigned>((nx + MX - 1) / MX), static_cast<unsigned>((ny + my - 1) / my),
+                    static_cast<unsigned>((nz + MZ - 1) / MZ));
     if (e == cudaSuccess) kernel<<<grid, 256, smem, s>>>(in, out, nx, ny, nz, t);
   };
-  if (rmax <= 1) go(smooth_fused_kernel<1>);
-  else if (rmax <= 2) go(smooth_fused_kernel<2>);
-  else if (rmax <= 3) go(smooth_fused_kernel<3>);
-  else if (rmax <= 4) go(smooth_fused_kernel<4>);
-  else if (rmax <= 6) go(smooth_fused_kernel<6>);
-  else go(smooth_fused_kernel<8>);
+  if (rmax <= 1) go(smooth_fused_kernel<1, 4>, 1, 4);
+  else if (rmax <= 2) go(smooth_fused_kernel<2, 4>, 2, 4);
+  else if (rmax <= 3) go(smooth_fused_kernel<3, 4>, 3, 4);
+  else if (rmax <= 4) go(smooth_fused_kernel<4, 2>, 4, 2);
+  else if (rmax <= 6) go(smooth_fused_kernel<6, 1>, 6, 1);
+  else go(smooth_fused_kernel<8, 1>, 8, 1);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -579,3 +579,29 @@ def test_volumes_of_different_dims_rejects_bad_input(W):
         W.warp3d_affine_batched_list([a, b], None, p, (8, 8, 8))   # mixed dtypes
     with pytest.raises(Exception):
         W.warp3d_affine_batched_list([a], None, p, (8, 8, 8))      # length mismatch
+
+
+@pytest.mark.parametrize("shape,sigma", [
+    ((70, 37, 45), (2.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0)),   # several z chunks, ragged x / y
+    ((130, 20, 33), (1.1, 0.0, 2.4)),                      # radius classes 4 / 8, sigma 0 axis
+    ((5, 9, 64), (0.3, 1.7, 0.9)),                         # fewer planes than the z halo
+])
+def test_fused_smoothing_equals_per_axis_passes_bitwise(W, shape, sigma, tmp_path):
+    """The z-marching fused lowpass keeps the per-axis passes' order and fp32 FMAs: equal
+    bit for bit to the three separate passes (W3D_SMOOTH_PASSES=1, another process)."""
+    import subprocess
+    import sys
+    img = synth.random_volume(shape, 11)[0].astype(np.float32)
+    src = tmp_path / "in.npy"
+    np.save(src, img)
+    script = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import paper_1811_11226_b200 as W\n"
+        "x = torch.from_numpy(np.load(%r)).cuda()\n"
+        "np.save(%r, W.warp3d_smooth3d(x, %r).cpu().numpy())\n"
+    ) % (os.getcwd(), str(src), str(tmp_path / "ref.npy"), tuple(sigma))
+    env = dict(os.environ, W3D_SMOOTH_PASSES="1")
+    subprocess.run([sys.executable, "-c", script], check=True, env=env, cwd=os.getcwd())
+    ref = np.load(tmp_path / "ref.npy")
+    got = W.warp3d_smooth3d(torch.from_numpy(img).cuda(), sigma).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
