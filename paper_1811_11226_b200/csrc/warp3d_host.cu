@@ -229,28 +229,47 @@ struct MapKey {
 // fits, cube_cp_box); returns false (and clears every box) when encoding is
 // unavailable.
 static bool prepare_tma(WarpArgs& args) {
-  static thread_local MapKey key_img[kTmaVolPerLaunch];
+  static thread_local MapKey key_img[kTmaVolPerLaunch], key_lbl[kTmaVolPerLaunch];
   bool ok = get_encode() != nullptr;
   const int eb = args.in16 ? 2 : 4;
+  // label maps: 16 B aligned rows and bases
+  static const bool no_tma_lbl = getenv("W3D_NO_TMA_LBL") && getenv("W3D_NO_TMA_LBL")[0] == '1';
+  bool lbl_ok = args.in_lbl != nullptr && args.nx % 16 == 0 && !no_tma_lbl;
+  for (int32_t i = 0; lbl_ok && i < args.nvol; ++i) lbl_ok = args.vol[i].lbl_addr % 16 == 0;
   for (int32_t i = 0; i < args.nvol && i < kTmaVolPerLaunch && ok; ++i) {
     VolDev& P = args.vol[i];
-    P.box_w = P.box_h = P.box_d = 0;
-    if (P.cp_rows == 0) continue;
+    P.box_w = P.box_d = 0;
+    if (P.cp_rows == 0) {
+      P.box_wl = 0;
+      continue;
+    }
     const void* base = reinterpret_cast<const void*>(P.in_addr);
     MapKey ki{base, args.nx, args.ny, args.nz, P.cp_w, P.cp_h, P.cp_d, eb};
     if (!(ki == key_img[i])) {
       key_img[i] = MapKey();
-      ok = encode_3d(&args.tm[i], eb, ki.base, args, ki.bw, ki.bh, ki.bd);
+      ok = encode_3d(&args.tm[2 * i], eb, ki.base, args, ki.bw, ki.bh, ki.bd);
       if (ok) key_img[i] = ki;
     }
     if (ok) {
       P.box_w = P.cp_w;
-      P.box_h = P.cp_h;
       P.box_d = P.cp_d;
+    }
+    if (ok && lbl_ok && P.box_wl != 0) {
+      MapKey kl{reinterpret_cast<const void*>(P.lbl_addr), args.nx, args.ny, args.nz, P.box_wl,
+                P.box_h, P.cp_d, 1};
+      bool lok = true;
+      if (!(kl == key_lbl[i])) {
+        key_lbl[i] = MapKey();
+        lok = encode_3d(&args.tm[2 * i + 1], 1, kl.base, args, kl.bw, kl.bh, kl.bd);
+        if (lok) key_lbl[i] = kl;
+      }
+      if (!lok) P.box_wl = 0;
+    } else {
+      P.box_wl = 0;
     }
   }
   if (!ok)
-    for (int32_t i = 0; i < args.nvol; ++i) args.vol[i].box_w = 0;
+    for (int32_t i = 0; i < args.nvol; ++i) args.vol[i].box_w = args.vol[i].box_wl = 0;
   return ok;
 }
 

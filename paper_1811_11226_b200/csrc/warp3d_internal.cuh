@@ -41,9 +41,10 @@ struct alignas(16) VolDev {
   int32_t cp_p;
   uint16_t cp_w_bytes, cp_p_bytes;  // cp_w, cp_p in bytes of the image element type
   int32_t occ_lo, occ_hi;  // occluded output z in [occ_lo, occ_hi]
-  // TMA image box of this volume's tiles (= cp_w, cp_h, cp_d when tm[vi] holds
-  // its tensor map; box_w == 0: the image box goes by cp.async)
-  uint16_t box_w, box_h, box_d, _box_pad;
+  // TMA boxes of this volume's tiles: box_w != 0 when tm[2 vi] holds the image
+  // map (box cp_w x cp_h x cp_d); box_wl != 0 when tm[2 vi + 1] holds the label
+  // map (box box_wl x box_h x cp_d bytes), else the labels go by cp.async
+  uint16_t box_w, box_h, box_d, box_wl;
   uint32_t rk0[10], rk1[10];  // Philox round keys k + r * (W0, W1), host-precomputed
   uint32_t ph_K0, ph_K1, ph_K2, ph_U3;  // PhiloxPrefix (philox.cuh), host-precomputed
   // box origin of a full tile (TMA and cp.async): floor(p(tile origin voxel) +
@@ -60,12 +61,12 @@ constexpr int kMaxVolPerLaunch = 112;  // sizeof(WarpArgs) < 32764 B of kernel p
 // Volumes per launch when TMA staging is used: the tensor maps must lie in the
 // first 4 KB of the kernel parameters (measured: TMA on a __grid_constant__
 // map at a larger parameter offset faults).
-constexpr int kTmaVolPerLaunch = 32;
+constexpr int kTmaVolPerLaunch = 16;
 
 struct alignas(64) WarpArgs {
-  // per volume i: tm[i] 3D (nx, ny, nz) image map (float32 or int16), box
-  // (box_w, box_h, box_d)
-  CUtensorMap tm[kTmaVolPerLaunch];
+  // per volume i: tm[2i] 3D (nx, ny, nz) image map (float32 or int16), box
+  // (cp_w, cp_h, cp_d); tm[2i+1] uint8 label map, box (box_wl, box_h, cp_d)
+  CUtensorMap tm[2 * kTmaVolPerLaunch];
   const float* in;        // non-null: float32 image input (per-volume addresses in vol[i])
   const int16_t* in16;    // non-null: int16 HU image input (NEXT-4)
   const uint8_t* in_lbl;  // may be null
