@@ -36,6 +36,9 @@ namespace cube {
 #ifndef W3D_TZ
 #define W3D_TZ 16
 #endif
+#ifndef W3D_PRE  // Philox blocks computed before the staging wait: 1, 2 or 4
+#define W3D_PRE 4
+#endif
 constexpr int TX = 16, TZ = W3D_TZ, THREADS = 16 * TZ;
 constexpr float kM = 12582912.0f;       // 1.5 * 2^23: rm(p + kM) = kM + floor(p), |p| < 2^22
 constexpr int32_t kMbits = 0x4B400000;  // bit pattern of kM
@@ -578,11 +581,16 @@ __device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
 // group's normals (computed while the staging copies were in flight); the next
 // group's Philox block is computed inside each iteration (independent chain).
 // ---------------------------------------------------------------------------
+// kPre: the first kPre (1, 2 or 4) groups' normals arrive precomputed (n, n1,
+// n2, n3; computed while the staging copies are in flight) and the loop
+// computes group g + kPre's block.
 template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
-          bool kSameLbl = false, bool kFull = false>
+          bool kSameLbl = false, bool kFull = false, int kPre = 1>
 __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
-                                            float4 n) {
+                                            float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
+                                            float4 n2 = make_float4(0.f, 0.f, 0.f, 0.f),
+                                            float4 n3 = make_float4(0.f, 0.f, 0.f, 0.f)) {
   const T* __restrict__ vin = vol_in<T>(P);
   const uint8_t* __restrict__ lin = kLabels ? vol_lbl(P) : nullptr;
   Vol V = V0;
@@ -627,7 +635,8 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
     const int y = y0 + 4 * g;
     if (!kFull && y >= my) break;
     float4 nn = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (noise && g + 1 < ng) nn = box_muller4(philox_block(q + mxu, pp, rk0, rk1));
+    if (noise && g + kPre < ng)
+      nn = box_muller4(philox_block(q + static_cast<uint32_t>(kPre) * mxu, pp, rk0, rk1));
     const float ns[4] = {n.x, n.y, n.z, n.w};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -659,7 +668,17 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
         pl = pl1 + row1;
       }
     }
-    n = nn;
+    if (kPre == 1) {
+      n = nn;
+    } else if (kPre == 2) {
+      n = n1;
+      n1 = nn;
+    } else {
+      n = n1;
+      n1 = n2;
+      n2 = n3;
+      n3 = nn;
+    }
     q += mxu;
   }
 }
@@ -921,6 +940,13 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     stage<T, kLabels>(a, vin, lin, b, simg, slbl);
   }
   const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, oy) : make_float4(0, 0, 0, 0);
+  // the training chain (kPhFull, launch-wide keys) computes kPre Philox blocks
+  // here, under the staging latency; the generic chain one (register budget)
+  constexpr int kPre = kPh == kPhFull ? W3D_PRE : 1;
+  const float4 z4 = make_float4(0, 0, 0, 0);
+  const float4 n1 = (kPre >= 2 && live) ? first_normals<kPh>(a, P, V, X, Z, oy + 4) : z4;
+  const float4 n2 = (kPre >= 4 && live) ? first_normals<kPh>(a, P, V, X, Z, oy + 8) : z4;
+  const float4 n3 = (kPre >= 4 && live) ? first_normals<kPh>(a, P, V, X, Z, oy + 12) : z4;
   View v = make_view<T>(a, b, simg, slbl);
   v.W4 = P.cp_w_bytes;  // straight from the parameters: uniform registers, folded
   v.P4 = P.cp_p_bytes;  // into the shared-memory addresses ([R + UR])
@@ -941,11 +967,11 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   }
   if (!live) return;
   if (oy + TY <= a.my)  // every row of the tile is an output row
-    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true>(a, P, V, v, vi, X, Z, oy,
-                                                                        TY / 4, n);
+    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre>(
+        a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
   else
-    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl>(a, P, V, v, vi, X, Z, oy,
-                                                                  TY / 4, n);
+    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre>(
+        a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
 }
 
 // grid = (tiles per volume, volumes); tiles x-fastest, then y, then z.
