@@ -939,14 +939,28 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   } else {
     stage<T, kLabels>(a, vin, lin, b, simg, slbl);
   }
-  const float4 n = live ? first_normals<kPh>(a, P, V, X, Z, oy) : make_float4(0, 0, 0, 0);
+  float4 n = (live && !(kPh == kPhFull && W3D_PRE == 4))
+                 ? first_normals<kPh>(a, P, V, X, Z, oy)
+                 : make_float4(0, 0, 0, 0);
   // the training chain (kPhFull, launch-wide keys) computes kPre Philox blocks
   // here, under the staging latency; the generic chain one (register budget)
   constexpr int kPre = kPh == kPhFull ? W3D_PRE : 1;
   const float4 z4 = make_float4(0, 0, 0, 0);
-  const float4 n1 = (kPre >= 2 && live) ? first_normals<kPh>(a, P, V, X, Z, oy + 4) : z4;
-  const float4 n2 = (kPre >= 4 && live) ? first_normals<kPh>(a, P, V, X, Z, oy + 8) : z4;
-  const float4 n3 = (kPre >= 4 && live) ? first_normals<kPh>(a, P, V, X, Z, oy + 12) : z4;
+  float4 n1 = z4, n2 = z4, n3 = z4;
+  if (kPre == 4 && live) {  // the column's four blocks in lockstep
+    const uint32_t gyn = static_cast<uint32_t>((a.my + 3) >> 2), mxu = static_cast<uint32_t>(a.mx);
+    const uint32_t q0 = static_cast<uint32_t>(X) +
+                        mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(oy >> 2));
+    const uint32_t qs[4] = {q0, q0 + mxu, q0 + 2u * mxu, q0 + 3u * mxu};
+    uint4 r[4];
+    philox_block4(qs, PhiloxPrefix{P.ph_K0, P.ph_K1, P.ph_K2, P.ph_U3}, a.rk0, a.rk1, r);
+    n = box_muller4(r[0]);
+    n1 = box_muller4(r[1]);
+    n2 = box_muller4(r[2]);
+    n3 = box_muller4(r[3]);
+  } else if (kPre == 2 && live) {
+    n1 = first_normals<kPh>(a, P, V, X, Z, oy + 4);
+  }
   View v = make_view<T>(a, b, simg, slbl);
   v.W4 = P.cp_w_bytes;  // straight from the parameters: uniform registers, folded
   v.P4 = P.cp_p_bytes;  // into the shared-memory addresses ([R + UR])
