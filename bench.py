@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--input", choices=["f32", "i16"], default="f32",
                     help="i16: the same volumes as int16 HU (NEXT-4; 2 B per input voxel)")
+    ap.add_argument("--fill", type=float, default=-1000.0,
+                    help="image fill (HU) outside the volume (air, the default)")
     ap.add_argument("--no-labels", action="store_true",
                     help="image-only warp (diagnostic; the headline includes labels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -274,7 +276,7 @@ def config_of(args, world):
             "volumes_per_gpu": per if per else wl["total"] // world,
             "global_batch": per * world if per else wl["total"],
             "transforms": wl["ranges"], "photometric": "noise+window+clamp+gamma",
-            "kernel_variant": args.variant, "input": args.input,
+            "kernel_variant": args.variant, "input": args.input, "fill_hu": args.fill,
             "l2": "flushed between timed steps (256 MiB write)",
             "parallelism": f"dp{world} (volume shards, no data-path collective)"}
 
@@ -398,7 +400,7 @@ def main():
         imgs = np.round(imgs).astype(np.int16)
     t_img = torch.from_numpy(imgs).to(dev)
     t_lbl = None if args.no_labels else torch.from_numpy(lbls).to(dev)
-    batch = W.AugmentBatch(t_img, t_lbl, params, fill=-1000.0, label_fill=0, variant=variant)
+    batch = W.AugmentBatch(t_img, t_lbl, params, fill=args.fill, label_fill=0, variant=variant)
 
     # algorithmic bytes: 5 B written per output voxel
     # + 4 B per distinct input image voxel read + 1 B per distinct label voxel read

@@ -818,60 +818,107 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-// fill over the out-of-volume elements of a TMA image box (TMA wrote 0).
-template <class T>
-__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint32_t simg) {
-  constexpr uint32_t kB = InT<T>::kBytes;
-  const uint32_t fw = fill_word<T>(a);
-  const int head = min(b.W, max(0, -b.bx)), tail = max(0, min(b.W, a.nx - b.bx));
-  for (int r = threadIdx.x; r < b.H * b.D; r += THREADS) {
-    const int z = r / b.H, y = r - z * b.H;
-    const bool row_out = static_cast<unsigned>(b.bz + z) >= static_cast<unsigned>(a.nz) ||
-                         static_cast<unsigned>(b.by + y) >= static_cast<unsigned>(a.ny);
-    const uint32_t irow = simg + kB * static_cast<uint32_t>(z * b.P + y * b.W);
-    if (row_out) {
-      for (int x = 0; x < b.W; x += 16 / kB)
-        asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(irow + kB * x), "r"(fw)
-                     : "memory");
-      continue;
+// Out-of-volume 16 B chunks of a TMA box (TMA wrote 0) set to `word`: a box of
+// D planes x Hb rows x CW chunks (rows and planes contiguous: row pitch CW
+// chunks, plane pitch Pb bytes) whose origin is (bx, by, bz) in elements of
+// kC per chunk (bx and nx multiples of kC, so a chunk is wholly in or out).
+// Three flat loops over just the chunks to write: the x-side chunks of the
+// in-volume rows, the rows outside in y of the in-volume planes, and the
+// planes outside in z.  q / d for small q, d by one fp32 multiply ((q + 1/2) / d
+// is >= 1/(2 d) from an integer; q < 2^16, d <= 2^8: error < 2^-8).
+__device__ __forceinline__ int small_div(int q, float inv_d) {
+  return __float2int_rz(__fmul_rn(static_cast<float>(q) + 0.5f, inv_d));
+}
+__device__ __forceinline__ void fix_chunks(uint32_t base, int CW, int Hb, uint32_t Pb, int D,
+                                           int bx, int by, int bz, int kC, int nx, int ny, int nz,
+                                           uint32_t word) {
+  const int hc = min(CW, max(0, -bx / kC)), tc = max(hc, min(CW, (nx - bx) / kC));
+  const int ylo = min(Hb, max(0, -by)), yhi = max(ylo, min(Hb, ny - by));
+  const int zlo = min(D, max(0, -bz)), zhi = max(zlo, min(D, nz - bz));
+  const uint32_t rowb = 16u * static_cast<uint32_t>(CW);
+  auto st = [&](uint32_t addr) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(word) : "memory");
+  };
+  // 1. x-side chunks [0, hc) and [tc, CW) of rows y in [ylo, yhi), z in [zlo, zhi)
+  const int side = hc + CW - tc, ny_in = yhi - ylo;
+  if (side > 0) {
+    const float inv_side = __frcp_rn(static_cast<float>(side));
+    const float inv_ny = __frcp_rn(static_cast<float>(ny_in));
+    for (int i = threadIdx.x; i < side * ny_in * (zhi - zlo); i += THREADS) {
+      const int r = small_div(i, inv_side), j = i - r * side;
+      const int z = small_div(r, inv_ny), y = r - z * ny_in;
+      const int c = j < hc ? j : tc + (j - hc);
+      st(base + static_cast<uint32_t>(zlo + z) * Pb + static_cast<uint32_t>(ylo + y) * rowb +
+         16u * static_cast<uint32_t>(c));
     }
-    for (int x = 0; x < head; ++x) {
-      if (kB == 4)
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
-      else
-        asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
+  }
+  // 2. rows y outside [ylo, yhi) of planes z in [zlo, zhi): whole rows
+  const int nyo = Hb - ny_in;
+  if (nyo > 0) {
+    const float inv_cw = __frcp_rn(static_cast<float>(CW));
+    const float inv_nyo = __frcp_rn(static_cast<float>(nyo));
+    for (int i = threadIdx.x; i < CW * nyo * (zhi - zlo); i += THREADS) {
+      const int r = small_div(i, inv_cw), c = i - r * CW;
+      const int z = small_div(r, inv_nyo), yy = r - z * nyo;
+      const int y = yy < ylo ? yy : yhi + (yy - ylo);
+      st(base + static_cast<uint32_t>(zlo + z) * Pb + static_cast<uint32_t>(y) * rowb +
+         16u * static_cast<uint32_t>(c));
     }
-    for (int x = tail; x < b.W; ++x) {
-      if (kB == 4)
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(irow + kB * x), "r"(fw) : "memory");
-      else
-        asm volatile("st.shared.b16 [%0], %1;" ::"r"(irow + kB * x), "h"(static_cast<unsigned short>(fw)) : "memory");
+  }
+  // 3. planes outside [zlo, zhi): Hb rows of CW chunks each, contiguous
+  const int nzo = D - (zhi - zlo), pc = Hb * CW;
+  if (nzo > 0) {
+    const float inv_pc = __frcp_rn(static_cast<float>(pc));
+    for (int i = threadIdx.x; i < pc * nzo; i += THREADS) {
+      const int zz = i / pc, c = i - zz * pc;  // pc up to ~2^11: integer division
+      const int z = zz < zlo ? zz : zhi + (zz - zlo);
+      st(base + static_cast<uint32_t>(z) * Pb + 16u * static_cast<uint32_t>(c));
     }
+    (void)inv_pc;
   }
 }
 
+// fill over the out-of-volume elements of a TMA image box (TMA wrote 0).
+template <class T>
+__device__ __forceinline__ void tma_fixup(const WarpArgs& a, const Box& b, uint32_t simg) {
+  constexpr int kC = InT<T>::kChunk;
+  fix_chunks(simg, b.W / kC, b.H, InT<T>::kBytes * static_cast<uint32_t>(b.P), b.D, b.bx, b.by,
+             b.bz, kC, a.nx, a.ny, a.nz, fill_word<T>(a));
+}
+
 // label_fill over the out-of-volume elements of a TMA label box (rows of Wl
-// bytes from bxl, plane pitch Pl).
+// bytes from bxl, a multiple of 16, as nx is; plane pitch Pl).
 __device__ __forceinline__ void tma_fixup_lbl(const WarpArgs& a, const Box& b, uint32_t slbl) {
-  const uint32_t lf4 = a.label_fill * 0x01010101u;
-  const int Hl = b.Pl / b.Wl;
-  const int headl = min(b.Wl, max(0, -b.bxl)), taill = max(0, min(b.Wl, a.nx - b.bxl));
-  for (int r = threadIdx.x; r < Hl * b.D; r += THREADS) {
-    const int z = r / Hl, y = r - z * Hl;
-    const bool row_out = static_cast<unsigned>(b.bz + z) >= static_cast<unsigned>(a.nz) ||
-                         static_cast<unsigned>(b.by + y) >= static_cast<unsigned>(a.ny);
-    const uint32_t lrow = slbl + static_cast<uint32_t>(z * b.Pl + y * b.Wl);
-    if (row_out) {
-      for (int x = 0; x < b.Wl; x += 16)
-        asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(lrow + x), "r"(lf4)
-                     : "memory");
-      continue;
+  fix_chunks(slbl, b.Wl / 16, b.Pl / b.Wl, static_cast<uint32_t>(b.Pl), b.D, b.bxl, b.by, b.bz,
+             16, a.nx, a.ny, a.nz, a.label_fill * 0x01010101u);
+}
+
+// Every trilinear corner / nearest voxel of the tile inside the volume:
+// 0 <= floor(p_min) and floor(p_max) + 1 <= n - 1 per axis, with p_min / p_max
+// = p(origin) + sum_j min / max(0, A_kj span_j), widened by a bound on the fp32
+// rounding of p (delta: 1e-3 + 2^-18 (|p0| + ext), far above a few ulp).
+template <int TY>
+__device__ __forceinline__ bool footprint_inside(const WarpArgs& a, const VolDev& P, int ox,
+                                                 int oy, int oz) {
+  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
+  const float span[3] = {TX - 1.0f, TY - 1.0f, TZ - 1.0f};
+  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                      static_cast<float>(a.nz)};
+  bool in = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float p0 = coord(P.A, k, X, Y, Z);
+    float lo = p0, hi = p0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float d = P.A[4 * k + j] * span[j];
+      lo += fminf(d, 0.0f);
+      hi += fmaxf(d, 0.0f);
     }
-    for (int x = 0; x < headl; ++x)
-      asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
-    for (int x = taill; x < b.Wl; ++x)
-      asm volatile("st.shared.u8 [%0], %1;" ::"r"(lrow + x), "r"(lf4) : "memory");
+    const float delta = 1e-3f + (fabsf(p0) + (hi - lo)) * 0x1.0p-18f;
+    in &= (lo - delta >= 0.0f) & (hi + delta < n[k] - 1.0f);
   }
+  return in;
 }
 
 // The tile's coordinates stay below 2^21 (magic-number floor, float indices):
@@ -972,7 +1019,10 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
                         b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
     const bool insidel = !kTmaLbl || (b.bxl >= 0 && b.bxl + b.Wl <= a.nx &&
                                       b.by + b.Pl / b.Wl <= a.ny && inside);
-    const bool fi = !inside && a.fill != 0.0f, fl = kTmaLbl && !insidel && a.label_fill != 0u;
+    bool fi = !inside && a.fill != 0.0f, fl = kTmaLbl && !insidel && a.label_fill != 0u;
+    // boxes carry margins: skip the fix-up when no sample of the tile can read
+    // an out-of-volume cell (every trilinear corner and nearest voxel inside)
+    if ((fi || fl) && footprint_inside<TY>(a, P, ox, oy, oz)) fi = fl = false;
     if (fi || fl) {  // uniform
       if (fi) tma_fixup<T>(a, b, simg);
       if (fl) tma_fixup_lbl(a, b, slbl);
