@@ -630,6 +630,47 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
   uint32_t q = static_cast<uint32_t>(X) +
                mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(y0 >> 2));
   float2 Y2 = make_float2(static_cast<float>(y0), static_cast<float>(y0 + 1));
+  // one y-pair (rows ya, ya + 1) with its two normals
+  auto pair = [&](int ya, float2 nsp) {
+    const float2 px = __ffma2_rn(f2(V.A1[0]), Y2, f2(t0));
+    const float2 py = __ffma2_rn(f2(V.A1[1]), Y2, f2(t1));
+    const float2 pz = __ffma2_rn(f2(V.A1[2]), Y2, f2(t2));
+    Y2 = __fadd2_rn(Y2, make_float2(2.0f, 2.0f));
+    float2 img;
+    uint32_t l0 = 0, l1 = 0;
+    if (kStaged) {
+      sample2<T, kLabels, kNearest, kClamp, kSameLbl>(v, px, py, pz, img, l0, l1);
+    } else {
+      sample_gather<T, kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
+      sample_gather<T, kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
+    }
+    float2 out = photometric2<kPh>(img, nsp, V);
+    if (occl) out = make_float2(0.0f, 0.0f);  // PAPER.md:437-438, R15
+    const bool second = kFull || ya + 1 < my;
+    float* po1 = po + row1;
+    st_f32(po, out.x);
+    if (second) st_f32(po1, out.y);
+    po = po1 + row1;
+    if (kLabels) {
+      uint8_t* pl1 = pl + row1;
+      st_u8(pl, l0);
+      if (second) st_u8(pl1, l1);
+      pl = pl1 + row1;
+    }
+  };
+  if constexpr (kFull && kPre == 4) {
+    if (ng == 4) {  // a whole 16-row column, normals precomputed: straight line, no rotation
+      pair(y0, make_float2(n.x, n.y));
+      pair(y0 + 2, make_float2(n.z, n.w));
+      pair(y0 + 4, make_float2(n1.x, n1.y));
+      pair(y0 + 6, make_float2(n1.z, n1.w));
+      pair(y0 + 8, make_float2(n2.x, n2.y));
+      pair(y0 + 10, make_float2(n2.z, n2.w));
+      pair(y0 + 12, make_float2(n3.x, n3.y));
+      pair(y0 + 14, make_float2(n3.z, n3.w));
+      return;
+    }
+  }
 #pragma unroll 1
   for (int g = 0; g < ng; ++g) {
     const int y = y0 + 4 * g;
@@ -637,37 +678,8 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
     float4 nn = make_float4(0.f, 0.f, 0.f, 0.f);
     if (noise && g + kPre < ng)
       nn = box_muller4(philox_block(q + static_cast<uint32_t>(kPre) * mxu, pp, rk0, rk1));
-    const float ns[4] = {n.x, n.y, n.z, n.w};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int ya = y + 2 * h;
-      if (!kFull && ya >= my) break;
-      const float2 px = __ffma2_rn(f2(V.A1[0]), Y2, f2(t0));
-      const float2 py = __ffma2_rn(f2(V.A1[1]), Y2, f2(t1));
-      const float2 pz = __ffma2_rn(f2(V.A1[2]), Y2, f2(t2));
-      Y2 = __fadd2_rn(Y2, make_float2(2.0f, 2.0f));
-      float2 img;
-      uint32_t l0 = 0, l1 = 0;
-      if (kStaged) {
-        sample2<T, kLabels, kNearest, kClamp, kSameLbl>(v, px, py, pz, img, l0, l1);
-      } else {
-        sample_gather<T, kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
-        sample_gather<T, kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
-      }
-      float2 out = photometric2<kPh>(img, make_float2(ns[2 * h], ns[2 * h + 1]), V);
-      if (occl) out = make_float2(0.0f, 0.0f);  // PAPER.md:437-438, R15
-      const bool second = kFull || ya + 1 < my;
-      float* po1 = po + row1;
-      st_f32(po, out.x);
-      if (second) st_f32(po1, out.y);
-      po = po1 + row1;
-      if (kLabels) {
-        uint8_t* pl1 = pl + row1;
-        st_u8(pl, l0);
-        if (second) st_u8(pl1, l1);
-        pl = pl1 + row1;
-      }
-    }
+    pair(y, make_float2(n.x, n.y));
+    if (kFull || y + 2 < my) pair(y + 2, make_float2(n.z, n.w));
     if (kPre == 1) {
       n = nn;
     } else if (kPre == 2) {
