@@ -935,11 +935,15 @@ __device__ __forceinline__ bool footprint_inside(const WarpArgs& a, const VolDev
 
 // The tile's coordinates stay below 2^21 (magic-number floor, float indices):
 // its origin voxel's p below 2^20 and the footprint extent below 200 (host).
-__device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz) {
+// p0 = p(tile origin voxel), computed once per tile.
+__device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz, float p0[3]) {
   const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
   bool sane = true;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) sane &= fabsf(coord(P.A, k, X, Y, Z)) < 1048576.0f;
+  for (int k = 0; k < 3; ++k) {
+    p0[k] = coord(P.A, k, X, Y, Z);
+    sane &= fabsf(p0[k]) < 1048576.0f;
+  }
   return sane;
 }
 
@@ -955,7 +959,7 @@ __device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz)
 // on the mbarrier alone.
 template <class T, int TY, bool kLabels, bool kNearest, int kPh, bool kTmaLbl = false>
 __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int vi, int ox, int oy,
-                                        int oz, bool tma, uint32_t mbar) {
+                                        int oz, bool tma, uint32_t mbar, const float p0[3]) {
   constexpr int kC = InT<T>::kChunk;
   constexpr uint32_t kB = InT<T>::kBytes;
   const uint32_t simg = smem_base();
@@ -967,13 +971,10 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   b.Wl = b.W;
   b.Pl = b.P;
   b.clamp = false;
-  {
-    const float fx = static_cast<float>(ox), fy = static_cast<float>(oy), fz = static_cast<float>(oz);
-    b.bx = __float2int_rd(__fadd_rd(coord(P.A, 0, fx, fy, fz), P.box_mlo[0])) & ~(kC - 1);
-    b.by = __float2int_rd(__fadd_rd(coord(P.A, 1, fx, fy, fz), P.box_mlo[1]));
-    b.bz = __float2int_rd(__fadd_rd(coord(P.A, 2, fx, fy, fz), P.box_mlo[2]));
-    b.bxl = kTmaLbl ? (b.bx & ~15) : b.bx;
-  }
+  b.bx = __float2int_rd(__fadd_rd(p0[0], P.box_mlo[0])) & ~(kC - 1);
+  b.by = __float2int_rd(__fadd_rd(p0[1], P.box_mlo[1]));
+  b.bz = __float2int_rd(__fadd_rd(p0[2], P.box_mlo[2]));
+  b.bxl = kTmaLbl ? (b.bx & ~15) : b.bx;
   if (kTmaLbl) {
     b.Wl = P.box_wl;
     b.Pl = b.Wl * P.box_h;
@@ -1065,14 +1066,15 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const uint32_t simg = smem_base();
   const VolDev& P = a.vol[vi];
   const int ylast = min(oy + TY, a.my) - 1;
-  if (!kGather && P.cp_rows == TY && cp_sane(P, ox, oy, oz)) {
+  float p0[3];
+  if (!kGather && P.cp_rows == TY && cp_sane(P, ox, oy, oz, p0)) {
     const bool tma = a.use_tma && vi < kTmaVolPerLaunch && P.box_w != 0;
     if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[tma ? 2 : 0], 1ull);
     const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
     if (kLabels && tma && P.box_wl != 0)
-      cp_tile<T, TY, kLabels, kNearest, kPh, true>(a, P, vi, ox, oy, oz, true, mbar);
+      cp_tile<T, TY, kLabels, kNearest, kPh, true>(a, P, vi, ox, oy, oz, true, mbar, p0);
     else
-      cp_tile<T, TY, kLabels, kNearest, kPh>(a, P, vi, ox, oy, oz, tma, mbar);
+      cp_tile<T, TY, kLabels, kNearest, kPh>(a, P, vi, ox, oy, oz, tma, mbar, p0);
     return;
   }
   // per-tile exact boxes (volumes whose worst-case box does not fit)
