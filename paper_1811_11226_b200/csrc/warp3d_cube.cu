@@ -356,6 +356,7 @@ struct View {
   float Wlf, Plf;         // label pitches as floats
   float Mby, Mbz;         // kM + by, kM + bz
   uint32_t W4, P4;        // byte pitches of the image buffer
+  uint32_t PW4;           // P4 + W4: the (y+1, z+1) corner row as one [R + UR] offset
   uint32_t cimg, clbl;    // image / label byte address = bits(L) * (4 | 1) + c
   float nx, ny, nz;       // clamp bounds
 };
@@ -373,6 +374,7 @@ __device__ __forceinline__ View make_view(const WarpArgs& a, const Box& b, uint3
   v.Mbz = pin(kM + static_cast<float>(b.bz));
   v.W4 = pin(kB * static_cast<uint32_t>(b.W));
   v.P4 = pin(kB * static_cast<uint32_t>(b.P));
+  v.PW4 = pin(v.P4 + v.W4);
   // bits(L) - kMbits = fx + W ry + P rz; element index = that - bx
   v.cimg = opaque(simg - kB * static_cast<uint32_t>(b.bx) - kB * static_cast<uint32_t>(kMbits));
   v.clbl = opaque(slbl - static_cast<uint32_t>(b.bxl) - static_cast<uint32_t>(kMbits));
@@ -498,7 +500,7 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
   }
   const uint32_t a0 = addrT<T>(L.x, v.cimg), b0 = addrT<T>(L.y, v.cimg);
   const uint32_t a1 = a0 + v.W4, b1 = b0 + v.W4, a2 = a0 + v.P4, b2 = b0 + v.P4;
-  const uint32_t a3 = a2 + v.W4, b3 = b2 + v.W4;
+  const uint32_t a3 = a0 + v.PW4, b3 = b0 + v.PW4;
   float2 c000, c100, c010, c110, c001, c101, c011, c111;
   lds_pair<T>(a0, c000.x, c100.x);
   lds_pair<T>(b0, c000.y, c100.y);
@@ -1024,6 +1026,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   View v = make_view<T>(a, b, simg, slbl);
   v.W4 = P.cp_w_bytes;  // straight from the parameters: uniform registers, folded
   v.P4 = P.cp_p_bytes;  // into the shared-memory addresses ([R + UR])
+  v.PW4 = static_cast<uint32_t>(P.cp_w_bytes) + static_cast<uint32_t>(P.cp_p_bytes);
   if (!kTmaLbl) cp_async_wait_all();
   __syncthreads();  // label copies (and the mbarrier init) visible to every thread
   if (tma) {
@@ -1244,20 +1247,37 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3])
   }
   if (!ok) return;
   const int W0 = (d[0] + kC - 1 + kC - 1) & ~(kC - 1), H0 = d[1], D = d[2];
+  // TMA label box candidate: rows of Wl bytes from the 16 B aligned x origin
+  // (lo & ~15 >= lo - 15), H0 rows per plane
+  const int Wl = (d[0] + 15 + 15) & ~15;
+  const int64_t lbl_bytes = int64_t(Wl) * H0 * D;
+  auto img_bytes_of = [&](int64_t plane) {
+    return (int64_t(elem_bytes) * plane * D + 127) & ~int64_t(127);
+  };
+  // smallest bank-spreading padding; one that also leaves room for the TMA
+  // label box wins over a smaller one that does not (labels by cp.async cost
+  // more than the bank conflicts the padding saves), and the unpadded layout
+  // wins when it alone makes the label box fit
   int best_w = 0, best_h = 0;
   int64_t best = INT64_MAX;
+  bool best_lbl = false;
+  const int64_t room = int64_t(kCapVox) * 5;
   for (int W = W0; W <= W0 + kC; W += kC)
     for (int h = H0; h < H0 + 8; ++h) {
       const int res = (W * h) & 31;
       const bool spread = elem_bytes == 4 ? (res == 12 || res == 16 || res == 20 || res == 24)
                                           : res == 16;
-      if (spread && int64_t(W) * h < best) {
+      if (!spread || int64_t(W) * h * D > cap) continue;
+      const bool lbl = img_bytes_of(int64_t(W) * h) + lbl_bytes <= room && Wl <= 256;
+      if ((lbl && !best_lbl) || (lbl == best_lbl && int64_t(W) * h < best)) {
         best = int64_t(W) * h;
         best_w = W;
         best_h = h;
+        best_lbl = lbl;
       }
     }
-  if (best_w == 0 || int64_t(best_w) * best_h * D > cap) {  // unpadded, if that fits
+  const bool plain_lbl = img_bytes_of(int64_t(W0) * H0) + lbl_bytes <= room && Wl <= 256;
+  if (best_w == 0 || (!best_lbl && plain_lbl)) {  // unpadded
     best_w = W0;
     best_h = H0;
   }
@@ -1270,12 +1290,9 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3])
   P.cp_rows = static_cast<uint16_t>(kTY);
   P.cp_w_bytes = static_cast<uint16_t>(best_w * elem_bytes);
   P.cp_p_bytes = static_cast<uint16_t>(Pp * elem_bytes);
-  // TMA label box candidate: rows of Wl bytes from the 16 B aligned x origin
-  // (lo & ~15 >= lo - 15), H0 rows per plane; used when it fits beside the
-  // image box (and prepare_tma makes its tensor map)
-  const int Wl = (d[0] + 15 + 15) & ~15;
-  const int64_t img_bytes = (int64_t(elem_bytes) * Pp * D + 127) & ~int64_t(127);
-  if (img_bytes + int64_t(Wl) * H0 * D <= int64_t(kCapVox) * 5 && Wl <= 256) {
+  // the TMA label box, used when it fits beside the image box (and
+  // prepare_tma makes its tensor map)
+  if (img_bytes_of(Pp) + lbl_bytes <= room && Wl <= 256) {
     P.box_wl = static_cast<uint16_t>(Wl);
     P.box_h = static_cast<uint16_t>(H0);
   }
