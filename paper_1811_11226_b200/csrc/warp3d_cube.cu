@@ -833,13 +833,16 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 }
 
 // Out-of-volume 16 B chunks of a TMA box (TMA wrote 0) set to `word`: a box of
-// D planes x Hb rows x CW chunks (rows and planes contiguous: row pitch CW
-// chunks, plane pitch Pb bytes) whose origin is (bx, by, bz) in elements of
-// kC per chunk (bx and nx multiples of kC, so a chunk is wholly in or out).
-// Three flat loops over just the chunks to write: the x-side chunks of the
-// in-volume rows, the rows outside in y of the in-volume planes, and the
-// planes outside in z.  q / d for small q, d by one fp32 multiply ((q + 1/2) / d
-// is >= 1/(2 d) from an integer; q < 2^16, d <= 2^8: error < 2^-8).
+// D planes x Hb rows x CW chunks (rows contiguous: row pitch CW chunks, plane
+// pitch Pb bytes) whose origin is (bx, by, bz) in elements of kC per chunk (bx
+// and nx multiples of kC, so a chunk is wholly in or out).  Thread t owns one
+// (chunk column, row) slot s = t / nsplit and the t % nsplit-th of nsplit
+// plane ranges (nsplit = THREADS / slots when the slots are fewer than the
+// threads, so small label boxes still spread over every thread): a slot
+// outside in x or y is written in every plane of its range, an inside one in
+// the planes outside [zlo, zhi) only.  q / d for small q, d by one fp32
+// multiply ((q + 1/2) / d is >= 1/(2 d) from an integer; q < 2^16, d <= 2^8:
+// error < 2^-8).
 __device__ __forceinline__ int small_div(int q, float inv_d) {
   return __float2int_rz(__fmul_rn(static_cast<float>(q) + 0.5f, inv_d));
 }
@@ -849,46 +852,35 @@ __device__ __forceinline__ void fix_chunks(uint32_t base, int CW, int Hb, uint32
   const int hc = min(CW, max(0, -bx / kC)), tc = max(hc, min(CW, (nx - bx) / kC));
   const int ylo = min(Hb, max(0, -by)), yhi = max(ylo, min(Hb, ny - by));
   const int zlo = min(D, max(0, -bz)), zhi = max(zlo, min(D, nz - bz));
-  const uint32_t rowb = 16u * static_cast<uint32_t>(CW);
+  const int slots = CW * Hb;
+  const int nsplit = max(1, THREADS / slots);
+  const int t = static_cast<int>(threadIdx.x);
+  const float inv_cw = __frcp_rn(static_cast<float>(CW));
   auto st = [&](uint32_t addr) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(word) : "memory");
   };
-  // 1. x-side chunks [0, hc) and [tc, CW) of rows y in [ylo, yhi), z in [zlo, zhi)
-  const int side = hc + CW - tc, ny_in = yhi - ylo;
-  if (side > 0) {
-    const float inv_side = __frcp_rn(static_cast<float>(side));
-    const float inv_ny = __frcp_rn(static_cast<float>(ny_in));
-    for (int i = threadIdx.x; i < side * ny_in * (zhi - zlo); i += THREADS) {
-      const int r = small_div(i, inv_side), j = i - r * side;
-      const int z = small_div(r, inv_ny), y = r - z * ny_in;
-      const int c = j < hc ? j : tc + (j - hc);
-      st(base + static_cast<uint32_t>(zlo + z) * Pb + static_cast<uint32_t>(ylo + y) * rowb +
-         16u * static_cast<uint32_t>(c));
-    }
+  if (nsplit > 1) {
+    const int s = small_div(t, __frcp_rn(static_cast<float>(nsplit)));
+    if (s >= slots) return;
+    const int part = t - s * nsplit;
+    const int zs = (D * part) / nsplit, ze = (D * (part + 1)) / nsplit;
+    const int r = small_div(s, inv_cw), c = s - r * CW;
+    const bool out = (c < hc) | (c >= tc) | (r < ylo) | (r >= yhi);
+    const uint32_t a0 = base + 16u * static_cast<uint32_t>(s);
+    for (int z = zs; z < ze; ++z)
+      if (out | (z < zlo) | (z >= zhi)) st(a0 + static_cast<uint32_t>(z) * Pb);
+    return;
   }
-  // 2. rows y outside [ylo, yhi) of planes z in [zlo, zhi): whole rows
-  const int nyo = Hb - ny_in;
-  if (nyo > 0) {
-    const float inv_cw = __frcp_rn(static_cast<float>(CW));
-    const float inv_nyo = __frcp_rn(static_cast<float>(nyo));
-    for (int i = threadIdx.x; i < CW * nyo * (zhi - zlo); i += THREADS) {
-      const int r = small_div(i, inv_cw), c = i - r * CW;
-      const int z = small_div(r, inv_nyo), yy = r - z * nyo;
-      const int y = yy < ylo ? yy : yhi + (yy - ylo);
-      st(base + static_cast<uint32_t>(zlo + z) * Pb + static_cast<uint32_t>(y) * rowb +
-         16u * static_cast<uint32_t>(c));
+  for (int s = t; s < slots; s += THREADS) {
+    const int r = small_div(s, inv_cw), c = s - r * CW;
+    const bool out = (c < hc) | (c >= tc) | (r < ylo) | (r >= yhi);
+    const uint32_t a0 = base + 16u * static_cast<uint32_t>(s);
+    if (out) {
+      for (int z = 0; z < D; ++z) st(a0 + static_cast<uint32_t>(z) * Pb);
+    } else {
+      for (int z = 0; z < zlo; ++z) st(a0 + static_cast<uint32_t>(z) * Pb);
+      for (int z = zhi; z < D; ++z) st(a0 + static_cast<uint32_t>(z) * Pb);
     }
-  }
-  // 3. planes outside [zlo, zhi): Hb rows of CW chunks each, contiguous
-  const int nzo = D - (zhi - zlo), pc = Hb * CW;
-  if (nzo > 0) {
-    const float inv_pc = __frcp_rn(static_cast<float>(pc));
-    for (int i = threadIdx.x; i < pc * nzo; i += THREADS) {
-      const int zz = i / pc, c = i - zz * pc;  // pc up to ~2^11: integer division
-      const int z = zz < zlo ? zz : zhi + (zz - zlo);
-      st(base + static_cast<uint32_t>(z) * Pb + 16u * static_cast<uint32_t>(c));
-    }
-    (void)inv_pc;
   }
 }
 
@@ -907,31 +899,19 @@ __device__ __forceinline__ void tma_fixup_lbl(const WarpArgs& a, const Box& b, u
              16, a.nx, a.ny, a.nz, a.label_fill * 0x01010101u);
 }
 
-// Every trilinear corner / nearest voxel of the tile inside the volume:
-// 0 <= floor(p_min) and floor(p_max) + 1 <= n - 1 per axis, with p_min / p_max
-// = p(origin) + sum_j min / max(0, A_kj span_j), widened by a bound on the fp32
-// rounding of p (delta: 1e-3 + 2^-18 (|p0| + ext), far above a few ulp).
-template <int TY>
-__device__ __forceinline__ bool footprint_inside(const WarpArgs& a, const VolDev& P, int ox,
-                                                 int oy, int oz) {
-  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
-  const float span[3] = {TX - 1.0f, TY - 1.0f, TZ - 1.0f};
+// Every trilinear corner / nearest voxel of the tile inside the volume, from
+// the tile's origin coordinate p0 and the per-volume offsets of the box (host,
+// cube_cp_box: the box margin bounds the fp32 rounding of every p of the
+// tile): lower corner floor(p0 + box_mlo) >= 0, upper corner p0 + box_mhi <
+// n - 1, the adds rounded outwards.
+__device__ __forceinline__ bool tile_inside(const WarpArgs& a, const VolDev& P, const float p0[3]) {
   const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
                       static_cast<float>(a.nz)};
   bool in = true;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const float p0 = coord(P.A, k, X, Y, Z);
-    float lo = p0, hi = p0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const float d = P.A[4 * k + j] * span[j];
-      lo += fminf(d, 0.0f);
-      hi += fmaxf(d, 0.0f);
-    }
-    const float delta = 1e-3f + (fabsf(p0) + (hi - lo)) * 0x1.0p-18f;
-    in &= (lo - delta >= 0.0f) & (hi + delta < n[k] - 1.0f);
-  }
+  for (int k = 0; k < 3; ++k)
+    in &= (__fadd_rd(p0[k], P.box_mlo[k]) >= 0.0f) &
+          (__fadd_ru(p0[k], P.box_mhi[k]) < n[k] - 1.0f);
   return in;
 }
 
@@ -1038,7 +1018,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     bool fi = !inside && a.fill != 0.0f, fl = kTmaLbl && !insidel && a.label_fill != 0u;
     // boxes carry margins: skip the fix-up when no sample of the tile can read
     // an out-of-volume cell (every trilinear corner and nearest voxel inside)
-    if ((fi || fl) && footprint_inside<TY>(a, P, ox, oy, oz)) fi = fl = false;
+    if ((fi || fl) && tile_inside(a, P, p0)) fi = fl = false;
     if (fi || fl) {  // uniform
       if (fi) tma_fixup<T>(a, b, simg);
       if (fl) tma_fixup_lbl(a, b, slbl);
@@ -1233,15 +1213,17 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3])
   const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
   bool ok = true;
   for (int k = 0; k < 3; ++k) {
-    double mag = std::fabs(double(A[4 * k + 3])), ext = 0.0, mlo = 0.0;
+    double mag = std::fabs(double(A[4 * k + 3])), ext = 0.0, mlo = 0.0, mhi = 0.0;
     for (int j = 0; j < 3; ++j) {
       const double a = double(A[4 * k + j]) * span[j];
       ext += std::fabs(a);
       mlo += a < 0.0 ? a : 0.0;
+      mhi += a > 0.0 ? a : 0.0;
       mag += std::fabs(double(A[4 * k + j])) * (out[j] + 16.0);  // any voxel of any tile
     }
     const double margin = 16.0 * mag * 0x1.0p-24 + 1e-3;
     P.box_mlo[k] = static_cast<float>(mlo - margin);
+    P.box_mhi[k] = std::nextafter(static_cast<float>(mhi + margin), INFINITY);  // rounded up
     if (ext > 200.0) ok = false;
     d[k] = ok ? static_cast<int>(std::floor(ext + 2.0 * margin)) + 3 : 0;
   }

@@ -51,13 +51,18 @@ struct alignas(16) VolDev {
   // box_mlo[k]) with box_mlo[k] = sum_j min(0, A_kj span_j) - rounding margin
   // (cube_box_mlo); a y-part of r rows adds -min(0, A_k1) (kTY - r)
   float box_mlo[3];
+  // fix-up test of a full tile: every trilinear corner and nearest voxel lies
+  // inside the volume iff floor(p0 + box_mlo[k]) >= 0 and p0 + box_mhi[k] <
+  // n_k - 1 (box_mhi[k] = sum_j max(0, A_kj span_j) + the same margin)
+  float box_mhi[3];
+  int32_t _pad0;
   int32_t out_slot;     // output volume index in the caller's batch (out + slot * out_stride)
   uint64_t in_addr;     // device address of this volume's image (float32 or int16)
   uint64_t lbl_addr;    // device address of its labels (0 without labels)
 };
-static_assert(sizeof(VolDev) == 240, "VolDev layout");
+static_assert(sizeof(VolDev) == 256, "VolDev layout");
 
-constexpr int kMaxVolPerLaunch = 112;  // sizeof(WarpArgs) < 32764 B of kernel parameters
+constexpr int kMaxVolPerLaunch = 104;  // sizeof(WarpArgs) < 32764 B of kernel parameters
 // Volumes per launch when TMA staging is used: the tensor maps must lie in the
 // first 4 KB of the kernel parameters (measured: TMA on a __grid_constant__
 // map at a larger parameter offset faults).

@@ -394,7 +394,7 @@ def test_variants_batch_splits_and_determinism_bitwise(W):
 
 
 def test_more_volumes_than_one_launch(W):
-    """batch > kTmaVolPerLaunch (16) / kMaxVolPerLaunch (128) is chunked; volume ids
+    """batch > kTmaVolPerLaunch (16) / kMaxVolPerLaunch (104) is chunked; volume ids
     stay per volume (both staging paths and the gather variant)."""
     shape = (16, 12, 32)
     B = 131
@@ -405,7 +405,7 @@ def test_more_volumes_than_one_launch(W):
     As = [_oracle_affine(d, shape, shape) for d in ds]
     for variant in (0, 1):
         g_img, g_lbl, ref = run_case(W, imgs, lbls, As, ds, FULL, list(range(B)),
-                                     oracle_volumes=[0, 1, 15, 16, 17, 127, 128, 130],
+                                     oracle_volumes=[0, 1, 15, 16, 17, 103, 104, 105, 127, 128, 130],
                                      variant=variant)
         check(g_img, g_lbl, ref, ds, FULL, f"chunked v{variant}")
 

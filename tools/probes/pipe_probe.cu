@@ -23,6 +23,11 @@ __global__ void probe(float* out, int n) {
       if (K == 5) u[i] = (u[i] ^ 0x5bd1e995u) + (u[i] >> 3);    // LOP3/IADD/SHF
       if (K == 6) { a[i].x = __fmaf_rn(a[i].x, m.x, c.x); a[i].y = __fadd_rn(a[i].y, c.y); }  // FFMA + FADD
       if (K == 7) { a[i] = __ffma2_rn(a[i], m, c); u[i] = (u[i] ^ 0x5bd1e995u) + 3u; }  // FFMA2 + LOP3/IADD
+      if (K == 8) { float r; asm volatile("set.ge.f32.f32 %0, %1, 0f3F000000;" : "=f"(r) : "f"(a[i].x)); a[i].x = __int_as_float(__float_as_int(r) ^ u[i]); }  // FSET + LOP3
+      if (K == 9) { u[i] = __float_as_uint(__uint2float_rn(u[i])) ^ 0x1234u; }  // I2FP + LOP3
+      if (K == 10) { uint64_t p = (uint64_t)u[i] * 0xD2511F53u; u[i] = (uint32_t)(p >> 32) + (uint32_t)p; a[i] = __fadd2_rn(a[i], c); }  // IMAD.WIDE + IADD + FADD2
+      if (K == 11) { a[i] = __fadd2_rn(a[i], c); u[i] = u[i] * 0x9E3779B9u + 7u; }  // FADD2 + IMAD
+      if (K == 12) { a[i].x = __fadd_rn(a[i].x, c.x); a[i].y = __fadd_rn(a[i].y, c.y); }  // 2 FADD
     }
   }
   float s = 0; for (int i = 0; i < 8; ++i) s += a[i].x + a[i].y + u[i];
@@ -55,5 +60,10 @@ int main() {
   run<5>("LOP3+SHF+IADD (alu)", out, 24);
   run<6>("FFMA+FADD", out, 16);
   run<7>("FFMA2+LOP3/IADD", out, 16);
+  run<8>("FSET+LOP3", out, 16);
+  run<9>("I2FP+LOP3", out, 16);
+  run<10>("IMAD.WIDE+IADD+FADD2", out, 24);
+  run<11>("FADD2+IMAD", out, 16);
+  run<12>("FADD x2", out, 16);
   return 0;
 }
