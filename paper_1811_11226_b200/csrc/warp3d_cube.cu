@@ -559,6 +559,127 @@ __device__ __forceinline__ void sample_gather(const WarpArgs& a, const T* __rest
   img = lerp1(lerp1(c00, c10, ty), lerp1(c01, c11, ty), tz);
 }
 
+// Gather sampling of a y-pair through L1/L2 (the GATHER kernel; tiles whose
+// footprint does not fit the buffer), same arithmetic as sample2: floor / frac
+// by the magic-number add, 32-bit cell offsets read back from the float bits
+// (o = fx + nx fy + nx ny fz, mod 2^32; the volume has < 2^31 voxels), the
+// same lerp nesting (R5) and nearest rule (R7).  The tile's class (host box
+// offsets, tile_inside / tile_outside) picks the mode:
+//   kGIn:  every trilinear corner and nearest voxel of the tile is inside --
+//          no clamps, no predicates;
+//   kGOut: every sample is outside (p_k < -1 or p_k > n_k for some axis k on
+//          the whole tile) -- fill / label_fill, no loads;
+//   kGEdge: p clamped to [-1, n] (a clamped coordinate reads only outside
+//          cells or gets weight 0 on an inside one: R6 / R8 exactly, as the
+//          clamped staging boxes) and every corner load predicated on its cell
+//          being inside, fill otherwise.
+enum { kGEdge = 0, kGIn = 1, kGOut = 2 };
+struct GView {
+  uint32_t nx, ny, nz;  // input dims
+  uint32_t sy, sz;      // element strides nx, nx ny
+  uint32_t C;           // -kMbits (1 + sy + sz) mod 2^32: o = bits(sx) + sy bits(sy) + sz bits(sz) + C
+  float fnx, fny, fnz;
+};
+__device__ __forceinline__ GView make_gview(const WarpArgs& a) {
+  GView g;
+  g.nx = static_cast<uint32_t>(a.nx);
+  g.ny = static_cast<uint32_t>(a.ny);
+  g.nz = static_cast<uint32_t>(a.nz);
+  g.sy = g.nx;
+  g.sz = g.nx * g.ny;
+  g.C = 0u - static_cast<uint32_t>(kMbits) * (1u + g.sy + g.sz);
+  g.fnx = static_cast<float>(a.nx);
+  g.fny = static_cast<float>(a.ny);
+  g.fnz = static_cast<float>(a.nz);
+  return g;
+}
+template <class T, bool kLabels, int kGMode>
+__device__ __forceinline__ void gather2(const WarpArgs& a, const T* __restrict__ vin,
+                                        const uint8_t* __restrict__ lin, const GView& g, float2 px,
+                                        float2 py, float2 pz, float2& img, uint32_t& l0,
+                                        uint32_t& l1) {
+  if (kGMode == kGOut) {
+    img = f2(a.fill);
+    l0 = l1 = a.label_fill;
+    return;
+  }
+  if (kGMode == kGEdge) {
+    px = make_float2(fminf(fmaxf(px.x, -1.0f), g.fnx), fminf(fmaxf(px.y, -1.0f), g.fnx));
+    py = make_float2(fminf(fmaxf(py.x, -1.0f), g.fny), fminf(fmaxf(py.y, -1.0f), g.fny));
+    pz = make_float2(fminf(fmaxf(pz.x, -1.0f), g.fnz), fminf(fmaxf(pz.y, -1.0f), g.fnz));
+  }
+  const float2 sx = add2_rm(px, f2(kM)), sy = add2_rm(py, f2(kM)), sz = add2_rm(pz, f2(kM));
+  const float2 tx = sub2(px, sub2(sx, f2(kM)));
+  const float2 ty = sub2(py, sub2(sy, f2(kM)));
+  const float2 tz = sub2(pz, sub2(sz, f2(kM)));
+  const float2 sxy[3] = {sx, sy, sz}, txy[3] = {tx, ty, tz};
+  float c[2][8];
+  uint32_t lab[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // the two voxels of the pair
+    const uint32_t bx = __float_as_uint(h ? sxy[0].y : sxy[0].x);
+    const uint32_t by = __float_as_uint(h ? sxy[1].y : sxy[1].x);
+    const uint32_t bz = __float_as_uint(h ? sxy[2].y : sxy[2].x);
+    const int32_t o = static_cast<int32_t>(bx + g.sy * by + g.sz * bz + g.C);
+    const T* b = vin + o;
+    const T* bY = b + g.sy;
+    const T* bZ = b + g.sz;
+    const T* bYZ = bZ + g.sy;
+    if (kGMode == kGIn) {
+      c[h][0] = InT<T>::load(b);
+      c[h][1] = InT<T>::load(b + 1);
+      c[h][2] = InT<T>::load(bY);
+      c[h][3] = InT<T>::load(bY + 1);
+      c[h][4] = InT<T>::load(bZ);
+      c[h][5] = InT<T>::load(bZ + 1);
+      c[h][6] = InT<T>::load(bYZ);
+      c[h][7] = InT<T>::load(bYZ + 1);
+    } else {
+      // cell coordinates in [-1, n]: corner k inside iff (unsigned) index < n
+      const uint32_t fx = bx - static_cast<uint32_t>(kMbits);
+      const uint32_t fy = by - static_cast<uint32_t>(kMbits);
+      const uint32_t fz = bz - static_cast<uint32_t>(kMbits);
+      const bool x0 = fx < g.nx, x1 = fx + 1u < g.nx, y0 = fy < g.ny, y1 = fy + 1u < g.ny;
+      const bool z0 = fz < g.nz, z1 = fz + 1u < g.nz;
+      const float f = a.fill;
+      c[h][0] = (x0 & y0 & z0) ? InT<T>::load(b) : f;
+      c[h][1] = (x1 & y0 & z0) ? InT<T>::load(b + 1) : f;
+      c[h][2] = (x0 & y1 & z0) ? InT<T>::load(bY) : f;
+      c[h][3] = (x1 & y1 & z0) ? InT<T>::load(bY + 1) : f;
+      c[h][4] = (x0 & y0 & z1) ? InT<T>::load(bZ) : f;
+      c[h][5] = (x1 & y0 & z1) ? InT<T>::load(bZ + 1) : f;
+      c[h][6] = (x0 & y1 & z1) ? InT<T>::load(bYZ) : f;
+      c[h][7] = (x1 & y1 & z1) ? InT<T>::load(bYZ + 1) : f;
+    }
+    if (kLabels) {  // nearest voxel (R7): + (t >= 0.5) per axis
+      const uint32_t hx = (h ? txy[0].y : txy[0].x) >= 0.5f;
+      const uint32_t hy = (h ? txy[1].y : txy[1].x) >= 0.5f;
+      const uint32_t hz = (h ? txy[2].y : txy[2].x) >= 0.5f;
+      const uint8_t* q = lin + (o + static_cast<int32_t>(hx + g.sy * hy + g.sz * hz));
+      if (kGMode == kGIn) {
+        lab[h] = __ldg(q);
+      } else {
+        const uint32_t nx_ = bx - static_cast<uint32_t>(kMbits) + hx;
+        const uint32_t ny_ = by - static_cast<uint32_t>(kMbits) + hy;
+        const uint32_t nz_ = bz - static_cast<uint32_t>(kMbits) + hz;
+        lab[h] = (nx_ < g.nx && ny_ < g.ny && nz_ < g.nz) ? static_cast<uint32_t>(__ldg(q))
+                                                          : a.label_fill;
+      }
+    }
+  }
+  const float2 c000 = make_float2(c[0][0], c[1][0]), c100 = make_float2(c[0][1], c[1][1]);
+  const float2 c010 = make_float2(c[0][2], c[1][2]), c110 = make_float2(c[0][3], c[1][3]);
+  const float2 c001 = make_float2(c[0][4], c[1][4]), c101 = make_float2(c[0][5], c[1][5]);
+  const float2 c011 = make_float2(c[0][6], c[1][6]), c111 = make_float2(c[0][7], c[1][7]);
+  const float2 c00 = lerp2(c000, c100, tx), c10 = lerp2(c010, c110, tx);
+  const float2 c01 = lerp2(c001, c101, tx), c11 = lerp2(c011, c111, tx);
+  img = lerp2(lerp2(c00, c10, ty), lerp2(c01, c11, ty), tz);
+  if (kLabels) {
+    l0 = lab[0];
+    l1 = lab[1];
+  }
+}
+
 __device__ __forceinline__ void st_f32(float* p, float v) {
   asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
@@ -587,7 +708,7 @@ __device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
 // n2, n3; computed while the staging copies are in flight) and the loop
 // computes group g + kPre's block.
 template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
-          bool kSameLbl = false, bool kFull = false, int kPre = 1>
+          bool kSameLbl = false, bool kFull = false, int kPre = 1, int kGMode = kGEdge>
 __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
@@ -632,6 +753,7 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
   uint32_t q = static_cast<uint32_t>(X) +
                mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(y0 >> 2));
   float2 Y2 = make_float2(static_cast<float>(y0), static_cast<float>(y0 + 1));
+  const GView gv = make_gview(a);
   // one y-pair (rows ya, ya + 1) with its two normals
   auto pair = [&](int ya, float2 nsp) {
     const float2 px = __ffma2_rn(f2(V.A1[0]), Y2, f2(t0));
@@ -642,6 +764,8 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
     uint32_t l0 = 0, l1 = 0;
     if (kStaged) {
       sample2<T, kLabels, kNearest, kClamp, kSameLbl>(v, px, py, pz, img, l0, l1);
+    } else if (!kNearest) {
+      gather2<T, kLabels, kGMode>(a, vin, lin, gv, px, py, pz, img, l0, l1);
     } else {
       sample_gather<T, kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
       sample_gather<T, kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
@@ -728,6 +852,49 @@ __device__ __forceinline__ float4 first_normals(const WarpArgs& a, const VolDev&
                                   kPh == kPhFull ? a.rk1 : P.rk1));
 }
 
+// Every trilinear corner / nearest voxel of the tile inside the volume, from
+// the tile's origin coordinate p0 and the per-volume offsets of the box (host,
+// cube_cp_box: the box margin bounds the fp32 rounding of every p of the
+// tile): lower corner floor(p0 + box_mlo) >= 0, upper corner p0 + box_mhi <
+// n - 1, the adds rounded outwards.
+__device__ __forceinline__ bool tile_inside(const WarpArgs& a, const VolDev& P, const float p0[3]) {
+  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                      static_cast<float>(a.nz)};
+  bool in = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    in &= (__fadd_rd(p0[k], P.box_mlo[k]) >= 0.0f) &
+          (__fadd_ru(p0[k], P.box_mhi[k]) < n[k] - 1.0f);
+  return in;
+}
+
+// Every sample of the tile outside the volume on some axis k: all p_k < -1
+// (every corner index <= -1, the nearest voxel too) or all p_k > n_k (every
+// index >= n_k), from the same per-volume offsets, adds rounded outwards.
+__device__ __forceinline__ bool tile_outside(const WarpArgs& a, const VolDev& P, const float p0[3]) {
+  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
+                      static_cast<float>(a.nz)};
+  bool out = false;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    out |= (__fadd_ru(p0[k], P.box_mhi[k]) < -1.0f) | (__fadd_rd(p0[k], P.box_mlo[k]) > n[k]);
+  return out;
+}
+
+// The tile's coordinates stay below 2^21 (magic-number floor, float indices):
+// its origin voxel's p below 2^20 and the footprint extent below 200 (host).
+// p0 = p(tile origin voxel), computed once per tile.
+__device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz, float p0[3]) {
+  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
+  bool sane = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    p0[k] = coord(P.A, k, X, Y, Z);
+    sane &= fabsf(p0[k]) < 1048576.0f;
+  }
+  return sane;
+}
+
 // Rare path (out of line): the tile in y-parts of TY/2, TY/4, ... rows, each
 // staged on its own, or gathered when even a 4-row part does not fit (or
 // always, for the W3D_KERNEL_GATHER variant).
@@ -759,8 +926,20 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
     if (threadIdx.x == 0) atomicAdd(&g_cube_tiles[1], 1ull);
     if (!live) return;
     View v;
-    column_rows<T, kLabels, kNearest, kPh, false, false>(a, P, V, v, vi, X, Z, oy, TY / 4,
-                                                      first_normals<kPh>(a, P, V, X, Z, oy));
+    const float4 n = first_normals<kPh>(a, P, V, X, Z, oy);
+    // tile class from the tile's origin coordinate and the per-volume box
+    // offsets (uniform): inside / outside / edge (gather2)
+    float p0[3];
+    const bool sane = cp_sane(P, ox, oy, oz, p0);
+    if (sane && tile_inside(a, P, p0))
+      column_rows<T, kLabels, kNearest, kPh, false, false, false, false, 1, kGIn>(
+          a, P, V, v, vi, X, Z, oy, TY / 4, n);
+    else if (sane && tile_outside(a, P, p0))
+      column_rows<T, kLabels, kNearest, kPh, false, false, false, false, 1, kGOut>(
+          a, P, V, v, vi, X, Z, oy, TY / 4, n);
+    else
+      column_rows<T, kLabels, kNearest, kPh, false, false, false, false, 1, kGEdge>(
+          a, P, V, v, vi, X, Z, oy, TY / 4, n);
     return;
   }
   if (threadIdx.x == 0) {
@@ -899,35 +1078,6 @@ __device__ __forceinline__ void tma_fixup_lbl(const WarpArgs& a, const Box& b, u
              16, a.nx, a.ny, a.nz, a.label_fill * 0x01010101u);
 }
 
-// Every trilinear corner / nearest voxel of the tile inside the volume, from
-// the tile's origin coordinate p0 and the per-volume offsets of the box (host,
-// cube_cp_box: the box margin bounds the fp32 rounding of every p of the
-// tile): lower corner floor(p0 + box_mlo) >= 0, upper corner p0 + box_mhi <
-// n - 1, the adds rounded outwards.
-__device__ __forceinline__ bool tile_inside(const WarpArgs& a, const VolDev& P, const float p0[3]) {
-  const float n[3] = {static_cast<float>(a.nx), static_cast<float>(a.ny),
-                      static_cast<float>(a.nz)};
-  bool in = true;
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    in &= (__fadd_rd(p0[k], P.box_mlo[k]) >= 0.0f) &
-          (__fadd_ru(p0[k], P.box_mhi[k]) < n[k] - 1.0f);
-  return in;
-}
-
-// The tile's coordinates stay below 2^21 (magic-number floor, float indices):
-// its origin voxel's p below 2^20 and the footprint extent below 200 (host).
-// p0 = p(tile origin voxel), computed once per tile.
-__device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz, float p0[3]) {
-  const float X = static_cast<float>(ox), Y = static_cast<float>(oy), Z = static_cast<float>(oz);
-  bool sane = true;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    p0[k] = coord(P.A, k, X, Y, Z);
-    sane &= fabsf(p0[k]) < 1048576.0f;
-  }
-  return sane;
-}
 
 // The common path: the whole tile staged as ONE box of the volume's fixed dims
 // (cp_w, cp_h, cp_d; host-computed by cube_cp_box to hold any tile's
@@ -1104,7 +1254,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
 #ifndef W3D_TY
 #define W3D_TY 16
 #endif
-constexpr int kTY = W3D_TY, kMinB = W3D_MINB;
+// the gather kernel has no staging buffer: more resident CTAs hide its L2 latency
+#ifndef W3D_GMINB
+#define W3D_GMINB 4  // C4 gather: 144.7 GVoxel/s at 4 (64 registers) vs 140.4 at 3, 124.2 at 6
+#endif
+constexpr int kTY = W3D_TY, kMinB = W3D_MINB, kGMinB = W3D_GMINB;
 // staging buffer (voxels of 5 B): kMinB * (kCapVox * 5 B + 256 + 1 KB) <= 228 KB
 constexpr int kCapVox = (233472 / kMinB - 1024 - 272) / 5;
 
@@ -1118,7 +1272,7 @@ static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured && !kGather) {
     const cudaError_t e = cudaFuncSetAttribute(
-        warp3d_cube_kernel<T, kTY, kMinB, kLabels, kNearest, kPh, kGather>,
+        warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>,
         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
@@ -1127,7 +1281,7 @@ static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
                   static_cast<unsigned>(tiles_z * a.nvol));
   const uint32_t tz_magic =
       tiles_z > 1 ? static_cast<uint32_t>(((uint64_t(1) << 32) + tiles_z - 1) / tiles_z) : 0u;
-  warp3d_cube_kernel<T, kTY, kMinB, kLabels, kNearest, kPh, kGather>
+  warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>
       <<<grid, THREADS, smem, s>>>(a, tiles_z, cap, tz_magic);
   return cudaGetLastError();
 }
