@@ -1190,6 +1190,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
     warp3d_cube_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap,
                        const uint32_t tz_magic) {
   __shared__ __align__(8) unsigned long long s_mbar;
+  // let a programmatic dependent launch (the next chunk of the same call,
+  // WarpArgs::pdl) start as this grid's last CTAs run; a no-op otherwise
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // grid = (tiles_x, tiles_y, tiles_z * volumes); vi = blockIdx.z / tiles_z by
   // multiply-high with tz_magic = ceil(2^32 / tiles_z) (exact for operands < 2^16)
   const int vi = tiles_z == 1 ? static_cast<int>(blockIdx.z)
@@ -1281,9 +1284,27 @@ static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
                   static_cast<unsigned>(tiles_z * a.nvol));
   const uint32_t tz_magic =
       tiles_z > 1 ? static_cast<uint32_t>(((uint64_t(1) << 32) + tiles_z - 1) / tiles_z) : 0u;
-  warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>
-      <<<grid, THREADS, smem, s>>>(a, tiles_z, cap, tz_magic);
-  return cudaGetLastError();
+  if (!a.pdl) {
+    warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>
+        <<<grid, THREADS, smem, s>>>(a, tiles_z, cap, tz_magic);
+    return cudaGetLastError();
+  }
+  // a later chunk of the same call: its CTAs may start while the previous
+  // chunk's last wave drains (every CTA triggers its dependents on entry; the
+  // chunks share no data, so the kernel never waits on its primary)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(
+      &cfg, warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>,
+      a, tiles_z, cap, tz_magic);
 }
 
 // The full photometric chain on every volume of the launch (the training

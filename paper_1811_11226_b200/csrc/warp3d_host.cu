@@ -347,6 +347,7 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       for (int32_t i = 0; i < nv; ++i) any_box |= args.vol[i].cp_rows != 0;
       gather = !any_box;
     }
+    args.pdl = v0 > 0 ? 1 : 0;  // the first chunk waits for all prior work on the stream
     const cudaError_t e = launch_cube(args, gather, stream);
     if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");
   }

@@ -88,7 +88,9 @@ struct alignas(64) WarpArgs {
   int32_t nvol;           // volumes in this launch
   int32_t use_tma;        // tensor maps valid for the volumes with box_w > 0
   int32_t in_aligned;     // every volume's image (labels) 16 B (8 B) aligned: staged paths
-  int32_t _pad[2];
+  int32_t pdl;            // host only: launch as a programmatic dependent of the previous
+                          // chunk of the same call (independent volumes: no data dependency)
+  int32_t _pad;
   // Philox round keys shared by every volume of the launch (all seeds equal;
   // required by the kPhFull kernels: fixed parameter offsets, so the round
   // function reads them as constant-bank operands)
