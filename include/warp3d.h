@@ -297,14 +297,24 @@ w3d_status warp3d_resample(const float* in, const uint8_t* in_labels, w3d_dims i
  * enqueues all jobs, makes them start after the work already queued on
  * `stream` and makes `stream` wait for the last copy-out, and returns without
  * synchronising (the outputs are valid after `stream` completes).
+ * `flags` (create): W3D_PIPE_LABELS (= 1, the former with_labels) allocates
+ * label slots; W3D_PIPE_CHAIN (= 2) orders each call after the previous calls
+ * on the same pipeline only (slot by slot), not after everything queued on
+ * `stream`: the next batch's copy-in then overlaps the previous batch's
+ * warp and copy-out instead of waiting for it to drain.  With CHAIN the caller
+ * guarantees that in_host holds its data when the call is made and that no
+ * pending device work still reads out_host; the first call of a pipeline
+ * still starts after the work queued on `stream`.  Unknown bits:
+ * W3D_ERR_INVALID_ARG.
  *   in_host          float [batch][in]   (read)
  *   in_labels_host   uint8 [batch][in] or NULL (requires with_labels)
  *   out_host         float [batch][out]  (written)
  *   out_labels_host  uint8 [batch][out]; NULL iff in_labels_host is NULL
  */
 typedef struct w3d_pipeline w3d_pipeline;
+enum { W3D_PIPE_LABELS = 1, W3D_PIPE_CHAIN = 2 };
 w3d_status warp3d_pipeline_create(int32_t depth, w3d_dims in_dims, w3d_dims out_dims,
-                                  int32_t with_labels, w3d_pipeline** out);
+                                  int32_t flags, w3d_pipeline** out);
 w3d_status warp3d_pipeline_run(w3d_pipeline* p, int32_t batch, const float* in_host,
                                const uint8_t* in_labels_host, const w3d_volume_params* params,
                                w3d_interp interp, float fill, uint8_t label_fill,

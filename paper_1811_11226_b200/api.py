@@ -190,12 +190,15 @@ class Pipeline:
     H2D of volume i+1, the warp of volume i and the D2H of volume i-1 overlap.
     Host tensors should be pinned (tensor.pin_memory())."""
 
-    def __init__(self, in_shape_zyx, out_shape_zyx=None, depth=3, labels=True):
+    def __init__(self, in_shape_zyx, out_shape_zyx=None, depth=3, labels=True, chain=False):
+        """chain=True: W3D_PIPE_CHAIN (calls ordered after the previous calls on this
+        pipeline only, so consecutive batches' transfers overlap; see warp3d.h)."""
         self.in_shape = tuple(in_shape_zyx)
         self.out_shape = self.in_shape if out_shape_zyx is None else tuple(out_shape_zyx)
         self._h = ctypes.c_void_p()
+        flags = (1 if labels else 0) | (2 if chain else 0)
         L.check(L.load().warp3d_pipeline_create(int(depth), L.dims(self.in_shape),
-                                                L.dims(self.out_shape), int(bool(labels)),
+                                                L.dims(self.out_shape), flags,
                                                 ctypes.byref(self._h)))
 
     def run(self, inp: torch.Tensor, labels, params, out: torch.Tensor, out_labels=None,

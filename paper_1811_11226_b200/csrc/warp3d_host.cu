@@ -850,6 +850,8 @@ struct w3d_pipeline {
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev_in[8] = {}, ev_comp[8] = {}, ev_out[8] = {};
   cudaEvent_t ev_start = nullptr;
+  bool chain = false;   // W3D_PIPE_CHAIN: calls ordered after the previous calls only
+  int64_t seq = 0;      // jobs submitted so far (slot of job j = j % depth, across calls)
 };
 
 static void pipeline_free(w3d_pipeline* p) {
@@ -868,18 +870,21 @@ static void pipeline_free(w3d_pipeline* p) {
 }
 
 w3d_status warp3d_pipeline_create(int32_t depth, w3d_dims in_dims, w3d_dims out_dims,
-                                  int32_t with_labels, w3d_pipeline** out) {
+                                  int32_t flags, w3d_pipeline** out) {
   if (!out) return fail(W3D_ERR_INVALID_ARG, "out must be non-NULL");
   *out = nullptr;
   if (depth < 1 || depth > 8) return fail(W3D_ERR_INVALID_ARG, "depth = %d must be in [1, 8]", depth);
   w3d_status st = check_dims(in_dims, "in_dims");
   if (st != W3D_OK) return st;
   if ((st = check_dims(out_dims, "out_dims")) != W3D_OK) return st;
+  if (flags & ~(W3D_PIPE_LABELS | W3D_PIPE_CHAIN))
+    return fail(W3D_ERR_INVALID_ARG, "flags = %d: unknown bits", flags);
   w3d_pipeline* p = new w3d_pipeline;
   p->depth = depth;
   p->in_dims = in_dims;
   p->out_dims = out_dims;
-  p->labels = with_labels != 0;
+  p->labels = (flags & W3D_PIPE_LABELS) != 0;
+  p->chain = (flags & W3D_PIPE_CHAIN) != 0;
   auto round256 = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t bi = round256(size_t(nvox(in_dims)) * 4), bo = round256(size_t(nvox(out_dims)) * 4);
   const size_t bli = p->labels ? round256(size_t(nvox(in_dims))) : 0;
@@ -938,11 +943,15 @@ w3d_status warp3d_pipeline_run(w3d_pipeline* p, int32_t batch, const float* in_h
   cudaStream_t user = static_cast<cudaStream_t>(stream);
   const size_t ni = size_t(nvox(p->in_dims)), no = size_t(nvox(p->out_dims));
   const bool lab = in_labels_host != nullptr;
-  cudaError_t e = cudaEventRecord(p->ev_start, user);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_in, p->ev_start, 0);
+  cudaError_t e = cudaSuccess;
+  if (!p->chain || p->seq == 0) {  // after the work already queued on `stream`
+    e = cudaEventRecord(p->ev_start, user);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_in, p->ev_start, 0);
+  }
   for (int32_t i = 0; i < batch && e == cudaSuccess; ++i) {
-    const int s = i % p->depth;
-    if (i >= p->depth) e = cudaStreamWaitEvent(p->s_in, p->ev_out[s], 0);  // slot free again
+    const int64_t j = p->seq + i;  // job number across calls
+    const int s = static_cast<int>(j % p->depth);
+    if (j >= p->depth) e = cudaStreamWaitEvent(p->s_in, p->ev_out[s], 0);  // slot free again
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(p->in_img[s], in_host + ni * size_t(i), ni * 4, cudaMemcpyHostToDevice,
                           p->s_in);
@@ -966,7 +975,9 @@ w3d_status warp3d_pipeline_run(w3d_pipeline* p, int32_t batch, const float* in_h
                           cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess) e = cudaEventRecord(p->ev_out[s], p->s_out);
   }
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(user, p->ev_out[(batch - 1) % p->depth], 0);
+  if (e == cudaSuccess)
+    e = cudaStreamWaitEvent(user, p->ev_out[(p->seq + batch - 1) % p->depth], 0);
+  p->seq += batch;
   if (e != cudaSuccess) return cuda_fail(e, "warp3d_pipeline_run");
   return ok();
 }

@@ -179,6 +179,7 @@ def test_pipeline_create_validates(W):
     assert L.warp3d_pipeline_create(0, _lib.Dims(4, 4, 4), _lib.Dims(4, 4, 4), 1, ctypes.byref(h)) == 1
     assert L.warp3d_pipeline_create(9, _lib.Dims(4, 4, 4), _lib.Dims(4, 4, 4), 1, ctypes.byref(h)) == 1
     assert L.warp3d_pipeline_create(2, _lib.Dims(0, 4, 4), _lib.Dims(4, 4, 4), 1, ctypes.byref(h)) == 1
+    assert L.warp3d_pipeline_create(2, _lib.Dims(4, 4, 4), _lib.Dims(4, 4, 4), 4, ctypes.byref(h)) == 1
     assert L.warp3d_pipeline_run(None, 1, None, None, None, 0, 0.0, 0, None, None, None) == 1
     assert L.warp3d_pipeline_destroy(None) == 0
 

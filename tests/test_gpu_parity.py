@@ -460,6 +460,34 @@ def test_pipeline_matches_device_batched(W, depth, B):
     pipe2.close()
 
 
+@pytest.mark.parametrize("depth,B", [(1, 2), (2, 3), (3, 4)])
+def test_pipeline_chained_calls_back_to_back(W, depth, B):
+    """W3D_PIPE_CHAIN: consecutive calls enqueued without a synchronisation between
+    them (each into its own host outputs, slots wrapping across calls) give the
+    device path's bits for every call."""
+    shape = (20, 24, 32)
+    calls = 3
+    imgs, lbls, ds, As = _batch_inputs(shape, B * calls, synth.TRAIN)
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B * calls)]
+    ref, ref_l = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(),
+                                         torch.from_numpy(lbls).cuda(), params, fill=-1000.0,
+                                         label_fill=3)
+    pipe = W.Pipeline(shape, shape, depth=depth, labels=True, chain=True)
+    h_img = torch.from_numpy(imgs).pin_memory()
+    h_lbl = torch.from_numpy(lbls).pin_memory()
+    outs = [(torch.full((B, *shape), 7.0).pin_memory(),
+             torch.zeros((B, *shape), dtype=torch.uint8).pin_memory()) for _ in range(calls)]
+    for c in range(calls):
+        sl = slice(c * B, (c + 1) * B)
+        pipe.run(h_img[sl], h_lbl[sl], params[sl], outs[c][0], outs[c][1], fill=-1000.0,
+                 label_fill=3)
+    torch.cuda.current_stream().synchronize()
+    for c in range(calls):
+        sl = slice(c * B, (c + 1) * B)
+        assert torch.equal(outs[c][0], ref[sl].cpu()) and torch.equal(outs[c][1], ref_l[sl].cpu())
+    pipe.close()
+
+
 # ----------------------------------------------------------------------------- NEXT-3 resampling
 @pytest.mark.parametrize("shape,sigma", [
     ((20, 17, 23), (2.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0)),
