@@ -34,6 +34,10 @@ import synth  # noqa: E402
 METRIC = "augmented GVoxel/s (image+label)"
 UNIT = "GVoxel/s"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+# context only, not a target: another machine, transfers included
+PAPER_CONTEXT = ("paper: 2.6-8.1x GPU over SciPy, 4x Titan X Pascal vs i7-6900K, "
+                 "74-125 ms per 3 mm CT volume incl. host<->device transfers "
+                 "(PAPER.md:777-779, 799-804)")
 
 WORKLOADS = {
     "c3": dict(shape=(160, 128, 128), per_gpu=16, ranges="train",
@@ -474,8 +478,10 @@ def main():
                          "alg_bytes_per_launch": per_launch_bytes,
                          "alg_bytes_per_voxel": alg_bytes / (B * nvox_out),
                          "naive_frac": naive_bytes / (total_ms / args.steps * 1e-3) / 1e9 / peak,
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
                          "footprint": {"F_img": f_img, "F_lbl": f_lbl}},
             "cpu_baseline": cpu,
+            "paper_context": PAPER_CONTEXT,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "tiles": {"staged": st0[0] - tiles_before[0], "gather": st0[1] - tiles_before[1],
