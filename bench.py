@@ -233,7 +233,17 @@ def oracle_sample(shape, vids, ranges, imgs, lbls, cpu_seconds, max_voxels=None)
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(max_workers=cores) as ex:
         vox = sum(ex.map(run, sel))
-    return vox, time.perf_counter() - t0, cores
+    return vox, time.perf_counter() - t0, cores, per_vox
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -252,7 +262,7 @@ def run_reference(args):
         oracle_sample(shape, vids, ranges, imgs, lbls, per_step)
     tot_vox, tot_s, cores = 0, 0.0, 1
     for _ in range(args.steps):
-        v, s, cores = oracle_sample(shape, vids, ranges, imgs, lbls, per_step)
+        v, s, cores, _ = oracle_sample(shape, vids, ranges, imgs, lbls, per_step)
         tot_vox += v
         tot_s += s
     value = tot_vox / tot_s / 1e9
@@ -455,10 +465,11 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, s, cores = oracle_sample(shape, vids, ranges, imgs, lbls, args.cpu_seconds)
+        v, s, cores, per_vox = oracle_sample(shape, vids, ranges, imgs, lbls, args.cpu_seconds)
         cpu = {"value": v / s / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{v} output voxels of this workload (z-slabs of its volumes), "
-                         f"oracle_warp_points on {cores} threads, {s:.1f} s wall"}
+                         f"oracle_warp_points on {cores} threads, {s:.1f} s wall",
+               "single_core_value": 1e-9 / per_vox, "cpu_model": cpu_model()}
 
     if rank == 0:
         peak, peak_src = measured_peaks()
