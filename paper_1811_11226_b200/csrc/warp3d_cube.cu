@@ -122,7 +122,14 @@ template <> struct InT<float> {
 };
 template <> struct InT<int16_t> {
   static constexpr int kBytes = 2, kChunk = 8;
-  __device__ static float load(const int16_t* p) { return static_cast<float>(__ldg(p)); }
+  __device__ static float load(const int16_t* p) {  // I2FP.F32.S32 (ALU), not I2F.S16 (XU)
+    float v;
+    // volatile: a predicated corner load must not be speculated (out-of-volume address)
+    asm volatile("{\n\t.reg .s32 h;\n\tld.global.nc.s16 h, [%1];\n\tcvt.rn.f32.s32 %0, h;\n\t}"
+        : "=f"(v)
+        : "l"(p));
+    return v;
+  }
 };
 // per-volume input addresses (uniform batches or per-volume allocations, NEXT-4)
 template <class T> __device__ __forceinline__ const T* vol_in(const VolDev& P) {
@@ -441,19 +448,21 @@ template <> __device__ __forceinline__ void lds_pair<float>(uint32_t a, float& v
                : "=f"(v0), "=f"(v1)
                : "r"(a));
 }
-// int16: exact conversion (cvt.rn.f32.s16; measured faster than an
-// integer-bias-then-FADD2 conversion on the FMA pipe: 211 vs 206 GVoxel/s)
+// int16: the load sign-extends into a 32-bit register and the exact
+// conversion is cvt.rn.f32.s32 (I2FP on the ALU pipe); cvt.rn.f32.s16 from a
+// 16-bit register compiles to I2F.S16 on the quarter-rate XU pipe, which the
+// Box-Muller / gamma MUFUs already load
 template <> __device__ __forceinline__ void lds_pair<int16_t>(uint32_t a, float& v0, float& v1) {
   asm volatile(
-      "{\n\t.reg .s16 h0, h1;\n\tld.shared.s16 h0, [%2];\n\tld.shared.s16 h1, [%2+2];\n\t"
-      "cvt.rn.f32.s16 %0, h0;\n\tcvt.rn.f32.s16 %1, h1;\n\t}"
+      "{\n\t.reg .s32 h0, h1;\n\tld.shared.s16 h0, [%2];\n\tld.shared.s16 h1, [%2+2];\n\t"
+      "cvt.rn.f32.s32 %0, h0;\n\tcvt.rn.f32.s32 %1, h1;\n\t}"
       : "=f"(v0), "=f"(v1)
       : "r"(a));
 }
 template <class T> __device__ __forceinline__ float lds_one(uint32_t a) {
   float v0, v1;
   if (InT<T>::kBytes == 4) return lds_f32(a);
-  asm volatile("{\n\t.reg .s16 h0;\n\tld.shared.s16 h0, [%1];\n\tcvt.rn.f32.s16 %0, h0;\n\t}"
+  asm volatile("{\n\t.reg .s32 h0;\n\tld.shared.s16 h0, [%1];\n\tcvt.rn.f32.s32 %0, h0;\n\t}"
                : "=f"(v0)
                : "r"(a));
   (void)v1;
