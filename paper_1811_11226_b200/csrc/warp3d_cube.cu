@@ -582,7 +582,9 @@ __device__ __forceinline__ void sample_gather(const WarpArgs& a, const T* __rest
 //          cells or gets weight 0 on an inside one: R6 / R8 exactly, as the
 //          clamped staging boxes) and every corner load predicated on its cell
 //          being inside, fill otherwise.
-enum { kGEdge = 0, kGIn = 1, kGOut = 2 };
+//   kGWide: a dim >= 2^21 (the magic-number floor needs |p| < 2^22): the
+//          per-voxel sample_gather with float floors and 64-bit offsets.
+enum { kGEdge = 0, kGIn = 1, kGOut = 2, kGWide = 3 };
 struct GView {
   uint32_t nx, ny, nz;  // input dims
   uint32_t sy, sz;      // element strides nx, nx ny
@@ -773,7 +775,7 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
     uint32_t l0 = 0, l1 = 0;
     if (kStaged) {
       sample2<T, kLabels, kNearest, kClamp, kSameLbl>(v, px, py, pz, img, l0, l1);
-    } else if (!kNearest) {
+    } else if (!kNearest && kGMode != kGWide) {
       gather2<T, kLabels, kGMode>(a, vin, lin, gv, px, py, pz, img, l0, l1);
     } else {
       sample_gather<T, kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
@@ -940,7 +942,10 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int tiles_z, int c
     // offsets (uniform): inside / outside / edge (gather2)
     float p0[3];
     const bool sane = cp_sane(P, ox, oy, oz, p0);
-    if (sane && tile_inside(a, P, p0))
+    if (a.nx >= (1 << 21) || a.ny >= (1 << 21) || a.nz >= (1 << 21))
+      column_rows<T, kLabels, kNearest, kPh, false, false, false, false, 1, kGWide>(
+          a, P, V, v, vi, X, Z, oy, TY / 4, n);
+    else if (sane && tile_inside(a, P, p0))
       column_rows<T, kLabels, kNearest, kPh, false, false, false, false, 1, kGIn>(
           a, P, V, v, vi, X, Z, oy, TY / 4, n);
     else if (sane && tile_outside(a, P, p0))

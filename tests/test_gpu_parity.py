@@ -268,6 +268,33 @@ def test_half_integer_ties_and_integer_coordinates(W):
         check(g_img, g_lbl, ref, [d, d], O.NOISE, f"ties v{v}")
 
 
+def test_gather_tile_classes_and_wide_rows(W):
+    """The gather sampler's tile classes on one volume -- inside (no predicates),
+    outside (fill, no loads), edge (clamped, predicated) -- and a row of >= 2^21
+    voxels (the per-voxel float-floor gather): oracle parity on both kernels."""
+    shape = (40, 36, 44)
+    img, lbl = synth.phantom(shape)
+    A = np.zeros((3, 4), np.float32)
+    c, s_ = np.cos(0.3), np.sin(0.3)
+    A[:, :3] = [[0.9 * c, -0.9 * s_, 0.05], [0.9 * s_, 0.9 * c, 0.0], [0.0, 0.1, 1.2]]
+    A[:, 3] = (30.0, -25.0, 8.0)  # part of the output far outside, part inside
+    d = synth.draw(synth.TRAIN, 9)
+    for variant in (0, 1):
+        g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], FULL, [4],
+                                     variant=variant, fill=-1000.0, label_fill=5)
+        check(g_img, g_lbl, ref, [d], FULL, f"tile classes v{variant}")
+    wide = (2, 2, (1 << 21) + 12)
+    rng = np.random.default_rng(11)
+    wimg = rng.normal(0.0, 300.0, wide).astype(np.float32)
+    wlbl = rng.integers(0, 6, wide, dtype=np.uint8)
+    A = np.zeros((3, 4), np.float32)
+    A[:, :3] = [[0.999, 0.02, 0.0], [0.0005, 1.0, 0.0], [0.0, 0.0, 1.0]]
+    A[:, 3] = (-3.25, 0.125, 0.0)
+    g_img, g_lbl, ref = run_case(W, wimg[None], wlbl[None], [A], [d], FULL, [4], variant=0,
+                                 fill=-1000.0, label_fill=5)
+    check(g_img, g_lbl, ref, [d], FULL, "wide rows")
+
+
 def test_single_volume_entry_point(W):
     img, _ = synth.phantom((20, 24, 28))
     d = synth.draw(synth.TRAIN, 9)
