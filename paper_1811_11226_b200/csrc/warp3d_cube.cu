@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdint>
+#include <cstring>
 
 #include "philox.cuh"
 #include "warp3d_internal.cuh"
@@ -1254,10 +1255,12 @@ __device__ __forceinline__ bool cube_tile(const WarpArgs& a, int cap, int vi, in
 // x-fastest, then y, then z.  (A persistent grid of 3 CTAs per SM walking the
 // tiles with the mbarrier phase carried across tiles measured 207 vs 272
 // GVoxel/s on C3: each CTA's staging latency is exposed between its tiles.)
-template <class T, int TY, int MINB, bool kLabels, bool kNearest, int kPh, bool kGather>
+template <class T, int TY, int MINB, bool kLabels, bool kNearest, int kPh, bool kGather, int NV>
 __global__ void __launch_bounds__(THREADS, MINB)
-    warp3d_cube_kernel(const __grid_constant__ WarpArgs a, const int tiles_z, const int cap,
+    warp3d_cube_kernel(const __grid_constant__ WarpArgsT<NV> an, const int tiles_z, const int cap,
                        const uint32_t tz_magic) {
+  // the WarpArgs prefix of the parameter block (vol[vi] read for vi < nvol <= NV only)
+  const WarpArgs& a = reinterpret_cast<const WarpArgs&>(an);
   __shared__ __align__(8) unsigned long long s_mbar;
   // let a programmatic dependent launch (the next chunk of the same call,
   // WarpArgs::pdl) start as this grid's last CTAs run; a no-op otherwise
@@ -1293,8 +1296,8 @@ constexpr int kTY = W3D_TY, kMinB = W3D_MINB, kGMinB = W3D_GMINB;
 // staging buffer (voxels of 5 B): kMinB * (kCapVox * 5 B + 256 + 1 KB) <= 228 KB
 constexpr int kCapVox = (233472 / kMinB - 1024 - 272) / 5;
 
-template <class T, bool kLabels, bool kNearest, int kPh, bool kGather = false>
-static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
+template <class T, bool kLabels, bool kNearest, int kPh, bool kGather, int NV>
+static cudaError_t launch_n(const WarpArgsT<NV>& a, cudaStream_t s) {
   const int tiles_x = (a.mx + TX - 1) / TX, tiles_y = (a.my + kTY - 1) / kTY;
   const int tiles_z = (a.mz + TZ - 1) / TZ;
   if (tiles_y > 65535 || int64_t(tiles_z) * a.nvol > 65535) return cudaErrorInvalidConfiguration;
@@ -1303,7 +1306,7 @@ static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured && !kGather) {
     const cudaError_t e = cudaFuncSetAttribute(
-        warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>,
+        warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>,
         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
@@ -1313,7 +1316,7 @@ static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
   const uint32_t tz_magic =
       tiles_z > 1 ? static_cast<uint32_t>(((uint64_t(1) << 32) + tiles_z - 1) / tiles_z) : 0u;
   if (!a.pdl) {
-    warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>
+    warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>
         <<<grid, THREADS, smem, s>>>(a, tiles_z, cap, tz_magic);
     return cudaGetLastError();
   }
@@ -1331,8 +1334,17 @@ static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(
-      &cfg, warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather>,
+      &cfg, warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>,
       a, tiles_z, cap, tz_magic);
+}
+
+// launches of at most kSmallVol volumes pass the small parameter block
+template <class T, bool kLabels, bool kNearest, int kPh, bool kGather = false>
+static cudaError_t launch_v(const WarpArgs& a, cudaStream_t s) {
+  if (a.nvol > kSmallVol) return launch_n<T, kLabels, kNearest, kPh, kGather>(a, s);
+  WarpArgsSmall b;
+  std::memcpy(&b, &a, sizeof(b));  // header, tensor maps and vol[0, kSmallVol)
+  return launch_n<T, kLabels, kNearest, kPh, kGather>(b, s);
 }
 
 // The full photometric chain on every volume of the launch (the training

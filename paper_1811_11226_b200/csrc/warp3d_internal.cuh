@@ -1,6 +1,7 @@
 // warp3d_internal.cuh -- launch-argument structs shared by the host entry
 // points (warp3d_host.cu) and the kernels (warp3d_cube.cu, warp3d_aux.cu).
 #pragma once
+#include <cstddef>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -68,7 +69,13 @@ constexpr int kMaxVolPerLaunch = 104;  // sizeof(WarpArgs) < 32764 B of kernel p
 // map at a larger parameter offset faults).
 constexpr int kTmaVolPerLaunch = 16;
 
-struct alignas(64) WarpArgs {
+// NV = volumes the parameter block holds.  Launches of at most kSmallVol
+// volumes pass WarpArgsT<kSmallVol> (~8.4 KB of parameters instead of ~31 KB:
+// the launch's parameter upload costs ~2.5 us more at 31 KB,
+// tools/probes/param_probe.cu); the kernels read it through the WarpArgs prefix
+// (same layout up to vol[NV], vol last) and never index past nvol <= NV.
+template <int NV>
+struct alignas(64) WarpArgsT {
   // per volume i: tm[2i] 3D (nx, ny, nz) image map (float32 or int16), box
   // (cp_w, cp_h, cp_d); tm[2i+1] uint8 label map, box (box_wl, box_h, cp_d)
   CUtensorMap tm[2 * kTmaVolPerLaunch];
@@ -95,9 +102,13 @@ struct alignas(64) WarpArgs {
   // required by the kPhFull kernels: fixed parameter offsets, so the round
   // function reads them as constant-bank operands)
   uint32_t rk0[10], rk1[10];
-  VolDev vol[kMaxVolPerLaunch];
+  VolDev vol[NV];
 };
+using WarpArgs = WarpArgsT<kMaxVolPerLaunch>;
+constexpr int kSmallVol = 16;
+using WarpArgsSmall = WarpArgsT<kSmallVol>;
 static_assert(sizeof(WarpArgs) <= 32764, "kernel parameter space");
+static_assert(offsetof(WarpArgs, vol) == offsetof(WarpArgsSmall, vol), "WarpArgs prefix layout");
 
 // Launchers.  All return cudaGetLastError() of the launch.
 // warp3d_cube.cu (the warp): cube_supported() = the staged layout requirements.
