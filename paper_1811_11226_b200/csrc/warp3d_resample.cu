@@ -59,6 +59,9 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
 #ifndef W3D_SM_STAGES
 #define W3D_SM_STAGES 6
 #endif
+#ifndef W3D_SM_NYT2  // rows per thread at radius <= 2 (the 1 mm -> 3 mm case)
+#define W3D_SM_NYT2 4
+#endif
 #ifndef W3D_SM_MZ
 #define W3D_SM_MZ 64
 #endif
@@ -260,7 +263,7 @@ cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int
     if (e == cudaSuccess) kernel<<<grid, 256, smem, s>>>(in, out, nx, ny, nz, t);
   };
   if (rmax <= 1) go(smooth_fused_kernel<1, 4>, 1, 4);
-  else if (rmax <= 2) go(smooth_fused_kernel<2, 4>, 2, 4);
+  else if (rmax <= 2) go(smooth_fused_kernel<2, W3D_SM_NYT2>, 2, W3D_SM_NYT2);
   else if (rmax <= 3) go(smooth_fused_kernel<3, 4>, 3, 4);
   else if (rmax <= 4) go(smooth_fused_kernel<4, 2>, 4, 2);
   else if (rmax <= 6) go(smooth_fused_kernel<6, 1>, 6, 1);
