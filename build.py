@@ -42,6 +42,10 @@ def build_oracle(force=False):
 CUDA_SOURCES = [
     "paper_1811_11226_b200/csrc/warp3d_host.cu",
     "paper_1811_11226_b200/csrc/warp3d_cube.cu",
+    "paper_1811_11226_b200/csrc/cube_inst_f32_s.cu",
+    "paper_1811_11226_b200/csrc/cube_inst_f32_l.cu",
+    "paper_1811_11226_b200/csrc/cube_inst_i16_s.cu",
+    "paper_1811_11226_b200/csrc/cube_inst_i16_l.cu",
     "paper_1811_11226_b200/csrc/warp3d_aux.cu",
     "paper_1811_11226_b200/csrc/warp3d_resample.cu",
 ]
@@ -49,20 +53,60 @@ CUDA_HEADERS = [
     "include/warp3d.h",
     "paper_1811_11226_b200/csrc/warp3d_internal.cuh",
     "paper_1811_11226_b200/csrc/philox.cuh",
+    "paper_1811_11226_b200/csrc/cube_config.cuh",
+    "paper_1811_11226_b200/csrc/cube_kernel.cuh",
 ]
+PRODUCT_LIB = os.path.join(ROOT, "paper_1811_11226_b200", "libwarp3d.so")
 
 
-def build_cuda(force=False):
+def _flags(extra):
+    # No --use_fast_math and -fmad=false: the coordinate contract (R4)
+    # and the trilinear lerp nesting use explicit __fmaf_rn, never contraction.
+    return [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-fmad=false",
+            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), *extra]
+
+
+def build_cuda(force=False, out=None, extra=None):
+    """Compile every CUDA unit to an object in parallel, then link the shared library.
+
+    extra: additional nvcc flags (default: $W3D_NVCC_EXTRA, experiment knobs such as
+    -DW3D_TZ=16).  The flags are recorded in a stamp file next to the library and a
+    build with different flags always rebuilds, so a knob build can never be mistaken
+    for the product build (or the reverse).  out: library path (default: the product
+    library the package loads)."""
+    import concurrent.futures as cf
+    import hashlib
+    import json
+    extra = os.environ.get("W3D_NVCC_EXTRA", "").split() if extra is None else list(extra)
+    out = out or PRODUCT_LIB
     srcs = [os.path.join(ROOT, s) for s in CUDA_SOURCES]
     hdrs = [os.path.join(ROOT, h) for h in CUDA_HEADERS]
-    out = os.path.join(ROOT, "paper_1811_11226_b200", "libwarp3d.so")
-    if force or _stale(out, srcs + hdrs):
-        # No --use_fast_math and -fmad=false: the coordinate contract (R4)
-        # and the trilinear lerp nesting use explicit __fmaf_rn, never contraction.
-        extra = os.environ.get("W3D_NVCC_EXTRA", "").split()  # experiment knobs (-DW3D_TZ=16)
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-              "-fmad=false", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), *extra,
-              "-o", out, *srcs])
+    flags = _flags(extra)
+    stamp = out + ".flags"
+    want = json.dumps({"nvcc": NVCC, "flags": flags, "sources": CUDA_SOURCES})
+    have = open(stamp).read() if os.path.exists(stamp) else None
+    if not (force or have != want or _stale(out, srcs + hdrs)):
+        return out
+    tag = hashlib.sha1(want.encode()).hexdigest()[:10]
+    objdir = os.path.join(ROOT, "build", "obj", tag)
+    os.makedirs(objdir, exist_ok=True)
+
+    def obj_of(src):
+        return os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+
+    def compile_one(src):
+        o = obj_of(src)
+        if force or _stale(o, [src] + hdrs):
+            _run([NVCC, *flags, "-c", "-o", o, src])
+        return o
+
+    with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, srcs))
+    if os.path.exists(stamp):
+        os.remove(stamp)
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs])
+    with open(stamp, "w") as f:
+        f.write(want)
     return out
 
 

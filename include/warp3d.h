@@ -66,13 +66,16 @@ typedef enum {
   W3D_KERNEL_GATHER = 1,   /* every corner gathered through L1/L2 (__ldg) with
                               per-corner bounds                                  */
   W3D_KERNEL_STAGED = 2    /* per-tile source footprint staged in shared memory
-                              by cp.async (16 x 16 x 16 output tiles); a footprint
-                              larger than the buffer is split into 2 / 4 y-parts,
+                              (16 x 16 x 16 output tiles): volumes whose worst-
+                              case tile box fits the buffer load one fixed-dims
+                              box per tile by TMA (cp.async.bulk.tensor; image
+                              and, when its 16 B aligned box fits beside it,
+                              labels -- else labels by cp.async); other volumes
+                              use per-tile exact boxes by cp.async, split into
+                              2 / 4 y-parts when larger than the buffer,
                               gathered beyond that.  Layouts without 16 B chunks
                               (nx % 4 != 0, unaligned input) and dims >= 2^21
-                              gather.  (Values 3-5 named TMA / bulk / persistent
-                              staging variants until ABI 1; removed after
-                              measuring slower.)               */
+                              gather.                         */
 } w3d_kernel;
 
 typedef struct {

@@ -31,13 +31,32 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _dev(t, dtype, name):
+def _dev(t, dtype, name, shape=None, device=None):
+    """Device pointer of a contiguous CUDA tensor, after checking its dtype, shape and
+    device (the C side trusts the sizes it derives from dims and batch)."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor")
     if t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} must be on {device}, got {t.device}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _host(t, dtype, name, shape):
+    """Address of a contiguous HOST tensor of exactly this dtype and shape."""
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a host (CPU) tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -89,7 +108,8 @@ def warp3d_affine(inp: torch.Tensor, affine, interp=INTERP_LINEAR, fill=0.0, ph=
     L.check(L.load().warp3d_affine(_dev(inp, torch.float32, "inp"), L.dims(inp.shape), A,
                                    int(interp), float(fill),
                                    None if ph is None else ctypes.byref(ph),
-                                   _dev(out, torch.float32, "out"), L.dims(out.shape), _stream()))
+                                   _dev(out, torch.float32, "out", out_shape, inp.device),
+                                   L.dims(out.shape), _stream()))
     return out
 
 
@@ -113,17 +133,20 @@ def warp3d_affine_batched(inp: torch.Tensor, labels: torch.Tensor | None, params
         arr = (VolumeParams * B)(*params)
     if len(arr) != B:
         raise ValueError(f"{len(arr)} params for a batch of {B}")
+    if (labels is None) != (out_labels is None):
+        raise ValueError("out_labels must be given exactly when labels are")
+    dev, oshape = inp.device, (B, *out_shape)
     if inp.dtype == torch.int16:  # NEXT-4: int16 HU input, float32 output
         fn, src = L.load().warp3d_affine_batched_i16_ex, _dev(inp, torch.int16, "inp")
     else:
         fn, src = L.load().warp3d_affine_batched_ex, _dev(inp, torch.float32, "inp")
     L.check(fn(
         B, src,
-        None if labels is None else _dev(labels, torch.uint8, "labels"),
+        None if labels is None else _dev(labels, torch.uint8, "labels", inp.shape, dev),
         L.dims(inp.shape[1:]), arr, int(interp), float(fill), int(label_fill),
-        _dev(out, torch.float32, "out"),
-        None if out_labels is None else _dev(out_labels, torch.uint8, "out_labels"),
-        L.dims(out.shape[1:]), int(variant), _stream()))
+        _dev(out, torch.float32, "out", oshape, dev),
+        None if out_labels is None else _dev(out_labels, torch.uint8, "out_labels", oshape, dev),
+        L.dims(out_shape), int(variant), _stream()))
     return out, out_labels
 
 
@@ -205,16 +228,21 @@ class Pipeline:
             interp=INTERP_LINEAR, fill=0.0, label_fill=0):
         """inp/out (and labels) are CPU tensors [B, nz, ny, nx]; returns immediately,
         results valid after torch.cuda.current_stream() completes."""
-        for t, name in ((inp, "inp"), (out, "out")):
-            if t.is_cuda or not t.is_contiguous():
-                raise ValueError(f"{name} must be a contiguous host tensor")
+        if inp.dim() != 4:
+            raise ValueError("inp must be [batch, nz, ny, nx]")
         B = inp.shape[0]
+        if len(params) != B:
+            raise ValueError(f"{len(params)} params for a batch of {B}")
+        if (labels is None) != (out_labels is None):
+            raise ValueError("out_labels must be given exactly when labels are")
+        ishape, oshape = (B, *self.in_shape), (B, *self.out_shape)
         arr = params if isinstance(params, ctypes.Array) else (VolumeParams * B)(*params)
         L.check(L.load().warp3d_pipeline_run(
-            self._h, B, ctypes.c_void_p(inp.data_ptr()),
-            None if labels is None else ctypes.c_void_p(labels.data_ptr()), arr, int(interp),
-            float(fill), int(label_fill), ctypes.c_void_p(out.data_ptr()),
-            None if out_labels is None else ctypes.c_void_p(out_labels.data_ptr()), _stream()))
+            self._h, B, _host(inp, torch.float32, "inp", ishape),
+            None if labels is None else _host(labels, torch.uint8, "labels", ishape), arr,
+            int(interp), float(fill), int(label_fill), _host(out, torch.float32, "out", oshape),
+            None if out_labels is None else _host(out_labels, torch.uint8, "out_labels", oshape),
+            _stream()))
         return out, out_labels
 
     def close(self):
@@ -279,7 +307,8 @@ def warp3d_resample(inp: torch.Tensor, labels, spacing_mm, target_mm=3.0, fill=-
     tmp = torch.empty(2 * inp.numel(), dtype=torch.float32, device=inp.device)
     L.check(L.load().warp3d_resample(
         _dev(inp, torch.float32, "inp"), None if labels is None else _dev(labels, torch.uint8,
-                                                                             "labels"),
+                                                                             "labels", inp.shape,
+                                                                             inp.device),
         L.dims(inp.shape), _u(spacing_mm), float(target_mm), float(fill), int(label_fill),
         _dev(out, torch.float32, "out"), None if out_l is None else _dev(out_l, torch.uint8,
                                                                          "out_labels"),

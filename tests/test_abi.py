@@ -201,3 +201,16 @@ def test_resample_host_functions_match_oracle(W):
                               O.resample_affine(shape, out_shape, u, r))
     with pytest.raises(W.Warp3DError):
         W.warp3d_resample_sigma((1.0, 0.0, 1.0), 3.0)
+
+
+def test_product_library_is_the_default_build():
+    """The library the package loads was built with the default flags (the flag stamp
+    written by build.py; a knob build with other flags always rebuilds)."""
+    import json
+    import build
+    build.build_cuda()
+    with open(build.PRODUCT_LIB + ".flags") as f:
+        stamp = json.load(f)
+    extra = [a for a in stamp["flags"] if a not in build._flags([])]
+    assert stamp["flags"] == build._flags([]) and not extra, extra
+    assert stamp["sources"] == build.CUDA_SOURCES

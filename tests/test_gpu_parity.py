@@ -3,6 +3,7 @@ element on seeded inputs, at sizes spanning many tiles and ragged tails, and at
 BASELINE.json's full sizes on sampled voxels.  Labels and Philox words are
 bit-exact; images within the north-star tolerance (tests/tolerance.py)."""
 import concurrent.futures as cf
+import itertools
 import os
 
 import numpy as np
@@ -10,6 +11,7 @@ import pytest
 
 import oracle as O
 import synth
+from exact_p import p_fp32_grid
 from tolerance import assert_image_close
 
 torch = pytest.importorskip("torch")
@@ -83,6 +85,16 @@ def check(g_img, g_lbl, ref, draws, flags, what=""):
         if r_lbl is not None:
             mism = int(np.sum(g_lbl[i] != r_lbl))
             assert mism == 0, f"{what} vol {i}: {mism} label mismatches"
+
+
+def _oracle_refs(imgs, lbls, As, ds, sel, flags=FULL, fill=-1000.0, label_fill=0,
+                 out_shape=None):
+    """Oracle outputs {i: (image, labels)} of volumes `sel` (volume id = index)."""
+    def one(i):
+        return i, O.warp_volume(imgs[i], None if lbls is None else lbls[i], As[i], out_shape,
+                                O.LINEAR, fill, label_fill, _oph(ds[i], flags, i))
+    with _pool() as ex:
+        return dict(ex.map(one, sel))
 
 
 # ----------------------------------------------------------------------------- RNG hooks
@@ -437,10 +449,54 @@ def test_more_volumes_than_one_launch(W):
         check(g_img, g_lbl, ref, ds, FULL, f"chunked v{variant}")
 
 
+def _footprint_host(A, in_shape, out_shape):
+    """(#F_img, #F_lbl) counted here from the exact fp32 p (tests/exact_p.py, R4):
+    F_img = in-volume trilinear corners floor(p) + {0,1}^3 of every sample with
+    -1 < p_k < n_k on every axis (R6: any other sample is exactly fill and reads
+    nothing); F_lbl = in-volume nearest voxels floor(p) + (t >= 1/2) (R7, R8)."""
+    nz, ny, nx = in_shape
+    n = np.array([nx, ny, nz], np.float64).reshape(3, 1)
+    p = p_fp32_grid(A, out_shape).reshape(3, -1).astype(np.float64)
+    live = np.all((p > -1.0) & (p < n), axis=0)
+    f = np.floor(p)
+    marks = np.zeros(in_shape, bool)
+    for c in itertools.product((0, 1), repeat=3):
+        q = f[:, live] + np.array(c, np.float64).reshape(3, 1)
+        ok = np.all((q >= 0) & (q < n), axis=0)
+        qi = q[:, ok].astype(np.int64)
+        marks[qi[2], qi[1], qi[0]] = True
+    r = f + (p - f >= 0.5)
+    ok = np.all((r >= 0) & (r < n), axis=0)
+    ri = r[:, ok].astype(np.int64)
+    lmarks = np.zeros(in_shape, bool)
+    lmarks[ri[2], ri[1], ri[0]] = True
+    return int(marks.sum()), int(lmarks.sum())
+
+
+@pytest.mark.parametrize("in_shape,out_shape,rname", [
+    ((20, 18, 24), (20, 18, 24), "TRAIN"),
+    ((24, 20, 32), (16, 12, 20), "TRAIN"),   # crop (output smaller than input)
+    ((18, 22, 16), (20, 25, 16), "LARGE"),   # large rotations, larger output
+])
+def test_footprint_counts_exact(W, in_shape, out_shape, rname):
+    """#F_img / #F_lbl, the roofline's algorithmic read bytes, equal
+    an independent host count of the same sets from the exact fp32 coordinates."""
+    B = 3
+    ds = [synth.draw(getattr(synth, rname), 40 + i) for i in range(B)]
+    As = [_oracle_affine(d, in_shape, out_shape) for d in ds]
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B)]
+    f_img, f_lbl = W.warp3d_footprint_batched(params, in_shape, out_shape)
+    h_img = h_lbl = 0
+    for A in As:
+        a, b = _footprint_host(A, in_shape, out_shape)
+        h_img += a
+        h_lbl += b
+    assert (f_img, f_lbl) == (h_img, h_lbl)
+
+
 def test_footprint_counts_match_oracle_marking(W):
-    """#F_img / #F_lbl (roofline accounting) equal a host count of the same sets."""
+    """#F_lbl equals the distinct in-volume codes the ORACLE's nearest warp reads."""
     shape = (20, 18, 24)
-    img, lbl = synth.random_volume(shape, 6)
     ds = [synth.draw(synth.TRAIN, i) for i in range(2)]
     As = [_oracle_affine(d, shape, shape) for d in ds]
     params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(2)]
@@ -472,16 +528,21 @@ def test_pipeline_matches_device_batched(W, depth, B):
     h_lbl = torch.from_numpy(lbls).pin_memory()
     out = torch.empty(imgs.shape, dtype=torch.float32).pin_memory()
     out_l = torch.empty(lbls.shape, dtype=torch.uint8).pin_memory()
+    oref = _oracle_refs(imgs, lbls, As, ds, range(B), fill=-1000.0, label_fill=3)
     for _ in range(2):  # reuse across runs
         out.fill_(7.0)
         pipe.run(h_img, h_lbl, params, out, out_l, fill=-1000.0, label_fill=3)
         torch.cuda.current_stream().synchronize()
+        # against the oracle (PAPER.md:379-387 path, the e2e leg of bench.py) ...
+        check(out.numpy(), out_l.numpy(), oref, ds, FULL, f"pipeline depth {depth}")
+        # ... and bitwise against the device-resident call
         assert torch.equal(out, ref.cpu()) and torch.equal(out_l, ref_l.cpu())
     # images only
     pipe2 = W.Pipeline(shape, shape, depth=depth, labels=False)
     out2 = torch.empty(imgs.shape, dtype=torch.float32).pin_memory()
     pipe2.run(h_img, None, params, out2, None, fill=-1000.0)
     torch.cuda.current_stream().synchronize()
+    check(out2.numpy(), None, {i: (oref[i][0], None) for i in oref}, ds, FULL, "pipeline img")
     assert torch.equal(out2, ref.cpu())
     pipe.close()
     pipe2.close()
@@ -509,8 +570,12 @@ def test_pipeline_chained_calls_back_to_back(W, depth, B):
         pipe.run(h_img[sl], h_lbl[sl], params[sl], outs[c][0], outs[c][1], fill=-1000.0,
                  label_fill=3)
     torch.cuda.current_stream().synchronize()
+    oref = _oracle_refs(imgs, lbls, As, ds, range(B * calls), fill=-1000.0, label_fill=3)
     for c in range(calls):
         sl = slice(c * B, (c + 1) * B)
+        part = {i - c * B: oref[i] for i in range(c * B, (c + 1) * B)}
+        check(outs[c][0].numpy(), outs[c][1].numpy(), part, ds[sl], FULL,
+              f"chained call {c} depth {depth}")
         assert torch.equal(outs[c][0], ref[sl].cpu()) and torch.equal(outs[c][1], ref_l[sl].cpu())
     pipe.close()
 
@@ -660,3 +725,37 @@ def test_fused_smoothing_equals_per_axis_passes_bitwise(W, shape, sigma, tmp_pat
     ref = np.load(tmp_path / "ref.npy")
     got = W.warp3d_smooth3d(torch.from_numpy(img).cuda(), sigma).cpu().numpy()
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+# ----------------------------------------------------------------------------- binding checks
+def test_binding_rejects_mismatched_buffers(W):
+    """The Python binding checks dtype, shape and device of every buffer against the
+    batch and dims before the C call (the library trusts the sizes it derives)."""
+    shape = (8, 8, 8)
+    img = torch.zeros((2, *shape), device="cuda")
+    lbl = torch.zeros((2, *shape), dtype=torch.uint8, device="cuda")
+    ps = [W.volume_params(np.eye(3, 4, dtype=np.float32)) for _ in range(2)]
+    with pytest.raises(ValueError):   # labels of another shape
+        W.warp3d_affine_batched(img, lbl[:, :4], ps)
+    with pytest.raises(ValueError):   # output too small for the batch
+        W.warp3d_affine_batched(img, None, ps, out=torch.empty((1, *shape), device="cuda"))
+    with pytest.raises(ValueError):   # output of another shape than out_shape
+        W.warp3d_affine_batched(img, lbl, ps, out_shape=(8, 8, 4),
+                                out_labels=torch.empty((2, *shape), dtype=torch.uint8,
+                                                       device="cuda"))
+    with pytest.raises(TypeError):    # wrong dtype
+        W.warp3d_affine_batched(img, lbl.float(), ps)
+    with pytest.raises(ValueError):   # params count
+        W.warp3d_affine_batched(img, lbl, ps[:1])
+    pipe = W.Pipeline(shape, shape, depth=2, labels=True)
+    h = torch.zeros((2, *shape))
+    hl = torch.zeros((2, *shape), dtype=torch.uint8)
+    with pytest.raises(ValueError):   # host output too small (would overrun the heap)
+        pipe.run(h, hl, ps, torch.zeros((1, *shape)), hl.clone())
+    with pytest.raises(TypeError):    # host labels of the wrong dtype
+        pipe.run(h, hl.float(), ps, h.clone(), hl.clone())
+    with pytest.raises(ValueError):   # params count
+        pipe.run(h, hl, ps[:1], h.clone(), hl.clone())
+    with pytest.raises(TypeError):    # device tensor where a host buffer is required
+        pipe.run(h.cuda(), hl, ps, h.clone(), hl.clone())
+    pipe.close()

@@ -5,7 +5,7 @@ each test to the passage it follows (P1..P14 numbering from SURVEY.md Sec. 8.c).
 import itertools
 import math
 import os
-from fractions import Fraction
+from exact_p import p_fp32, p_fp32_grid
 
 import numpy as np
 import pytest
@@ -285,22 +285,8 @@ def _nearest_brute(n, p):
     return out
 
 
-def _fma32(a, x, c):
-    """Correctly rounded fp32 fma(a, x, c) from exact rational arithmetic."""
-    exact = Fraction(float(a)) * x + Fraction(float(c))
-    f = np.float32(float(exact))
-    best = f
-    for cand in (np.nextafter(f, np.float32(-np.inf)), np.nextafter(f, np.float32(np.inf))):
-        dc, db = abs(Fraction(float(cand)) - exact), abs(Fraction(float(best)) - exact)
-        if dc < db or (dc == db and (int(cand.view(np.uint32)) & 1) == 0):
-            best = cand
-    return np.float32(best)
-
-
 def _p_fp32(A, x, y, z):
-    """p_k = fma(A_k1, y, fma(A_k0, x, fma(A_k2, z, b_k))) in fp32 (R4)."""
-    return [float(_fma32(A[k, 1], y, _fma32(A[k, 0], x, _fma32(A[k, 2], z, A[k, 3]))))
-            for k in range(3)]
+    return p_fp32(A, x, y, z)
 
 
 def test_brute_force_8cubed():
@@ -421,3 +407,15 @@ def test_occlusion_full_height_is_zero_and_input_independent():
     out2, _ = O.warp_volume(img2, lbl, _aff(np.eye(3), (0, 0, 0)), ph=ph)
     assert np.all(out2[2:4] == 0.0)
     assert np.all(out[[0, 1, 4, 5]] == np.clip((img[[0, 1, 4, 5]].astype(np.float64) + 150) / 380, 0, 1).astype(np.float32))
+
+
+def test_exact_p_grid_equals_rational_fma():
+    """The vectorised exact-p helper (used to count footprints in the GPU tests) gives
+    the bits of the rational fp32 FMA chain (R4) at every voxel of a small grid."""
+    for rname, idx in (("TRAIN", 1), ("LARGE", 2)):
+        d = synth.draw(getattr(synth, rname), idx)
+        A = O.compose_affine(O.make_geom(d.rot_rad, d.scale, d.shear, d.flip, d.generic,
+                                         d.disp), (9, 7, 11), (5, 6, 7))[1]
+        g = p_fp32_grid(A, (5, 6, 7))
+        for z, y, x in itertools.product(range(5), range(6), range(7)):
+            assert [float(v) for v in g[:, z, y, x]] == p_fp32(A, x, y, z)
