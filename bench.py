@@ -2,13 +2,18 @@
 """Benchmark of the arXiv 1811.11226 Sec. IV augmentation hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c3|c5|c2|c4] [--variant auto|gather|staged]
+                    [--workload c3|c1|c2|c4|c5|resample] [--variant auto|gather|staged]
+                    [--occlusion] [--dry-run]
 
 One step = one pass of the whole hot path (affine warp of image + labels with
 noise, window/clamp and gamma) over one batch.
 Default workload = BASELINE.json configs[2] ("c3": 16 x 128x128x160 volumes
 per GPU, the training-iteration shape); N GPUs shard volumes by GLOBAL index
 (weak scaling, no collective on the data path; NCCL only gathers timings).
+With --gpus N > 1 and no torchrun environment the script re-launches itself
+under torch.distributed.run with N ranks (one per GPU); a box with fewer than N
+GPUs is an error, never a silent 1-GPU measurement.  --dry-run exercises the
+multi-rank host logic on CPU (gloo) without a GPU.
 
 Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
 """
@@ -19,7 +24,9 @@ import concurrent.futures as cf
 import ctypes
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -39,20 +46,25 @@ PAPER_CONTEXT = ("paper: 2.6-8.1x GPU over SciPy, 4x Titan X Pascal vs i7-6900K,
                  "74-125 ms per 3 mm CT volume incl. host<->device transfers "
                  "(PAPER.md:777-779, 799-804)")
 
+# photometric chains (w3d flags): the training chain and C1's noise-only chain
+PH_FULL, PH_NOISE = 1 | 2 | 4 | 8, 1
 WORKLOADS = {
-    "c3": dict(shape=(160, 128, 128), per_gpu=16, ranges="train",
-               desc="16 x 128x128x160 f32 CT + u8 labels per GPU (BASELINE configs[2])"),
-    "c5": dict(shape=(160, 128, 128), total=256, ranges="train",
-               desc="256 x 128x128x160 f32 CT + u8 labels sharded over N GPUs (configs[4])"),
-    "c2": dict(shape=(160, 128, 128), per_gpu=1, ranges="train",
+    "c1": dict(shape=(32, 32, 32), per_gpu=1, ranges="c1", ph=PH_NOISE,
+               desc="1 x 32^3 f32 + u8 labels per GPU, one fixed affine, noise sigma 10 HU "
+                    "(BASELINE configs[0])"),
+    "c2": dict(shape=(160, 128, 128), per_gpu=1, ranges="train", ph=PH_FULL,
                desc="1 x 128x128x160 f32 CT + u8 labels per GPU (configs[1])"),
-    "c4": dict(shape=(512, 512, 512), per_gpu=1, ranges="large",
+    "c3": dict(shape=(160, 128, 128), per_gpu=16, ranges="train", ph=PH_FULL,
+               desc="16 x 128x128x160 f32 CT + u8 labels per GPU (BASELINE configs[2])"),
+    "c4": dict(shape=(512, 512, 512), per_gpu=1, ranges="large", ph=PH_FULL,
                desc="1 x 512^3 f32 CT + u8 labels per GPU, large rotations (configs[3])"),
+    "c5": dict(shape=(160, 128, 128), total=256, ranges="train", ph=PH_FULL,
+               desc="256 x 128x128x160 f32 CT + u8 labels sharded over N GPUs (configs[4])"),
 }
 N_DISTINCT_PHANTOMS = 4  # input volumes cycle over 4 seeded phantoms (DESIGN.md input recipe)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -61,7 +73,11 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["resample"], default="c3",
                     help="resample: the NEXT-3 step (1 mm^3 512^3 CT -> 3 mm^3), its own metric")
     ap.add_argument("--variant", choices=["auto", "gather", "staged"], default="auto")
+    ap.add_argument("--occlusion", action="store_true",
+                    help="random occlusion per example (PAPER.md:420-438, synth.TRAIN_OCC)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the configs[4] strong-scaling key of the c3 line")
     ap.add_argument("--input", choices=["f32", "i16"], default="f32",
                     help="i16: the same volumes as int16 HU (NEXT-4; 2 B per input voxel)")
     ap.add_argument("--fill", type=float, default=-1000.0,
@@ -70,8 +86,33 @@ def parse():
                     help="image-only warp (diagnostic; the headline includes labels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="target CPU work of the bounded oracle sample")
-    return ap.parse_args()
+                    help="CPU work (core-seconds) of the bounded oracle sample")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank host logic only (gloo on CPU, no GPU, no kernels)")
+    return ap.parse_args(argv)
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: re-exec this script as N ranks (one per GPU) under
+    torch.distributed.run, exactly as the driver launches it; rank 0 prints the line."""
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} requested but {have} CUDA device(s) visible",
+                  file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 def dist_env():
@@ -102,8 +143,22 @@ def reduce_max_ms(ms, dist, device):
     return float(t.item())
 
 
-def ranges_of(workload):
-    return synth.TRAIN if WORKLOADS[workload]["ranges"] == "train" else synth.LARGE
+def ranges_of(workload, occlusion=False):
+    r = WORKLOADS[workload]["ranges"]
+    if r == "c1":
+        return None
+    if r == "train":
+        return synth.TRAIN_OCC if occlusion else synth.TRAIN
+    return synth.LARGE
+
+
+def draws_of(workload, vids, occlusion=False):
+    """Per-volume draws of the workload (keyed by GLOBAL volume index)."""
+    ranges = ranges_of(workload, occlusion)
+    if ranges is None:
+        return [synth.C1_DRAW for _ in vids]
+    mz = WORKLOADS[workload]["shape"][0]
+    return [synth.draw(ranges, v, out_mz=mz if ranges.occ_dmax > 0 else None) for v in vids]
 
 
 def host_inputs(shape, vids):
@@ -128,15 +183,15 @@ def measured_peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload, variant):
-    """dram bytes per launch of the warp kernel from the committed ncu --set full summary."""
+def ncu_evidence(workload, variant):
+    """Per-launch figures of the warp kernel from the committed ncu --set full summary
+    (profiles/ncu_traffic.json): dram bytes (read + write) and SASS instructions per
+    output voxel; None when no capture of this workload/variant is committed."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        d = json.load(f)
-    e = d.get(f"{workload}/{variant}")
-    return None if e is None else float(e["dram_bytes_per_launch"])
+        return json.load(f).get(f"{workload}/{variant}")
 
 
 class ClockSampler:
@@ -191,49 +246,73 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle arm
-def oracle_sample(shape, vids, ranges, imgs, lbls, cpu_seconds, max_voxels=None):
-    """Time the oracle (as it stands) on whole volumes of the workload, threads =
-    host cores, one oracle call per (volume, z-slab).  Returns (voxels, seconds, cores)."""
-    import oracle as O
-    cores = os.cpu_count() or 1
-    nz, ny, nx = shape
-    slab = max(1, nz // 8)
-    jobs = []
-    for i, v in enumerate(vids):
-        d = synth.draw(ranges, v)
-        A = O.compose_affine(O.make_geom(d.rot_rad, d.scale, d.shear, d.flip, d.generic, d.disp),
-                             shape, shape)[1]
-        ph = O.photometric(O.NOISE | O.WINDOW | O.CLAMP | O.GAMMA, window=d.window,
-                           gamma=d.gamma, sigma=d.sigma, seed=synth.MASTER_SEED, volume_id=v)
-        for z0 in range(0, nz, slab):
-            zz = np.arange(z0, min(nz, z0 + slab))
-            xyz = np.stack(np.meshgrid(np.arange(nx), np.arange(ny), zz, indexing="ij"),
-                           -1).reshape(-1, 3).astype(np.int32)
-            jobs.append((i, A, ph, xyz))
-    # calibrate: one slab single-threaded, then size the sample to ~cpu_seconds of CPU work
-    t0 = time.perf_counter()
-    i, A, ph, xyz = jobs[0]
-    O.warp_points(imgs[i], lbls[i], A, xyz, shape, 0, -1000.0, 0, ph)
-    per_vox = (time.perf_counter() - t0) / len(xyz)
-    budget_vox = int(cpu_seconds / max(per_vox, 1e-12))
-    if max_voxels:
-        budget_vox = min(budget_vox, max_voxels)
-    sel, acc = [], 0
-    k = 0
-    while acc < budget_vox:
-        sel.append(jobs[k % len(jobs)])
-        acc += len(jobs[k % len(jobs)][3])
-        k += 1
+class OracleSampler:
+    """The oracle (as it stands) on the workload's volumes, on every host core.
 
-    def run(job):
-        i, A, ph, xyz = job
-        O.warp_points(imgs[i], lbls[i], A, xyz, shape, 0, -1000.0, 0, ph)
+    Work unit = one output z-plane of one volume through oracle_warp_points (the
+    oracle's public point entry; per-volume affine and photometric parameters built
+    once).  run(seconds) times ~seconds of wall work on a persistent thread pool, the
+    units spread evenly over the cores, so the rate is not diluted by pool start-up
+    or by fewer jobs than cores."""
+
+    def __init__(self, workload, shape, vids, draws, imgs, lbls, flags, fill=-1000.0):
+        import oracle as O
+        self.O = O
+        self.shape = shape
+        self.cores = os.cpu_count() or 1
+        nz, ny, nx = shape
+        X, Y = np.meshgrid(np.arange(nx), np.arange(ny), indexing="xy")
+        self.xy = np.stack([X.ravel(), Y.ravel()], axis=1).astype(np.int32)
+        self.vols = []
+        for i, (v, d) in enumerate(zip(vids, draws)):
+            A = O.compose_affine(O.make_geom(d.rot_rad, d.scale, d.shear, d.flip, d.generic,
+                                             d.disp), shape, shape)[1]
+            f = flags
+            occ = dict(occ_z0=0.0, occ_height=0.0)
+            if getattr(d, "occ_height", -1.0) >= 0.0:
+                f |= O.OCCLUDE
+                occ = dict(occ_z0=d.occ_z0, occ_height=d.occ_height)
+            ph = O.photometric(f, window=d.window, gamma=d.gamma, sigma=d.sigma,
+                               seed=synth.MASTER_SEED, volume_id=v, **occ)
+            self.vols.append((imgs[i], lbls[i], A, ph))
+        self.fill = fill
+        planes = max(1, -(-16384 // (nx * ny)))  # >= 16k voxels per unit (call overhead)
+        self.units = [(i, z, min(nz, z + planes)) for z in range(0, nz, planes)
+                      for i in range(len(self.vols))]
+        self.next = 0
+        self.pool = cf.ThreadPoolExecutor(max_workers=self.cores)
+        t0 = time.perf_counter()
+        self._unit(self.units[0])
+        self.t_unit = time.perf_counter() - t0  # single-core seconds per unit
+        # calibration on the pool (2 units per core): effective core-seconds per unit
+        k = 2 * self.cores
+        t0 = time.perf_counter()
+        list(self.pool.map(self._unit, [self.units[j % len(self.units)] for j in range(k)]))
+        self.t_unit_pool = (time.perf_counter() - t0) * self.cores / k
+
+    def _unit(self, u):
+        i, z0, z1 = u
+        img, lbl, A, ph = self.vols[i]
+        n = len(self.xy)
+        xyz = np.empty(((z1 - z0) * n, 3), np.int32)
+        for z in range(z0, z1):
+            xyz[(z - z0) * n:(z - z0 + 1) * n, :2] = self.xy
+            xyz[(z - z0) * n:(z - z0 + 1) * n, 2] = z
+        self.O.warp_points(img, lbl, A, xyz, self.shape, 0, self.fill, 0, ph)
         return len(xyz)
 
-    t0 = time.perf_counter()
-    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
-        vox = sum(ex.map(run, sel))
-    return vox, time.perf_counter() - t0, cores, per_vox
+    def run(self, seconds):
+        """(voxels, wall seconds) of ~seconds of work on all cores."""
+        n = max(self.cores, int(round(seconds * self.cores / max(self.t_unit_pool, 1e-9))))
+        n = (n + self.cores - 1) // self.cores * self.cores
+        sel = [self.units[(self.next + k) % len(self.units)] for k in range(n)]
+        self.next = (self.next + n) % len(self.units)
+        t0 = time.perf_counter()
+        vox = sum(self.pool.map(self._unit, sel))
+        return vox, time.perf_counter() - t0
+
+    def close(self):
+        self.pool.shutdown()
 
 
 def cpu_model():
@@ -247,24 +326,31 @@ def cpu_model():
 
 
 def run_reference(args):
+    """The reference arm: there is no reference implementation (the reference is the
+    paper's text), so this is the oracle, as it stands, on the box's host cores, on
+    this arm's workload, metric and unit.  Each step is a bounded sample of the
+    workload sized so that the whole --steps K --warmup W run takes about 2.5 minutes
+    (0.2-2 s of wall per step).  Rank 0 only; other ranks exit 0."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     wl = WORKLOADS[args.workload]
     shape = wl["shape"]
-    vids, total = shard(args.workload, world, 0)
-    ranges = ranges_of(args.workload)
-    imgs, lbls = host_inputs(shape, vids[:N_DISTINCT_PHANTOMS])
+    vids, _ = shard(args.workload, world, 0)
     vids = vids[:N_DISTINCT_PHANTOMS]
-    # each step: a bounded sample (~0.25 s of CPU work) of the same workload
-    per_step = max(0.05, min(0.25, 120.0 / max(1, args.steps + args.warmup)))
+    imgs, lbls = host_inputs(shape, vids)
+    sampler = OracleSampler(args.workload, shape, vids, draws_of(args.workload, vids,
+                                                                 args.occlusion),
+                            imgs, lbls, wl["ph"], args.fill)
+    per_step = max(0.2, min(2.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        oracle_sample(shape, vids, ranges, imgs, lbls, per_step)
-    tot_vox, tot_s, cores = 0, 0.0, 1
+        sampler.run(per_step)
+    tot_vox, tot_s = 0, 0.0
     for _ in range(args.steps):
-        v, s, cores, _ = oracle_sample(shape, vids, ranges, imgs, lbls, per_step)
+        v, sec = sampler.run(per_step)
         tot_vox += v
-        tot_s += s
+        tot_s += sec
+    sampler.close()
     value = tot_vox / tot_s / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -272,44 +358,41 @@ def run_reference(args):
         "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_of(args, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{tot_vox} output voxels of the workload's volumes "
-                                   f"(z-slabs, {len(vids)} volumes cycled), oracle_warp_points "
-                                   f"on {cores} threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": sampler.cores, "kind": "oracle",
+                         "sample": f"{tot_vox} output voxels ({args.steps} steps of "
+                                   f"~{per_step:.2f} s wall): output z-planes of the workload's "
+                                   f"volumes ({len(vids)} cycled) through oracle_warp_points on "
+                                   f"{sampler.cores} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_of(args, world):
-    wl = WORKLOADS[args.workload]
+def config_of(args, world, workload=None):
+    workload = workload or args.workload
+    wl = WORKLOADS[workload]
     nz, ny, nx = wl["shape"]
     per = wl.get("per_gpu")
-    return {"workload": f"{args.workload}: {wl['desc']}", "dims_xyz": [nx, ny, nz],
+    ph = "noise (sigma 10 HU)" if wl["ph"] == PH_NOISE else "noise+window+clamp+gamma"
+    return {"workload": f"{workload}: {wl['desc']}", "dims_xyz": [nx, ny, nz],
             "volumes_per_gpu": per if per else wl["total"] // world,
             "global_batch": per * world if per else wl["total"],
-            "transforms": wl["ranges"], "photometric": "noise+window+clamp+gamma",
+            "transforms": wl["ranges"], "photometric": ph,
+            "occlusion": bool(args.occlusion and wl["ranges"] == "train"),
             "kernel_variant": args.variant, "input": args.input, "fill_hu": args.fill,
             "l2": "flushed between timed steps (256 MiB write)",
             "parallelism": f"dp{world} (volume shards, no data-path collective)"}
 
 
 # ----------------------------------------------------------------------------- our arm
-def run_resample(args):
+def run_resample(args, world, rank, dev, dist):
     """NEXT-3: one 512^3 CT volume + labels at 1 mm -> 3 mm per GPU per
     step (Gaussian lowpass sigma = 2/3 voxel on each axis, then trilinear / nearest).
     Metric: input voxels per second.  Roofline: the dominant kernel, the fused separable
     lowpass (one pass: 4 B read + 4 B written per input voxel), timed on its own through
     warp3d_smooth3d with CUDA events."""
     import torch
-    import torch.distributed as dist
-    world, rank, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
-    torch.cuda.set_device(dev)
     import build
     if rank == 0:
         build.build_cuda()
@@ -375,21 +458,170 @@ def run_resample(args):
     return 0
 
 
-def main():
-    args = parse()
-    if args.workload == "resample":
-        return 0 if args.impl == "reference" else run_resample(args)
-    if args.impl == "reference":
-        return run_reference(args)
+def init_dist(args):
+    """One process per GPU (torchrun env); NCCL for the timing reduction (gloo on
+    --dry-run).  The world size must equal --gpus, and this node must have a GPU per
+    local rank: a mismatch is an error, never a silent smaller measurement."""
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if args.dry_run:
+        import torch.distributed as dist
+        if world > 1:
+            dist.init_process_group("gloo")
+        return world, rank, local, None, dist
     import torch
     import torch.distributed as dist
-
-    world, rank, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if torch.cuda.device_count() < (local + 1 if world > 1 else 1):
+        raise SystemExit(f"bench.py: rank {rank} needs CUDA device {local}, "
+                         f"{torch.cuda.device_count()} visible")
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
+    if world > 1:
+        # communicator set-up lines (rank count) on stderr; the JSON line stays alone on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group("nccl", device_id=dev)
+    return world, rank, local, dev, dist
+
+
+def run_dry(args, world, rank, dist):
+    """--dry-run: the N-rank host logic on CPU -- sharding by global index, per-volume
+    parameters (host-only composition), the max-over-ranks reduction -- no kernels."""
+    import torch
+    from paper_1811_11226_b200.augment import build_params
+    wl = WORKLOADS[args.workload]
+    vids, gb = shard(args.workload, world, rank)
+    params = build_params(draws_of(args.workload, vids, args.occlusion), vids, wl["shape"],
+                          wl["shape"], wl["ph"], seed=synth.MASTER_SEED)
+    raw = bytes(ctypes.string_at(ctypes.addressof(params), ctypes.sizeof(params)))
+    mx = reduce_max_ms(1.0 + rank, dist if world > 1 else None, torch.device("cpu"))
+    got = [None] * world
+    if world > 1:
+        dist.all_gather_object(got, (rank, vids, len(raw)))
+    else:
+        got = [(rank, vids, len(raw))]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "global_batch": gb,
+                          "max_ms": mx, "shards": [g[1] for g in got],
+                          "param_bytes": [g[2] for g in got],
+                          "config": config_of(args, world)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def make_batch(W, args, workload, vids, dev, torch):
+    """Device-resident inputs, params and the AugmentBatch of this rank's volumes."""
+    from paper_1811_11226_b200.augment import build_params
+    wl = WORKLOADS[workload]
+    shape = wl["shape"]
+    draws = draws_of(workload, vids, args.occlusion)
+    params = build_params(draws, vids, shape, shape, wl["ph"], seed=synth.MASTER_SEED)
+    imgs, lbls = host_inputs(shape, vids)
+    if args.input == "i16":  # NEXT-4: 12-bit HU as int16 (the phantom rounded)
+        imgs = np.round(imgs).astype(np.int16)
+    t_img = torch.from_numpy(imgs).to(dev)
+    t_lbl = None if args.no_labels else torch.from_numpy(lbls).to(dev)
+    variant = {"auto": W.KERNEL_AUTO, "gather": W.KERNEL_GATHER,
+               "staged": W.KERNEL_STAGED}[args.variant]
+    batch = W.AugmentBatch(t_img, t_lbl, params, fill=args.fill, label_fill=0, variant=variant)
+    return batch, params, imgs, lbls, draws
+
+
+def alg_bytes_of(W, params, shape, dev, in_bytes, labels):
+    """Algorithmic bytes of one pass: 5 B written per output voxel +
+    4 (2) B per distinct input image voxel read + 1 B per distinct label voxel read."""
+    f_img = f_lbl = 0
+    for c0 in range(0, len(params), 64):
+        a, b = W.warp3d_footprint_batched(params[c0:c0 + 64], shape, shape, device=dev)
+        f_img += a
+        f_lbl += b
+    nvox = len(params) * int(np.prod(shape))
+    return (5 if labels else 4) * nvox + in_bytes * f_img + (f_lbl if labels else 0), f_img, f_lbl
+
+
+def time_steps(W, batch, dev, steps, warmup, world, dist, torch, flush):
+    """Device time of `steps` passes (CUDA events on the launching stream around each
+    pass; L2 flushed by a 256 MiB write between passes, outside the events).  Returns
+    (max-over-ranks total ms, per-step ms, launches, clocks)."""
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, warmup)):
+        flush.fill_(1)
+        batch.run()
+    torch.cuda.synchronize(dev)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    launches0 = W.warp3d_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clk:
+        for k in range(steps):
+            flush.fill_(k & 0xFF)            # L2 flush between timed steps (not timed)
+            starts[k].record(stream)
+            batch.run()
+            ends[k].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = W.warp3d_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    total = reduce_max_ms(float(sum(step_ms)), dist if world > 1 else None, dev)
+    return total, step_ms, launches, clk.summary()
+
+
+def latency_modes(W, batch, dev, torch, reps=50, rounds=20):
+    """C1/C2 latency: the same pass as back-to-back launches (no
+    flush, one event pair around `reps` passes) and as a CUDA graph of `reps` passes
+    replayed `rounds` times.  Per-pass device microseconds."""
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(5):
+        batch.run()
+    torch.cuda.synchronize(dev)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(reps * rounds):
+        batch.run()
+    e.record(stream)
+    torch.cuda.synchronize(dev)
+    b2b = s.elapsed_time(e) * 1e3 / (reps * rounds)
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream(dev)
+    cs.wait_stream(stream)
+    with torch.cuda.stream(cs):
+        batch.run()  # warm on the capture stream
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(g, stream=cs):
+            for _ in range(reps):
+                batch.run()
+    torch.cuda.synchronize(dev)
+    g.replay()
+    torch.cuda.synchronize(dev)
+    s.record(stream)
+    for _ in range(rounds):
+        g.replay()
+    e.record(stream)
+    torch.cuda.synchronize(dev)
+    graph = s.elapsed_time(e) * 1e3 / (reps * rounds)
+    return {"back_to_back_us_per_pass": b2b, "graph_us_per_pass": graph,
+            "passes": reps * rounds, "graph_passes_per_replay": reps,
+            "note": "no L2 flush between passes (latency regime)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return 0 if args.workload == "resample" else run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    world, rank, local, dev, dist = init_dist(args)
+    if args.dry_run:
+        return run_dry(args, world, rank, dist)
+    if args.workload == "resample":
+        return run_resample(args, world, rank, dev, dist)
+    import torch
 
     import build
     if rank == 0:
@@ -397,65 +629,45 @@ def main():
     if world > 1:
         dist.barrier()
     import paper_1811_11226_b200 as W
-    from paper_1811_11226_b200.augment import FULL, build_params
 
-    variant = {"auto": W.KERNEL_AUTO, "gather": W.KERNEL_GATHER,
-               "staged": W.KERNEL_STAGED}[args.variant]
     wl = WORKLOADS[args.workload]
     shape = wl["shape"]
-    vids, global_batch = shard(args.workload, world, rank)
-    ranges = ranges_of(args.workload)
-    draws = [synth.draw(ranges, v) for v in vids]
-    params = build_params(draws, vids, shape, shape, FULL, seed=synth.MASTER_SEED)
-    imgs, lbls = host_inputs(shape, vids)
-    B = len(vids)
     nvox_out = int(np.prod(shape))
-    if args.input == "i16":  # NEXT-4: 12-bit HU as int16 (the phantom rounded)
-        imgs = np.round(imgs).astype(np.int16)
-    t_img = torch.from_numpy(imgs).to(dev)
-    t_lbl = None if args.no_labels else torch.from_numpy(lbls).to(dev)
-    batch = W.AugmentBatch(t_img, t_lbl, params, fill=args.fill, label_fill=0, variant=variant)
-
-    # algorithmic bytes: 5 B written per output voxel
-    # + 4 B per distinct input image voxel read + 1 B per distinct label voxel read
-    f_img = f_lbl = 0
-    for c0 in range(0, B, 64):
-        a, b = W.warp3d_footprint_batched(params[c0:c0 + 64], shape, shape, device=dev)
-        f_img += a
-        f_lbl += b
+    vids, global_batch = shard(args.workload, world, rank)
+    batch, params, imgs, lbls, draws = make_batch(W, args, args.workload, vids, dev, torch)
+    B = len(vids)
     in_bytes = 2 if args.input == "i16" else 4
-    alg_bytes = 5 * B * nvox_out + in_bytes * f_img + (0 if args.no_labels else 1) * f_lbl
+    alg_bytes, f_img, f_lbl = alg_bytes_of(W, params, shape, dev, in_bytes, not args.no_labels)
     naive_bytes = 10 * B * nvox_out
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     tiles_before = W.warp3d_tile_stats()
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(max(3, args.warmup)):
-        flush.fill_(1)
-        batch.run()
-    torch.cuda.synchronize(dev)
-
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches0 = W.warp3d_launch_count()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(dev.index) as clk:
-        for k in range(args.steps):
-            flush.fill_(k & 0xFF)            # L2 flush between timed steps (not timed)
-            starts[k].record(stream)
-            batch.run()
-            ends[k].record(stream)
-        torch.cuda.synchronize(dev)
-    launches = W.warp3d_launch_count() - launches0
+    max_ms, step_ms, launches, clocks = time_steps(W, batch, dev, args.steps, args.warmup,
+                                                   world, dist, torch, flush)
     st0 = W.warp3d_tile_stats()
-    if world > 1:
-        dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
-    max_ms = reduce_max_ms(total_ms, dist if world > 1 else None, dev)
     value = global_batch * nvox_out * args.steps / (max_ms * 1e-3) / 1e9
+
+    latency = None
+    if args.workload in ("c1", "c2"):
+        latency = latency_modes(W, batch, dev, torch)
+
+    # configs[4] next to the weak-scaling c3 line: 256 volumes sharded over the ranks
+    c5 = None
+    if args.workload == "c3" and not args.no_c5 and not args.occlusion:
+        del batch
+        torch.cuda.empty_cache()
+        cvids, cgb = shard("c5", world, rank)
+        cbatch = make_batch(W, args, "c5", cvids, dev, torch)[0]
+        csteps = max(3, min(args.steps, 10))
+        cms, _, claunch, cclk = time_steps(W, cbatch, dev, csteps, 3, world, dist, torch, flush)
+        c5 = {"metric": METRIC, "workload": config_of(args, world, "c5")["workload"],
+              "value": cgb * nvox_out * csteps / (cms * 1e-3) / 1e9, "unit": UNIT,
+              "ms_per_step": cms / csteps, "steps": csteps, "scaling": "strong",
+              "volumes_per_gpu": len(cvids), "global_batch": cgb,
+              "gpu_launches": int(claunch), "clocks": cclk}
+        del cbatch
+        torch.cuda.empty_cache()
 
     # e2e: pinned host buffers -> H2D -> warp -> D2H, inside the timed region
     e2e = None
@@ -465,26 +677,36 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, s, cores, per_vox = oracle_sample(shape, vids, ranges, imgs, lbls, args.cpu_seconds)
-        cpu = {"value": v / s / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{v} output voxels of this workload (z-slabs of its volumes), "
-                         f"oracle_warp_points on {cores} threads, {s:.1f} s wall",
-               "single_core_value": 1e-9 / per_vox, "cpu_model": cpu_model()}
+        smp = OracleSampler(args.workload, shape, vids[:N_DISTINCT_PHANTOMS],
+                            draws[:N_DISTINCT_PHANTOMS], imgs, lbls, wl["ph"], args.fill)
+        v, sec = smp.run(args.cpu_seconds / smp.cores)
+        smp.close()
+        cpu = {"value": v / sec / 1e9, "unit": UNIT, "cores": smp.cores, "kind": "oracle",
+               "sample": f"{v} output voxels of this workload (output z-planes of its "
+                         f"volumes), oracle_warp_points on {smp.cores} threads, "
+                         f"{sec:.2f} s wall (~{args.cpu_seconds:.0f} core-seconds)",
+               "single_core_value": 1e-9 * smp._unit(smp.units[0]) / smp.t_unit,
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         peak, peak_src = measured_peaks()
-        avg_launch_s = (total_ms / args.steps) * 1e-3 / max(1, launches // max(1, args.steps))
-        per_launch_bytes = alg_bytes / max(1, launches // max(1, args.steps))
+        per_step = max(1, launches // max(1, args.steps))
+        avg_launch_s = (total_ms / args.steps) * 1e-3 / per_step
+        per_launch_bytes = alg_bytes / per_step
         achieved = per_launch_bytes / avg_launch_s / 1e9
-        traffic = ncu_traffic(args.workload, args.variant)
+        ev = ncu_evidence(args.workload, args.variant) if not args.occlusion else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if "per_gpu" in wl else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_of(args, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak,
+                         "traffic": None if ev is None else float(ev["dram_bytes_per_launch"]),
+                         "inst_per_voxel": None if ev is None else ev.get("inst_per_voxel"),
+                         "ncu_source": None if ev is None else ev.get("source"),
                          "peak_source": peak_src,
                          "alg_bytes_per_launch": per_launch_bytes,
                          "alg_bytes_per_voxel": alg_bytes / (B * nvox_out),
@@ -497,10 +719,14 @@ def main():
             "gpu_launches": int(launches),
             "tiles": {"staged": st0[0] - tiles_before[0], "gather": st0[1] - tiles_before[1],
                       "tma": st0[2] - tiles_before[2], "parts": st0[3] - tiles_before[3]},
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms),
                         "max": max(step_ms)},
         }
+        if c5 is not None:
+            line["c5"] = c5
+        if latency is not None:
+            line["latency"] = latency
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -127,12 +127,9 @@ def warp3d_affine_batched(inp: torch.Tensor, labels: torch.Tensor | None, params
         out = torch.empty((B, *out_shape), dtype=torch.float32, device=inp.device)
     if labels is not None and out_labels is None:
         out_labels = torch.empty((B, *out_shape), dtype=torch.uint8, device=inp.device)
-    if isinstance(params, ctypes.Array):
-        arr = params
-    else:
-        arr = (VolumeParams * B)(*params)
-    if len(arr) != B:
-        raise ValueError(f"{len(arr)} params for a batch of {B}")
+    if len(params) != B:  # before the ctypes array (which would zero-pad a short list)
+        raise ValueError(f"{len(params)} params for a batch of {B}")
+    arr = params if isinstance(params, ctypes.Array) else (VolumeParams * B)(*params)
     if (labels is None) != (out_labels is None):
         raise ValueError("out_labels must be given exactly when labels are")
     dev, oshape = inp.device, (B, *out_shape)

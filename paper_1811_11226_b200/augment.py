@@ -10,14 +10,22 @@ from __future__ import annotations
 import ctypes
 
 from . import api
-from ._lib import PH_CLAMP, PH_GAMMA, PH_NOISE, PH_WINDOW, VolumeParams
+from ._lib import PH_CLAMP, PH_GAMMA, PH_NOISE, PH_OCCLUDE, PH_WINDOW, VolumeParams
 
 FULL = PH_NOISE | PH_WINDOW | PH_CLAMP | PH_GAMMA
 
 
 def photometric_from_draw(draw, flags, seed, volume_id):
+    """w3d_photometric of one draw; a draw with an occlusion prism (occ_height >= 0,
+    PAPER.md:420-438) adds W3D_PH_OCCLUDE."""
+    occ = getattr(draw, "occ_height", -1.0)
+    if occ is not None and occ >= 0.0:
+        flags |= PH_OCCLUDE
+    else:
+        occ = 0.0
     return api.photometric(flags, window=draw.window, gamma=draw.gamma, sigma=draw.sigma,
-                           seed=seed, volume_id=volume_id)
+                           seed=seed, volume_id=volume_id,
+                           occ_z0=getattr(draw, "occ_z0", 0.0), occ_height=occ)
 
 
 def build_params(draws, volume_ids, in_shape_zyx, out_shape_zyx=None, flags=FULL, seed=0,

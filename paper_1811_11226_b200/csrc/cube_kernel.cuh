@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstdint>
@@ -521,6 +522,37 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
   img = lerp2(lerp2(c00, c10, ty), lerp2(c01, c11, ty), tz);
 }
 
+// The label of a y-pair alone (an occluded column, R15: the image is 0 and its
+// fetch skipped): the index arithmetic of sample2's label
+// path, op for op, so the labels are the same bits.
+template <bool kClamp, bool kSameLbl>
+__device__ __forceinline__ void label2(const View& v, float2 px, float2 py, float2 pz,
+                                       uint32_t& l0, uint32_t& l1) {
+  if (kClamp) {
+    px = make_float2(fminf(fmaxf(px.x, -1.0f), v.nx), fminf(fmaxf(px.y, -1.0f), v.nx));
+    py = make_float2(fminf(fmaxf(py.x, -1.0f), v.ny), fminf(fmaxf(py.y, -1.0f), v.ny));
+    pz = make_float2(fminf(fmaxf(pz.x, -1.0f), v.nz), fminf(fmaxf(pz.y, -1.0f), v.nz));
+  }
+  const float2 sx = add2_rm(px, f2(kM)), sy = add2_rm(py, f2(kM)), sz = add2_rm(pz, f2(kM));
+  const float2 tx = sub2(px, sub2(sx, f2(kM)));
+  const float2 ty = sub2(py, sub2(sy, f2(kM)));
+  const float2 tz = sub2(pz, sub2(sz, f2(kM)));
+  const float2 ry = sub2(sy, f2(v.Mby)), rz = sub2(sz, f2(v.Mbz));
+  const float2 hx = make_float2(fset_ge_half(tx.x), fset_ge_half(tx.y));
+  const float2 hy = make_float2(fset_ge_half(ty.x), fset_ge_half(ty.y));
+  const float2 hz = make_float2(fset_ge_half(tz.x), fset_ge_half(tz.y));
+  float2 Ll;
+  if (kSameLbl) {
+    const float2 L = __ffma2_rn(rz, f2(v.Pf), __ffma2_rn(ry, f2(v.Wf), sx));
+    Ll = __ffma2_rn(hz, f2(v.Pf), __ffma2_rn(hy, f2(v.Wf), __fadd2_rn(L, hx)));
+  } else {
+    Ll = __ffma2_rn(__fadd2_rn(rz, hz), f2(v.Plf),
+                    __ffma2_rn(__fadd2_rn(ry, hy), f2(v.Wlf), __fadd2_rn(sx, hx)));
+  }
+  l0 = lds_u8(addr1(Ll.x, v.clbl));
+  l1 = lds_u8(addr1(Ll.y, v.clbl));
+}
+
 // ---------------------------------------------------------------------------
 // Gather sampling of one voxel through L1/L2 with per-corner bounds (R6-R8,
 // NaN-safe float compares first).  Used for parts whose box does not fit.
@@ -716,8 +748,8 @@ __device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
 // n2, n3; computed while the staging copies are in flight) and the loop
 // computes group g + kPre's block.
 template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
-          bool kSameLbl = false, bool kFull = false, int kPre = 1, int kGMode = kGEdge>
-__device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V0,
+          bool kSameLbl, bool kFull, int kPre, int kGMode, bool kOccOnly>
+__device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
                                             float4 n2 = make_float4(0.f, 0.f, 0.f, 0.f),
@@ -745,7 +777,6 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
 #else
   const bool noise = kPh == kPhFull || (V.flags & kNoise);
 #endif
-  const bool occl = kPh != kPhFull && (V.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi;
   const PhiloxPrefix pp{pin(P.ph_K0), pin(P.ph_K1), pin(P.ph_K2), pin(P.ph_U3)};
   uint32_t rk0[10], rk1[10];
 #pragma unroll
@@ -762,15 +793,21 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
                mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(y0 >> 2));
   float2 Y2 = make_float2(static_cast<float>(y0), static_cast<float>(y0 + 1));
   const GView gv = make_gview(a);
-  // one y-pair (rows ya, ya + 1) with its two normals
-  auto pair = [&](int ya, float2 nsp) {
+  // one y-pair (rows ya, ya + 1) with its two normals; kOcc (an occluded column,
+  // R15): the image is 0 and every step after the occlusion test is skipped,
+  // the texture fetch included -- only the labels are warped
+  auto pair = [&](int ya, float2 nsp, auto occ_tag) {
+    constexpr bool kOcc = decltype(occ_tag)::value;
     const float2 px = __ffma2_rn(f2(V.A1[0]), Y2, f2(t0));
     const float2 py = __ffma2_rn(f2(V.A1[1]), Y2, f2(t1));
     const float2 pz = __ffma2_rn(f2(V.A1[2]), Y2, f2(t2));
     Y2 = __fadd2_rn(Y2, make_float2(2.0f, 2.0f));
     float2 img;
     uint32_t l0 = 0, l1 = 0;
-    if (kStaged) {
+    if (kOcc && kStaged) {
+      if (kLabels) label2<kClamp, kSameLbl>(v, px, py, pz, l0, l1);
+    } else if (kOcc && !kLabels) {
+    } else if (kStaged) {
       sample2<T, kLabels, kNearest, kClamp, kSameLbl>(v, px, py, pz, img, l0, l1);
     } else if (!kNearest && kGMode != kGWide) {
       gather2<T, kLabels, kGMode>(a, vin, lin, gv, px, py, pz, img, l0, l1);
@@ -778,8 +815,7 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
       sample_gather<T, kLabels, kNearest>(a, vin, lin, px.x, py.x, pz.x, img.x, l0);
       sample_gather<T, kLabels, kNearest>(a, vin, lin, px.y, py.y, pz.y, img.y, l1);
     }
-    float2 out = photometric2<kPh>(img, nsp, V);
-    if (occl) out = make_float2(0.0f, 0.0f);  // PAPER.md:437-438, R15
+    const float2 out = kOcc ? make_float2(0.0f, 0.0f) : photometric2<kPh>(img, nsp, V);
     const bool second = kFull || ya + 1 < my;
     float* po1 = po + row1;
     st_f32(po, out.x);
@@ -792,16 +828,23 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
       pl = pl1 + row1;
     }
   };
+  if constexpr (kOccOnly) {  // R15: labels only (no Philox block, no image fetch)
+#pragma unroll 1
+    for (int ya = y0; ya < y0 + 4 * ng && ya < my; ya += 2)
+      pair(ya, make_float2(0.f, 0.f), std::true_type());
+    return;
+  }
   if constexpr (kFull && kPre == 4) {
     if (ng == 4) {  // a whole 16-row column, normals precomputed: straight line, no rotation
-      pair(y0, make_float2(n.x, n.y));
-      pair(y0 + 2, make_float2(n.z, n.w));
-      pair(y0 + 4, make_float2(n1.x, n1.y));
-      pair(y0 + 6, make_float2(n1.z, n1.w));
-      pair(y0 + 8, make_float2(n2.x, n2.y));
-      pair(y0 + 10, make_float2(n2.z, n2.w));
-      pair(y0 + 12, make_float2(n3.x, n3.y));
-      pair(y0 + 14, make_float2(n3.z, n3.w));
+      const std::false_type live_col;
+      pair(y0, make_float2(n.x, n.y), live_col);
+      pair(y0 + 2, make_float2(n.z, n.w), live_col);
+      pair(y0 + 4, make_float2(n1.x, n1.y), live_col);
+      pair(y0 + 6, make_float2(n1.z, n1.w), live_col);
+      pair(y0 + 8, make_float2(n2.x, n2.y), live_col);
+      pair(y0 + 10, make_float2(n2.z, n2.w), live_col);
+      pair(y0 + 12, make_float2(n3.x, n3.y), live_col);
+      pair(y0 + 14, make_float2(n3.z, n3.w), live_col);
       return;
     }
   }
@@ -812,8 +855,8 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
     float4 nn = make_float4(0.f, 0.f, 0.f, 0.f);
     if (noise && g + kPre < ng)
       nn = box_muller4(philox_block(q + static_cast<uint32_t>(kPre) * mxu, pp, rk0, rk1));
-    pair(y, make_float2(n.x, n.y));
-    if (kFull || y + 2 < my) pair(y + 2, make_float2(n.z, n.w));
+    pair(y, make_float2(n.x, n.y), std::false_type());
+    if (kFull || y + 2 < my) pair(y + 2, make_float2(n.z, n.w), std::false_type());
     if (kPre == 1) {
       n = nn;
     } else if (kPre == 2) {
@@ -827,6 +870,24 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
     }
     q += mxu;
   }
+}
+
+// The rows of one column: an occluded column (R15: output z in
+// the volume's prism) takes the label-only instance, every other column the full
+// chain.  The column is one thread, so the test is per thread.
+template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
+          bool kSameLbl = false, bool kFull = false, int kPre = 1, int kGMode = kGEdge>
+__device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V,
+                                            const View& v, int vi, int X, int Z, int y0, int ng,
+                                            float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
+                                            float4 n2 = make_float4(0.f, 0.f, 0.f, 0.f),
+                                            float4 n3 = make_float4(0.f, 0.f, 0.f, 0.f)) {
+  if ((V.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi)
+    column_rows_impl<T, kLabels, kNearest, kPh, kStaged, kClamp, kSameLbl, kFull, kPre, kGMode,
+                     true>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
+  else
+    column_rows_impl<T, kLabels, kNearest, kPh, kStaged, kClamp, kSameLbl, kFull, kPre, kGMode,
+                     false>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
 }
 
 __device__ __forceinline__ Vol load_vol(const VolDev& P) {
@@ -1135,7 +1196,9 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   } else {
     stage<T, kLabels>(a, vin, lin, b, simg, slbl);
   }
-  float4 n = (live && !(kPh == kPhFull && W3D_PRE == 4))
+  // an occluded column (R15) needs no noise: its Philox blocks are skipped
+  const bool need_noise = live && !((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi);
+  float4 n = (need_noise && !(kPh == kPhFull && W3D_PRE == 4))
                  ? first_normals<kPh>(a, P, V, X, Z, oy)
                  : make_float4(0, 0, 0, 0);
   // the training chain (kPhFull, launch-wide keys) computes kPre Philox blocks
@@ -1143,7 +1206,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   constexpr int kPre = kPh == kPhFull ? W3D_PRE : 1;
   const float4 z4 = make_float4(0, 0, 0, 0);
   float4 n1 = z4, n2 = z4, n3 = z4;
-  if (kPre == 4 && live) {  // the column's four blocks in lockstep
+  if (kPre == 4 && need_noise) {  // the column's four blocks in lockstep
     const uint32_t gyn = static_cast<uint32_t>((a.my + 3) >> 2), mxu = static_cast<uint32_t>(a.mx);
     const uint32_t q0 = static_cast<uint32_t>(X) +
                         mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(oy >> 2));
@@ -1154,7 +1217,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     n1 = box_muller4(r[1]);
     n2 = box_muller4(r[2]);
     n3 = box_muller4(r[3]);
-  } else if (kPre == 2 && live) {
+  } else if (kPre == 2 && need_noise) {
     n1 = first_normals<kPh>(a, P, V, X, Z, oy + 4);
   }
   View v = make_view<T>(a, b, simg, slbl);
@@ -1328,13 +1391,15 @@ static cudaError_t launch_n(const WarpArgsT<NV>& a, cudaStream_t s) {
 }
 
 // The full photometric chain on every volume of the launch (the training
-// configuration): noise, window + clamp to [0, 1], gamma != 1, no occlusion.
+// configuration): noise, window + clamp to [0, 1], gamma != 1, with or without
+// occlusion (R15: per-column test in column_rows).
 // ... and one seed for every volume (the round keys are launch constants, a.rk*).
 template <int NV>
 static bool all_full(const WarpArgsT<NV>& a) {
   for (int i = 0; i < a.nvol; ++i) {
     const VolDev& P = a.vol[i];
-    if (P.flags != (kNoise | kGamma) || P.clamp_lo != 0.0f || P.clamp_hi != 1.0f) return false;
+    if ((P.flags & ~kOcclude) != (kNoise | kGamma) || P.clamp_lo != 0.0f || P.clamp_hi != 1.0f)
+      return false;
     if (P.rk0[0] != a.vol[0].rk0[0] || P.rk1[0] != a.vol[0].rk1[0]) return false;
   }
   return true;

@@ -98,11 +98,16 @@ class AugmentRanges:
     window_hi: tuple = (230.0, 1500.0)        # b ~ U
     gamma: tuple = (0.7, 1.5)
     sigma: tuple = (0.0, 20.0)                # HU
+    occ_dmax: float = 0.0                     # occlusion prism height bound (output z
+                                              # voxels); 0 = no occlusion
 
 
 TRAIN = AugmentRanges()
 LARGE = AugmentRanges(rot_deg=(45.0, 45.0, 180.0), scale=(0.8, 1.2), shear=0.0,
                       flip_p=(0.0, 0.0, 0.0), disp=(0.0, 0.0, 0.0))
+# TRAIN plus random occlusion: prism height delta ~ U[0, 48] output
+# planes (the paper gives no value; 48 of the 160 planes of a 3 mm volume)
+TRAIN_OCC = AugmentRanges(occ_dmax=48.0)
 
 
 @dataclass(frozen=True)
@@ -116,10 +121,18 @@ class VolumeDraw:
     window: tuple
     gamma: float
     sigma: float
+    occ_z0: float = 0.0        # occlusion prism start z (output voxels)
+    occ_height: float = -1.0   # delta; < 0 = no occlusion
 
 
-def draw(ranges: AugmentRanges, global_index: int, master_seed: int = MASTER_SEED) -> VolumeDraw:
-    """Per-volume random draws, keyed by (master_seed, GLOBAL volume index)."""
+def draw(ranges: AugmentRanges, global_index: int, master_seed: int = MASTER_SEED,
+         out_mz: int | None = None) -> VolumeDraw:
+    """Per-volume random draws, keyed by (master_seed, GLOBAL volume index).
+
+    Occlusion (ranges.occ_dmax > 0; needs the output depth out_mz): delta ~ U[0, dmax]
+    and z0 ~ U[-dmax, z_max] with z_max = out_mz - 1, so that every output plane has the
+    same chance of being occluded.  Drawn after every other value,
+    so the other draws do not depend on whether occlusion is on."""
     rng = np.random.default_rng([master_seed, global_index])
     rot = tuple(float(rng.uniform(-r, r)) * math.pi / 180.0 for r in ranges.rot_deg)
     scale = tuple(float(rng.uniform(*ranges.scale)) for _ in range(3))
@@ -133,7 +146,14 @@ def draw(ranges: AugmentRanges, global_index: int, master_seed: int = MASTER_SEE
         b = float(rng.uniform(*ranges.window_hi))
     gamma = float(rng.uniform(*ranges.gamma))
     sigma = float(rng.uniform(*ranges.sigma))
-    return VolumeDraw(rot, scale, shear, flip, generic, disp, (a, b), gamma, sigma)
+    occ_z0, occ_h = 0.0, -1.0
+    if ranges.occ_dmax > 0.0:
+        if out_mz is None:
+            raise ValueError("occlusion draws need the output depth out_mz")
+        occ_h = float(rng.uniform(0.0, ranges.occ_dmax))
+        occ_z0 = float(rng.uniform(-ranges.occ_dmax, out_mz - 1.0))
+    return VolumeDraw(rot, scale, shear, flip, generic, disp, (a, b), gamma, sigma, occ_z0,
+                      occ_h)
 
 
 # The fixed C1 transform: Rz 25, Ry -7, Rx 10 degrees,

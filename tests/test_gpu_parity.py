@@ -343,6 +343,42 @@ def test_c3_batch16(W):
     check(g_img, g_lbl, ref, ds, FULL, "C3")
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_c3_training_batch_with_occlusion(W, variant):
+    """A C3 training batch with the paper's random occlusion: per
+    example delta ~ U[0, dmax], z0 ~ U[-dmax, z_max] (synth.TRAIN_OCC), parameters from
+    the product path (augment.build_params), every volume against the oracle (R15:
+    occluded output planes exactly 0, labels warped as usual)."""
+    from paper_1811_11226_b200.augment import FULL as WFULL, build_params
+    shape = (160, 128, 128)
+    B = 16
+    imgs, lbls, _, _ = _batch_inputs(shape, B, synth.TRAIN)
+    ds = [synth.draw(synth.TRAIN_OCC, i, out_mz=shape[0]) for i in range(B)]
+    As = [_oracle_affine(d, shape, shape) for d in ds]
+    params = build_params(ds, list(range(B)), shape, shape, WFULL, seed=SEED)
+    out, out_l = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(),
+                                         torch.from_numpy(lbls).cuda(), params, fill=-1000.0,
+                                         variant=variant)
+    torch.cuda.synchronize()
+    g_img, g_lbl = out.cpu().numpy(), out_l.cpu().numpy()
+
+    def one(i):
+        d = ds[i]
+        ph = O.photometric(FULL | O.OCCLUDE, window=d.window, gamma=d.gamma, sigma=d.sigma,
+                           seed=SEED, volume_id=i, occ_z0=d.occ_z0, occ_height=d.occ_height)
+        return i, O.warp_volume(imgs[i], lbls[i], As[i], None, O.LINEAR, -1000.0, 0, ph)
+    with _pool() as ex:
+        ref = dict(ex.map(one, range(B)))
+    check(g_img, g_lbl, ref, ds, FULL, f"C3 occlusion v{variant}")
+    occluded = 0
+    for i, d in enumerate(ds):
+        z = np.arange(shape[0])
+        planes = (z >= d.occ_z0) & (z <= d.occ_z0 + d.occ_height)
+        assert np.all(g_img[i][planes] == 0.0)
+        occluded += int(planes.sum())
+    assert occluded > 0
+
+
 # ----------------------------------------------------------------------------- configs[3] (C4)
 def _sampled_check(W, imgs, lbls, As, ds, flags, vids, n_pts, variant=0, seed=0):
     B = len(As)

@@ -85,3 +85,37 @@ def test_gloo_world2_params_and_timing():
     for rank, vids, raw in gathered:
         assert vids == list(range(16 * rank, 16 * rank + 16))
         assert raw == one[per * vids[0]: per * (vids[-1] + 1)]
+
+
+def test_bench_gpus2_dry_run_spawns_two_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself as two
+    ranks (torch.distributed.run, gloo on --dry-run) that shard the global batch and
+    reduce the elapsed time by max over ranks; rank 0 prints one JSON line."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    for workload, gb in (("c3", 32), ("c5", 256)):
+        out = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--gpus", "2",
+                              "--dry-run", "--workload", workload], capture_output=True,
+                             text=True, env=env, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+        assert len(lines) == 1, out.stdout
+        d = json.loads(lines[0])
+        assert d["n_gpus"] == 2 and d["global_batch"] == gb
+        assert d["max_ms"] == 2.0  # max of the ranks' 1.0 and 2.0
+        assert sorted(sum(d["shards"], [])) == list(range(gb))
+        assert d["config"]["parallelism"].startswith("dp2")
+
+
+def test_bench_world_mismatch_fails_loudly():
+    """A torchrun world that does not match --gpus is an error (never a silent
+    smaller measurement)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--gpus", "2",
+                          "--dry-run"], capture_output=True, text=True, env=env, timeout=120)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in (out.stderr + out.stdout)

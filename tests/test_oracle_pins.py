@@ -419,3 +419,23 @@ def test_exact_p_grid_equals_rational_fma():
         g = p_fp32_grid(A, (5, 6, 7))
         for z, y, x in itertools.product(range(5), range(6), range(7)):
             assert [float(v) for v in g[:, z, y, x]] == p_fp32(A, x, y, z)
+
+
+def test_occlusion_draw_is_uniform_over_planes():
+    """The occlusion draw (delta ~ U[0, dmax], z0 ~ U[-dmax, z_max])
+    gives every output plane the same chance E[delta] / (z_max + dmax) of being
+    occluded; the other draws do not change when occlusion is switched on."""
+    mz, n = 64, 6000
+    dmax = synth.TRAIN_OCC.occ_dmax
+    hits = np.zeros(mz)
+    z = np.arange(mz)
+    for v in range(n):
+        d = synth.draw(synth.TRAIN_OCC, v, out_mz=mz)
+        assert 0.0 <= d.occ_height <= dmax and -dmax <= d.occ_z0 <= mz - 1
+        hits += (z >= d.occ_z0) & (z <= d.occ_z0 + d.occ_height)
+        if v < 20:
+            base = synth.draw(synth.TRAIN, v)
+            assert base.rot_rad == d.rot_rad and base.sigma == d.sigma and base.window == d.window
+    p = (dmax / 2.0) / (mz - 1 + dmax)
+    sd = np.sqrt(p * (1 - p) / n)
+    assert np.all(np.abs(hits / n - p) < 5 * sd), (hits.min() / n, hits.max() / n, p)
