@@ -276,7 +276,7 @@ class OracleSampler:
                                seed=synth.MASTER_SEED, volume_id=v, **occ)
             self.vols.append((imgs[i], lbls[i], A, ph))
         self.fill = fill
-        planes = max(1, -(-16384 // (nx * ny)))  # >= 16k voxels per unit (call overhead)
+        planes = max(1, -(-131072 // (nx * ny)))  # >= 128k voxels per unit (GIL share)
         self.units = [(i, z, min(nz, z + planes)) for z in range(0, nz, planes)
                       for i in range(len(self.vols))]
         self.next = 0

@@ -29,13 +29,19 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def build_oracle(force=False):
+def build_oracle(force=False, sanitize=False):
+    """The C oracle (test infrastructure).  sanitize=True: the same sources with
+    AddressSanitizer + UndefinedBehaviorSanitizer (no recovery: the first report
+    aborts) into oracle/liboracle_warp3d_asan.so, loaded with libasan preloaded."""
     srcs = [os.path.join(ROOT, "oracle", f) for f in ("oracle_warp3d.c", "oracle_resample.c")]
     hdr = os.path.join(ROOT, "oracle", "oracle_warp3d.h")
-    out = os.path.join(ROOT, "oracle", "liboracle_warp3d.so")
+    name = "liboracle_warp3d_asan.so" if sanitize else "liboracle_warp3d.so"
+    out = os.path.join(ROOT, "oracle", name)
+    san = (["-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+            "-fno-omit-frame-pointer", "-g"] if sanitize else [])
     if force or _stale(out, srcs + [hdr]):
         _run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-              "-shared", "-Wall", "-Wextra", "-D_GNU_SOURCE", "-o", out, *srcs, "-lm"])
+              "-shared", "-Wall", "-Wextra", "-D_GNU_SOURCE", *san, "-o", out, *srcs, "-lm"])
     return out
 
 
@@ -115,6 +121,8 @@ def main(argv):
     force = "--force" in argv
     if what in ("oracle", "all"):
         build_oracle(force)
+    if what == "oracle-asan":
+        build_oracle(force, sanitize=True)
     if what in ("cuda", "all"):
         build_cuda(force)
 

@@ -27,7 +27,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboracle_warp3d.so")
+# W3D_ORACLE_LIB: the same C sources built with -fsanitize=address,undefined
+# (build.py oracle-asan; tests/test_oracle_sanitized.py runs the pins against it)
+LIB_PATH = os.environ.get("W3D_ORACLE_LIB") or os.path.join(_HERE, "liboracle_warp3d.so")
 
 NOISE, WINDOW, CLAMP, GAMMA, OCCLUDE = 1, 2, 4, 8, 16
 LINEAR, NEAREST = 0, 1

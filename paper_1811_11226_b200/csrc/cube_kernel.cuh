@@ -364,7 +364,25 @@ struct View {
   uint32_t PW4;           // P4 + W4: the (y+1, z+1) corner row as one [R + UR] offset
   uint32_t cimg, clbl;    // image / label byte address = bits(L) * (4 | 1) + c
   float nx, ny, nz;       // clamp bounds
+#ifdef W3D_CHECK_BOX
+  uint32_t img_lo, img_hi, lbl_lo, lbl_hi;  // staged boxes [lo, hi) (byte addresses)
+#endif
 };
+
+// W3D_CHECK_BOX (debug build, tools/sanitize.sh): every staged shared-memory
+// access must fall inside its box -- a margin too small in cube_cp_box / make_box
+// would otherwise read a neighbouring row of the box silently.  Traps (a launch
+// error) on the first violation.
+#ifdef W3D_CHECK_BOX
+#define W3D_IN_BOX(addr, bytes, lo, hi) \
+  do {                                   \
+    if (!((addr) >= (lo) && (addr) + (bytes) <= (hi))) __trap(); \
+  } while (0)
+#else
+#define W3D_IN_BOX(addr, bytes, lo, hi) \
+  do {                                   \
+  } while (0)
+#endif
 
 template <class T>
 __device__ __forceinline__ View make_view(const WarpArgs& a, const Box& b, uint32_t simg,
@@ -386,6 +404,12 @@ __device__ __forceinline__ View make_view(const WarpArgs& a, const Box& b, uint3
   v.nx = static_cast<float>(a.nx);
   v.ny = static_cast<float>(a.ny);
   v.nz = static_cast<float>(a.nz);
+#ifdef W3D_CHECK_BOX
+  v.img_lo = simg;
+  v.img_hi = simg + kB * static_cast<uint32_t>(b.P * b.D);
+  v.lbl_lo = slbl;
+  v.lbl_hi = slbl + static_cast<uint32_t>(b.Pl * b.D);
+#endif
   return v;
 }
 
@@ -497,17 +521,26 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
                                : __ffma2_rn(hz, f2(v.Pf), __ffma2_rn(hy, f2(v.Wf), __fadd2_rn(L, hx))))
                    : __ffma2_rn(__fadd2_rn(rz, hz), f2(v.Plf),
                                 __ffma2_rn(__fadd2_rn(ry, hy), f2(v.Wlf), __fadd2_rn(sx, hx)));
+      W3D_IN_BOX(addr1(Ll.x, v.clbl), 1u, v.lbl_lo, v.lbl_hi);
+      W3D_IN_BOX(addr1(Ll.y, v.clbl), 1u, v.lbl_lo, v.lbl_hi);
       l0 = lds_u8(addr1(Ll.x, v.clbl));
       l1 = lds_u8(addr1(Ll.y, v.clbl));
     }
   }
   if (kNearest) {
+    W3D_IN_BOX(addrT<T>(Ln.x, v.cimg), InT<T>::kBytes, v.img_lo, v.img_hi);
+    W3D_IN_BOX(addrT<T>(Ln.y, v.cimg), InT<T>::kBytes, v.img_lo, v.img_hi);
     img = make_float2(lds_one<T>(addrT<T>(Ln.x, v.cimg)), lds_one<T>(addrT<T>(Ln.y, v.cimg)));
     return;
   }
   const uint32_t a0 = addrT<T>(L.x, v.cimg), b0 = addrT<T>(L.y, v.cimg);
   const uint32_t a1 = a0 + v.W4, b1 = b0 + v.W4, a2 = a0 + v.P4, b2 = b0 + v.P4;
   const uint32_t a3 = a0 + v.PW4, b3 = b0 + v.PW4;
+  // the 8 corners span [a0, a3 + 2 elements) (pitches > 0)
+  W3D_IN_BOX(a0, 2u * InT<T>::kBytes, v.img_lo, v.img_hi);
+  W3D_IN_BOX(a3, 2u * InT<T>::kBytes, v.img_lo, v.img_hi);
+  W3D_IN_BOX(b0, 2u * InT<T>::kBytes, v.img_lo, v.img_hi);
+  W3D_IN_BOX(b3, 2u * InT<T>::kBytes, v.img_lo, v.img_hi);
   float2 c000, c100, c010, c110, c001, c101, c011, c111;
   lds_pair<T>(a0, c000.x, c100.x);
   lds_pair<T>(b0, c000.y, c100.y);
@@ -549,6 +582,8 @@ __device__ __forceinline__ void label2(const View& v, float2 px, float2 py, floa
     Ll = __ffma2_rn(__fadd2_rn(rz, hz), f2(v.Plf),
                     __ffma2_rn(__fadd2_rn(ry, hy), f2(v.Wlf), __fadd2_rn(sx, hx)));
   }
+  W3D_IN_BOX(addr1(Ll.x, v.clbl), 1u, v.lbl_lo, v.lbl_hi);
+  W3D_IN_BOX(addr1(Ll.y, v.clbl), 1u, v.lbl_lo, v.lbl_hi);
   l0 = lds_u8(addr1(Ll.x, v.clbl));
   l1 = lds_u8(addr1(Ll.y, v.clbl));
 }
