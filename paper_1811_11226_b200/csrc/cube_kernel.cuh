@@ -701,6 +701,9 @@ __device__ __forceinline__ void gather2(const WarpArgs& a, const T* __restrict__
     const T* bZ = b + g.sz;
     const T* bYZ = bZ + g.sy;
     if (kGMode == kGIn) {
+#ifdef W3D_CHECK_BOX  // an inside tile's corners are all in the volume (tile_inside)
+      if (o < 0 || int64_t(o) + g.sz + g.sy + 1 >= int64_t(g.sz) * g.nz) __trap();
+#endif
       c[h][0] = InT<T>::load(b);
       c[h][1] = InT<T>::load(b + 1);
       c[h][2] = InT<T>::load(bY);
@@ -999,6 +1002,66 @@ __device__ __forceinline__ bool cp_sane(const VolDev& P, int ox, int oy, int oz,
   return sane;
 }
 
+#ifdef W3D_CHECK_BOX
+// Debug build: after staging (TMA + fix-up, or cp.async) and the barrier that
+// publishes it, every cell of the tile's boxes must hold the volume's value
+// (in-volume cells) or fill / label_fill (out-of-volume cells, when the box was
+// fixed up; a skipped fix-up leaves TMA's zeros, which no sample reads).  This
+// checks the async-proxy -> generic-proxy ordering (mbarrier wait, barrier) and
+// the fix-up's chunk coverage from inside the kernel (compute-sanitizer is not
+// available on this pool).  Traps on the first mismatch.
+template <class T>
+__device__ __noinline__ void check_box_content(const WarpArgs& a, const VolDev& P, const Box& b,
+                                               uint32_t simg, uint32_t slbl, bool labels,
+                                               bool img_fixed, bool lbl_fixed) {
+  const T* vin = vol_in<T>(P);
+  const uint8_t* lin = vol_lbl(P);
+  const int64_t sy = a.nx, sz = int64_t(a.nx) * a.ny;
+  const uint32_t fw = fill_word<T>(a);
+  const int cells = b.W * b.H * b.D;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+    const int x = c % b.W, y = (c / b.W) % b.H, z = c / (b.W * b.H);
+    const int gx = b.bx + x, gy = b.by + y, gz = b.bz + z;
+    const bool in = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny && gz >= 0 && gz < a.nz;
+    const uint32_t s = simg + InT<T>::kBytes * static_cast<uint32_t>(z * b.P + y * b.W + x);
+    uint32_t got;
+    if (InT<T>::kBytes == 4) {
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(got) : "r"(s));
+      if (in && got != __float_as_uint(__ldg(reinterpret_cast<const float*>(vin) +
+                                             (gz * sz + gy * sy + gx))))
+        __trap();
+      if (!in && img_fixed && got != fw) __trap();
+    } else {
+      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(got) : "r"(s));
+      const uint16_t want = in ? static_cast<uint16_t>(__ldg(reinterpret_cast<const short*>(vin) +
+                                                             (gz * sz + gy * sy + gx)))
+                               : static_cast<uint16_t>(fw);
+      if ((in || img_fixed) && got != want) __trap();
+    }
+  }
+  if (!labels) return;
+  const int hl = b.Pl / b.Wl;  // label rows per plane
+  const int lcells = b.Wl * hl * b.D;
+  for (int c = threadIdx.x; c < lcells; c += blockDim.x) {
+    const int x = c % b.Wl, y = (c / b.Wl) % hl, z = c / (b.Wl * hl);
+    if (y >= b.H) continue;  // padding rows of a cp.async box
+    const int gx = b.bxl + x, gy = b.by + y, gz = b.bz + z;
+    const bool in = gx >= 0 && gx < a.nx && gy >= 0 && gy < a.ny && gz >= 0 && gz < a.nz;
+    uint32_t got;
+    asm volatile("ld.shared.u8 %0, [%1];"
+                 : "=r"(got)
+                 : "r"(slbl + static_cast<uint32_t>(z * b.Pl + y * b.Wl + x)));
+    if (in && got != __ldg(lin + (gz * sz + gy * sy + gx))) __trap();
+    if (!in && lbl_fixed && got != a.label_fill) __trap();
+  }
+}
+#define W3D_CHECK_CONTENT(T, ...) check_box_content<T>(__VA_ARGS__)
+#else
+#define W3D_CHECK_CONTENT(T, ...) \
+  do {                            \
+  } while (0)
+#endif
+
 // Rare path (out of line): the tile in y-parts of TY/2, TY/4, ... rows, each
 // staged on its own, or gathered when even a 4-row part does not fit (or
 // always, for the W3D_KERNEL_GATHER variant).
@@ -1059,6 +1122,7 @@ __device__ __forceinline__ void tile_parts(const WarpArgs& a, int cap, bool gath
     const View v = make_view<T>(a, b, simg, slbl);
     cp_async_wait_all();
     __syncthreads();
+    W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels, true, true);
     if (!live) continue;
     if (b.clamp)
       column_rows<T, kLabels, kNearest, kPh, true, true, true>(a, P, V, v, vi, X, Z, y, rows / 4, n);
@@ -1176,6 +1240,7 @@ __device__ __forceinline__ void tma_fixup_lbl(const WarpArgs& a, const Box& b, u
 }
 
 
+
 // The common path: the whole tile staged as ONE box of the volume's fixed dims
 // (cp_w, cp_h, cp_d; host-computed by cube_cp_box to hold any tile's
 // footprint) whose origin follows from the tile's origin voxel alone -- every
@@ -1276,6 +1341,11 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
       if (fl) tma_fixup_lbl(a, b, slbl);
       __syncthreads();
     }
+    // zero fill / label_fill equal TMA's out-of-volume zeros: fixed without a fix-up
+    W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels, fi || (inside || a.fill == 0.0f),
+                      !kTmaLbl || fl || (insidel || a.label_fill == 0u));
+  } else {
+    W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels, true, true);
   }
   if (!live) return;
   if (oy + TY <= a.my)  // every row of the tile is an output row
@@ -1326,6 +1396,7 @@ __device__ __forceinline__ bool cube_tile(const WarpArgs& a, int cap, int vi, in
   const View v = make_view<T>(a, b, simg, slbl);
   cp_async_wait_all();
   __syncthreads();
+  W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels, true, true);
   if (!live) return false;
 #ifdef W3D_DBG_NOCOMPUTE
   if (n.x == 12345.0f) a.out[X] = n.y;  // keep the first Philox block alive
