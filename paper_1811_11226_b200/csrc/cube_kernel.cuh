@@ -43,6 +43,25 @@ constexpr int kPlaneRes = 20;           // plane pitch = 20 (mod 32) words (bank
 constexpr float kSane = 2097152.0f;     // 2^21: unclamped boxes only for |p| below this
 
 extern __shared__ __align__(16) unsigned char cube_smem[];
+#ifndef W3D_NO_ABS
+constexpr bool kUseAbs = true;  // fixed-box tiles index in absolute coordinates (sample2)
+#else
+constexpr bool kUseAbs = false;  // A/B knob
+#endif
+
+// float(y) for output rows y < kYTab, in constant memory: the full-column walk
+// reads each row pair's (y, y + 1) as a uniform-register pair (LDCU.64; y is
+// CTA-uniform), so the coordinate FFMA2 p = fma(A_k1, Y, inner) (R4) reads two
+// per-thread registers instead of three and no FADD2 steps Y.  Bit-identical:
+// the same y values enter the same FMA.
+constexpr int kYTab = 4096;
+struct YTable {
+  float v[kYTab];
+  constexpr YTable() : v() {
+    for (int i = 0; i < kYTab; ++i) v[i] = static_cast<float>(i);
+  }
+};
+static __constant__ YTable c_ytab = YTable();
 
 // one copy per instantiation unit (cube_inst_*.cu); warp3d_cube.cu sums them
 static __device__ unsigned long long g_cube_tiles[4];  // [staged, gathered, TMA, parts] (warp3d_tile_stats)
@@ -493,7 +512,14 @@ template <class T> __device__ __forceinline__ float lds_one(uint32_t a) {
 
 // Staged sampling of a y-pair: image (trilinear or nearest) and label.
 // kSameLbl: the label box has the image box's pitches (cp.async boxes).
-template <class T, bool kLabels, bool kNearest, bool kClamp, bool kSameLbl>
+// kAbs: the index in absolute volume coordinates, kM + fx + W fy + P fz (fy, fz
+// = floor(p) already formed for the fractions), the box origin folded into the
+// view's address constants -- two FADD2 fewer per pair than the box-relative
+// kM + fx + W (fy - by) + P (fz - bz).  Exact while |fx + W fy + P fz| < 2^22:
+// the host enables it per volume (VolDev::cp_abs) from the volume's dims, box
+// pitches and footprint extent, and tiles entirely outside the volume (which
+// could exceed it) never sample (cp_tile).
+template <class T, bool kLabels, bool kNearest, bool kClamp, bool kSameLbl, bool kAbs = false>
 __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, float2 pz,
                                         float2& img, uint32_t& l0, uint32_t& l1) {
   if (kClamp) {
@@ -503,10 +529,11 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
   }
   // floor on the FMA pipe: rm(p + kM) = kM + floor(p) exactly (|p| < 2^22)
   const float2 sx = add2_rm(px, f2(kM)), sy = add2_rm(py, f2(kM)), sz = add2_rm(pz, f2(kM));
+  const float2 fy = sub2(sy, f2(kM)), fz = sub2(sz, f2(kM));  // floor(p), exact
   const float2 tx = sub2(px, sub2(sx, f2(kM)));
-  const float2 ty = sub2(py, sub2(sy, f2(kM)));
-  const float2 tz = sub2(pz, sub2(sz, f2(kM)));
-  const float2 ry = sub2(sy, f2(v.Mby)), rz = sub2(sz, f2(v.Mbz));
+  const float2 ty = sub2(py, fy);
+  const float2 tz = sub2(pz, fz);
+  const float2 ry = kAbs ? fy : sub2(sy, f2(v.Mby)), rz = kAbs ? fz : sub2(sz, f2(v.Mbz));
   // kM + fx + W ry + P rz: exact integers below 2^24
   const float2 L = __ffma2_rn(rz, f2(v.Pf), __ffma2_rn(ry, f2(v.Wf), sx));
   float2 Ln = L;
@@ -558,7 +585,7 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
 // The label of a y-pair alone (an occluded column, R15: the image is 0 and its
 // fetch skipped): the index arithmetic of sample2's label
 // path, op for op, so the labels are the same bits.
-template <bool kClamp, bool kSameLbl>
+template <bool kClamp, bool kSameLbl, bool kAbs = false>
 __device__ __forceinline__ void label2(const View& v, float2 px, float2 py, float2 pz,
                                        uint32_t& l0, uint32_t& l1) {
   if (kClamp) {
@@ -567,10 +594,11 @@ __device__ __forceinline__ void label2(const View& v, float2 px, float2 py, floa
     pz = make_float2(fminf(fmaxf(pz.x, -1.0f), v.nz), fminf(fmaxf(pz.y, -1.0f), v.nz));
   }
   const float2 sx = add2_rm(px, f2(kM)), sy = add2_rm(py, f2(kM)), sz = add2_rm(pz, f2(kM));
+  const float2 fy = sub2(sy, f2(kM)), fz = sub2(sz, f2(kM));
   const float2 tx = sub2(px, sub2(sx, f2(kM)));
-  const float2 ty = sub2(py, sub2(sy, f2(kM)));
-  const float2 tz = sub2(pz, sub2(sz, f2(kM)));
-  const float2 ry = sub2(sy, f2(v.Mby)), rz = sub2(sz, f2(v.Mbz));
+  const float2 ty = sub2(py, fy);
+  const float2 tz = sub2(pz, fz);
+  const float2 ry = kAbs ? fy : sub2(sy, f2(v.Mby)), rz = kAbs ? fz : sub2(sz, f2(v.Mbz));
   const float2 hx = make_float2(fset_ge_half(tx.x), fset_ge_half(tx.y));
   const float2 hy = make_float2(fset_ge_half(ty.x), fset_ge_half(ty.y));
   const float2 hz = make_float2(fset_ge_half(tz.x), fset_ge_half(tz.y));
@@ -764,6 +792,14 @@ __device__ __forceinline__ void st_f32(float* p, float v) {
 __device__ __forceinline__ void st_u8(uint8_t* p, uint32_t v) {
   asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// p + bytes (a 64-bit byte step, kept as an add: ptxas would turn p + 4 * mx
+// into IMAD.WIDE.U32, ~4 dispatch cycles against 2 for the add pair)
+template <class P>
+__device__ __forceinline__ P* step(P* p, int64_t bytes) {
+  P* r;
+  asm("add.s64 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(bytes));
+  return r;
+}
 // base + element offset in one IMAD.WIDE.U32
 __device__ __forceinline__ float* at(float* base, uint32_t off) {
   float* r;
@@ -786,7 +822,7 @@ __device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
 // n2, n3; computed while the staging copies are in flight) and the loop
 // computes group g + kPre's block.
 template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
-          bool kSameLbl, bool kFull, int kPre, int kGMode, bool kOccOnly>
+          bool kSameLbl, bool kFull, int kPre, int kGMode, bool kOccOnly, bool kAbs>
 __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
@@ -796,7 +832,9 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
   const uint8_t* __restrict__ lin = kLabels ? vol_lbl(P) : nullptr;
   Vol V = V0;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) V.A1[k] = pin(V0.A1[k]);
+  for (int k = 0; k < 3; ++k)  // per-thread registers (opaque): the FFMA2's one uniform
+    V.A1[k] = __int_as_float(static_cast<int>(  // operand slot goes to the row pair Y
+        opaque(static_cast<uint32_t>(__float_as_int(V0.A1[k])))));
   V.sigma = pin(V0.sigma);
   V.ws = pin(V0.ws);
   V.wo = pin(V0.wo);
@@ -843,10 +881,10 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
     float2 img;
     uint32_t l0 = 0, l1 = 0;
     if (kOcc && kStaged) {
-      if (kLabels) label2<kClamp, kSameLbl>(v, px, py, pz, l0, l1);
+      if (kLabels) label2<kClamp, kSameLbl, kAbs>(v, px, py, pz, l0, l1);
     } else if (kOcc && !kLabels) {
     } else if (kStaged) {
-      sample2<T, kLabels, kNearest, kClamp, kSameLbl>(v, px, py, pz, img, l0, l1);
+      sample2<T, kLabels, kNearest, kClamp, kSameLbl, kAbs>(v, px, py, pz, img, l0, l1);
     } else if (!kNearest && kGMode != kGWide) {
       gather2<T, kLabels, kGMode>(a, vin, lin, gv, px, py, pz, img, l0, l1);
     } else {
@@ -855,6 +893,19 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
     }
     const float2 out = kOcc ? make_float2(0.0f, 0.0f) : photometric2<kPh>(img, nsp, V);
     const bool second = kFull || ya + 1 < my;
+#ifndef W3D_PTR_WIDE
+    // next row: 64-bit adds of the parameter pitch (IADD3 + IADD3.X on the ALU pipe)
+    float* po1 = step(po, a.out_row_bytes);
+    st_f32(po, out.x);
+    if (second) st_f32(po1, out.y);
+    po = step(po1, a.out_row_bytes);
+    if (kLabels) {
+      uint8_t* pl1 = step(pl, a.out_lrow_bytes);
+      st_u8(pl, l0);
+      if (second) st_u8(pl1, l1);
+      pl = step(pl1, a.out_lrow_bytes);
+    }
+#else  // A/B: the element offset scaled by IMAD.WIDE.U32
     float* po1 = po + row1;
     st_f32(po, out.x);
     if (second) st_f32(po1, out.y);
@@ -865,6 +916,7 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
       if (second) st_u8(pl1, l1);
       pl = pl1 + row1;
     }
+#endif
   };
   if constexpr (kOccOnly) {  // R15: labels only (no Philox block, no image fetch)
 #pragma unroll 1
@@ -875,6 +927,24 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
   if constexpr (kFull && kPre == 4) {
     if (ng == 4) {  // a whole 16-row column, normals precomputed: straight line, no rotation
       const std::false_type live_col;
+#ifndef W3D_NO_YTAB
+      // the tile's first row from the block index itself, so ptxas sees it uniform
+      const int yb = static_cast<int>(blockIdx.y) * kTY;
+      if (y0 == yb && yb + 16 <= kYTab) {  // row pairs from the uniform table
+        auto yt = [&](int j) {
+          return make_float2(c_ytab.v[yb + 2 * j], c_ytab.v[yb + 2 * j + 1]);
+        };
+        Y2 = yt(0); pair(y0, make_float2(n.x, n.y), live_col);
+        Y2 = yt(1); pair(y0 + 2, make_float2(n.z, n.w), live_col);
+        Y2 = yt(2); pair(y0 + 4, make_float2(n1.x, n1.y), live_col);
+        Y2 = yt(3); pair(y0 + 6, make_float2(n1.z, n1.w), live_col);
+        Y2 = yt(4); pair(y0 + 8, make_float2(n2.x, n2.y), live_col);
+        Y2 = yt(5); pair(y0 + 10, make_float2(n2.z, n2.w), live_col);
+        Y2 = yt(6); pair(y0 + 12, make_float2(n3.x, n3.y), live_col);
+        Y2 = yt(7); pair(y0 + 14, make_float2(n3.z, n3.w), live_col);
+        return;
+      }
+#endif
       pair(y0, make_float2(n.x, n.y), live_col);
       pair(y0 + 2, make_float2(n.z, n.w), live_col);
       pair(y0 + 4, make_float2(n1.x, n1.y), live_col);
@@ -914,7 +984,8 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
 // the volume's prism) takes the label-only instance, every other column the full
 // chain.  The column is one thread, so the test is per thread.
 template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
-          bool kSameLbl = false, bool kFull = false, int kPre = 1, int kGMode = kGEdge>
+          bool kSameLbl = false, bool kFull = false, int kPre = 1, int kGMode = kGEdge,
+          bool kAbs = false>
 __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
@@ -922,10 +993,10 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
                                             float4 n3 = make_float4(0.f, 0.f, 0.f, 0.f)) {
   if ((V.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi)
     column_rows_impl<T, kLabels, kNearest, kPh, kStaged, kClamp, kSameLbl, kFull, kPre, kGMode,
-                     true>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
+                     true, kAbs>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
   else
     column_rows_impl<T, kLabels, kNearest, kPh, kStaged, kClamp, kSameLbl, kFull, kPre, kGMode,
-                     false>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
+                     false, kAbs>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
 }
 
 __device__ __forceinline__ Vol load_vol(const VolDev& P) {
@@ -1258,6 +1329,17 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   constexpr int kC = InT<T>::kChunk;
   constexpr uint32_t kB = InT<T>::kBytes;
   const uint32_t simg = smem_base();
+  if (tile_outside(a, P, p0)) {  // uniform: every sample is fill / label_fill (R6, R8)
+    // nothing to stage or fetch; noise, window and gamma still apply (R9)
+    const int lane = threadIdx.x & 31;
+    const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
+    if (X >= a.mx || Z >= a.mz) return;
+    const Vol V = load_vol(P);
+    const View none{};
+    column_rows<T, kLabels, kNearest, kPh, false, false, false, false, 1, kGOut>(
+        a, P, V, none, vi, X, Z, oy, TY / 4, first_normals<kPh>(a, P, V, X, Z, oy));
+    return;
+  }
   Box b;
   b.W = P.cp_w;
   b.H = P.cp_h;
@@ -1324,6 +1406,12 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   v.W4 = P.cp_w_bytes;  // straight from the parameters: uniform registers, folded
   v.P4 = P.cp_p_bytes;  // into the shared-memory addresses ([R + UR])
   v.PW4 = static_cast<uint32_t>(P.cp_w_bytes) + static_cast<uint32_t>(P.cp_p_bytes);
+  // absolute index (sample2 kAbs, host-checked P.cp_abs): the box origin in y and z
+  // moves from the float index into the address constants
+  if (kUseAbs) {
+    v.cimg = opaque(v.cimg - kB * static_cast<uint32_t>(b.W * b.by + b.P * b.bz));
+    v.clbl = opaque(v.clbl - static_cast<uint32_t>(b.Wl * b.by + b.Pl * b.bz));
+  }
   if (!kTmaLbl) cp_async_wait_all();
   __syncthreads();  // label copies (and the mbarrier init) visible to every thread
   if (tma) {
@@ -1349,10 +1437,10 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   }
   if (!live) return;
   if (oy + TY <= a.my)  // every row of the tile is an output row
-    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre>(
+    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre, kGEdge, kUseAbs>(
         a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
   else
-    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre>(
+    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre, kGEdge, kUseAbs>(
         a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
 }
 

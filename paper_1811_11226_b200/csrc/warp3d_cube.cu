@@ -5,6 +5,7 @@
 // cube_kernel.cuh.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -64,15 +65,17 @@ bool cube_tma_supported(const WarpArgs& a) { return cube_supported(a); }
 // half-warps over the banks (tools/model_tiles.py); cp_p = cp_w * cp_h, so the
 // TMA box (cp_w, cp_h, cp_d) lands with the same pitches.  cp_rows = kTY when
 // the box fits the buffer, else 0 (per-tile exact boxes, parts, gathers).
-void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3]) {
+void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], const int out[3]) {
   using namespace cube;
   const int kC = 16 / elem_bytes;
   const int cap = kCapVox * 5 / (elem_bytes + 1);
   P.cp_w = P.cp_h = P.cp_d = P.cp_rows = 0;
+  P.cp_abs = 0;
   P.cp_p = 0;
   P.cp_w_bytes = P.cp_p_bytes = 0;
   P.box_w = P.box_h = P.box_d = P.box_wl = 0;
   int d[3];
+  double ext_k[3] = {0.0, 0.0, 0.0};
   const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
   bool ok = true;
   for (int k = 0; k < 3; ++k) {
@@ -87,6 +90,7 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3])
     const double margin = 16.0 * mag * 0x1.0p-24 + 1e-3;
     P.box_mlo[k] = static_cast<float>(mlo - margin);
     P.box_mhi[k] = std::nextafter(static_cast<float>(mhi + margin), INFINITY);  // rounded up
+    ext_k[k] = ext;
     if (ext > 200.0) ok = false;
     d[k] = ok ? static_cast<int>(std::floor(ext + 2.0 * margin)) + 3 : 0;
   }
@@ -128,6 +132,21 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3])
   }
   const int64_t Pp = int64_t(best_w) * best_h;
   if (Pp * D > cap || best_w > 4 * THREADS || best_w > 256 || best_h > 256 || D > 256) return;
+  // the staged index in absolute coordinates (cube_kernel.cuh sample2 kAbs): a tile
+  // not entirely outside the volume has, on each axis, p within the footprint extent
+  // (+ the rounding margin and the +1 corner) of [-1, n]; |fx + W fy + P fz| must
+  // stay below 2^22 there (the magic-number index kM +- 2^22).  Otherwise the volume
+  // takes the per-tile boxes.
+  {
+    double lim = 0.0;
+    const double pitch[3] = {1.0, double(best_w), double(Pp)};
+    for (int k = 0; k < 3; ++k) {
+      const double e = std::ceil(ext_k[k]) + 4.0;
+      lim += pitch[k] * std::max(double(in[k]) + e, 1.0 + e);
+    }
+    if (!(lim < 4194304.0)) return;
+  }
+  P.cp_abs = 1;
   P.cp_w = static_cast<uint16_t>(best_w);
   P.cp_h = static_cast<uint16_t>(best_h);
   P.cp_d = static_cast<uint16_t>(D);

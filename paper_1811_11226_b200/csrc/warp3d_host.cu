@@ -313,6 +313,8 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
     args.mx = out_dims.nx; args.my = out_dims.ny; args.mz = out_dims.nz;
     args.in_stride = in_n;
     args.out_stride = out_n;
+    args.out_row_bytes = 4 * int64_t(out_dims.nx);
+    args.out_lrow_bytes = out_dims.nx;
     args.fill = fill;
     args.label_fill = label_fill;
     args.interp = interp;
@@ -325,8 +327,9 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       P.lbl_addr = reinterpret_cast<uint64_t>(vols[v0 + i].lbl);
       P.out_slot = vols[v0 + i].slot;
       if (P.in_addr % 16 || P.lbl_addr % 8) args.in_aligned = 0;
+      const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
       const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
-      cube_cp_box(affines[v0 + i], P, elem, od);
+      cube_cp_box(affines[v0 + i], P, elem, id, od);
     }
     for (int r = 0; r < 10; ++r) {  // volume 0's key schedule (used when all seeds agree)
       args.rk0[r] = args.vol[0].rk0[r];

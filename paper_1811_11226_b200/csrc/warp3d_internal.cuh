@@ -56,7 +56,9 @@ struct alignas(16) VolDev {
   // inside the volume iff floor(p0 + box_mlo[k]) >= 0 and p0 + box_mhi[k] <
   // n_k - 1 (box_mhi[k] = sum_j max(0, A_kj span_j) + the same margin)
   float box_mhi[3];
-  int32_t _pad0;
+  int32_t cp_abs;       // cp_rows != 0 only with 1: the staged index kM + fx + W fy + P fz
+                        // (absolute volume coordinates) is exact for every tile not
+                        // entirely outside the volume (cube_cp_box)
   int32_t out_slot;     // output volume index in the caller's batch (out + slot * out_stride)
   uint64_t in_addr;     // device address of this volume's image (float32 or int16)
   uint64_t lbl_addr;    // device address of its labels (0 without labels)
@@ -88,6 +90,9 @@ struct alignas(64) WarpArgsT {
   int32_t mx, my, mz;     // output dims
   int64_t in_stride;      // voxels per input volume
   int64_t out_stride;     // voxels per output volume
+  int64_t out_row_bytes;  // 4 * mx: the float output row pitch in bytes, and mx: the
+  int64_t out_lrow_bytes; // label row pitch (kernel parameters, so the per-row pointer
+                          // steps are plain 64-bit adds of a parameter, not IMAD.WIDE)
   float fill;
   uint32_t label_fill;
   uint32_t fill16_pair;   // int16 input: (int16)fill in both halves (staged boxes)
@@ -117,7 +122,7 @@ bool cube_tma_supported(const WarpArgs& a);
 // staging box (TMA image box and cp.async boxes) of one volume's tiles and its
 // origin offsets (out = output dims x, y, z: the rounding margin scales with
 // the largest |p|)
-void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int out[3]);
+void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], const int out[3]);
 cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s);
 cudaError_t read_cube_stats(unsigned long long out[4]);
 // warp3d_resample.cu (NEXT-3): one separable Gaussian pass along `axis` (0 x, 1 y, 2 z)
