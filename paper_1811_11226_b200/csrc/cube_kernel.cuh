@@ -517,8 +517,7 @@ template <class T> __device__ __forceinline__ float lds_one(uint32_t a) {
 // view's address constants -- two FADD2 fewer per pair than the box-relative
 // kM + fx + W (fy - by) + P (fz - bz).  Exact while |fx + W fy + P fz| < 2^22:
 // the host enables it per volume (VolDev::cp_abs) from the volume's dims, box
-// pitches and footprint extent, and tiles entirely outside the volume (which
-// could exceed it) never sample (cp_tile).
+// pitches and the range of p over the whole output volume.
 template <class T, bool kLabels, bool kNearest, bool kClamp, bool kSameLbl, bool kAbs = false>
 __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, float2 pz,
                                         float2& img, uint32_t& l0, uint32_t& l1) {
@@ -1329,17 +1328,6 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   constexpr int kC = InT<T>::kChunk;
   constexpr uint32_t kB = InT<T>::kBytes;
   const uint32_t simg = smem_base();
-  if (tile_outside(a, P, p0)) {  // uniform: every sample is fill / label_fill (R6, R8)
-    // nothing to stage or fetch; noise, window and gamma still apply (R9)
-    const int lane = threadIdx.x & 31;
-    const int X = ox + (lane & 15), Z = oz + 2 * static_cast<int>(threadIdx.x >> 5) + (lane >> 4);
-    if (X >= a.mx || Z >= a.mz) return;
-    const Vol V = load_vol(P);
-    const View none{};
-    column_rows<T, kLabels, kNearest, kPh, false, false, false, false, 1, kGOut>(
-        a, P, V, none, vi, X, Z, oy, TY / 4, first_normals<kPh>(a, P, V, X, Z, oy));
-    return;
-  }
   Box b;
   b.W = P.cp_w;
   b.H = P.cp_h;

@@ -65,7 +65,8 @@ bool cube_tma_supported(const WarpArgs& a) { return cube_supported(a); }
 // half-warps over the banks (tools/model_tiles.py); cp_p = cp_w * cp_h, so the
 // TMA box (cp_w, cp_h, cp_d) lands with the same pitches.  cp_rows = kTY when
 // the box fits the buffer, else 0 (per-tile exact boxes, parts, gathers).
-void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], const int out[3]) {
+void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[3],
+                 const int out[3]) {
   using namespace cube;
   const int kC = 16 / elem_bytes;
   const int cap = kCapVox * 5 / (elem_bytes + 1);
@@ -75,7 +76,6 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], 
   P.cp_w_bytes = P.cp_p_bytes = 0;
   P.box_w = P.box_h = P.box_d = P.box_wl = 0;
   int d[3];
-  double ext_k[3] = {0.0, 0.0, 0.0};
   const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
   bool ok = true;
   for (int k = 0; k < 3; ++k) {
@@ -90,7 +90,6 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], 
     const double margin = 16.0 * mag * 0x1.0p-24 + 1e-3;
     P.box_mlo[k] = static_cast<float>(mlo - margin);
     P.box_mhi[k] = std::nextafter(static_cast<float>(mhi + margin), INFINITY);  // rounded up
-    ext_k[k] = ext;
     if (ext > 200.0) ok = false;
     d[k] = ok ? static_cast<int>(std::floor(ext + 2.0 * margin)) + 3 : 0;
   }
@@ -132,17 +131,24 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], 
   }
   const int64_t Pp = int64_t(best_w) * best_h;
   if (Pp * D > cap || best_w > 4 * THREADS || best_w > 256 || best_h > 256 || D > 256) return;
-  // the staged index in absolute coordinates (cube_kernel.cuh sample2 kAbs): a tile
-  // not entirely outside the volume has, on each axis, p within the footprint extent
-  // (+ the rounding margin and the +1 corner) of [-1, n]; |fx + W fy + P fz| must
-  // stay below 2^22 there (the magic-number index kM +- 2^22).  Otherwise the volume
-  // takes the per-tile boxes.
+  // the staged index in absolute coordinates (cube_kernel.cuh sample2 kAbs):
+  // |fx + W fy + P fz| < 2^22 (the magic-number index kM +- 2^22) for every p of
+  // the output volume (p is affine: its range is spanned by the 8 output corners;
+  // + the rounding margin, the +1 corner and the box slack).  Otherwise the
+  // volume takes the per-tile boxes.
   {
     double lim = 0.0;
-    const double pitch[3] = {1.0, double(best_w), double(Pp)};
+    // the image and (TMA) label pitches, whichever is larger
+    const double pitch[3] = {1.0, double(std::max(best_w, Wl)),
+                             double(std::max<int64_t>(Pp, int64_t(Wl) * H0))};
     for (int k = 0; k < 3; ++k) {
-      const double e = std::ceil(ext_k[k]) + 4.0;
-      lim += pitch[k] * std::max(double(in[k]) + e, 1.0 + e);
+      double lo = A[4 * k + 3], hi = A[4 * k + 3];
+      for (int j = 0; j < 3; ++j) {
+        const double t = double(A[4 * k + j]) * (out[j] - 1);
+        lo += t < 0.0 ? t : 0.0;
+        hi += t > 0.0 ? t : 0.0;
+      }
+      lim += pitch[k] * (std::max(std::fabs(lo), std::fabs(hi)) + 8.0);
     }
     if (!(lim < 4194304.0)) return;
   }
