@@ -1368,12 +1368,12 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   }
   // an occluded column (R15) needs no noise: its Philox blocks are skipped
   const bool need_noise = live && !((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi);
-  float4 n = (need_noise && !(kPh == kPhFull && W3D_PRE == 4))
-                 ? first_normals<kPh>(a, P, V, X, Z, oy)
-                 : make_float4(0, 0, 0, 0);
   // the training chain (kPhFull, launch-wide keys) computes kPre Philox blocks
-  // here, under the staging latency; the generic chain one (register budget)
-  constexpr int kPre = kPh == kPhFull ? W3D_PRE : 1;
+  // here, under the staging latency (at most the tile's TY / 4); the generic
+  // chain one (register budget)
+  constexpr int kPre = kPh == kPhFull ? (W3D_PRE < TY / 4 ? W3D_PRE : TY / 4) : 1;
+  float4 n = (need_noise && kPre != 4) ? first_normals<kPh>(a, P, V, X, Z, oy)
+                                       : make_float4(0, 0, 0, 0);
   const float4 z4 = make_float4(0, 0, 0, 0);
   float4 n1 = z4, n2 = z4, n3 = z4;
   if (kPre == 4 && need_noise) {  // the column's four blocks in lockstep
@@ -1520,9 +1520,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
 // Launch
 // ---------------------------------------------------------------------------
 
-template <class T, bool kLabels, bool kNearest, int kPh, bool kGather, int NV>
+template <class T, bool kLabels, bool kNearest, int kPh, bool kGather, int NV, int TY = kTY>
 static cudaError_t launch_n(const WarpArgsT<NV>& a, cudaStream_t s) {
-  const int tiles_x = (a.mx + TX - 1) / TX, tiles_y = (a.my + kTY - 1) / kTY;
+  const int tiles_x = (a.mx + TX - 1) / TX, tiles_y = (a.my + TY - 1) / TY;
   const int tiles_z = (a.mz + TZ - 1) / TZ;
   if (tiles_y > 65535 || int64_t(tiles_z) * a.nvol > 65535) return cudaErrorInvalidConfiguration;
   const size_t smem = kGather ? 0 : static_cast<size_t>(kCapVox) * 5 + 256;
@@ -1536,7 +1536,7 @@ static cudaError_t launch_n(const WarpArgsT<NV>& a, cudaStream_t s) {
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(configured.load(std::memory_order_acquire) & bit)) {
       const cudaError_t e = cudaFuncSetAttribute(
-          warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>,
+          warp3d_cube_kernel<T, TY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>,
           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) return e;
       configured.fetch_or(bit, std::memory_order_acq_rel);
@@ -1547,7 +1547,7 @@ static cudaError_t launch_n(const WarpArgsT<NV>& a, cudaStream_t s) {
   const uint32_t tz_magic =
       tiles_z > 1 ? static_cast<uint32_t>(((uint64_t(1) << 32) + tiles_z - 1) / tiles_z) : 0u;
   if (!a.pdl) {
-    warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>
+    warp3d_cube_kernel<T, TY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>
         <<<grid, THREADS, smem, s>>>(a, tiles_z, cap, tz_magic);
     return cudaGetLastError();
   }
@@ -1568,7 +1568,7 @@ static cudaError_t launch_n(const WarpArgsT<NV>& a, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(
-      &cfg, warp3d_cube_kernel<T, kTY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>,
+      &cfg, warp3d_cube_kernel<T, TY, kGather ? kGMinB : kMinB, kLabels, kNearest, kPh, kGather, NV>,
       a, tiles_z, cap, tz_magic);
 }
 
@@ -1600,6 +1600,14 @@ cudaError_t launch_typed_nv(const WarpArgsT<NV>& a, bool gather_only, cudaStream
     return labels ? launch_n<T, true, false, kPhGeneric, true>(a, s)
                   : launch_n<T, false, false, kPhGeneric, true>(a, s);
   }
+  if (a.tile_rows == kTY / 2 && !nearest) {  // AUTO's 8-row tiles (large footprints)
+    if (all_full(a))
+      return labels ? launch_n<T, true, false, kPhFull, false, NV, kTY / 2>(a, s)
+                    : launch_n<T, false, false, kPhFull, false, NV, kTY / 2>(a, s);
+    return labels ? launch_n<T, true, false, kPhGeneric, false, NV, kTY / 2>(a, s)
+                  : launch_n<T, false, false, kPhGeneric, false, NV, kTY / 2>(a, s);
+  }
+  if (a.tile_rows != kTY) return cudaErrorInvalidValue;
   if (nearest)
     return labels ? launch_n<T, true, true, kPhGeneric, false>(a, s)
                   : launch_n<T, false, true, kPhGeneric, false>(a, s);

@@ -66,7 +66,7 @@ bool cube_tma_supported(const WarpArgs& a) { return cube_supported(a); }
 // TMA box (cp_w, cp_h, cp_d) lands with the same pitches.  cp_rows = kTY when
 // the box fits the buffer, else 0 (per-tile exact boxes, parts, gathers).
 void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[3],
-                 const int out[3]) {
+                 const int out[3], int tile_rows) {
   using namespace cube;
   const int kC = 16 / elem_bytes;
   const int cap = kCapVox * 5 / (elem_bytes + 1);
@@ -76,7 +76,7 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[
   P.cp_w_bytes = P.cp_p_bytes = 0;
   P.box_w = P.box_h = P.box_d = P.box_wl = 0;
   int d[3];
-  const double span[3] = {TX - 1.0, kTY - 1.0, TZ - 1.0};
+  const double span[3] = {TX - 1.0, tile_rows - 1.0, TZ - 1.0};
   bool ok = true;
   for (int k = 0; k < 3; ++k) {
     double mag = std::fabs(double(A[4 * k + 3])), ext = 0.0, mlo = 0.0, mhi = 0.0;
@@ -157,7 +157,7 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[
   P.cp_h = static_cast<uint16_t>(best_h);
   P.cp_d = static_cast<uint16_t>(D);
   P.cp_p = static_cast<int32_t>(Pp);
-  P.cp_rows = static_cast<uint16_t>(kTY);
+  P.cp_rows = static_cast<uint16_t>(tile_rows);
   P.cp_w_bytes = static_cast<uint16_t>(best_w * elem_bytes);
   P.cp_p_bytes = static_cast<uint16_t>(Pp * elem_bytes);
   // the TMA label box, used when it fits beside the image box (and

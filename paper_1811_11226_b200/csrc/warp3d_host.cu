@@ -21,8 +21,12 @@
 #include "philox.cuh"
 #include "warp3d.h"
 #include "warp3d_internal.cuh"
+#include "cube_config.cuh"
 
 namespace w3d {
+// tile heights of the staged warp kernel: kTY rows, or half as many for launches
+// whose kTY-row boxes do not fit the staging buffer (AUTO, launch_group)
+constexpr int kTileRows = cube::kTY, kTileRowsSmall = cube::kTY / 2;
 
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
@@ -329,7 +333,32 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       if (P.in_addr % 16 || P.lbl_addr % 8) args.in_aligned = 0;
       const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
       const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
-      cube_cp_box(affines[v0 + i], P, elem, id, od);
+      cube_cp_box(affines[v0 + i], P, elem, id, od, kTileRows);
+    }
+    // AUTO: when no volume's 16-row box fits the buffer (large rotations / scales),
+    // 8-row tiles (half the box height) usually do: stage those by TMA rather than
+    // gathering every corner through L1 (C4)
+    args.tile_rows = kTileRows;
+    if (variant == W3D_KERNEL_AUTO && interp == W3D_INTERP_LINEAR) {
+      bool any16 = false, any8 = false;
+      for (int32_t i = 0; i < nv; ++i) any16 |= args.vol[i].cp_rows != 0;
+      if (!any16) {
+        for (int32_t i = 0; i < nv; ++i) {
+          const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
+          const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
+          cube_cp_box(affines[v0 + i], args.vol[i], elem, id, od, kTileRowsSmall);
+          any8 |= args.vol[i].cp_rows != 0;
+        }
+        if (any8) {
+          args.tile_rows = kTileRowsSmall;
+        } else {  // neither fits: back to the 16-row offsets (the gather kernel's tile classes)
+          for (int32_t i = 0; i < nv; ++i) {
+            const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
+            const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
+            cube_cp_box(affines[v0 + i], args.vol[i], elem, id, od, kTileRows);
+          }
+        }
+      }
     }
     for (int r = 0; r < 10; ++r) {  // volume 0's key schedule (used when all seeds agree)
       args.rk0[r] = args.vol[0].rk0[r];

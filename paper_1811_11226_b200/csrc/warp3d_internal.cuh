@@ -102,7 +102,9 @@ struct alignas(64) WarpArgsT {
   int32_t in_aligned;     // every volume's image (labels) 16 B (8 B) aligned: staged paths
   int32_t pdl;            // host only: launch as a programmatic dependent of the previous
                           // chunk of the same call (independent volumes: no data dependency)
-  int32_t _pad;
+  int32_t tile_rows;      // output rows per tile (kTY = 16, or 8 for launches whose
+                          // 16-row boxes do not fit: large rotations, AUTO); the
+                          // per-volume boxes and offsets are computed for it
   // Philox round keys shared by every volume of the launch (all seeds equal;
   // required by the kPhFull kernels: fixed parameter offsets, so the round
   // function reads them as constant-bank operands)
@@ -122,7 +124,8 @@ bool cube_tma_supported(const WarpArgs& a);
 // staging box (TMA image box and cp.async boxes) of one volume's tiles and its
 // origin offsets (out = output dims x, y, z: the rounding margin scales with
 // the largest |p|)
-void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], const int out[3]);
+void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int in[3], const int out[3],
+                 int tile_rows);
 cudaError_t launch_cube(const WarpArgs& a, bool gather_only, cudaStream_t s);
 cudaError_t read_cube_stats(unsigned long long out[4]);
 // warp3d_resample.cu (NEXT-3): one separable Gaussian pass along `axis` (0 x, 1 y, 2 z)
