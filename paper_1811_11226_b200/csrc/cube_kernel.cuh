@@ -1504,8 +1504,21 @@ __global__ void __launch_bounds__(THREADS, MINB)
   // tiles_z) (exact for operands < 2^16)
   const int vi = tiles_z == 1 ? static_cast<int>(blockIdx.z)
                               : static_cast<int>(__umulhi(blockIdx.z, tz_magic));
-  const int ox = static_cast<int>(blockIdx.x) * TX, oy = static_cast<int>(blockIdx.y) * TY;
-  const int oz = (static_cast<int>(blockIdx.z) - vi * tiles_z) * TZ;
+  int tx = static_cast<int>(blockIdx.x), ty = static_cast<int>(blockIdx.y);
+  int tz = static_cast<int>(blockIdx.z) - vi * tiles_z;
+  if (a.brick) {  // launch order (x, y, z fastest to slowest) -> bricks of tiles
+    const uint32_t f = static_cast<uint32_t>(a.brick);
+    const int sx = f & 15, sy = (f >> 4) & 15, sz = (f >> 8) & 15, lbx = (f >> 12) & 15,
+              lby = (f >> 16) & 15;
+    const uint32_t L = static_cast<uint32_t>(tx) +
+                       gridDim.x * (static_cast<uint32_t>(ty) + gridDim.y * static_cast<uint32_t>(tz));
+    const uint32_t w = L & ((1u << (sx + sy + sz)) - 1u), bi = L >> (sx + sy + sz);
+    tx = static_cast<int>(((bi & ((1u << lbx) - 1u)) << sx) | (w & ((1u << sx) - 1u)));
+    ty = static_cast<int>((((bi >> lbx) & ((1u << lby) - 1u)) << sy) |
+                          ((w >> sx) & ((1u << sy) - 1u)));
+    tz = static_cast<int>(((bi >> (lbx + lby)) << sz) | (w >> (sx + sy)));
+  }
+  const int ox = tx * TX, oy = ty * TY, oz = tz * TZ;
   cube_tile<T, TY, kLabels, kNearest, kPh, kGather>(a, cap, vi, ox, oy, oz, mbar, 0u, true);
   // A programmatic dependent (a later chunk of the same call) never reads its
   // primary's output, but the grid must not COMPLETE before its primary: work

@@ -277,6 +277,31 @@ static bool prepare_tma(WarpArgs& args) {
   return ok;
 }
 
+// Tile order of a launch (WarpArgs::brick): volumes much larger than L2 whose
+// footprint boxes are large (the 8-row launches: large rotations) traverse the
+// output in bricks of 2^s x 2^s x 2^s tiles (y doubled for 8-row tiles), so the
+// input a wave reads is compact and its reuse by neighbouring tiles hits in L2.
+// Needs power-of-two tile counts per brick row / column (else 0: launch order).
+// W3D_BRICK=<log2 tiles> overrides (0 = off; experiments).
+static int32_t brick_order(const WarpArgs& a, bool gather) {
+  static const int env = getenv("W3D_BRICK") ? atoi(getenv("W3D_BRICK")) : -1;
+  const int s = env >= 0 ? env : (a.tile_rows != kTileRows && !gather ? 2 : 0);
+  if (s <= 0) return 0;
+  const int sy = s + (a.tile_rows == kTileRows ? 0 : 1);
+  const int64_t tx = (a.mx + cube::TX - 1) / cube::TX, ty = (a.my + a.tile_rows - 1) / a.tile_rows;
+  const int64_t tz = (a.mz + cube::TZ - 1) / cube::TZ;
+  auto lg = [](int64_t v) {
+    int l = 0;
+    while ((int64_t(1) << l) < v) ++l;
+    return (int64_t(1) << l) == v ? l : -1;
+  };
+  if (tx % (1 << s) || ty % (1 << sy) || tz % (1 << s)) return 0;
+  const int lbx = lg(tx >> s), lby = lg(ty >> sy);
+  if (lbx < 0 || lby < 0 || lbx > 15 || lby > 15 || s > 15 || sy > 15) return 0;
+  return int32_t(0x80000000u | uint32_t(s) | uint32_t(sy) << 4 | uint32_t(s) << 8 |
+                 uint32_t(lbx) << 12 | uint32_t(lby) << 16);
+}
+
 // One group of volumes with the same in_dims, already validated; chunks of
 // kMaxVolPerLaunch (kTmaVolPerLaunch with TMA) volumes.  Volume i reads
 // vols[i] (image: float32 if elem == 4, int16 if elem == 2; labels nullable)
@@ -379,6 +404,7 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       for (int32_t i = 0; i < nv; ++i) any_box |= args.vol[i].cp_rows != 0;
       gather = !any_box;
     }
+    args.brick = brick_order(args, gather);
     args.pdl = v0 > 0 ? 1 : 0;  // the first chunk waits for all prior work on the stream
     const cudaError_t e = launch_cube(args, gather, stream);
     if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");

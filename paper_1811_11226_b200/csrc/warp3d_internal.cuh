@@ -105,6 +105,10 @@ struct alignas(64) WarpArgsT {
   int32_t tile_rows;      // output rows per tile (kTY = 16, or 8 for launches whose
                           // 16-row boxes do not fit: large rotations, AUTO); the
                           // per-volume boxes and offsets are computed for it
+  int32_t brick;          // 0, or the tile order in bricks of 2^sx x 2^sy x 2^sz tiles
+                          // (bit 31 set; sx, sy, sz, log2 bricks per row / column in
+                          // 4-bit fields from bit 0): consecutive CTAs cover compact
+                          // output regions, so a wave's input footprint stays in L2
   // Philox round keys shared by every volume of the launch (all seeds equal;
   // required by the kPhFull kernels: fixed parameter offsets, so the round
   // function reads them as constant-bank operands)
