@@ -923,6 +923,16 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
       pair(ya, make_float2(0.f, 0.f), std::true_type());
     return;
   }
+  if constexpr (kFull && kPre == 2) {
+    if (ng == 2) {  // a whole 8-row column (8-row tiles), normals precomputed
+      const std::false_type live_col;
+      pair(y0, make_float2(n.x, n.y), live_col);
+      pair(y0 + 2, make_float2(n.z, n.w), live_col);
+      pair(y0 + 4, make_float2(n1.x, n1.y), live_col);
+      pair(y0 + 6, make_float2(n1.z, n1.w), live_col);
+      return;
+    }
+  }
   if constexpr (kFull && kPre == 4) {
     if (ng == 4) {  // a whole 16-row column, normals precomputed: straight line, no rotation
       const std::false_type live_col;
@@ -1372,8 +1382,9 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   // here, under the staging latency (at most the tile's TY / 4); the generic
   // chain one (register budget)
   constexpr int kPre = kPh == kPhFull ? (W3D_PRE < TY / 4 ? W3D_PRE : TY / 4) : 1;
-  float4 n = (need_noise && kPre != 4) ? first_normals<kPh>(a, P, V, X, Z, oy)
-                                       : make_float4(0, 0, 0, 0);
+  float4 n = (need_noise && kPre != 4 && !(kPre == 2 && kPh == kPhFull))
+                  ? first_normals<kPh>(a, P, V, X, Z, oy)
+                  : make_float4(0, 0, 0, 0);
   const float4 z4 = make_float4(0, 0, 0, 0);
   float4 n1 = z4, n2 = z4, n3 = z4;
   if (kPre == 4 && need_noise) {  // the column's four blocks in lockstep
@@ -1382,11 +1393,20 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
                         mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(oy >> 2));
     const uint32_t qs[4] = {q0, q0 + mxu, q0 + 2u * mxu, q0 + 3u * mxu};
     uint4 r[4];
-    philox_block4(qs, PhiloxPrefix{P.ph_K0, P.ph_K1, P.ph_K2, P.ph_U3}, a.rk0, a.rk1, r);
+    philox_block4<4>(qs, PhiloxPrefix{P.ph_K0, P.ph_K1, P.ph_K2, P.ph_U3}, a.rk0, a.rk1, r);
     n = box_muller4(r[0]);
     n1 = box_muller4(r[1]);
     n2 = box_muller4(r[2]);
     n3 = box_muller4(r[3]);
+  } else if (kPre == 2 && kPh == kPhFull && need_noise) {  // 8-row tiles: two in lockstep
+    const uint32_t gyn = static_cast<uint32_t>((a.my + 3) >> 2), mxu = static_cast<uint32_t>(a.mx);
+    const uint32_t q0 = static_cast<uint32_t>(X) +
+                        mxu * (gyn * static_cast<uint32_t>(Z) + static_cast<uint32_t>(oy >> 2));
+    const uint32_t qs[2] = {q0, q0 + mxu};
+    uint4 r[2];
+    philox_block4<2>(qs, PhiloxPrefix{P.ph_K0, P.ph_K1, P.ph_K2, P.ph_U3}, a.rk0, a.rk1, r);
+    n = box_muller4(r[0]);
+    n1 = box_muller4(r[1]);
   } else if (kPre == 2 && need_noise) {
     n1 = first_normals<kPh>(a, P, V, X, Z, oy + 4);
   }

@@ -81,15 +81,16 @@ __device__ __forceinline__ uint4 philox_block(uint32_t q, const PhiloxPrefix& P,
   return make_uint4(c0, c1, c2, c3);
 }
 
-// Four blocks (counters q[0..3]) in lockstep: each round key is read once for
-// the four, and the four independent multiply chains overlap.  Bit-identical
-// to four philox_block calls.
-__device__ __forceinline__ void philox_block4(const uint32_t q[4], const PhiloxPrefix& P,
+// NB (4, or 2 for 8-row tiles) blocks (counters q[0..NB-1]) in lockstep: each
+// round key is read once for all, and the independent multiply chains overlap.
+// Bit-identical to NB philox_block calls.
+template <int NB = 4>
+__device__ __forceinline__ void philox_block4(const uint32_t q[NB], const PhiloxPrefix& P,
                                               const uint32_t* rk0, const uint32_t* rk1,
-                                              uint4 out[4]) {
-  uint32_t c0[4], c1[4], c2[4], c3[4];
+                                              uint4 out[NB]) {
+  uint32_t c0[NB], c1[NB], c2[NB], c3[NB];
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
+  for (int b = 0; b < NB; ++b) {
     const uint64_t a = static_cast<uint64_t>(kPhiloxM0) * q[b];
     const uint32_t c2a = static_cast<uint32_t>(a >> 32) ^ P.K0;
     const uint32_t c3a = static_cast<uint32_t>(a);
@@ -103,10 +104,10 @@ __device__ __forceinline__ void philox_block4(const uint32_t q[4], const PhiloxP
   for (int r = 2; r < 10; ++r) {
     const uint32_t k0 = rk0[r], k1 = rk1[r];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) philox_round(c0[b], c1[b], c2[b], c3[b], k0, k1);
+    for (int b = 0; b < NB; ++b) philox_round(c0[b], c1[b], c2[b], c3[b], k0, k1);
   }
 #pragma unroll
-  for (int b = 0; b < 4; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
+  for (int b = 0; b < NB; ++b) out[b] = make_uint4(c0[b], c1[b], c2[b], c3[b]);
 }
 
 __device__ __forceinline__ float lg2_approx(float x) {
