@@ -1376,6 +1376,15 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   } else {
     stage<T, kLabels>(a, vin, lin, b, simg, slbl);
   }
+#ifndef W3D_LATE_BAR
+  // image and labels both by TMA: the only thing to publish is the mbarrier init,
+  // so the barrier comes here, where the CTA's warps arrive together, not after
+  // the Philox prologue (whose finish times differ from warp to warp)
+  constexpr bool kEarlyBar = kTmaLbl;
+#else
+  constexpr bool kEarlyBar = false;  // A/B knob
+#endif
+  if (kEarlyBar) __syncthreads();
   // an occluded column (R15) needs no noise: its Philox blocks are skipped
   const bool need_noise = live && !((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi);
   // the training chain (kPhFull, launch-wide keys) computes kPre Philox blocks
@@ -1421,7 +1430,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     v.clbl = opaque(v.clbl - static_cast<uint32_t>(b.Wl * b.by + b.Pl * b.bz));
   }
   if (!kTmaLbl) cp_async_wait_all();
-  __syncthreads();  // label copies (and the mbarrier init) visible to every thread
+  if (!kEarlyBar) __syncthreads();  // label copies (and the mbarrier init) visible to all
   if (tma) {
     mbar_wait(mbar, phase);
     const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
