@@ -1376,13 +1376,14 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   } else {
     stage<T, kLabels>(a, vin, lin, b, simg, slbl);
   }
-#ifndef W3D_LATE_BAR
-  // image and labels both by TMA: the only thing to publish is the mbarrier init,
-  // so the barrier comes here, where the CTA's warps arrive together, not after
-  // the Philox prologue (whose finish times differ from warp to warp)
+#ifdef W3D_EARLY_BAR
+  // A/B knob: with image and labels both by TMA the barrier only publishes the
+  // mbarrier init and could come before the Philox prologue -- measured slower
+  // (266.7 vs 272.5 GVoxel/s, profiles/round2/HISTORY.md r3k): the barrier after
+  // the prologue re-aligns the CTA's warps before the straight-line rows
   constexpr bool kEarlyBar = kTmaLbl;
 #else
-  constexpr bool kEarlyBar = false;  // A/B knob
+  constexpr bool kEarlyBar = false;
 #endif
   if (kEarlyBar) __syncthreads();
   // an occluded column (R15) needs no noise: its Philox blocks are skipped
