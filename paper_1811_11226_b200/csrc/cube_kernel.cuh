@@ -576,9 +576,26 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
   lds_pair<T>(b2, c001.y, c101.y);
   lds_pair<T>(a3, c011.x, c111.x);
   lds_pair<T>(b3, c011.y, c111.y);
+#ifdef W3D_LERP_CP
+  // A/B knob: corner pairs of ONE voxel in the packed lanes ((z0, z1) corners at
+  // x0 / x1), the fraction as a broadcast scalar; same lerps in the same order
+  // (R5), so the same bits
+  auto vox = [](float a000, float a100, float a010, float a110, float a001, float a101,
+                float a011, float a111, float fx, float fy, float fz) {
+    const float2 lo = lerp2(make_float2(a000, a001), make_float2(a100, a101), f2(fx));  // (c00, c01)
+    const float2 hi = lerp2(make_float2(a010, a011), make_float2(a110, a111), f2(fx));  // (c10, c11)
+    const float2 cz = lerp2(lo, hi, f2(fy));                                             // (c0, c1)
+    return lerp1(cz.x, cz.y, fz);
+  };
+  img = make_float2(vox(c000.x, c100.x, c010.x, c110.x, c001.x, c101.x, c011.x, c111.x, tx.x,
+                        ty.x, tz.x),
+                    vox(c000.y, c100.y, c010.y, c110.y, c001.y, c101.y, c011.y, c111.y, tx.y,
+                        ty.y, tz.y));
+#else
   const float2 c00 = lerp2(c000, c100, tx), c10 = lerp2(c010, c110, tx);
   const float2 c01 = lerp2(c001, c101, tx), c11 = lerp2(c011, c111, tx);
   img = lerp2(lerp2(c00, c10, ty), lerp2(c01, c11, ty), tz);
+#endif
 }
 
 // The label of a y-pair alone (an occluded column, R15: the image is 0 and its
