@@ -323,11 +323,42 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
   const bool want_tma = variant != W3D_KERNEL_GATHER && !no_tma;
   const int32_t chunk = want_tma ? kTmaVolPerLaunch : kMaxVolPerLaunch;
   const bool labels = vols[0].lbl != nullptr;
-  for (int32_t v0 = 0; v0 < batch; v0 += chunk) {
-    const int32_t nv = (batch - v0 < chunk) ? batch - v0 : chunk;
+  const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
+  const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
+  // AUTO splits a batch by box size: the volumes whose 16-row box fits the staging
+  // buffer first, then the others (their own launches: 8-row tiles),
+  // so one large-footprint volume does not send a whole chunk to the slow paths.  Each
+  // volume carries its own output slot, so the order is free.
+  static thread_local std::vector<int32_t> order;
+  order.resize(static_cast<size_t>(batch));
+  int32_t n16 = batch;
+  if (variant == W3D_KERNEL_AUTO && interp == W3D_INTERP_LINEAR && want_tma) {
+    int32_t lo = 0;
+    static thread_local std::vector<int32_t> big;
+    big.clear();
+    for (int32_t i = 0; i < batch; ++i) {
+      VolDev P{};
+      cube_cp_box(affines[i], P, elem, id, od, kTileRows);
+      if (P.cp_rows != 0)
+        order[lo++] = i;
+      else
+        big.push_back(i);
+    }
+    for (int32_t i : big) order[lo++] = i;
+    n16 = batch - static_cast<int32_t>(big.size());
+  } else {
+    for (int32_t i = 0; i < batch; ++i) order[i] = i;
+  }
+  // chunks never straddle the two classes
+  auto next_chunk = [&](int32_t v0) {
+    const int32_t end = v0 < n16 ? n16 : batch;
+    return (end - v0 < chunk) ? end - v0 : chunk;
+  };
+  for (int32_t v0 = 0; v0 < batch; v0 += next_chunk(v0)) {
+    const int32_t nv = next_chunk(v0);
     // type flags (the kernels read every address from vol[i])
-    args.in = elem == 4 ? static_cast<const float*>(vols[v0].img) : nullptr;
-    args.in16 = elem == 2 ? static_cast<const int16_t*>(vols[v0].img) : nullptr;
+    args.in = elem == 4 ? static_cast<const float*>(vols[order[v0]].img) : nullptr;
+    args.in16 = elem == 2 ? static_cast<const int16_t*>(vols[order[v0]].img) : nullptr;
     {
       const float f = std::nearbyint(fill) == fill && fill >= -32768.0f && fill <= 32767.0f
                           ? fill
@@ -335,7 +366,7 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       const uint32_t h = static_cast<uint16_t>(static_cast<int16_t>(f));
       args.fill16_pair = h | (h << 16);
     }
-    args.in_lbl = labels ? vols[v0].lbl : nullptr;
+    args.in_lbl = labels ? vols[order[v0]].lbl : nullptr;
     args.out = out;
     args.out_lbl = out_labels;
     args.nx = in_dims.nx; args.ny = in_dims.ny; args.nz = in_dims.nz;
@@ -351,14 +382,12 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
     args.in_aligned = 1;
     for (int32_t i = 0; i < nv; ++i) {
       VolDev& P = args.vol[i];
-      P = derive(affines[v0 + i], phs[v0 + i]);
-      P.in_addr = reinterpret_cast<uint64_t>(vols[v0 + i].img);
-      P.lbl_addr = reinterpret_cast<uint64_t>(vols[v0 + i].lbl);
-      P.out_slot = vols[v0 + i].slot;
+      P = derive(affines[order[v0 + i]], phs[order[v0 + i]]);
+      P.in_addr = reinterpret_cast<uint64_t>(vols[order[v0 + i]].img);
+      P.lbl_addr = reinterpret_cast<uint64_t>(vols[order[v0 + i]].lbl);
+      P.out_slot = vols[order[v0 + i]].slot;
       if (P.in_addr % 16 || P.lbl_addr % 8) args.in_aligned = 0;
-      const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
-      const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
-      cube_cp_box(affines[v0 + i], P, elem, id, od, kTileRows);
+      cube_cp_box(affines[order[v0 + i]], P, elem, id, od, kTileRows);
     }
     // AUTO: when no volume's 16-row box fits the buffer (large rotations / scales),
     // 8-row tiles (half the box height) usually do: stage those by TMA rather than
@@ -369,18 +398,14 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       for (int32_t i = 0; i < nv; ++i) any16 |= args.vol[i].cp_rows != 0;
       if (!any16) {
         for (int32_t i = 0; i < nv; ++i) {
-          const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
-          const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
-          cube_cp_box(affines[v0 + i], args.vol[i], elem, id, od, kTileRowsSmall);
+          cube_cp_box(affines[order[v0 + i]], args.vol[i], elem, id, od, kTileRowsSmall);
           any8 |= args.vol[i].cp_rows != 0;
         }
         if (any8) {
           args.tile_rows = kTileRowsSmall;
         } else {  // neither fits: back to the 16-row offsets (the gather kernel's tile classes)
           for (int32_t i = 0; i < nv; ++i) {
-            const int id[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
-            const int od[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
-            cube_cp_box(affines[v0 + i], args.vol[i], elem, id, od, kTileRows);
+            cube_cp_box(affines[order[v0 + i]], args.vol[i], elem, id, od, kTileRows);
           }
         }
       }

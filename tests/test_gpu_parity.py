@@ -795,3 +795,66 @@ def test_binding_rejects_mismatched_buffers(W):
     with pytest.raises(TypeError):    # device tensor where a host buffer is required
         pipe.run(h.cuda(), hl, ps, h.clone(), hl.clone())
     pipe.close()
+
+
+# ----------------------------------------------------------------------------- 8-row tiles, bricks
+@pytest.mark.parametrize("in_dtype", ["f32", "i16"])
+def test_auto_8row_tiles_in_bricks_match_oracle_and_gather(W, in_dtype):
+    """Large rotations on a 128^3 batch: AUTO launches the volumes whose 16-row box does
+    not fit separately, as 8-row tiles staged by TMA and walked in bricks (power-of-two
+    tile counts).  Every voxel of both volumes against the oracle, and bitwise against
+    the gather variant; the tile counters show that every tile was staged by TMA."""
+    shape = (128, 128, 128)
+    B = 2
+    base = [synth.phantom(shape, seed=synth.MASTER_SEED + k) for k in range(B)]
+    imgs = np.stack([b[0] for b in base])
+    if in_dtype == "i16":
+        imgs = np.round(imgs).astype(np.float32)
+    lbls = np.stack([b[1] for b in base])
+    ds = [synth.draw(synth.LARGE, 100 + i) for i in range(B)]
+    As = [_oracle_affine(d, shape, shape) for d in ds]
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B)]
+    t_img = torch.from_numpy(imgs).cuda()
+    if in_dtype == "i16":
+        t_img = t_img.to(torch.int16)
+    t_lbl = torch.from_numpy(lbls).cuda()
+    s0 = W.warp3d_tile_stats()
+    out, out_l = W.warp3d_affine_batched(t_img, t_lbl, params, fill=-1000.0, label_fill=2)
+    torch.cuda.synchronize()
+    s1 = W.warp3d_tile_stats()
+    t16, t8 = (128 // 16) ** 3, (128 // 16) * (128 // 8) * (128 // 16)
+    assert s1[1] == s0[1] and s1[3] == s0[3], "no gathered or y-part tiles expected"
+    assert s1[2] - s0[2] >= t16 + t8, "expected TMA tiles only (16-row and 8-row)"
+    g_out, g_l = W.warp3d_affine_batched(t_img, t_lbl, params, fill=-1000.0, label_fill=2,
+                                         variant=W.KERNEL_GATHER)
+    torch.cuda.synchronize()
+    assert torch.equal(out, g_out) and torch.equal(out_l, g_l)
+
+    def one(i):
+        return i, O.warp_volume(imgs[i], lbls[i], As[i], None, O.LINEAR, -1000.0, 2,
+                                _oph(ds[i], FULL, i))
+    with _pool() as ex:
+        ref = dict(ex.map(one, range(B)))
+    check(out.cpu().numpy(), out_l.cpu().numpy(), ref, ds, FULL, f"8-row AUTO {in_dtype}")
+
+
+def test_auto_8row_tiles_with_occlusion_and_window_only(W):
+    """8-row tiles on the generic photometric chain (window without gamma) with the
+    occlusion prism: the label-only occluded walk inside the 8-row instance."""
+    shape = (96, 128, 128)
+    img, lbl = synth.phantom(shape)
+    d = synth.draw(synth.LARGE, 3)
+    A = _oracle_affine(d, shape, shape)
+    flags = O.NOISE | O.WINDOW | O.CLAMP | O.OCCLUDE
+    kw = dict(window=d.window, sigma=d.sigma, seed=SEED, volume_id=5, occ_z0=20.5,
+              occ_height=30.0)
+    params = [W.volume_params(A, W.photometric(flags, **kw))]
+    out, out_l = W.warp3d_affine_batched(torch.from_numpy(img[None]).cuda(),
+                                         torch.from_numpy(lbl[None]).cuda(), params,
+                                         fill=-1000.0)
+    torch.cuda.synchronize()
+    r_img, r_lbl = O.warp_volume(img, lbl, A, None, O.LINEAR, -1000.0, 0,
+                                 O.photometric(flags, **kw))
+    assert_image_close(out[0].cpu().numpy(), r_img, d.window, 1.0, True, "8-row occl")
+    assert np.array_equal(out_l[0].cpu().numpy(), r_lbl)
+    assert np.all(out[0, 21:51].cpu().numpy() == 0.0)
