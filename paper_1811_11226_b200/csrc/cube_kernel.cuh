@@ -1290,6 +1290,45 @@ __device__ __forceinline__ void fix_chunks(uint32_t base, int CW, int Hb, uint32
   const int ylo = min(Hb, max(0, -by)), yhi = max(ylo, min(Hb, ny - by));
   const int zlo = min(D, max(0, -bz)), zhi = max(zlo, min(D, nz - bz));
   const int slots = CW * Hb;
+  // plane ranges per slot: 4, 2 or 1 threads share a slot (a power of two: no divisions)
+  const int lg = 4 * slots <= THREADS ? 2 : (2 * slots <= THREADS ? 1 : 0);
+  const int t = static_cast<int>(threadIdx.x);
+  const float inv_cw = __frcp_rn(static_cast<float>(CW));
+  const uint4 w4 = make_uint4(word, word, word, word);
+  auto st = [&](uint32_t addr) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w4.x), "r"(w4.y),
+                 "r"(w4.z), "r"(w4.w)
+                 : "memory");
+  };
+  // the out-of-volume planes of slot s in [zs, ze): all of them when the slot's
+  // (chunk column, row) is outside, else those below zlo and from zhi on
+  auto slot = [&](int s, int zs, int ze) {
+    const int r = small_div(s, inv_cw), c = s - r * CW;
+    const bool out = (c < hc) | (c >= tc) | (r < ylo) | (r >= yhi);
+    const uint32_t a0 = base + 16u * static_cast<uint32_t>(s);
+    if (out) {
+      for (int z = zs; z < ze; ++z) st(a0 + static_cast<uint32_t>(z) * Pb);
+    } else {
+      for (int z = zs; z < min(ze, zlo); ++z) st(a0 + static_cast<uint32_t>(z) * Pb);
+      for (int z = max(zs, zhi); z < ze; ++z) st(a0 + static_cast<uint32_t>(z) * Pb);
+    }
+  };
+  if (lg > 0) {
+    const int s = t >> lg, part = t & ((1 << lg) - 1);
+    if (s < slots) slot(s, (D * part) >> lg, (D * (part + 1)) >> lg);
+    return;
+  }
+  for (int s = t; s < slots; s += THREADS) slot(s, 0, D);
+}
+
+#ifdef W3D_OLD_FIXUP  // A/B knob: the round-1 slot scheduling (integer divisions)
+__device__ __forceinline__ void fix_chunks_div(uint32_t base, int CW, int Hb, uint32_t Pb, int D,
+                                           int bx, int by, int bz, int kC, int nx, int ny, int nz,
+                                           uint32_t word) {
+  const int hc = min(CW, max(0, -bx / kC)), tc = max(hc, min(CW, (nx - bx) / kC));
+  const int ylo = min(Hb, max(0, -by)), yhi = max(ylo, min(Hb, ny - by));
+  const int zlo = min(D, max(0, -bz)), zhi = max(zlo, min(D, nz - bz));
+  const int slots = CW * Hb;
   const int nsplit = max(1, THREADS / slots);
   const int t = static_cast<int>(threadIdx.x);
   const float inv_cw = __frcp_rn(static_cast<float>(CW));
@@ -1320,6 +1359,8 @@ __device__ __forceinline__ void fix_chunks(uint32_t base, int CW, int Hb, uint32
     }
   }
 }
+#define fix_chunks fix_chunks_div
+#endif
 
 // fill over the out-of-volume elements of a TMA image box (TMA wrote 0).
 template <class T>
