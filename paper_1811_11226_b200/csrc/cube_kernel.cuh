@@ -1379,6 +1379,40 @@ __device__ __forceinline__ void tma_fixup_lbl(const WarpArgs& a, const Box& b, u
 
 
 
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void decode_brick(int32_t brick, int& tx, int& ty, int& tz);
+
+// L2 prefetch of the boxes of the tile a.prefetch_ahead CTAs later in launch order
+// (same volume only): by the time that CTA issues its TMA the box is in L2 (C4,
+// where the box wait -- not dispatch -- bounds the kernel).
+template <class T, int TY, bool kTmaLbl>
+__device__ __noinline__ void prefetch_ahead(const WarpArgs& a, const VolDev& P, int vi) {
+  constexpr int kC = InT<T>::kChunk;
+  const uint32_t gx = gridDim.x, gy = gridDim.y;
+  const uint32_t tiles_z = static_cast<uint32_t>((a.mz + TZ - 1) / TZ);
+  const uint32_t z0 = blockIdx.z - static_cast<uint32_t>(vi) * tiles_z;
+  const uint32_t L = blockIdx.x + gx * (blockIdx.y + gy * z0) + static_cast<uint32_t>(a.prefetch_ahead);
+  if (L >= gx * gy * tiles_z) return;
+  int tx = static_cast<int>(L % gx), ty = static_cast<int>((L / gx) % gy);
+  int tz = static_cast<int>(L / (gx * gy));
+  if (a.brick) decode_brick(a.brick, tx, ty, tz);
+  float p0[3];
+  const float X = static_cast<float>(tx * TX), Y = static_cast<float>(ty * TY),
+              Z = static_cast<float>(tz * TZ);
+  for (int k = 0; k < 3; ++k) p0[k] = coord(P.A, k, X, Y, Z);
+  if (!(fabsf(p0[0]) < 1048576.0f && fabsf(p0[1]) < 1048576.0f && fabsf(p0[2]) < 1048576.0f)) return;
+  const int bx = __float2int_rd(__fadd_rd(p0[0], P.box_mlo[0])) & ~(kC - 1);
+  const int by = __float2int_rd(__fadd_rd(p0[1], P.box_mlo[1]));
+  const int bz = __float2int_rd(__fadd_rd(p0[2], P.box_mlo[2]));
+  tma_prefetch_3d(&a.tm[2 * vi], bx, by, bz);
+  if (kTmaLbl) tma_prefetch_3d(&a.tm[2 * vi + 1], bx & ~15, by, bz);
+}
+
 // The common path: the whole tile staged as ONE box of the volume's fixed dims
 // (cp_w, cp_h, cp_d; host-computed by cube_cp_box to hold any tile's
 // footprint) whose origin follows from the tile's origin voxel alone -- every
@@ -1430,6 +1464,8 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
       tma_load_3d(simg, &a.tm[2 * vi], b.bx, b.by, b.bz, mbar);
       if (kTmaLbl) tma_load_3d(slbl, &a.tm[2 * vi + 1], b.bxl, b.by, b.bz, mbar);
     }
+    if (a.prefetch_ahead > 0 && threadIdx.x == 32)  // another warp than the issuer
+      prefetch_ahead<T, TY, kTmaLbl>(a, P, vi);
     if (kLabels && !kTmaLbl) stage_lbl<T>(a, lin, b, slbl);
   } else {
     stage<T, kLabels>(a, vin, lin, b, simg, slbl);
@@ -1573,6 +1609,20 @@ __device__ __forceinline__ bool cube_tile(const WarpArgs& a, int cap, int vi, in
   return false;
 }
 
+// Launch order (x, y, z fastest to slowest, within one volume) -> bricks of
+// 2^sx x 2^sy x 2^sz tiles (WarpArgs::brick; shifts and masks only).
+__device__ __forceinline__ void decode_brick(int32_t brick, int& tx, int& ty, int& tz) {
+  const uint32_t f = static_cast<uint32_t>(brick);
+  const int sx = f & 15, sy = (f >> 4) & 15, sz = (f >> 8) & 15, lbx = (f >> 12) & 15,
+            lby = (f >> 16) & 15;
+  const uint32_t L = static_cast<uint32_t>(tx) +
+                     gridDim.x * (static_cast<uint32_t>(ty) + gridDim.y * static_cast<uint32_t>(tz));
+  const uint32_t w = L & ((1u << (sx + sy + sz)) - 1u), bi = L >> (sx + sy + sz);
+  tx = static_cast<int>(((bi & ((1u << lbx) - 1u)) << sx) | (w & ((1u << sx) - 1u)));
+  ty = static_cast<int>((((bi >> lbx) & ((1u << lby) - 1u)) << sy) | ((w >> sx) & ((1u << sy) - 1u)));
+  tz = static_cast<int>(((bi >> (lbx + lby)) << sz) | (w >> (sx + sy)));
+}
+
 // grid = (tiles_x, tiles_y, tiles_z * volumes): one tile per CTA, tiles
 // x-fastest, then y, then z.  (A persistent grid of 3 CTAs per SM walking the
 // tiles with the mbarrier phase carried across tiles measured 207 vs 272
@@ -1594,18 +1644,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                               : static_cast<int>(__umulhi(blockIdx.z, tz_magic));
   int tx = static_cast<int>(blockIdx.x), ty = static_cast<int>(blockIdx.y);
   int tz = static_cast<int>(blockIdx.z) - vi * tiles_z;
-  if (a.brick) {  // launch order (x, y, z fastest to slowest) -> bricks of tiles
-    const uint32_t f = static_cast<uint32_t>(a.brick);
-    const int sx = f & 15, sy = (f >> 4) & 15, sz = (f >> 8) & 15, lbx = (f >> 12) & 15,
-              lby = (f >> 16) & 15;
-    const uint32_t L = static_cast<uint32_t>(tx) +
-                       gridDim.x * (static_cast<uint32_t>(ty) + gridDim.y * static_cast<uint32_t>(tz));
-    const uint32_t w = L & ((1u << (sx + sy + sz)) - 1u), bi = L >> (sx + sy + sz);
-    tx = static_cast<int>(((bi & ((1u << lbx) - 1u)) << sx) | (w & ((1u << sx) - 1u)));
-    ty = static_cast<int>((((bi >> lbx) & ((1u << lby) - 1u)) << sy) |
-                          ((w >> sx) & ((1u << sy) - 1u)));
-    tz = static_cast<int>(((bi >> (lbx + lby)) << sz) | (w >> (sx + sy)));
-  }
+  if (a.brick) decode_brick(a.brick, tx, ty, tz);
   const int ox = tx * TX, oy = ty * TY, oz = tz * TZ;
   cube_tile<T, TY, kLabels, kNearest, kPh, kGather>(a, cap, vi, ox, oy, oz, mbar, 0u, true);
   // A programmatic dependent (a later chunk of the same call) never reads its

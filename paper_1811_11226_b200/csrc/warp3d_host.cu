@@ -430,6 +430,10 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
       gather = !any_box;
     }
     args.brick = brick_order(args, gather);
+    {  // L2 prefetch one resident wave ahead (8-row launches; W3D_PREFETCH=<CTAs> overrides)
+      static const int pf = getenv("W3D_PREFETCH") ? atoi(getenv("W3D_PREFETCH")) : -1;
+      args.prefetch_ahead = pf >= 0 ? pf : 0;
+    }
     args.pdl = v0 > 0 ? 1 : 0;  // the first chunk waits for all prior work on the stream
     const cudaError_t e = launch_cube(args, gather, stream);
     if (e != cudaSuccess) return cuda_fail(e, "warp3d kernel launch");

@@ -109,6 +109,9 @@ struct alignas(64) WarpArgsT {
                           // (bit 31 set; sx, sy, sz, log2 bricks per row / column in
                           // 4-bit fields from bit 0): consecutive CTAs cover compact
                           // output regions, so a wave's input footprint stays in L2
+  int32_t prefetch_ahead; // > 0: each CTA of the fixed-box path also prefetches into L2
+                          // the boxes of the tile this many CTAs later in launch order
+                          // (same volume; 8-row launches, W3D_PREFETCH)
   // Philox round keys shared by every volume of the launch (all seeds equal;
   // required by the kPhFull kernels: fixed parameter offsets, so the round
   // function reads them as constant-bank operands)
