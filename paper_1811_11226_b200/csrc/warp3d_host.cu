@@ -396,6 +396,8 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
     if (variant == W3D_KERNEL_AUTO && interp == W3D_INTERP_LINEAR) {
       bool any16 = false, any8 = false;
       for (int32_t i = 0; i < nv; ++i) any16 |= args.vol[i].cp_rows != 0;
+      static const int force8 = getenv("W3D_TILE_ROWS") ? atoi(getenv("W3D_TILE_ROWS")) : 0;
+      if (force8 == kTileRowsSmall) any16 = false;  // A/B knob
       if (!any16) {
         for (int32_t i = 0; i < nv; ++i) {
           cube_cp_box(affines[order[v0 + i]], args.vol[i], elem, id, od, kTileRowsSmall);
