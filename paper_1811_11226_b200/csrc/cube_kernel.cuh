@@ -1481,7 +1481,11 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
 #endif
   if (kEarlyBar) __syncthreads();
   // an occluded column (R15) needs no noise: its Philox blocks are skipped
+#ifndef W3D_DBG_NONOISE
   const bool need_noise = live && !((P.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi);
+#else
+  const bool need_noise = false;  // diagnostic knock-out: no Philox / Box-Muller at all
+#endif
   // the training chain (kPhFull, launch-wide keys) computes kPre Philox blocks
   // here, under the staging latency (at most the tile's TY / 4); the generic
   // chain one (register budget)
