@@ -802,12 +802,21 @@ __device__ __forceinline__ void gather2(const WarpArgs& a, const T* __restrict__
   }
 }
 
+#ifndef W3D_DBG_NOSTORE
 __device__ __forceinline__ void st_f32(float* p, float v) {
   asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 __device__ __forceinline__ void st_u8(uint8_t* p, uint32_t v) {
   asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+#else  // diagnostic: a store only for values no real voxel produces (kept alive, ~never taken)
+__device__ __forceinline__ void st_f32(float* p, float v) {
+  if (v == 1234.5f) asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_u8(uint8_t* p, uint32_t v) {
+  if (v == 251u) asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+#endif
 // p + bytes (a 64-bit byte step, kept as an add: ptxas would turn p + 4 * mx
 // into IMAD.WIDE.U32, ~4 dispatch cycles against 2 for the add pair)
 template <class P>
@@ -1531,7 +1540,9 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   if (!kTmaLbl) cp_async_wait_all();
   if (!kEarlyBar) __syncthreads();  // label copies (and the mbarrier init) visible to all
   if (tma) {
+#ifndef W3D_DBG_LATEWAIT
     mbar_wait(mbar, phase);
+#endif
     const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
                         b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
     const bool insidel = !kTmaLbl || (b.bxl >= 0 && b.bxl + b.Wl <= a.nx &&
@@ -1551,13 +1562,20 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   } else {
     W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels, true, true);
   }
-  if (!live) return;
-  if (oy + TY <= a.my)  // every row of the tile is an output row
-    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre, kGEdge, kUseAbs>(
-        a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
-  else
-    column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre, kGEdge, kUseAbs>(
-        a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+#ifdef W3D_DBG_LATEWAIT  // diagnostic: compute as if the box had arrived (garbage outputs)
+  const bool late_wait = true;
+#endif
+  if (live) {
+    if (oy + TY <= a.my)  // every row of the tile is an output row
+      column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre, kGEdge, kUseAbs>(
+          a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+    else
+      column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre, kGEdge, kUseAbs>(
+          a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+  }
+#ifdef W3D_DBG_LATEWAIT
+  if (tma && late_wait) mbar_wait(mbar, phase);
+#endif
 }
 
 // One output tile (volume vi, origin ox, oy, oz).  mbar / phase: the CTA's
