@@ -859,3 +859,37 @@ def test_auto_8row_tiles_with_occlusion_and_window_only(W):
     assert_image_close(out[0].cpu().numpy(), r_img, d.window, 1.0, True, "8-row occl")
     assert np.array_equal(out_l[0].cpu().numpy(), r_lbl)
     assert np.all(out[0, 21:51].cpu().numpy() == 0.0)
+
+
+def test_auto_mixed_batch_split_by_box_fit_pdl_chunks(W):
+    """A batch that mixes train and large-rotation volumes, more than one TMA chunk:
+    AUTO reorders it into 16-row launches (boxes that fit) and 8-row launches (the
+    others), several of them programmatic dependents.  Every volume lands in its own
+    output slot: bitwise equal to the gather variant, a sample of volumes against the
+    oracle."""
+    shape = (48, 64, 64)
+    B = 21
+    base = [synth.phantom(shape, seed=synth.MASTER_SEED + k) for k in range(3)]
+    imgs = np.stack([base[i % 3][0] for i in range(B)])
+    lbls = np.stack([base[i % 3][1] for i in range(B)])
+    ds = [synth.draw(synth.LARGE if i % 3 == 1 else synth.TRAIN, 200 + i) for i in range(B)]
+    As = [_oracle_affine(d, shape, shape) for d in ds]
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B)]
+    t_img, t_lbl = torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda()
+    s0 = W.warp3d_tile_stats()
+    out, out_l = W.warp3d_affine_batched(t_img, t_lbl, params, fill=-1000.0, label_fill=1)
+    torch.cuda.synchronize()
+    s1 = W.warp3d_tile_stats()
+    g, gl = W.warp3d_affine_batched(t_img, t_lbl, params, fill=-1000.0, label_fill=1,
+                                    variant=W.KERNEL_GATHER)
+    torch.cuda.synchronize()
+    assert torch.equal(out, g) and torch.equal(out_l, gl)
+    assert s1[2] > s0[2]  # staged by TMA
+    sel = [0, 1, 4, 19, 20]
+
+    def one(i):
+        return i, O.warp_volume(imgs[i], lbls[i], As[i], None, O.LINEAR, -1000.0, 1,
+                                _oph(ds[i], FULL, i))
+    with _pool() as ex:
+        ref = dict(ex.map(one, sel))
+    check(out.cpu().numpy(), out_l.cpu().numpy(), ref, ds, FULL, "mixed AUTO batch")
