@@ -330,16 +330,24 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
   // so one large-footprint volume does not send a whole chunk to the slow paths.  Each
   // volume carries its own output slot, so the order is free.
   static thread_local std::vector<int32_t> order;
+  static thread_local std::vector<VolDev> pre;  // per volume, derived once per call
   order.resize(static_cast<size_t>(batch));
+  pre.resize(static_cast<size_t>(batch));
+  for (int32_t i = 0; i < batch; ++i) {
+    VolDev& P = pre[i];
+    P = derive(affines[i], phs[i]);
+    P.in_addr = reinterpret_cast<uint64_t>(vols[i].img);
+    P.lbl_addr = reinterpret_cast<uint64_t>(vols[i].lbl);
+    P.out_slot = vols[i].slot;
+    cube_cp_box(affines[i], P, elem, id, od, kTileRows);
+  }
   int32_t n16 = batch;
   if (variant == W3D_KERNEL_AUTO && interp == W3D_INTERP_LINEAR && want_tma) {
     int32_t lo = 0;
     static thread_local std::vector<int32_t> big;
     big.clear();
     for (int32_t i = 0; i < batch; ++i) {
-      VolDev P{};
-      cube_cp_box(affines[i], P, elem, id, od, kTileRows);
-      if (P.cp_rows != 0)
+      if (pre[i].cp_rows != 0)
         order[lo++] = i;
       else
         big.push_back(i);
@@ -381,13 +389,8 @@ static w3d_status launch_group(int32_t batch, const VolIn* vols, int elem, w3d_d
     args.nvol = nv;
     args.in_aligned = 1;
     for (int32_t i = 0; i < nv; ++i) {
-      VolDev& P = args.vol[i];
-      P = derive(affines[order[v0 + i]], phs[order[v0 + i]]);
-      P.in_addr = reinterpret_cast<uint64_t>(vols[order[v0 + i]].img);
-      P.lbl_addr = reinterpret_cast<uint64_t>(vols[order[v0 + i]].lbl);
-      P.out_slot = vols[order[v0 + i]].slot;
+      const VolDev& P = args.vol[i] = pre[order[v0 + i]];
       if (P.in_addr % 16 || P.lbl_addr % 8) args.in_aligned = 0;
-      cube_cp_box(affines[order[v0 + i]], P, elem, id, od, kTileRows);
     }
     // AUTO: when no volume's 16-row box fits the buffer (large rotations / scales),
     // 8-row tiles (half the box height) usually do: stage those by TMA rather than

@@ -18,7 +18,7 @@ import synth  # noqa: E402
 
 dev = torch.device("cuda", 0)
 shape = (160, 128, 128)
-for B in (16, 256):
+for B in (1, 16, 256):
     vids = list(range(B))
     params = build_params([synth.draw(synth.TRAIN, v) for v in vids], vids, shape, shape, FULL,
                           seed=synth.MASTER_SEED)
