@@ -27,8 +27,15 @@ __all__ = [
 ]
 
 
-def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _stream(device=None):
+    """The caller's current CUDA stream as a raw handle (the launches go there)."""
+    if _raw_stream is not None:
+        idx = torch.cuda.current_device() if device is None else device.index
+        return ctypes.c_void_p(_raw_stream(idx))
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 def _dev(t, dtype, name, shape=None, device=None):
@@ -145,6 +152,30 @@ def warp3d_affine_batched(inp: torch.Tensor, labels: torch.Tensor | None, params
         None if out_labels is None else _dev(out_labels, torch.uint8, "out_labels", oshape, dev),
         L.dims(out_shape), int(variant), _stream()))
     return out, out_labels
+
+
+def prepared_batched_call(inp, labels, params, fill, label_fill, out, out_labels,
+                          variant=KERNEL_AUTO):
+    """A no-argument callable that repeats one (already validated) warp3d_affine_batched
+    launch on the caller's current stream: the ctypes arguments are marshalled once.
+    The tensors must stay alive and unchanged in shape; `params` must be a ctypes array
+    (its contents may change between calls)."""
+    if not isinstance(params, ctypes.Array):
+        raise TypeError("params must be a ctypes array of VolumeParams")
+    fn = (L.load().warp3d_affine_batched_i16_ex if inp.dtype == torch.int16
+          else L.load().warp3d_affine_batched_ex)
+    fixed = (int(inp.shape[0]), ctypes.c_void_p(inp.data_ptr()),
+             None if labels is None else ctypes.c_void_p(labels.data_ptr()),
+             L.dims(inp.shape[1:]), params, INTERP_LINEAR, float(fill), int(label_fill),
+             ctypes.c_void_p(out.data_ptr()),
+             None if out_labels is None else ctypes.c_void_p(out_labels.data_ptr()),
+             L.dims(out.shape[1:]), int(variant))
+    device = inp.device
+    check = L.check
+
+    def call():
+        check(fn(*fixed, _stream(device)))
+    return call
 
 
 def warp3d_affine_batched_list(inputs, labels, params, out_shape, interp=INTERP_LINEAR,

@@ -57,8 +57,21 @@ class AugmentBatch:
             (B, *self.out_shape), dtype=torch.uint8, device=image.device)
         self.fill, self.label_fill, self.variant = fill, label_fill, variant
 
+        # the first run goes through the checked entry point (validates every buffer);
+        # later runs reuse its marshalled arguments: the buffers are fixed for the life
+        # of the batch and `params` is the same ctypes array (updated in place between
+        # training steps if the caller draws new transforms)
+        self._call = None
+
     def run(self):
-        return api.warp3d_affine_batched(self.image, self.labels, self.params, fill=self.fill,
-                                         label_fill=self.label_fill, out_shape=self.out_shape,
-                                         out=self.out, out_labels=self.out_labels,
-                                         variant=self.variant)
+        if self._call is None:
+            api.warp3d_affine_batched(self.image, self.labels, self.params, fill=self.fill,
+                                      label_fill=self.label_fill, out_shape=self.out_shape,
+                                      out=self.out, out_labels=self.out_labels,
+                                      variant=self.variant)
+            self._call = api.prepared_batched_call(
+                self.image, self.labels, self.params, self.fill, self.label_fill, self.out,
+                self.out_labels, self.variant)
+            return self.out, self.out_labels
+        self._call()
+        return self.out, self.out_labels
