@@ -1439,6 +1439,15 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   constexpr int kC = InT<T>::kChunk;
   constexpr uint32_t kB = InT<T>::kBytes;
   const uint32_t simg = smem_base();
+#ifdef W3D_DBG_TIMING  // diagnostic: per-tile phase times of a few CTAs (printf)
+  const long long dbg_t0 = clock64();
+  long long dbg_t[5] = {0, 0, 0, 0, 0};
+#define W3D_T(i) dbg_t[i] = clock64() - dbg_t0
+#else
+#define W3D_T(i) \
+  do {           \
+  } while (0)
+#endif
   Box b;
   b.W = P.cp_w;
   b.H = P.cp_h;
@@ -1488,6 +1497,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
 #else
   constexpr bool kEarlyBar = false;
 #endif
+  W3D_T(0);  // TMA issued
   if (kEarlyBar) __syncthreads();
   // an occluded column (R15) needs no noise: its Philox blocks are skipped
 #ifndef W3D_DBG_NONOISE
@@ -1538,11 +1548,14 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     v.clbl = opaque(v.clbl - static_cast<uint32_t>(b.Wl * b.by + b.Pl * b.bz));
   }
   if (!kTmaLbl) cp_async_wait_all();
+  W3D_T(1);  // Philox prologue done
   if (!kEarlyBar) __syncthreads();  // label copies (and the mbarrier init) visible to all
+  W3D_T(2);  // barrier passed
   if (tma) {
 #ifndef W3D_DBG_LATEWAIT
     mbar_wait(mbar, phase);
 #endif
+    W3D_T(3);  // box landed
     const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
                         b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
     const bool insidel = !kTmaLbl || (b.bxl >= 0 && b.bxl + b.Wl <= a.nx &&
@@ -1576,6 +1589,13 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
 #ifdef W3D_DBG_LATEWAIT
   if (tma && late_wait) mbar_wait(mbar, phase);
 #endif
+  W3D_T(4);  // rows done
+#ifdef W3D_DBG_TIMING
+  if ((threadIdx.x & 31) == 0 && blockIdx.x == 3 && blockIdx.y == 3 && blockIdx.z % 37 == 0)
+    printf("W3DT z %d warp %d: issue %lld philox %lld bar %lld box %lld rows %lld\n",
+           blockIdx.z, threadIdx.x >> 5, dbg_t[0], dbg_t[1], dbg_t[2], dbg_t[3], dbg_t[4]);
+#endif
+#undef W3D_T
 }
 
 // One output tile (volume vi, origin ox, oy, oz).  mbar / phase: the CTA's
