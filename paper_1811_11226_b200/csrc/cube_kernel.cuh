@@ -1396,6 +1396,35 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, i
 }
 __device__ __forceinline__ void decode_brick(int32_t brick, int& tx, int& ty, int& tz);
 
+// The next volume of the launch into L2, one disjoint slice per tile: tile t of
+// volume vi prefetches slice t of volume vi + 1's image and labels (contiguous bytes,
+// cp.async.bulk.prefetch.L2), so when that volume's tiles start -- about one volume's
+// worth of CTAs later -- their TMA boxes hit in L2 instead of waiting for DRAM.  The
+// slices add up to the volume exactly once (no extra DRAM traffic).
+template <class T>
+__device__ __forceinline__ void prefetch_next_volume(const WarpArgs& a, int vi, int oz, int oy,
+                                                     int ox, int TY) {
+  const VolDev& N = a.vol[vi + 1];
+  const int64_t tiles_x = (a.mx + TX - 1) / TX, tiles_y = (a.my + TY - 1) / TY;
+  const int64_t tiles = tiles_x * tiles_y * ((a.mz + TZ - 1) / TZ);
+  const int64_t t = ox / TX + tiles_x * (oy / TY + tiles_y * (oz / TZ));
+  const int64_t nvox = a.in_stride;
+  const int64_t chunk = ((nvox + tiles - 1) / tiles + 15) & ~int64_t(15);  // elements
+  const int64_t lo = t * chunk;
+  if (lo >= nvox) return;
+  const int64_t n = min(chunk, nvox - lo) & ~int64_t(15);
+  if (n <= 0) return;
+  const uint64_t img = N.in_addr + static_cast<uint64_t>(lo) * InT<T>::kBytes;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(img),
+               "r"(static_cast<uint32_t>(n * InT<T>::kBytes))
+               : "memory");
+  if (N.lbl_addr != 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(N.lbl_addr +
+                                                                   static_cast<uint64_t>(lo)),
+                 "r"(static_cast<uint32_t>(n))
+                 : "memory");
+}
+
 // L2 prefetch of the boxes of the tile a.prefetch_ahead CTAs later in launch order
 // (same volume only): by the time that CTA issues its TMA the box is in L2 (C4,
 // where the box wait -- not dispatch -- bounds the kernel).
@@ -1484,6 +1513,9 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     }
     if (a.prefetch_ahead > 0 && threadIdx.x == 32)  // another warp than the issuer
       prefetch_ahead<T, TY, kTmaLbl>(a, P, vi);
+#ifndef W3D_NO_VOLPF
+    if (threadIdx.x == 64 && vi + 1 < a.nvol) prefetch_next_volume<T>(a, vi, oz, oy, ox, TY);
+#endif
     if (kLabels && !kTmaLbl) stage_lbl<T>(a, lin, b, slbl);
   } else {
     stage<T, kLabels>(a, vin, lin, b, simg, slbl);
