@@ -1513,7 +1513,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     }
     if (a.prefetch_ahead > 0 && threadIdx.x == 32)  // another warp than the issuer
       prefetch_ahead<T, TY, kTmaLbl>(a, P, vi);
-#ifndef W3D_NO_VOLPF
+#ifdef W3D_VOLPF  // A/B knob, off: no gain measured (274.0 vs 275.0) and +5 % DRAM reads
     if (threadIdx.x == 64 && vi + 1 < a.nvol) prefetch_next_volume<T>(a, vi, oz, oy, ox, TY);
 #endif
     if (kLabels && !kTmaLbl) stage_lbl<T>(a, lin, b, slbl);
