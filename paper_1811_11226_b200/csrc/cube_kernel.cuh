@@ -510,6 +510,50 @@ template <class T> __device__ __forceinline__ float lds_one(uint32_t a) {
   return v0;
 }
 
+struct GView {
+  uint32_t nx, ny, nz;  // input dims
+  uint32_t sy, sz;      // element strides nx, nx ny
+  uint32_t C;           // -kMbits (1 + sy + sz) mod 2^32: o = bits(sx) + sy bits(sy) + sz bits(sz) + C
+  float fnx, fny, fnz;
+};
+__device__ __forceinline__ GView make_gview(const WarpArgs& a) {
+  GView g;
+  g.nx = static_cast<uint32_t>(a.nx);
+  g.ny = static_cast<uint32_t>(a.ny);
+  g.nz = static_cast<uint32_t>(a.nz);
+  g.sy = g.nx;
+  g.sz = g.nx * g.ny;
+  g.C = 0u - static_cast<uint32_t>(kMbits) * (1u + g.sy + g.sz);
+  g.fnx = static_cast<float>(a.nx);
+  g.fny = static_cast<float>(a.ny);
+  g.fnz = static_cast<float>(a.nz);
+  return g;
+}
+// Labels gathered from global memory (the 8-row tiles of large footprints: no
+// label box, so the TMA moves half the rows -- the box wait, not dispatch, bounds
+// those tiles).  The nearest voxel (R7) in volume coordinates straight from the
+// magic-number floats kM + n_k, its offset mod 2^32 as gather2's; kChecked (tiles
+// that can sample outside): label_fill for a nearest voxel outside the volume (R8).
+template <bool kChecked>
+__device__ __forceinline__ void label_gather2(const uint8_t* __restrict__ lin, const GView& g,
+                                              uint32_t lfill, float2 sx, float2 sy, float2 sz,
+                                              float2 hx, float2 hy, float2 hz, uint32_t& l0,
+                                              uint32_t& l1) {
+  const float2 nx = __fadd2_rn(sx, hx), ny = __fadd2_rn(sy, hy), nz = __fadd2_rn(sz, hz);
+  auto one = [&](float fx, float fy, float fz) -> uint32_t {
+    const uint32_t bx = __float_as_uint(fx), by = __float_as_uint(fy), bz = __float_as_uint(fz);
+    const uint32_t o = bx + g.sy * by + g.sz * bz + g.C;
+    if (kChecked) {
+      const uint32_t ix = bx - static_cast<uint32_t>(kMbits), iy = by - static_cast<uint32_t>(kMbits),
+                     iz = bz - static_cast<uint32_t>(kMbits);
+      if (!((ix < g.nx) & (iy < g.ny) & (iz < g.nz))) return lfill;
+    }
+    return __ldg(lin + static_cast<size_t>(o));
+  };
+  l0 = one(nx.x, ny.x, nz.x);
+  l1 = one(nx.y, ny.y, nz.y);
+}
+
 // Staged sampling of a y-pair: image (trilinear or nearest) and label.
 // kSameLbl: the label box has the image box's pitches (cp.async boxes).
 // kAbs: the index in absolute volume coordinates, kM + fx + W fy + P fz (fy, fz
@@ -518,9 +562,12 @@ template <class T> __device__ __forceinline__ float lds_one(uint32_t a) {
 // kM + fx + W (fy - by) + P (fz - bz).  Exact while |fx + W fy + P fz| < 2^22:
 // the host enables it per volume (VolDev::cp_abs) from the volume's dims, box
 // pitches and the range of p over the whole output volume.
-template <class T, bool kLabels, bool kNearest, bool kClamp, bool kSameLbl, bool kAbs = false>
+template <class T, bool kLabels, bool kNearest, bool kClamp, bool kSameLbl, bool kAbs = false,
+          int kLG = 0>
 __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, float2 pz,
-                                        float2& img, uint32_t& l0, uint32_t& l1) {
+                                        float2& img, uint32_t& l0, uint32_t& l1,
+                                        const uint8_t* lin = nullptr, const GView* gv = nullptr,
+                                        uint32_t lfill = 0u) {
   if (kClamp) {
     px = make_float2(fminf(fmaxf(px.x, -1.0f), v.nx), fminf(fmaxf(px.y, -1.0f), v.nx));
     py = make_float2(fminf(fmaxf(py.x, -1.0f), v.ny), fminf(fmaxf(py.y, -1.0f), v.ny));
@@ -541,7 +588,9 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
     const float2 hy = make_float2(fset_ge_half(ty.x), fset_ge_half(ty.y));
     const float2 hz = make_float2(fset_ge_half(tz.x), fset_ge_half(tz.y));
     if (kNearest) Ln = __ffma2_rn(hz, f2(v.Pf), __ffma2_rn(hy, f2(v.Wf), __fadd2_rn(L, hx)));
-    if (kLabels) {  // label buffer: own pitches (kM + fx + hx - bx + Wl (ry + hy) + Pl (rz + hz))
+    if (kLabels && kLG != 0) {  // no label box: gathered (8-row tiles)
+      label_gather2<kLG == 2>(lin, *gv, lfill, sx, sy, sz, hx, hy, hz, l0, l1);
+    } else if (kLabels) {  // label buffer: own pitches (kM + fx + hx - bx + Wl (ry + hy) + Pl (rz + hz))
       const float2 Ll =
           kSameLbl ? (kNearest ? Ln
                                : __ffma2_rn(hz, f2(v.Pf), __ffma2_rn(hy, f2(v.Wf), __fadd2_rn(L, hx))))
@@ -601,9 +650,10 @@ __device__ __forceinline__ void sample2(const View& v, float2 px, float2 py, flo
 // The label of a y-pair alone (an occluded column, R15: the image is 0 and its
 // fetch skipped): the index arithmetic of sample2's label
 // path, op for op, so the labels are the same bits.
-template <bool kClamp, bool kSameLbl, bool kAbs = false>
+template <bool kClamp, bool kSameLbl, bool kAbs = false, int kLG = 0>
 __device__ __forceinline__ void label2(const View& v, float2 px, float2 py, float2 pz,
-                                       uint32_t& l0, uint32_t& l1) {
+                                       uint32_t& l0, uint32_t& l1, const uint8_t* lin = nullptr,
+                                       const GView* gv = nullptr, uint32_t lfill = 0u) {
   if (kClamp) {
     px = make_float2(fminf(fmaxf(px.x, -1.0f), v.nx), fminf(fmaxf(px.y, -1.0f), v.nx));
     py = make_float2(fminf(fmaxf(py.x, -1.0f), v.ny), fminf(fmaxf(py.y, -1.0f), v.ny));
@@ -618,6 +668,10 @@ __device__ __forceinline__ void label2(const View& v, float2 px, float2 py, floa
   const float2 hx = make_float2(fset_ge_half(tx.x), fset_ge_half(tx.y));
   const float2 hy = make_float2(fset_ge_half(ty.x), fset_ge_half(ty.y));
   const float2 hz = make_float2(fset_ge_half(tz.x), fset_ge_half(tz.y));
+  if (kLG != 0) {
+    label_gather2<kLG == 2>(lin, *gv, lfill, sx, sy, sz, hx, hy, hz, l0, l1);
+    return;
+  }
   float2 Ll;
   if (kSameLbl) {
     const float2 L = __ffma2_rn(rz, f2(v.Pf), __ffma2_rn(ry, f2(v.Wf), sx));
@@ -693,25 +747,6 @@ __device__ __forceinline__ void sample_gather(const WarpArgs& a, const T* __rest
 //   kGWide: a dim >= 2^21 (the magic-number floor needs |p| < 2^22): the
 //          per-voxel sample_gather with float floors and 64-bit offsets.
 enum { kGEdge = 0, kGIn = 1, kGOut = 2, kGWide = 3 };
-struct GView {
-  uint32_t nx, ny, nz;  // input dims
-  uint32_t sy, sz;      // element strides nx, nx ny
-  uint32_t C;           // -kMbits (1 + sy + sz) mod 2^32: o = bits(sx) + sy bits(sy) + sz bits(sz) + C
-  float fnx, fny, fnz;
-};
-__device__ __forceinline__ GView make_gview(const WarpArgs& a) {
-  GView g;
-  g.nx = static_cast<uint32_t>(a.nx);
-  g.ny = static_cast<uint32_t>(a.ny);
-  g.nz = static_cast<uint32_t>(a.nz);
-  g.sy = g.nx;
-  g.sz = g.nx * g.ny;
-  g.C = 0u - static_cast<uint32_t>(kMbits) * (1u + g.sy + g.sz);
-  g.fnx = static_cast<float>(a.nx);
-  g.fny = static_cast<float>(a.ny);
-  g.fnz = static_cast<float>(a.nz);
-  return g;
-}
 template <class T, bool kLabels, int kGMode>
 __device__ __forceinline__ void gather2(const WarpArgs& a, const T* __restrict__ vin,
                                         const uint8_t* __restrict__ lin, const GView& g, float2 px,
@@ -847,7 +882,7 @@ __device__ __forceinline__ uint8_t* at(uint8_t* base, uint32_t off) {
 // n2, n3; computed while the staging copies are in flight) and the loop
 // computes group g + kPre's block.
 template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
-          bool kSameLbl, bool kFull, int kPre, int kGMode, bool kOccOnly, bool kAbs>
+          bool kSameLbl, bool kFull, int kPre, int kGMode, bool kOccOnly, bool kAbs, int kLG>
 __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev& P, const Vol& V0,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
@@ -906,10 +941,11 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
     float2 img;
     uint32_t l0 = 0, l1 = 0;
     if (kOcc && kStaged) {
-      if (kLabels) label2<kClamp, kSameLbl, kAbs>(v, px, py, pz, l0, l1);
+      if (kLabels) label2<kClamp, kSameLbl, kAbs, kLG>(v, px, py, pz, l0, l1, lin, &gv, a.label_fill);
     } else if (kOcc && !kLabels) {
     } else if (kStaged) {
-      sample2<T, kLabels, kNearest, kClamp, kSameLbl, kAbs>(v, px, py, pz, img, l0, l1);
+      sample2<T, kLabels, kNearest, kClamp, kSameLbl, kAbs, kLG>(v, px, py, pz, img, l0, l1, lin,
+                                                                &gv, a.label_fill);
     } else if (!kNearest && kGMode != kGWide) {
       gather2<T, kLabels, kGMode>(a, vin, lin, gv, px, py, pz, img, l0, l1);
     } else {
@@ -1020,7 +1056,7 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
 // chain.  The column is one thread, so the test is per thread.
 template <class T, bool kLabels, bool kNearest, int kPh, bool kStaged, bool kClamp,
           bool kSameLbl = false, bool kFull = false, int kPre = 1, int kGMode = kGEdge,
-          bool kAbs = false>
+          bool kAbs = false, int kLG = 0>
 __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, const Vol& V,
                                             const View& v, int vi, int X, int Z, int y0, int ng,
                                             float4 n, float4 n1 = make_float4(0.f, 0.f, 0.f, 0.f),
@@ -1028,10 +1064,10 @@ __device__ __forceinline__ void column_rows(const WarpArgs& a, const VolDev& P, 
                                             float4 n3 = make_float4(0.f, 0.f, 0.f, 0.f)) {
   if ((V.flags & kOcclude) && Z >= P.occ_lo && Z <= P.occ_hi)
     column_rows_impl<T, kLabels, kNearest, kPh, kStaged, kClamp, kSameLbl, kFull, kPre, kGMode,
-                     true, kAbs>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
+                     true, kAbs, kLG>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
   else
     column_rows_impl<T, kLabels, kNearest, kPh, kStaged, kClamp, kSameLbl, kFull, kPre, kGMode,
-                     false, kAbs>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
+                     false, kAbs, kLG>(a, P, V, v, vi, X, Z, y0, ng, n, n1, n2, n3);
 }
 
 __device__ __forceinline__ Vol load_vol(const VolDev& P) {
@@ -1467,6 +1503,14 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
                                         uint32_t phase = 0u, bool init = true) {
   constexpr int kC = InT<T>::kChunk;
   constexpr uint32_t kB = InT<T>::kBytes;
+  // 8-row tiles (large footprints) gather their labels instead of staging a label
+  // box: the TMA then moves half the rows (the box wait bounds these tiles)
+#ifndef W3D_NO_LBL_GATHER
+  constexpr bool kLblG = kLabels && !kNearest && TY < kTY;
+#else
+  constexpr bool kLblG = false;
+#endif
+  constexpr bool kTmaL = kTmaLbl && !kLblG;  // a label box by TMA
   const uint32_t simg = smem_base();
 #ifdef W3D_DBG_TIMING  // diagnostic: per-tile phase times of a few CTAs (printf)
   const long long dbg_t0 = clock64();
@@ -1507,18 +1551,18 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       }
       mbar_expect_tx(mbar, kB * static_cast<uint32_t>(b.P * b.D) +
-                               (kTmaLbl ? static_cast<uint32_t>(b.Pl * b.D) : 0u));
+                               (kTmaL ? static_cast<uint32_t>(b.Pl * b.D) : 0u));
       tma_load_3d(simg, &a.tm[2 * vi], b.bx, b.by, b.bz, mbar);
-      if (kTmaLbl) tma_load_3d(slbl, &a.tm[2 * vi + 1], b.bxl, b.by, b.bz, mbar);
+      if (kTmaL) tma_load_3d(slbl, &a.tm[2 * vi + 1], b.bxl, b.by, b.bz, mbar);
     }
     if (a.prefetch_ahead > 0 && threadIdx.x == 32)  // another warp than the issuer
       prefetch_ahead<T, TY, kTmaLbl>(a, P, vi);
 #ifdef W3D_VOLPF  // A/B knob, off: no gain measured (274.0 vs 275.0) and +5 % DRAM reads
     if (threadIdx.x == 64 && vi + 1 < a.nvol) prefetch_next_volume<T>(a, vi, oz, oy, ox, TY);
 #endif
-    if (kLabels && !kTmaLbl) stage_lbl<T>(a, lin, b, slbl);
+    if (kLabels && !kTmaLbl && !kLblG) stage_lbl<T>(a, lin, b, slbl);
   } else {
-    stage<T, kLabels>(a, vin, lin, b, simg, slbl);
+    stage<T, kLabels && !kLblG>(a, vin, lin, b, simg, slbl);
   }
 #ifdef W3D_EARLY_BAR
   // A/B knob: with image and labels both by TMA the barrier only publishes the
@@ -1579,7 +1623,7 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     v.cimg = opaque(v.cimg - kB * static_cast<uint32_t>(b.W * b.by + b.P * b.bz));
     v.clbl = opaque(v.clbl - static_cast<uint32_t>(b.Wl * b.by + b.Pl * b.bz));
   }
-  if (!kTmaLbl) cp_async_wait_all();
+  if (!kTmaL) cp_async_wait_all();
   W3D_T(1);  // Philox prologue done
   if (!kEarlyBar) __syncthreads();  // label copies (and the mbarrier init) visible to all
   W3D_T(2);  // barrier passed
@@ -1590,9 +1634,9 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     W3D_T(3);  // box landed
     const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
                         b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
-    const bool insidel = !kTmaLbl || (b.bxl >= 0 && b.bxl + b.Wl <= a.nx &&
-                                      b.by + b.Pl / b.Wl <= a.ny && inside);
-    bool fi = !inside && a.fill != 0.0f, fl = kTmaLbl && !insidel && a.label_fill != 0u;
+    const bool insidel = !kTmaL || (b.bxl >= 0 && b.bxl + b.Wl <= a.nx &&
+                                    b.by + b.Pl / b.Wl <= a.ny && inside);
+    bool fi = !inside && a.fill != 0.0f, fl = kTmaL && !insidel && a.label_fill != 0u;
     // boxes carry margins: skip the fix-up when no sample of the tile can read
     // an out-of-volume cell (every trilinear corner and nearest voxel inside)
     if ((fi || fl) && tile_inside(a, P, p0)) fi = fl = false;
@@ -1602,21 +1646,34 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
       __syncthreads();
     }
     // zero fill / label_fill equal TMA's out-of-volume zeros: fixed without a fix-up
-    W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels, fi || (inside || a.fill == 0.0f),
-                      !kTmaLbl || fl || (insidel || a.label_fill == 0u));
+    W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels && !kLblG,
+                      fi || (inside || a.fill == 0.0f), !kTmaL || fl || (insidel || a.label_fill == 0u));
   } else {
-    W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels, true, true);
+    W3D_CHECK_CONTENT(T, a, P, b, simg, slbl, kLabels && !kLblG, true, true);
   }
 #ifdef W3D_DBG_LATEWAIT  // diagnostic: compute as if the box had arrived (garbage outputs)
   const bool late_wait = true;
 #endif
   if (live) {
-    if (oy + TY <= a.my)  // every row of the tile is an output row
-      column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre, kGEdge, kUseAbs>(
-          a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
-    else
-      column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre, kGEdge, kUseAbs>(
-          a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+    if constexpr (kLblG) {  // gathered labels: unchecked when no sample can leave the volume
+      const bool edge = !tile_inside(a, P, p0);
+      if (oy + TY <= a.my && !edge)
+        column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre, kGEdge, kUseAbs,
+                    1>(a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+      else if (oy + TY <= a.my)
+        column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre, kGEdge, kUseAbs,
+                    2>(a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+      else
+        column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre, kGEdge, kUseAbs,
+                    2>(a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+    } else {
+      if (oy + TY <= a.my)  // every row of the tile is an output row
+        column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, true, kPre, kGEdge, kUseAbs>(
+            a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+      else
+        column_rows<T, kLabels, kNearest, kPh, true, false, !kTmaLbl, false, kPre, kGEdge, kUseAbs>(
+            a, P, V, v, vi, X, Z, oy, TY / 4, n, n1, n2, n3);
+    }
   }
 #ifdef W3D_DBG_LATEWAIT
   if (tma && late_wait) mbar_wait(mbar, phase);
