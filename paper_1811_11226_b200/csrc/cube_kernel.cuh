@@ -1503,9 +1503,11 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
                                         uint32_t phase = 0u, bool init = true) {
   constexpr int kC = InT<T>::kChunk;
   constexpr uint32_t kB = InT<T>::kBytes;
-  // 8-row tiles (large footprints) gather their labels instead of staging a label
-  // box: the TMA then moves half the rows (the box wait bounds these tiles)
-#ifndef W3D_NO_LBL_GATHER
+  // A/B knob W3D_LBL_GATHER: 8-row tiles gather their labels from global memory
+  // instead of staging a label box (half the TMA rows) -- measured slower on C4
+  // (164 vs 190 GVoxel/s: the rotated gathers stall the rows more than the box wait
+  // they save), so off
+#ifdef W3D_LBL_GATHER
   constexpr bool kLblG = kLabels && !kNearest && TY < kTY;
 #else
   constexpr bool kLblG = false;
