@@ -893,3 +893,48 @@ def test_auto_mixed_batch_split_by_box_fit_pdl_chunks(W):
     with _pool() as ex:
         ref = dict(ex.map(one, sel))
     check(out.cpu().numpy(), out_l.cpu().numpy(), ref, ds, FULL, "mixed AUTO batch")
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_far_translations_take_the_per_tile_path(W):
+    """Outputs that map 10^5 voxels away from the input: the absolute staged index
+    would leave the magic-number range, so the host sends these volumes to the per-tile
+    boxes (VolDev::cp_abs = 0); every voxel is fill (+ photometrics) and label_fill,
+    as the oracle says (R6, R8), in every variant."""
+    shape = (24, 20, 32)
+    img, lbl = synth.random_volume(shape, 3)
+    d = synth.draw(synth.TRAIN, 17)
+    for shift in ((1.0e5, 0.0, 0.0), (0.0, -2.5e5, 0.0), (0.0, 0.0, 7.0e4)):
+        A = np.zeros((3, 4), np.float32)
+        A[:, :3] = np.eye(3)
+        A[:, 3] = shift
+        for variant in (0, 1, 2):
+            g_img, g_lbl, ref = run_case(W, img[None], lbl[None], [A], [d], FULL, [0],
+                                         variant=variant, fill=-1000.0, label_fill=4)
+            check(g_img, g_lbl, ref, [d], FULL, f"far {shift} v{variant}")
+            assert np.all(g_lbl == 4)
+
+
+@pytest.mark.parametrize("interp", [0, 1])
+def test_int16_with_occlusion_matches_float(W, interp):
+    """int16 input with the occlusion prism (and nearest interpolation): bitwise equal
+    to the float32 input of the same values, labels against the oracle."""
+    shape = (40, 36, 48)
+    img, lbl = synth.phantom(shape)
+    img = np.round(img).astype(np.float32)
+    d = synth.draw(synth.TRAIN_OCC, 5, out_mz=shape[0])
+    A = _oracle_affine(d, shape, shape)
+    flags = FULL | O.OCCLUDE
+    kw = dict(window=d.window, gamma=d.gamma, sigma=d.sigma, seed=SEED, volume_id=2,
+              occ_z0=d.occ_z0, occ_height=d.occ_height)
+    params = [W.volume_params(A, W.photometric(flags, **kw))]
+    ti = torch.from_numpy(img[None]).cuda()
+    tl = torch.from_numpy(lbl[None]).cuda()
+    o32, l32 = W.warp3d_affine_batched(ti, tl, params, interp=interp, fill=-1000.0)
+    o16, l16 = W.warp3d_affine_batched(ti.to(torch.int16), tl, params, interp=interp,
+                                       fill=-1000.0)
+    torch.cuda.synchronize()
+    assert torch.equal(o32, o16) and torch.equal(l32, l16)
+    r_img, r_lbl = O.warp_volume(img, lbl, A, None, interp, -1000.0, 0, O.photometric(flags, **kw))
+    assert np.array_equal(l32[0].cpu().numpy(), r_lbl)
+    assert_image_close(o32[0].cpu().numpy(), r_img, d.window, d.gamma, True, "i16 occl")
