@@ -60,9 +60,11 @@ typedef enum {
 /* Kernel variant selector for warp3d_affine_batched_ex (tests / benchmarks).
    Both variants compute bit-identical results (same arithmetic, R4-R14).     */
 typedef enum {
-  W3D_KERNEL_AUTO = 0,     /* library choice: STAGED, or GATHER for a launch in
-                              which no volume's tile footprint box fits the
-                              staging buffer (large rotations / scales)          */
+  W3D_KERNEL_AUTO = 0,     /* library choice: STAGED for the volumes whose
+                              16-row tile box fits the staging buffer; the others
+                              (large rotations / scales) in their own launches of
+                              16 x 8 x 16 tiles with fixed-dims TMA boxes (half the
+                              box height), GATHER when even those do not fit     */
   W3D_KERNEL_GATHER = 1,   /* every corner gathered through L1/L2 (__ldg) with
                               per-corner bounds                                  */
   W3D_KERNEL_STAGED = 2    /* per-tile source footprint staged in shared memory
