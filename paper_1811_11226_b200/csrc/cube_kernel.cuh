@@ -1507,7 +1507,9 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
   // instead of staging a label box (half the TMA rows) -- measured slower on C4
   // (164 vs 190 GVoxel/s: the rotated gathers stall the rows more than the box wait
   // they save), so off
-#ifdef W3D_LBL_GATHER
+#if defined(W3D_LBL_GATHER_ALL)  // A/B knob: every fixed-box tile
+  constexpr bool kLblG = kLabels && !kNearest;
+#elif defined(W3D_LBL_GATHER)
   constexpr bool kLblG = kLabels && !kNearest && TY < kTY;
 #else
   constexpr bool kLblG = false;
