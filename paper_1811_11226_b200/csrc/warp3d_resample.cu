@@ -13,6 +13,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
+#include <utility>
 
 #include "warp3d_internal.cuh"
 
@@ -48,16 +50,19 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
 }
 
 // Fused separable smoothing, z-marching (2.5D): a CTA owns a 32 x 8 NYT column of
-// outputs and walks MZ output planes along z.  Each input plane's tile
-// plus its x/y halo (edge voxels replicated by clamped coordinates) streams
-// into a ring of shared-memory stages by cp.async, kStages - 1 planes ahead of
-// the compute; per plane the x pass runs over the halo rows (shared memory ->
-// shared memory), the y pass gives each thread its (x, y) value, and the z pass
-// runs in registers over a window of the last 2 RM + 1 planes.  Same passes,
-// order and fp32 FMAs as smooth_axis_kernel (bit-identical results); HBM sees
-// one read (+ the z halo of 2 RM planes per MZ) and one write per voxel.
+// outputs and walks MZ output planes along z.  Each input plane's tile plus its x/y halo (edge voxels replicated by
+// clamped coordinates) streams into a ring of shared-memory stages by cp.async,
+// kStages - 1 planes ahead of the compute; per plane the x pass runs over the
+// halo rows (shared memory -> shared memory), the y pass gives each thread its
+// (x, y) value, and the z pass runs in registers over a window of the last
+// 2 RM + 1 planes (the plane loop unrolled by 2 RM + 1, so the window is a fixed
+// set of register slots).  The x pass reads 16 B words (4 outputs per thread)
+// and writes one of two buffers, so the x pass of plane i and the y / z passes
+// of plane i - 1 share one barrier interval.  Same passes, order and fp32 FMAs
+// as smooth_axis_kernel (bit-identical results); HBM sees one read (+ the z
+// halo of 2 RM planes per run) and one write per voxel.
 #ifndef W3D_SM_STAGES
-#define W3D_SM_STAGES 6
+#define W3D_SM_STAGES 4
 #endif
 #ifndef W3D_SM_NYT2  // rows per thread at radius <= 2 (the 1 mm -> 3 mm case)
 #define W3D_SM_NYT2 4
@@ -65,13 +70,16 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
 #ifndef W3D_SM_MZ
 #define W3D_SM_MZ 64
 #endif
+#ifndef W3D_SM_MINB  // __launch_bounds__ minimum CTAs per SM (register cap)
+#define W3D_SM_MINB 1
+#endif
 constexpr int kFuseR = 8, MX = 32, MZ = W3D_SM_MZ, kStages = W3D_SM_STAGES;
 struct Taps3 {
   float wx[2 * kFuseR + 1], wy[2 * kFuseR + 1], wz[2 * kFuseR + 1];
   int32_t rx, ry, rz;
 };
 
-extern __shared__ float fuse_smem[];
+extern __shared__ __align__(128) float fuse_smem[];
 
 __device__ __forceinline__ void cp_async4(float* s, const float* g) {
   const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s));
@@ -84,15 +92,30 @@ __device__ __forceinline__ void cp_async16(float* s, const float* g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// ld.shared.v4 as written: the compiler narrows a float4 load whose outer words
+// are unused to LDS.64 pieces, and two rows' LDS.64 halves (160 B apart) share
+// banks -- a 2-way conflict the full-width load does not have.
+__device__ __forceinline__ void lds128(const float* p, float* v) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+      : "r"(a));
+}
 
 // RM: compile-time tap radius >= every axis' radius; an axis with a smaller
 // radius has its weights centred and zero-padded (fma(0, v, acc) = acc exactly,
 // so the result equals the per-axis passes bit for bit).  NYT: output rows per
 // thread (warp w owns rows NYT w .. NYT w + NYT - 1 of the MY = 8 NYT rows).
+// f(i0 + U, integral_constant<U>) for U = 0 .. P-1 while i0 + U < n (compile-time slots)
+template <typename F, int... U>
+__device__ __forceinline__ void for_each_slot(F& f, int i0, int n, std::integer_sequence<int, U...>) {
+  ((i0 + U < n ? f(i0 + U, std::integral_constant<int, U>()) : void()), ...);
+}
+
 template <int RM, int NYT>
-__global__ void __launch_bounds__(256) smooth_fused_kernel(const float* __restrict__ in,
-                                                           float* __restrict__ out, int nx, int ny,
-                                                           int nz, const __grid_constant__ Taps3 t) {
+__global__ void __launch_bounds__(256, W3D_SM_MINB)
+    smooth_fused_kernel(const float* __restrict__ in, float* __restrict__ out, int nx, int ny, int nz,
+                        const __grid_constant__ Taps3 t) {
   constexpr int MYT = 8 * NYT;
   // plane tile: x range [ox - XP, ox + 32 + XP) (16 B aligned chunks), y halo RM
   constexpr int XP = RM <= 4 ? 4 : 8;
@@ -100,7 +123,9 @@ __global__ void __launch_bounds__(256) smooth_fused_kernel(const float* __restri
   constexpr int CX = AX / 4, PC = CX * AY;   // 16 B chunks per row / plane
   constexpr int kPer = (PL + 255) / 256;     // elements per thread (edge tiles)
   constexpr int kPerC = (PC + 255) / 256;    // chunks per thread (interior tiles)
-  float* X = fuse_smem + kStages * PL;       // [AY][MX] x-pass result of the current plane
+  constexpr int P = 2 * RM + 1;              // z window; the plane loop's unroll
+  constexpr int NL = (XP + RM + 4 + 3) / 4;  // 16 B words per x-pass thread
+  float* X = fuse_smem + kStages * PL;       // [2][AY][MX] x-pass results, two planes
   float wx[2 * RM + 1], wy[2 * RM + 1], wz[2 * RM + 1];
 #pragma unroll
   for (int k = 0; k <= 2 * RM; ++k) {
@@ -108,99 +133,153 @@ __global__ void __launch_bounds__(256) smooth_fused_kernel(const float* __restri
     wy[k] = (k >= RM - t.ry && k <= RM + t.ry) ? t.wy[k - (RM - t.ry)] : 0.0f;
     wz[k] = (k >= RM - t.rz && k <= RM + t.rz) ? t.wz[k - (RM - t.rz)] : 0.0f;
   }
-  const int ox = static_cast<int>(blockIdx.x) * MX, oy = static_cast<int>(blockIdx.y) * MYT,
-            oz = static_cast<int>(blockIdx.z) * MZ;
   const int lx = static_cast<int>(threadIdx.x & 31), w = static_cast<int>(threadIdx.x >> 5);
-  const int nin = min(MZ, nz - oz) + 2 * RM;  // input planes oz - RM + i, i < nin
-  // interior in x (whole aligned chunks inside the rows): 16 B copies, else 4 B
-  // copies of clamped coordinates (edge replication)
-  const bool chunked = ox - XP >= 0 && ox + MX + XP <= nx && (nx & 3) == 0 &&
-                       (reinterpret_cast<uintptr_t>(in) & 15) == 0;
-  int soff[kPer];
-  uint32_t goff[kPer];
-  if (chunked) {
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int e = static_cast<int>(threadIdx.x) + 256 * j;  // chunk index
-      const int r = e / CX, c = e - r * CX;
-      const int gy = min(max(oy - RM + r, 0), ny - 1);
-      soff[j] = (j < kPerC && e < PC) ? r * AX + 4 * c : -1;
-      goff[j] = static_cast<uint32_t>(gy) * static_cast<uint32_t>(nx) +
-                static_cast<uint32_t>(ox - XP + 4 * c);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int e = static_cast<int>(threadIdx.x) + 256 * j;
-      const int r = e / AX, c = e - r * AX;
-      const int gx = min(max(ox - XP + c, 0), nx - 1), gy = min(max(oy - RM + r, 0), ny - 1);
-      soff[j] = e < PL ? e : -1;
-      goff[j] = static_cast<uint32_t>(gy) * static_cast<uint32_t>(nx) + static_cast<uint32_t>(gx);
-    }
-  }
+  // x pass: 8 threads per row (4 outputs each), 32 rows per sweep
+  const int xr = static_cast<int>(threadIdx.x) >> 3, xj = static_cast<int>(threadIdx.x) & 7;
   const size_t plane = static_cast<size_t>(nx) * static_cast<size_t>(ny);
-  auto load_plane = [&](int i) {
-    const int zc = min(max(oz - RM + i, 0), nz - 1);
-    const float* src = in + static_cast<size_t>(zc) * plane;
-    float* dst = fuse_smem + (i % kStages) * PL;
-    if (chunked) {
-#pragma unroll
-      for (int j = 0; j < kPerC; ++j)
-        if (soff[j] >= 0) cp_async16(dst + soff[j], src + goff[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < kPer; ++j)
-        if (soff[j] >= 0) cp_async4(dst + soff[j], src + goff[j]);
-    }
-  };
-#pragma unroll
-  for (int i = 0; i < kStages - 1; ++i) {
-    if (i < nin) load_plane(i);
-    cp_async_commit();
-  }
-  const int gx = ox + lx, gy0 = oy + NYT * w;
-  float* po = out + (static_cast<size_t>(oz) * ny + gy0) * nx + gx;
-  float ring[NYT][2 * RM + 1];
+  float ring[NYT][2 * RM + 1];  // z window: slot i mod P holds the y-pass value of plane i
 #pragma unroll
   for (int q = 0; q < NYT; ++q)
 #pragma unroll
     for (int k = 0; k <= 2 * RM; ++k) ring[q][k] = 0.0f;
-  for (int i = 0; i < nin; ++i) {
-    cp_async_wait<kStages - 2>();
-    __syncthreads();  // plane i landed; X free (previous y pass done)
-    const float* A = fuse_smem + (i % kStages) * PL;
-    for (int r = w; r < AY; r += 8) {  // x pass over the halo rows
-      const float* a = A + r * AX + lx + (XP - RM);
-      float acc = 0.0f;
+
+  {
+    const int ox = static_cast<int>(blockIdx.x) * MX, oy = static_cast<int>(blockIdx.y) * MYT,
+              oz = static_cast<int>(blockIdx.z) * MZ;
+    const int nout = min(MZ, nz - oz);
+    const int nin = nout + 2 * RM;  // input planes oz - RM + i, i < nin
+    // interior in x (whole aligned chunks inside the rows): 16 B copies, else 4 B
+    // copies of clamped coordinates (edge replication)
+    const bool chunked = ox - XP >= 0 && ox + MX + XP <= nx && (nx & 3) == 0 &&
+                         (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    int soff[kPer];
+    uint32_t goff[kPer];
+    if (chunked) {
 #pragma unroll
-      for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], a[k], acc);
-      X[r * MX + lx] = acc;
-    }
-    if (i + kStages - 1 < nin) load_plane(i + kStages - 1);  // into plane i-1's stage
-    cp_async_commit();
-    __syncthreads();
-    float xv[NYT + 2 * RM];  // y pass: the thread's rows share their x-pass inputs
-#pragma unroll
-    for (int k = 0; k < NYT + 2 * RM; ++k) xv[k] = X[(NYT * w + k) * MX + lx];
-#pragma unroll
-    for (int q = 0; q < NYT; ++q) {
-      float yv = 0.0f;
-#pragma unroll
-      for (int k = 0; k <= 2 * RM; ++k) yv = __fmaf_rn(wy[k], xv[q + k], yv);
-#pragma unroll
-      for (int k = 0; k < 2 * RM; ++k) ring[q][k] = ring[q][k + 1];
-      ring[q][2 * RM] = yv;
-    }
-    if (i >= 2 * RM) {  // z pass: output plane oz + i - 2 RM complete
-#pragma unroll
-      for (int q = 0; q < NYT; ++q) {
-        float acc = 0.0f;
-#pragma unroll
-        for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wz[k], ring[q][k], acc);
-        if (gx < nx && gy0 + q < ny) po[static_cast<size_t>(q) * nx] = acc;
+      for (int j = 0; j < kPer; ++j) {
+        const int e = static_cast<int>(threadIdx.x) + 256 * j;  // chunk index
+        const int r = e / CX, c = e - r * CX;
+        const int gy = min(max(oy - RM + r, 0), ny - 1);
+        soff[j] = (j < kPerC && e < PC) ? r * AX + 4 * c : -1;
+        goff[j] = static_cast<uint32_t>(gy) * static_cast<uint32_t>(nx) +
+                  static_cast<uint32_t>(ox - XP + 4 * c);
       }
-      po += plane;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int e = static_cast<int>(threadIdx.x) + 256 * j;
+        const int r = e / AX, c = e - r * AX;
+        const int gx = min(max(ox - XP + c, 0), nx - 1), gy = min(max(oy - RM + r, 0), ny - 1);
+        soff[j] = e < PL ? e : -1;
+        goff[j] = static_cast<uint32_t>(gy) * static_cast<uint32_t>(nx) + static_cast<uint32_t>(gx);
+      }
     }
+    auto load_plane = [&](int i) {
+      const int zc = min(max(oz - RM + i, 0), nz - 1);
+      const float* src = in + static_cast<size_t>(zc) * plane;
+      float* dst = fuse_smem + (i % kStages) * PL;
+      if (chunked) {
+#pragma unroll
+        for (int j = 0; j < kPerC; ++j)
+          if (soff[j] >= 0) cp_async16(dst + soff[j], src + goff[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kPer; ++j)
+          if (soff[j] >= 0) cp_async4(dst + soff[j], src + goff[j]);
+      }
+    };
+    // (the previous segment's stages were last read before its final barrier)
+#pragma unroll
+    for (int i = 0; i < kStages - 1; ++i) {
+      if (i < nin) load_plane(i);
+      cp_async_commit();
+    }
+    const int gx = ox + lx, gy0 = oy + NYT * w;
+    float* po = out + (static_cast<size_t>(oz) * ny + gy0) * nx + gx;
+    bool ok[NYT];  // store bounds per row
+#pragma unroll
+    for (int q = 0; q < NYT; ++q) ok[q] = gx < nx && gy0 + q < ny;
+    // One barrier per plane: the x pass of plane i (into X buffer i & 1) and the y /
+    // z passes of plane i - 1 (from buffer (i - 1) & 1) share a phase.  Behind the
+    // barrier of step i: plane i has landed, buffer (i - 1) & 1 is complete, buffer
+    // i & 1 was last read by the y pass of plane i - 2 (step i - 1), and the stage
+    // the next load overwrites was last read by the x pass of plane i - 1.
+    auto plane_step = [&](int i, auto slot_tag) {
+      constexpr int u = decltype(slot_tag)::value;  // slot of plane i: u = i mod P
+      cp_async_wait<kStages - 2>();
+      __syncthreads();
+      if (i < nin) {
+        const float* A = fuse_smem + (i % kStages) * PL;
+        float* Xb = X + (i & 1) * (AY * MX);
+#ifndef W3D_SM_SCALAR_X
+        // 4 outputs per thread from NL aligned 16 B loads (the taps of neighbouring
+        // outputs overlap: ~1 LDS per output instead of 2 RM + 1); same FMA order
+        // per output as the per-axis pass
+#pragma unroll
+        for (int r0 = 0; r0 < AY; r0 += 32) {
+          const int r = r0 + xr;
+          if (r0 + 32 <= AY || r < AY) {
+            float v[4 * NL];
+#pragma unroll
+            for (int l = 0; l < NL; ++l)  // whole 16 B words even where only half is
+              lds128(A + r * AX + 4 * xj + 4 * l, v + 4 * l);  // used: no bank conflicts
+            float o[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              float acc = 0.0f;
+#pragma unroll
+              for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], v[c + k + XP - RM], acc);
+              o[c] = acc;
+            }
+            *reinterpret_cast<float4*>(Xb + r * MX + 4 * xj) = make_float4(o[0], o[1], o[2], o[3]);
+          }
+        }
+#else
+        for (int r = w; r < AY; r += 8) {  // A/B knob: one output per thread
+          const float* a = A + r * AX + lx + (XP - RM);
+          float acc = 0.0f;
+#pragma unroll
+          for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], a[k], acc);
+          Xb[r * MX + lx] = acc;
+        }
+#endif
+      }
+      if (i + kStages - 1 < nin) load_plane(i + kStages - 1);  // into plane i-1's stage
+      cp_async_commit();
+      if (i >= 1) {
+        const float* Xp = X + ((i - 1) & 1) * (AY * MX);
+        constexpr int up = (u + P - 1) % P;  // slot of plane i - 1
+        float xv[NYT + 2 * RM];  // y pass: the thread's rows share their x-pass inputs
+#pragma unroll
+        for (int k = 0; k < NYT + 2 * RM; ++k) xv[k] = Xp[(NYT * w + k) * MX + lx];
+#pragma unroll
+        for (int q = 0; q < NYT; ++q) {
+          float yv = 0.0f;
+#pragma unroll
+          for (int k = 0; k <= 2 * RM; ++k) yv = __fmaf_rn(wy[k], xv[q + k], yv);
+          ring[q][up] = yv;
+        }
+        if (i - 1 >= 2 * RM) {  // z pass: output plane oz + i - 1 - 2 RM complete
+          float acc[NYT];
+#pragma unroll
+          for (int q = 0; q < NYT; ++q) {
+            acc[q] = 0.0f;
+#pragma unroll
+            for (int k = 0; k <= 2 * RM; ++k)  // oldest (plane i - 1 - 2 RM: slot u) first
+              acc[q] = __fmaf_rn(wz[k], ring[q][(u + k) % P], acc[q]);
+          }
+          float* pq = po;
+#pragma unroll
+          for (int q = 0; q < NYT; ++q) {
+            if (ok[q]) *pq = acc[q];
+            pq += nx;
+          }
+          po += plane;
+        }
+      }
+    };
+    for (int i0 = 0; i0 <= nin; i0 += P)
+      for_each_slot(plane_step, i0, nin + 1, std::make_integer_sequence<int, P>());
   }
 }
 
@@ -254,7 +333,7 @@ cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int
   auto go = [&](auto kernel, int RM, int nyt) {
     const int my = 8 * nyt, xp = RM <= 4 ? 4 : 8;
     const size_t smem =
-        sizeof(float) * (size_t(kStages) * (MX + 2 * xp) * (my + 2 * RM) + size_t(my + 2 * RM) * MX);
+        sizeof(float) * (size_t(kStages) * (MX + 2 * xp) * (my + 2 * RM) + 2 * size_t(my + 2 * RM) * MX);
     if (smem > 48 * 1024)
       e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem));
