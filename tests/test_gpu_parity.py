@@ -622,6 +622,7 @@ def test_pipeline_chained_calls_back_to_back(W, depth, B):
     ((9, 33, 40), (1.7, 0.0, 0.4)),
     ((1, 1, 5), (0.0, 0.0, 1.0)),
     ((31, 2, 3), (3.3, 1.0, 0.0)),
+    ((70, 40, 136), (2.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0)),   # 16 B cp.async tiles, two z runs
 ])
 def test_smooth3d_matches_oracle(W, shape, sigma):
     img, _ = synth.phantom(shape) if min(shape) >= 8 else synth.random_volume(shape, 2)
@@ -741,6 +742,14 @@ def test_volumes_of_different_dims_rejects_bad_input(W):
     ((70, 37, 45), (2.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0)),   # several z chunks, ragged x / y
     ((130, 20, 33), (1.1, 0.0, 2.4)),                      # radius classes 4 / 8, sigma 0 axis
     ((5, 9, 64), (0.3, 1.7, 0.9)),                         # fewer planes than the z halo
+    # nx = 136: x tiles 1-3 take the 16 B cp.async path, tiles 0 and 4 the clamped one;
+    # every radius class of the fused kernel (R = ceil(3 sigma): 1, 2, 3, 4, 6, 8)
+    ((150, 45, 136), (0.3, 0.3, 0.3)),
+    ((150, 45, 136), (2.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0)),
+    ((36, 45, 136), (1.0, 0.5, 0.2)),
+    ((36, 45, 136), (1.3, 1.3, 1.3)),
+    ((36, 45, 136), (2.0, 0.0, 1.5)),
+    ((36, 45, 136), (2.6, 2.6, 2.6)),
 ])
 def test_fused_smoothing_equals_per_axis_passes_bitwise(W, shape, sigma, tmp_path):
     """The z-marching fused lowpass keeps the per-axis passes' order and fp32 FMAs: equal
