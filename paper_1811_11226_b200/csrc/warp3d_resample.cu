@@ -70,10 +70,14 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
 #ifndef W3D_SM_MZ
 #define W3D_SM_MZ 64
 #endif
+#ifndef W3D_SM_THREADS  // threads per CTA (warps = rows of 32 columns x NYT)
+#define W3D_SM_THREADS 256
+#endif
 #ifndef W3D_SM_MINB  // __launch_bounds__ minimum CTAs per SM (register cap)
 #define W3D_SM_MINB 1
 #endif
-constexpr int kFuseR = 8, MX = 32, MZ = W3D_SM_MZ, kStages = W3D_SM_STAGES;
+constexpr int kFuseR = 8, MX = 32, MZ = W3D_SM_MZ, kStages = W3D_SM_STAGES,
+              kSmThreads = W3D_SM_THREADS;
 struct Taps3 {
   float wx[2 * kFuseR + 1], wy[2 * kFuseR + 1], wz[2 * kFuseR + 1];
   int32_t rx, ry, rz;
@@ -113,16 +117,17 @@ __device__ __forceinline__ void for_each_slot(F& f, int i0, int n, std::integer_
 }
 
 template <int RM, int NYT>
-__global__ void __launch_bounds__(256, W3D_SM_MINB)
+__global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
     smooth_fused_kernel(const float* __restrict__ in, float* __restrict__ out, int nx, int ny, int nz,
                         const __grid_constant__ Taps3 t) {
-  constexpr int MYT = 8 * NYT;
+  constexpr int NT = kSmThreads, NW = NT / 32;
+  constexpr int MYT = NW * NYT;
   // plane tile: x range [ox - XP, ox + 32 + XP) (16 B aligned chunks), y halo RM
   constexpr int XP = RM <= 4 ? 4 : 8;
   constexpr int AX = MX + 2 * XP, AY = MYT + 2 * RM, PL = AX * AY;
   constexpr int CX = AX / 4, PC = CX * AY;   // 16 B chunks per row / plane
-  constexpr int kPer = (PL + 255) / 256;     // elements per thread (edge tiles)
-  constexpr int kPerC = (PC + 255) / 256;    // chunks per thread (interior tiles)
+  constexpr int kPer = (PL + NT - 1) / NT;   // elements per thread (edge tiles)
+  constexpr int kPerC = (PC + NT - 1) / NT;  // chunks per thread (interior tiles)
   constexpr int P = 2 * RM + 1;              // z window; the plane loop's unroll
   constexpr int NL = (XP + RM + 4 + 3) / 4;  // 16 B words per x-pass thread
   float* X = fuse_smem + kStages * PL;       // [2][AY][MX] x-pass results, two planes
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(256, W3D_SM_MINB)
     if (chunked) {
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
-        const int e = static_cast<int>(threadIdx.x) + 256 * j;  // chunk index
+        const int e = static_cast<int>(threadIdx.x) + NT * j;  // chunk index
         const int r = e / CX, c = e - r * CX;
         const int gy = min(max(oy - RM + r, 0), ny - 1);
         soff[j] = (j < kPerC && e < PC) ? r * AX + 4 * c : -1;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(256, W3D_SM_MINB)
     } else {
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
-        const int e = static_cast<int>(threadIdx.x) + 256 * j;
+        const int e = static_cast<int>(threadIdx.x) + NT * j;
         const int r = e / AX, c = e - r * AX;
         const int gx = min(max(ox - XP + c, 0), nx - 1), gy = min(max(oy - RM + r, 0), ny - 1);
         soff[j] = e < PL ? e : -1;
@@ -216,9 +221,9 @@ __global__ void __launch_bounds__(256, W3D_SM_MINB)
         // outputs overlap: ~1 LDS per output instead of 2 RM + 1); same FMA order
         // per output as the per-axis pass
 #pragma unroll
-        for (int r0 = 0; r0 < AY; r0 += 32) {
+        for (int r0 = 0; r0 < AY; r0 += 4 * NW) {
           const int r = r0 + xr;
-          if (r0 + 32 <= AY || r < AY) {
+          if (r0 + 4 * NW <= AY || r < AY) {
             float v[4 * NL];
 #pragma unroll
             for (int l = 0; l < NL; ++l)  // whole 16 B words even where only half is
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(256, W3D_SM_MINB)
           }
         }
 #else
-        for (int r = w; r < AY; r += 8) {  // A/B knob: one output per thread
+        for (int r = w; r < AY; r += NW) {  // A/B knob: one output per thread
           const float* a = A + r * AX + lx + (XP - RM);
           float acc = 0.0f;
 #pragma unroll
@@ -331,7 +336,7 @@ cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int
   const int rmax = max(t.rx, max(t.ry, t.rz));
   cudaError_t e = cudaSuccess;
   auto go = [&](auto kernel, int RM, int nyt) {
-    const int my = 8 * nyt, xp = RM <= 4 ? 4 : 8;
+    const int my = (kSmThreads / 32) * nyt, xp = RM <= 4 ? 4 : 8;
     const size_t smem =
         sizeof(float) * (size_t(kStages) * (MX + 2 * xp) * (my + 2 * RM) + 2 * size_t(my + 2 * RM) * MX);
     if (smem > 48 * 1024)
@@ -339,7 +344,7 @@ cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int
                                static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>((nx + MX - 1) / MX), static_cast<unsigned>((ny + my - 1) / my),
                     static_cast<unsigned>((nz + MZ - 1) / MZ));
-    if (e == cudaSuccess) kernel<<<grid, 256, smem, s>>>(in, out, nx, ny, nz, t);
+    if (e == cudaSuccess) kernel<<<grid, kSmThreads, smem, s>>>(in, out, nx, ny, nz, t);
   };
   if (rmax <= 1) go(smooth_fused_kernel<1, 4>, 1, 4);
   else if (rmax <= 2) go(smooth_fused_kernel<2, W3D_SM_NYT2>, 2, W3D_SM_NYT2);
