@@ -1627,6 +1627,16 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     v.cimg = opaque(v.cimg - kB * static_cast<uint32_t>(b.W * b.by + b.P * b.bz));
     v.clbl = opaque(v.clbl - static_cast<uint32_t>(b.Wl * b.by + b.Pl * b.bz));
   }
+  // which boxes need a fix-up: decided before the barrier and the box wait (under
+  // the staging latency), not after them on the tile's critical path
+  const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
+                      b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
+  const bool insidel = !kTmaL || (b.bxl >= 0 && b.bxl + b.Wl <= a.nx &&
+                                  b.by + b.Pl / b.Wl <= a.ny && inside);
+  bool fi = tma && !inside && a.fill != 0.0f, fl = tma && kTmaL && !insidel && a.label_fill != 0u;
+  // boxes carry margins: skip the fix-up when no sample of the tile can read
+  // an out-of-volume cell (every trilinear corner and nearest voxel inside)
+  if ((fi || fl) && tile_inside(a, P, p0)) fi = fl = false;
   if (!kTmaL) cp_async_wait_all();
   W3D_T(1);  // Philox prologue done
   if (!kEarlyBar) __syncthreads();  // label copies (and the mbarrier init) visible to all
@@ -1636,14 +1646,6 @@ __device__ __forceinline__ void cp_tile(const WarpArgs& a, const VolDev& P, int 
     mbar_wait(mbar, phase);
 #endif
     W3D_T(3);  // box landed
-    const bool inside = b.bx >= 0 && b.by >= 0 && b.bz >= 0 && b.bx + b.W <= a.nx &&
-                        b.by + b.H <= a.ny && b.bz + b.D <= a.nz;
-    const bool insidel = !kTmaL || (b.bxl >= 0 && b.bxl + b.Wl <= a.nx &&
-                                    b.by + b.Pl / b.Wl <= a.ny && inside);
-    bool fi = !inside && a.fill != 0.0f, fl = kTmaL && !insidel && a.label_fill != 0u;
-    // boxes carry margins: skip the fix-up when no sample of the tile can read
-    // an out-of-volume cell (every trilinear corner and nearest voxel inside)
-    if ((fi || fl) && tile_inside(a, P, p0)) fi = fl = false;
     if (fi || fl) {  // uniform
       if (fi) tma_fixup<T>(a, b, simg);
       if (fl) tma_fixup_lbl(a, b, slbl);
