@@ -31,3 +31,6 @@ for n in ['lts__throughput.avg.pct_of_peak_sustained_elapsed', 'l1tex__throughpu
         print(f"{n:70s} {v[h.index(n)]:>16s} {u[h.index(n)]}")
 PY
 done
+if [ -f $G/ev_${TAG}_resample.ncu-rep ]; then
+  python3 tools/ncu_summary.py $G/ev_${TAG}_resample.ncu-rep 134217728 > $OUT/ncu_full_resample_${TAG}.txt 2>&1
+fi

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round evidence on one B200: build, gpu suite, smoke, every workload's bench line (no
 # ncu), the reference arm, the ncu launch list of the default bench command and
-# ncu --set full of the C3 and C4 warp launches.  Output: gpurun_out/ev_<TAG>_*
+# ncu --set full of the C3 and C4 warp launches and of the resample lowpass.  Output: gpurun_out/ev_<TAG>_*
 mkdir -p gpurun_out
 TAG=${TAG:-r}
 python __graft_entry__.py build > gpurun_out/build.log 2>&1 || { echo build failed; tail gpurun_out/build.log; exit 1; }
@@ -26,4 +26,5 @@ if [ "${NCU:-1}" == "1" ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_${TAG}_launches_c3.csv $CMD > /dev/null 2>&1; echo "ncu launches rc=$?"
   ncu --set full --clock-control none --import-source on -k regex:warp3d_cube -s 3 -c 1 -o gpurun_out/ev_${TAG}_c3 -f $CMD > /dev/null 2>&1; echo "ncu c3 rc=$?"
   ncu --set full --clock-control none --import-source on -k regex:warp3d_cube -s 3 -c 1 -o gpurun_out/ev_${TAG}_c4 -f $CMD --workload c4 > /dev/null 2>&1; echo "ncu c4 rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:smooth_fused -s 3 -c 1 -o gpurun_out/ev_${TAG}_resample -f $CMD --workload resample > /dev/null 2>&1; echo "ncu resample rc=$?"
 fi
