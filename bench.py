@@ -434,6 +434,7 @@ def run_resample(args, world, rank, dev, dist):
         peak, peak_src = measured_peaks()
         sec = ms * 1e-3 / args.steps
         moved = 8 * n_in  # fused lowpass: one read + one write of the volume
+        ev = ncu_evidence("resample", "auto")
         line = {
             "metric": "resampled input GVoxel/s (1 mm^3 -> 3 mm^3, image + labels)",
             "value": world * n_in / sec / 1e9, "unit": "GVoxel/s", "n_gpus": world,
@@ -446,7 +447,10 @@ def run_resample(args, world, rank, dev, dist):
                        "l2": "inputs (671 MB) exceed L2"},
             "roofline": {"bound": "hbm", "kernel": "smooth_fused_kernel",
                          "achieved": moved / smooth_sec / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": moved / smooth_sec / 1e9 / peak, "traffic": None,
+                         "unit": "GB/s", "frac": moved / smooth_sec / 1e9 / peak,
+                         "traffic": None if ev is None else float(ev["dram_bytes_per_launch"]),
+                         "inst_per_voxel": None if ev is None else ev.get("inst_per_voxel"),
+                         "ncu_source": None if ev is None else ev.get("source"),
                          "peak_source": peak_src, "alg_bytes_per_launch": moved,
                          "smooth_ms": smooth_sec * 1e3,
                          "compulsory_bytes_per_step": 5 * n_in + 5 * n_out},

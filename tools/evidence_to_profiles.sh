@@ -34,3 +34,4 @@ done
 if [ -f $G/ev_${TAG}_resample.ncu-rep ]; then
   python3 tools/ncu_summary.py $G/ev_${TAG}_resample.ncu-rep 134217728 > $OUT/ncu_full_resample_${TAG}.txt 2>&1
 fi
+python3 tools/ncu_traffic.py $TAG > /dev/null
