@@ -76,6 +76,8 @@ def parse(argv=None):
     ap.add_argument("--occlusion", action="store_true",
                     help="random occlusion per example (PAPER.md:420-438, synth.TRAIN_OCC)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pipe-vols", type=int, default=0,
+                    help="e2e leg: volumes per pipeline job (0: the library's choice)")
     ap.add_argument("--no-c5", action="store_true",
                     help="skip the configs[4] strong-scaling key of the c3 line")
     ap.add_argument("--input", choices=["f32", "i16"], default="f32",
@@ -677,7 +679,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(W, torch, dev, imgs, lbls, params, shape, min(args.steps, 20), world,
-                      global_batch, nvox_out)
+                      global_batch, nvox_out, args.pipe_vols)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -737,7 +739,8 @@ def main():
     return 0
 
 
-def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch, nvox_out):
+def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch, nvox_out,
+            vols_per_job=0):
     """End to end through the library's FIFO host pipeline (warp3d_pipeline_run,
     PAPER.md:379-387): pinned host inputs -> H2D -> warp -> D2H into pinned host
     outputs, every step inside the timed region."""
@@ -749,7 +752,7 @@ def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch
     h_out_l = torch.empty((B, *shape), dtype=torch.uint8).pin_memory()
     # chained calls: step k+1's copy-in overlaps step k's warp and copy-out (the FIFO
     # keeps running across training iterations instead of draining every batch)
-    pipe = W.Pipeline(shape, shape, depth=3, labels=True, chain=True)
+    pipe = W.Pipeline(shape, shape, depth=3, labels=True, chain=True, vols_per_job=vols_per_job)
 
     def step():
         pipe.run(h_img, h_lbl, params, h_out, h_out_l, fill=-1000.0)
@@ -766,12 +769,14 @@ def run_e2e(W, torch, dev, imgs, lbls, params, shape, steps, world, global_batch
     e.record()
     torch.cuda.synchronize(dev)
     ms = reduce_max_ms(s.elapsed_time(e), dist if world > 1 else None, dev)
+    k = pipe.vols_per_job
     pipe.close()
     value = global_batch * nvox_out * steps / (ms * 1e-3) / 1e9
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(B * nvox_out * 5),
             "d2h_bytes_per_step": int(B * nvox_out * 5), "steps": steps,
-            "path": "warp3d_pipeline_run (FIFO, depth 3, chained calls): pinned host -> "
-                    "H2D stream -> warp stream -> D2H stream -> pinned host"}
+            "vols_per_job": k,
+            "path": f"warp3d_pipeline_run (FIFO, depth 3, jobs of {k} volumes, chained calls): "
+                    "pinned host -> H2D stream -> warp stream -> D2H stream -> pinned host"}
 
 
 if __name__ == "__main__":

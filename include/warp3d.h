@@ -290,12 +290,19 @@ w3d_status warp3d_resample(const float* in, const uint8_t* in_labels, w3d_dims i
 /*
  * FIFO pipeline ("a first-in first-out (FIFO) queue to
  * pipeline jobs ... while one image is being processed, the next has already
- * begun transferring"): augments a batch held in HOST memory.  Volume i is job
- * i; it uses device slot i % depth: copy-in stream (H2D image + labels) ->
- * compute stream (warp3d_affine_batched on the slot) -> copy-out stream (D2H),
- * each ordered by events, so H2D of job i+1, the warp of job i and the D2H of
- * job i-1 overlap.  Host buffers should be pinned (cudaHostAlloc /
- * cudaHostRegister) for the copies to be asynchronous.
+ * begun transferring"): augments a batch held in HOST memory.  A job is
+ * vols_per_job consecutive volumes of the batch (the last job of a call may
+ * hold fewer); job j uses device slot j % depth: copy-in stream (one H2D of the
+ * job's images, one of its labels) -> compute stream (warp3d_affine_batched on
+ * the slot) -> copy-out stream (D2H), each ordered by events, so H2D of job
+ * j+1, the warp of job j and the D2H of job j-1 overlap.  The paper's jobs are
+ * single volumes (vols_per_job = 1); warp3d_pipeline_create picks vols_per_job
+ * automatically (jobs of >= 96 MB of input, at most 8 volumes: with both copy
+ * directions busy, per-volume copies of a 13 MB volume reach 47 GB/s per
+ * direction on a B200 host link, 4-volume copies 49), warp3d_pipeline_create_ex
+ * takes it as an argument (0 = automatic; 1 .. 104; else W3D_ERR_INVALID_ARG)
+ * and warp3d_pipeline_vols_per_job reports it.  Host buffers should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous.
  *
  * warp3d_pipeline_create allocates the slots' device buffers, streams and
  * events (not on the hot path); warp3d_pipeline_run performs no allocation: it
@@ -320,6 +327,9 @@ typedef struct w3d_pipeline w3d_pipeline;
 enum { W3D_PIPE_LABELS = 1, W3D_PIPE_CHAIN = 2 };
 w3d_status warp3d_pipeline_create(int32_t depth, w3d_dims in_dims, w3d_dims out_dims,
                                   int32_t flags, w3d_pipeline** out);
+w3d_status warp3d_pipeline_create_ex(int32_t depth, int32_t vols_per_job, w3d_dims in_dims,
+                                     w3d_dims out_dims, int32_t flags, w3d_pipeline** out);
+int32_t warp3d_pipeline_vols_per_job(const w3d_pipeline* p);
 w3d_status warp3d_pipeline_run(w3d_pipeline* p, int32_t batch, const float* in_host,
                                const uint8_t* in_labels_host, const w3d_volume_params* params,
                                w3d_interp interp, float fill, uint8_t label_fill,

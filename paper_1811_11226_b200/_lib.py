@@ -29,6 +29,7 @@ EXPORTS = (
     "warp3d_pipeline_destroy", "warp3d_resample_sigma", "warp3d_resample_dims",
     "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample",
     "warp3d_affine_batched_i16", "warp3d_affine_batched_i16_ex", "warp3d_affine_batched_v",
+    "warp3d_pipeline_create_ex", "warp3d_pipeline_vols_per_job",
 )
 
 
@@ -97,6 +98,11 @@ def load():
     L.warp3d_philox4x32_10.argtypes = [P, U64, P, I64, P]
     L.warp3d_footprint_batched.argtypes = [I32, Dims, P, Dims, P, P, P]
     L.warp3d_pipeline_create.argtypes = [I32, Dims, Dims, I32, ctypes.POINTER(ctypes.c_void_p)]
+    L.warp3d_pipeline_create_ex.argtypes = [I32, I32, Dims, Dims, I32,
+                                            ctypes.POINTER(ctypes.c_void_p)]
+    L.warp3d_pipeline_create_ex.restype = ctypes.c_int
+    L.warp3d_pipeline_vols_per_job.argtypes = [P]
+    L.warp3d_pipeline_vols_per_job.restype = I32
     L.warp3d_pipeline_run.argtypes = [P, I32, P, P, P, I32, F, ctypes.c_uint8, P, P, P]
     L.warp3d_pipeline_destroy.argtypes = [P]
     for name in ("warp3d_pipeline_create", "warp3d_pipeline_run", "warp3d_pipeline_destroy"):

@@ -238,19 +238,22 @@ def warp3d_footprint_batched(params, in_shape_zyx, out_shape_zyx=None, device="c
 
 class Pipeline:
     """FIFO host pipeline (include/warp3d.h warp3d_pipeline_*):
-    H2D of volume i+1, the warp of volume i and the D2H of volume i-1 overlap.
+    H2D of job j+1, the warp of job j and the D2H of job j-1 overlap (a job is
+    `vols_per_job` consecutive volumes; 0 lets the library choose).
     Host tensors should be pinned (tensor.pin_memory())."""
 
-    def __init__(self, in_shape_zyx, out_shape_zyx=None, depth=3, labels=True, chain=False):
+    def __init__(self, in_shape_zyx, out_shape_zyx=None, depth=3, labels=True, chain=False,
+                 vols_per_job=0):
         """chain=True: W3D_PIPE_CHAIN (calls ordered after the previous calls on this
         pipeline only, so consecutive batches' transfers overlap; see warp3d.h)."""
         self.in_shape = tuple(in_shape_zyx)
         self.out_shape = self.in_shape if out_shape_zyx is None else tuple(out_shape_zyx)
         self._h = ctypes.c_void_p()
         flags = (1 if labels else 0) | (2 if chain else 0)
-        L.check(L.load().warp3d_pipeline_create(int(depth), L.dims(self.in_shape),
-                                                L.dims(self.out_shape), flags,
-                                                ctypes.byref(self._h)))
+        L.check(L.load().warp3d_pipeline_create_ex(int(depth), int(vols_per_job),
+                                                   L.dims(self.in_shape), L.dims(self.out_shape),
+                                                   flags, ctypes.byref(self._h)))
+        self.vols_per_job = int(L.load().warp3d_pipeline_vols_per_job(self._h))
 
     def run(self, inp: torch.Tensor, labels, params, out: torch.Tensor, out_labels=None,
             interp=INTERP_LINEAR, fill=0.0, label_fill=0):

@@ -944,7 +944,19 @@ struct w3d_pipeline {
   cudaEvent_t ev_start = nullptr;
   bool chain = false;   // W3D_PIPE_CHAIN: calls ordered after the previous calls only
   int64_t seq = 0;      // jobs submitted so far (slot of job j = j % depth, across calls)
+  int32_t vols = 1;     // volumes per job (one H2D / warp / D2H per job)
 };
+
+// Volumes per job when the caller leaves it to the library: jobs of at least
+// kJobBytes of input (image + labels), at most 8 volumes.  Per-volume copies of a
+// C3 volume (13 MB each way) reach 47.1 GB/s per direction on a B200 box with both
+// directions busy, 4-volume copies 49.1, one 210 MB copy 49.9 (tools/pcie_probe.py);
+// C3 end to end: 8.67 GVoxel/s in jobs of 1 volume, 9.18 of 2, 9.35 of 4, 9.46 of 8.
+static int32_t auto_vols_per_job(size_t in_bytes_per_volume) {
+  constexpr size_t kJobBytes = size_t(96) << 20;
+  const size_t k = (kJobBytes + in_bytes_per_volume - 1) / std::max<size_t>(in_bytes_per_volume, 1);
+  return static_cast<int32_t>(std::min<size_t>(8, std::max<size_t>(1, k)));
+}
 
 static void pipeline_free(w3d_pipeline* p) {
   if (!p) return;
@@ -963,9 +975,17 @@ static void pipeline_free(w3d_pipeline* p) {
 
 w3d_status warp3d_pipeline_create(int32_t depth, w3d_dims in_dims, w3d_dims out_dims,
                                   int32_t flags, w3d_pipeline** out) {
+  return warp3d_pipeline_create_ex(depth, 0, in_dims, out_dims, flags, out);
+}
+
+w3d_status warp3d_pipeline_create_ex(int32_t depth, int32_t vols_per_job, w3d_dims in_dims,
+                                     w3d_dims out_dims, int32_t flags, w3d_pipeline** out) {
   if (!out) return fail(W3D_ERR_INVALID_ARG, "out must be non-NULL");
   *out = nullptr;
   if (depth < 1 || depth > 8) return fail(W3D_ERR_INVALID_ARG, "depth = %d must be in [1, 8]", depth);
+  if (vols_per_job < 0 || vols_per_job > kMaxVolPerLaunch)
+    return fail(W3D_ERR_INVALID_ARG, "vols_per_job = %d must be in [0, %d]", vols_per_job,
+                kMaxVolPerLaunch);
   w3d_status st = check_dims(in_dims, "in_dims");
   if (st != W3D_OK) return st;
   if ((st = check_dims(out_dims, "out_dims")) != W3D_OK) return st;
@@ -977,10 +997,15 @@ w3d_status warp3d_pipeline_create(int32_t depth, w3d_dims in_dims, w3d_dims out_
   p->out_dims = out_dims;
   p->labels = (flags & W3D_PIPE_LABELS) != 0;
   p->chain = (flags & W3D_PIPE_CHAIN) != 0;
+  p->vols = vols_per_job > 0
+                ? vols_per_job
+                : auto_vols_per_job(size_t(nvox(in_dims)) * (p->labels ? 5 : 4));
   auto round256 = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t bi = round256(size_t(nvox(in_dims)) * 4), bo = round256(size_t(nvox(out_dims)) * 4);
-  const size_t bli = p->labels ? round256(size_t(nvox(in_dims))) : 0;
-  const size_t blo = p->labels ? round256(size_t(nvox(out_dims))) : 0;
+  const size_t k = size_t(p->vols);  // a slot holds one job's volumes, contiguous
+  const size_t bi = round256(k * size_t(nvox(in_dims)) * 4);
+  const size_t bo = round256(k * size_t(nvox(out_dims)) * 4);
+  const size_t bli = p->labels ? round256(k * size_t(nvox(in_dims))) : 0;
+  const size_t blo = p->labels ? round256(k * size_t(nvox(out_dims))) : 0;
   const size_t per = bi + bo + bli + blo;
   cudaError_t e = cudaMalloc(&p->mem, per * size_t(depth));
   if (e == cudaSuccess) {
@@ -1040,39 +1065,41 @@ w3d_status warp3d_pipeline_run(w3d_pipeline* p, int32_t batch, const float* in_h
     e = cudaEventRecord(p->ev_start, user);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_in, p->ev_start, 0);
   }
-  for (int32_t i = 0; i < batch && e == cudaSuccess; ++i) {
-    const int64_t j = p->seq + i;  // job number across calls
+  int64_t j = p->seq;  // job number across calls
+  for (int32_t i = 0; i < batch && e == cudaSuccess; i += p->vols, ++j) {
+    const int32_t kk = std::min(p->vols, batch - i);  // volumes i .. i + kk - 1
     const int s = static_cast<int>(j % p->depth);
     if (j >= p->depth) e = cudaStreamWaitEvent(p->s_in, p->ev_out[s], 0);  // slot free again
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(p->in_img[s], in_host + ni * size_t(i), ni * 4, cudaMemcpyHostToDevice,
-                          p->s_in);
+      e = cudaMemcpyAsync(p->in_img[s], in_host + ni * size_t(i), ni * 4 * size_t(kk),
+                          cudaMemcpyHostToDevice, p->s_in);
     if (e == cudaSuccess && lab)
-      e = cudaMemcpyAsync(p->in_lbl[s], in_labels_host + ni * size_t(i), ni,
+      e = cudaMemcpyAsync(p->in_lbl[s], in_labels_host + ni * size_t(i), ni * size_t(kk),
                           cudaMemcpyHostToDevice, p->s_in);
     if (e == cudaSuccess) e = cudaEventRecord(p->ev_in[s], p->s_in);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_comp, p->ev_in[s], 0);
     if (e != cudaSuccess) break;
-    st = warp3d_affine_batched(1, p->in_img[s], lab ? p->in_lbl[s] : nullptr, p->in_dims,
+    st = warp3d_affine_batched(kk, p->in_img[s], lab ? p->in_lbl[s] : nullptr, p->in_dims,
                                params + i, interp, fill, label_fill, p->out_img[s],
                                lab ? p->out_lbl[s] : nullptr, p->out_dims, p->s_comp);
     if (st != W3D_OK) return st;
     e = cudaEventRecord(p->ev_comp[s], p->s_comp);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_out, p->ev_comp[s], 0);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(out_host + no * size_t(i), p->out_img[s], no * 4,
+      e = cudaMemcpyAsync(out_host + no * size_t(i), p->out_img[s], no * 4 * size_t(kk),
                           cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess && lab)
-      e = cudaMemcpyAsync(out_labels_host + no * size_t(i), p->out_lbl[s], no,
+      e = cudaMemcpyAsync(out_labels_host + no * size_t(i), p->out_lbl[s], no * size_t(kk),
                           cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess) e = cudaEventRecord(p->ev_out[s], p->s_out);
   }
-  if (e == cudaSuccess)
-    e = cudaStreamWaitEvent(user, p->ev_out[(p->seq + batch - 1) % p->depth], 0);
-  p->seq += batch;
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(user, p->ev_out[(j - 1) % p->depth], 0);
+  p->seq = j;
   if (e != cudaSuccess) return cuda_fail(e, "warp3d_pipeline_run");
   return ok();
 }
+
+int32_t warp3d_pipeline_vols_per_job(const w3d_pipeline* p) { return p ? p->vols : 0; }
 
 w3d_status warp3d_pipeline_destroy(w3d_pipeline* p) {
   if (!p) return ok();

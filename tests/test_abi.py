@@ -182,6 +182,11 @@ def test_pipeline_create_validates(W):
     assert L.warp3d_pipeline_create(2, _lib.Dims(4, 4, 4), _lib.Dims(4, 4, 4), 4, ctypes.byref(h)) == 1
     assert L.warp3d_pipeline_run(None, 1, None, None, None, 0, 0.0, 0, None, None, None) == 1
     assert L.warp3d_pipeline_destroy(None) == 0
+    d = _lib.Dims(4, 4, 4)
+    assert L.warp3d_pipeline_create_ex(2, -1, d, d, 1, ctypes.byref(h)) == 1   # vols_per_job < 0
+    assert L.warp3d_pipeline_create_ex(2, 105, d, d, 1, ctypes.byref(h)) == 1  # > 104
+    assert L.warp3d_pipeline_create_ex(0, 1, d, d, 1, ctypes.byref(h)) == 1    # depth
+    assert L.warp3d_pipeline_vols_per_job(None) == 0
 
 
 def test_resample_host_functions_match_oracle(W):

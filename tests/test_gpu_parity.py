@@ -550,16 +550,18 @@ def test_footprint_counts_match_oracle_marking(W):
 
 
 # ----------------------------------------------------------------------------- FIFO pipeline
-@pytest.mark.parametrize("depth,B", [(1, 3), (2, 5), (3, 3), (3, 7)])
-def test_pipeline_matches_device_batched(W, depth, B):
-    """The host FIFO pipeline gives the device path's bits."""
+@pytest.mark.parametrize("depth,B,vols", [(1, 3, 1), (2, 5, 1), (3, 3, 0), (3, 7, 3), (2, 5, 2)])
+def test_pipeline_matches_device_batched(W, depth, B, vols):
+    """The host FIFO pipeline gives the device path's bits, for jobs
+    of one volume (the paper's), several, and a last job with fewer (B % vols)."""
     shape = (24, 32, 48)
     imgs, lbls, ds, As = _batch_inputs(shape, B, synth.TRAIN)
     params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(B)]
     ref, ref_l = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(),
                                          torch.from_numpy(lbls).cuda(), params, fill=-1000.0,
                                          label_fill=3)
-    pipe = W.Pipeline(shape, shape, depth=depth, labels=True)
+    pipe = W.Pipeline(shape, shape, depth=depth, labels=True, vols_per_job=vols)
+    assert pipe.vols_per_job == (vols or 8)   # automatic: 8 for volumes this small
     h_img = torch.from_numpy(imgs).pin_memory()
     h_lbl = torch.from_numpy(lbls).pin_memory()
     out = torch.empty(imgs.shape, dtype=torch.float32).pin_memory()
@@ -574,7 +576,7 @@ def test_pipeline_matches_device_batched(W, depth, B):
         # ... and bitwise against the device-resident call
         assert torch.equal(out, ref.cpu()) and torch.equal(out_l, ref_l.cpu())
     # images only
-    pipe2 = W.Pipeline(shape, shape, depth=depth, labels=False)
+    pipe2 = W.Pipeline(shape, shape, depth=depth, labels=False, vols_per_job=vols)
     out2 = torch.empty(imgs.shape, dtype=torch.float32).pin_memory()
     pipe2.run(h_img, None, params, out2, None, fill=-1000.0)
     torch.cuda.current_stream().synchronize()
@@ -584,8 +586,8 @@ def test_pipeline_matches_device_batched(W, depth, B):
     pipe2.close()
 
 
-@pytest.mark.parametrize("depth,B", [(1, 2), (2, 3), (3, 4)])
-def test_pipeline_chained_calls_back_to_back(W, depth, B):
+@pytest.mark.parametrize("depth,B,vols", [(1, 2, 1), (2, 3, 1), (3, 4, 1), (2, 5, 2), (3, 4, 0)])
+def test_pipeline_chained_calls_back_to_back(W, depth, B, vols):
     """W3D_PIPE_CHAIN: consecutive calls enqueued without a synchronisation between
     them (each into its own host outputs, slots wrapping across calls) give the
     device path's bits for every call."""
@@ -596,7 +598,7 @@ def test_pipeline_chained_calls_back_to_back(W, depth, B):
     ref, ref_l = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(),
                                          torch.from_numpy(lbls).cuda(), params, fill=-1000.0,
                                          label_fill=3)
-    pipe = W.Pipeline(shape, shape, depth=depth, labels=True, chain=True)
+    pipe = W.Pipeline(shape, shape, depth=depth, labels=True, chain=True, vols_per_job=vols)
     h_img = torch.from_numpy(imgs).pin_memory()
     h_lbl = torch.from_numpy(lbls).pin_memory()
     outs = [(torch.full((B, *shape), 7.0).pin_memory(),
