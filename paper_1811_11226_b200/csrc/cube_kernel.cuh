@@ -999,9 +999,12 @@ __device__ __forceinline__ void column_rows_impl(const WarpArgs& a, const VolDev
     if (ng == 4) {  // a whole 16-row column, normals precomputed: straight line, no rotation
       const std::false_type live_col;
 #ifndef W3D_NO_YTAB
-      // the tile's first row from the block index itself, so ptxas sees it uniform
+      // the tile's first row from the block index itself, so ptxas sees it uniform:
+      // without bricks the tile's y0 IS blockIdx.y * kTY (testing y0 == yb instead
+      // lets the compiler substitute y0's per-thread register for yb, and the table
+      // reads become per-thread LDC)
       const int yb = static_cast<int>(blockIdx.y) * kTY;
-      if (y0 == yb && yb + 16 <= kYTab) {  // row pairs from the uniform table
+      if (a.brick == 0 && yb + 16 <= kYTab) {  // row pairs from the uniform table
         auto yt = [&](int j) {
           return make_float2(c_ytab.v[yb + 2 * j], c_ytab.v[yb + 2 * j + 1]);
         };
