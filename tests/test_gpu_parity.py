@@ -343,6 +343,32 @@ def test_c3_batch16(W):
     check(g_img, g_lbl, ref, ds, FULL, "C3")
 
 
+def test_c3_batch16_through_the_pipeline_as_benched(W):
+    """The e2e leg's launch configuration at C3's full size: pinned host buffers through
+    the chained FIFO pipeline (depth 3, the library's job size: 8 volumes of C3), two
+    calls back to back; every voxel of both calls against the oracle and bitwise against
+    the device-resident call."""
+    shape = (160, 128, 128)
+    imgs, lbls, ds, As = _batch_inputs(shape, 16, synth.TRAIN)
+    params = [W.volume_params(As[i], _wph(W, ds[i], FULL, i)) for i in range(16)]
+    ref, ref_l = W.warp3d_affine_batched(torch.from_numpy(imgs).cuda(),
+                                         torch.from_numpy(lbls).cuda(), params, fill=-1000.0)
+    pipe = W.Pipeline(shape, shape, depth=3, labels=True, chain=True)
+    assert pipe.vols_per_job == 8
+    h_img = torch.from_numpy(imgs).pin_memory()
+    h_lbl = torch.from_numpy(lbls).pin_memory()
+    outs = [(torch.empty(imgs.shape, dtype=torch.float32).pin_memory(),
+             torch.empty(lbls.shape, dtype=torch.uint8).pin_memory()) for _ in range(2)]
+    for o, ol in outs:
+        pipe.run(h_img, h_lbl, params, o, ol, fill=-1000.0)
+    torch.cuda.current_stream().synchronize()
+    oref = _oracle_refs(imgs, lbls, As, ds, range(16), fill=-1000.0, label_fill=0)
+    for c, (o, ol) in enumerate(outs):
+        check(o.numpy(), ol.numpy(), oref, ds, FULL, f"C3 pipeline call {c}")
+        assert torch.equal(o, ref.cpu()) and torch.equal(ol, ref_l.cpu())
+    pipe.close()
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2])
 def test_c3_training_batch_with_occlusion(W, variant):
     """A C3 training batch with the paper's random occlusion: per
