@@ -78,6 +78,11 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
 #endif
 constexpr int kFuseR = 8, MX = 32, MZ = W3D_SM_MZ, kStages = W3D_SM_STAGES,
               kSmThreads = W3D_SM_THREADS;
+#ifdef W3D_SM_PAIR  // A/B knob: two planes per barrier
+constexpr int kLook = kStages - 2, kXBuf = 4;  // planes loaded ahead; x-result buffers
+#else
+constexpr int kLook = kStages - 1, kXBuf = 2;
+#endif
 struct Taps3 {
   float wx[2 * kFuseR + 1], wy[2 * kFuseR + 1], wz[2 * kFuseR + 1];
   int32_t rx, ry, rz;
@@ -130,7 +135,7 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
   constexpr int kPerC = (PC + NT - 1) / NT;  // chunks per thread (interior tiles)
   constexpr int P = 2 * RM + 1;              // z window; the plane loop's unroll
   constexpr int NL = (XP + RM + 4 + 3) / 4;  // 16 B words per x-pass thread
-  float* X = fuse_smem + kStages * PL;       // [2][AY][MX] x-pass results, two planes
+  float* X = fuse_smem + kStages * PL;       // [kXBuf][AY][MX] x-pass results
   float wx[2 * RM + 1], wy[2 * RM + 1], wz[2 * RM + 1];
 #pragma unroll
   for (int k = 0; k <= 2 * RM; ++k) {
@@ -193,9 +198,9 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
           if (soff[j] >= 0) cp_async4(dst + soff[j], src + goff[j]);
       }
     };
-    // (the previous segment's stages were last read before its final barrier)
+    // prologue: the first kLook planes, one cp.async group each
 #pragma unroll
-    for (int i = 0; i < kStages - 1; ++i) {
+    for (int i = 0; i < kLook; ++i) {
       if (i < nin) load_plane(i);
       cp_async_commit();
     }
@@ -204,6 +209,75 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
     bool ok[NYT];  // store bounds per row
 #pragma unroll
     for (int q = 0; q < NYT; ++q) ok[q] = gx < nx && gy0 + q < ny;
+    // x pass of plane i (its stage) into Xb
+    auto xpass = [&](int i, float* Xb) {
+      const float* A = fuse_smem + (i % kStages) * PL;
+#ifndef W3D_SM_SCALAR_X
+      // 4 outputs per thread from NL aligned 16 B loads (the taps of neighbouring
+      // outputs overlap: ~1 LDS per output instead of 2 RM + 1); same FMA order
+      // per output as the per-axis pass
+#pragma unroll
+      for (int r0 = 0; r0 < AY; r0 += 4 * NW) {
+        const int r = r0 + xr;
+        if (r0 + 4 * NW <= AY || r < AY) {
+          float v[4 * NL];
+#pragma unroll
+          for (int l = 0; l < NL; ++l)  // whole 16 B words even where only half is
+            lds128(A + r * AX + 4 * xj + 4 * l, v + 4 * l);  // used: no bank conflicts
+          float o[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], v[c + k + XP - RM], acc);
+            o[c] = acc;
+          }
+          *reinterpret_cast<float4*>(Xb + r * MX + 4 * xj) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+      }
+#else
+      for (int r = w; r < AY; r += NW) {  // A/B knob: one output per thread
+        const float* a = A + r * AX + lx + (XP - RM);
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], a[k], acc);
+        Xb[r * MX + lx] = acc;
+      }
+#endif
+    };
+    // y pass of plane j (x results in Xp) into ring slot S = j mod P, then, once the
+    // window is full (j >= 2 RM), its z pass: output plane oz + j - 2 RM
+    auto yzpass = [&](int j, auto slot_tag, const float* Xp) {
+      constexpr int S = decltype(slot_tag)::value;
+      float xv[NYT + 2 * RM];  // y pass: the thread's rows share their x-pass inputs
+#pragma unroll
+      for (int k = 0; k < NYT + 2 * RM; ++k) xv[k] = Xp[(NYT * w + k) * MX + lx];
+#pragma unroll
+      for (int q = 0; q < NYT; ++q) {
+        float yv = 0.0f;
+#pragma unroll
+        for (int k = 0; k <= 2 * RM; ++k) yv = __fmaf_rn(wy[k], xv[q + k], yv);
+        ring[q][S] = yv;
+      }
+      if (j >= 2 * RM) {
+        float acc[NYT];
+#pragma unroll
+        for (int q = 0; q < NYT; ++q) {
+          acc[q] = 0.0f;
+#pragma unroll
+          for (int k = 0; k <= 2 * RM; ++k)  // oldest (plane j - 2 RM: slot S + 1) first
+            acc[q] = __fmaf_rn(wz[k], ring[q][(S + 1 + k) % P], acc[q]);
+        }
+        float* pq = po;
+#pragma unroll
+        for (int q = 0; q < NYT; ++q) {
+          if (ok[q]) *pq = acc[q];
+          pq += nx;
+        }
+        po += plane;
+      }
+    };
+#ifndef W3D_SM_PAIR
     // One barrier per plane: the x pass of plane i (into X buffer i & 1) and the y /
     // z passes of plane i - 1 (from buffer (i - 1) & 1) share a phase.  Behind the
     // barrier of step i: plane i has landed, buffer (i - 1) & 1 is complete, buffer
@@ -211,80 +285,47 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
     // the next load overwrites was last read by the x pass of plane i - 1.
     auto plane_step = [&](int i, auto slot_tag) {
       constexpr int u = decltype(slot_tag)::value;  // slot of plane i: u = i mod P
-      cp_async_wait<kStages - 2>();
+      cp_async_wait<kLook - 1>();
       __syncthreads();
-      if (i < nin) {
-        const float* A = fuse_smem + (i % kStages) * PL;
-        float* Xb = X + (i & 1) * (AY * MX);
-#ifndef W3D_SM_SCALAR_X
-        // 4 outputs per thread from NL aligned 16 B loads (the taps of neighbouring
-        // outputs overlap: ~1 LDS per output instead of 2 RM + 1); same FMA order
-        // per output as the per-axis pass
-#pragma unroll
-        for (int r0 = 0; r0 < AY; r0 += 4 * NW) {
-          const int r = r0 + xr;
-          if (r0 + 4 * NW <= AY || r < AY) {
-            float v[4 * NL];
-#pragma unroll
-            for (int l = 0; l < NL; ++l)  // whole 16 B words even where only half is
-              lds128(A + r * AX + 4 * xj + 4 * l, v + 4 * l);  // used: no bank conflicts
-            float o[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float acc = 0.0f;
-#pragma unroll
-              for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], v[c + k + XP - RM], acc);
-              o[c] = acc;
-            }
-            *reinterpret_cast<float4*>(Xb + r * MX + 4 * xj) = make_float4(o[0], o[1], o[2], o[3]);
-          }
-        }
-#else
-        for (int r = w; r < AY; r += NW) {  // A/B knob: one output per thread
-          const float* a = A + r * AX + lx + (XP - RM);
-          float acc = 0.0f;
-#pragma unroll
-          for (int k = 0; k <= 2 * RM; ++k) acc = __fmaf_rn(wx[k], a[k], acc);
-          Xb[r * MX + lx] = acc;
-        }
-#endif
-      }
-      if (i + kStages - 1 < nin) load_plane(i + kStages - 1);  // into plane i-1's stage
+      if (i < nin) xpass(i, X + (i & 1) * (AY * MX));
+      if (i + kLook < nin) load_plane(i + kLook);  // into plane i-1's stage
       cp_async_commit();
-      if (i >= 1) {
-        const float* Xp = X + ((i - 1) & 1) * (AY * MX);
-        constexpr int up = (u + P - 1) % P;  // slot of plane i - 1
-        float xv[NYT + 2 * RM];  // y pass: the thread's rows share their x-pass inputs
-#pragma unroll
-        for (int k = 0; k < NYT + 2 * RM; ++k) xv[k] = Xp[(NYT * w + k) * MX + lx];
-#pragma unroll
-        for (int q = 0; q < NYT; ++q) {
-          float yv = 0.0f;
-#pragma unroll
-          for (int k = 0; k <= 2 * RM; ++k) yv = __fmaf_rn(wy[k], xv[q + k], yv);
-          ring[q][up] = yv;
-        }
-        if (i - 1 >= 2 * RM) {  // z pass: output plane oz + i - 1 - 2 RM complete
-          float acc[NYT];
-#pragma unroll
-          for (int q = 0; q < NYT; ++q) {
-            acc[q] = 0.0f;
-#pragma unroll
-            for (int k = 0; k <= 2 * RM; ++k)  // oldest (plane i - 1 - 2 RM: slot u) first
-              acc[q] = __fmaf_rn(wz[k], ring[q][(u + k) % P], acc[q]);
-          }
-          float* pq = po;
-#pragma unroll
-          for (int q = 0; q < NYT; ++q) {
-            if (ok[q]) *pq = acc[q];
-            pq += nx;
-          }
-          po += plane;
-        }
-      }
+      if (i >= 1)
+        yzpass(i - 1, std::integral_constant<int, (u + P - 1) % P>(),
+               X + ((i - 1) & 1) * (AY * MX));
     };
     for (int i0 = 0; i0 <= nin; i0 += P)
       for_each_slot(plane_step, i0, nin + 1, std::make_integer_sequence<int, P>());
+#else
+    // Two planes per barrier: step s x-passes planes 2s, 2s + 1 into buffers
+    // X[s & 1][0 / 1] and y / z-passes planes 2s - 2, 2s - 1 from X[(s - 1) & 1].
+    // Behind the barrier of step s: planes up to 2s + 1 have landed, X[(s - 1) & 1]
+    // is complete, X[s & 1] was last read in step s - 1, and the stages the next
+    // two loads overwrite (planes 2s + kLook, + 1; kStages >= kLook + 2) were last
+    // read by step s - 1's x passes.
+    auto pair_step = [&](int st, auto slot_tag) {
+      constexpr int u = decltype(slot_tag)::value;  // step st = u (mod P)
+      const int ia = 2 * st;
+      cp_async_wait<kLook - 2>();
+      __syncthreads();
+      float* Xc = X + (st & 1) * (2 * AY * MX);
+      if (ia < nin) xpass(ia, Xc);
+      if (ia + 1 < nin) xpass(ia + 1, Xc + AY * MX);
+      if (ia + kLook < nin) load_plane(ia + kLook);
+      cp_async_commit();
+      if (ia + 1 + kLook < nin) load_plane(ia + 1 + kLook);
+      cp_async_commit();
+      if (st >= 1) {
+        const float* Xp = X + ((st - 1) & 1) * (2 * AY * MX);
+        if (ia - 2 < nin) yzpass(ia - 2, std::integral_constant<int, (2 * u + 2 * P - 2) % P>(), Xp);
+        if (ia - 1 < nin)
+          yzpass(ia - 1, std::integral_constant<int, (2 * u + 2 * P - 1) % P>(), Xp + AY * MX);
+      }
+    };
+    const int nsteps = (nin + 1) / 2 + 1;
+    for (int s0 = 0; s0 < nsteps; s0 += P)
+      for_each_slot(pair_step, s0, nsteps, std::make_integer_sequence<int, P>());
+#endif
   }
 }
 
@@ -338,7 +379,7 @@ cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int
   auto go = [&](auto kernel, int RM, int nyt) {
     const int my = (kSmThreads / 32) * nyt, xp = RM <= 4 ? 4 : 8;
     const size_t smem =
-        sizeof(float) * (size_t(kStages) * (MX + 2 * xp) * (my + 2 * RM) + 2 * size_t(my + 2 * RM) * MX);
+        sizeof(float) * (size_t(kStages) * (MX + 2 * xp) * (my + 2 * RM) + kXBuf * size_t(my + 2 * RM) * MX);
     if (smem > 48 * 1024)
       e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem));
