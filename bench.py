@@ -700,7 +700,9 @@ def main():
         avg_launch_s = (total_ms / args.steps) * 1e-3 / per_step
         per_launch_bytes = alg_bytes / per_step
         achieved = per_launch_bytes / avg_launch_s / 1e9
-        ev = ncu_evidence(args.workload, args.variant) if not args.occlusion else None
+        # the committed captures are of the f32, occlusion-free launches only
+        ev = (ncu_evidence(args.workload, args.variant)
+              if not args.occlusion and args.input == "f32" else None)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
