@@ -65,6 +65,54 @@ bool cube_tma_supported(const WarpArgs& a) { return cube_supported(a); }
 // half-warps over the banks (tools/model_tiles.py); cp_p = cp_w * cp_h, so the
 // TMA box (cp_w, cp_h, cp_d) lands with the same pitches.  cp_rows = kTY when
 // the box fits the buffer, else 0 (per-tile exact boxes, parts, gathers).
+// Bank model of the staged corner loads (tools/bank_model.py): a warp's 32 lanes
+// (16 output x by 2 output z) read floor(p) + W floor(p_y) + W h floor(p_z) (+ a
+// corner offset, which rotates every lane's bank alike), so the shared-memory
+// wavefronts of a load depend on the plane pitch (W, W h) and on A.  kBankSamples
+// warp-rows of two sample tiles; their floors do not depend on the pitch.
+constexpr int kBankSamples = 4;
+struct BankFloors {
+  int32_t f[kBankSamples][3][32];
+};
+static void bank_floors(const float A[12], const int out[3], int tile_rows, BankFloors& F) {
+  const int tiles[3] = {(out[0] + 15) / 16, (out[1] + tile_rows - 1) / tile_rows, (out[2] + 15) / 16};
+  for (int smp = 0; smp < kBankSamples; ++smp) {
+    const int q = smp < kBankSamples / 2 ? 1 : 3;  // tiles at 1/4 and 3/4 of the grid
+    const int ox = 16 * ((tiles[0] * q) / 4), oy = tile_rows * ((tiles[1] * q) / 4);
+    const int oz = 16 * ((tiles[2] * q) / 4);
+    const int w = (5 * smp + 2 * (smp & 1)) % (cube::THREADS / 32);
+    const int r = (smp & 1) ? tile_rows - 1 : (smp * tile_rows) / (2 * kBankSamples);
+    for (int l = 0; l < 32; ++l) {
+      const float x = float(ox + (l & 15)), y = float(oy + r), z = float(oz + 2 * w + (l >> 4));
+      for (int k = 0; k < 3; ++k)
+        F.f[smp][k][l] = static_cast<int32_t>(
+            std::floor(A[4 * k] * x + A[4 * k + 1] * y + A[4 * k + 2] * z + A[4 * k + 3]));
+    }
+  }
+}
+// mean over the samples of max over banks of the distinct words addressed (<= 4 tracked)
+static int bank_cost(const BankFloors& F, int W, int h) {
+  const int32_t Pp = W * h;
+  int tot = 0;
+  for (int smp = 0; smp < kBankSamples; ++smp) {
+    int32_t tab[32][4];
+    uint8_t n[32] = {};
+    int worst = 1;
+    for (int l = 0; l < 32; ++l) {
+      const int32_t idx = F.f[smp][0][l] + W * F.f[smp][1][l] + Pp * F.f[smp][2][l];
+      const int b = idx & 31;
+      bool dup = false;
+      for (int k = 0; k < n[b]; ++k) dup |= tab[b][k] == idx;
+      if (!dup && n[b] < 4) {
+        tab[b][n[b]++] = idx;
+        worst = std::max(worst, int(n[b]));
+      }
+    }
+    tot += worst;
+  }
+  return tot;  // in units of 1 / kBankSamples wavefronts per load
+}
+
 void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[3],
                  const int out[3], int tile_rows) {
   using namespace cube;
@@ -128,6 +176,31 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[
   if (best_w == 0 || (!best_lbl && plain_lbl)) {  // unpadded
     best_w = W0;
     best_h = H0;
+  }
+  // the pitch the bank model prefers among the widths W0, W0 + chunk and up to 7 rows
+  // of padding, keeping the label box beside the image box if the rule above did
+  // (f32 16-row boxes; W3D_BANK_MODEL=0 restores the residue rule alone)
+  static const bool bank_model = !(getenv("W3D_BANK_MODEL") && getenv("W3D_BANK_MODEL")[0] == '0');
+  if (bank_model && elem_bytes == 4 && tile_rows == kTY) {
+    BankFloors F;
+    bank_floors(A, out, tile_rows, F);
+    const bool want_lbl = img_bytes_of(int64_t(best_w) * best_h) + lbl_bytes <= room && Wl <= 256;
+    int bc = bank_cost(F, best_w, best_h);
+    // search only when the rule's pitch averages more than 2 wavefronts per load (the
+    // volumes with the costly conflicts; ~5 us of host time per searched volume)
+    const bool search = bc > 2 * kBankSamples;
+    for (int Wc = W0; search && Wc <= W0 + kC && bc > kBankSamples; Wc += kC)
+      for (int h = H0; h < H0 + 8 && bc > kBankSamples; ++h) {
+        if (int64_t(Wc) * h * D > cap || (Wc == best_w && h == best_h)) continue;
+        const bool lbl = img_bytes_of(int64_t(Wc) * h) + lbl_bytes <= room && Wl <= 256;
+        if (want_lbl && !lbl) continue;
+        const int c = bank_cost(F, Wc, h);
+        if (c < bc || (c == bc && int64_t(Wc) * h < int64_t(best_w) * best_h)) {
+          bc = c;
+          best_w = Wc;
+          best_h = h;
+        }
+      }
   }
   const int64_t Pp = int64_t(best_w) * best_h;
   if (Pp * D > cap || best_w > 4 * THREADS || best_w > 256 || best_h > 256 || D > 256) return;
