@@ -181,14 +181,15 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[
   // of padding, keeping the label box beside the image box if the rule above did
   // (f32 16-row boxes; W3D_BANK_MODEL=0 restores the residue rule alone)
   static const bool bank_model = !(getenv("W3D_BANK_MODEL") && getenv("W3D_BANK_MODEL")[0] == '0');
-  if (bank_model && elem_bytes == 4 && tile_rows == kTY) {
+  if (bank_model && elem_bytes == 4) {
     BankFloors F;
     bank_floors(A, out, tile_rows, F);
     const bool want_lbl = img_bytes_of(int64_t(best_w) * best_h) + lbl_bytes <= room && Wl <= 256;
     int bc = bank_cost(F, best_w, best_h);
     // search only when the rule's pitch averages more than 2 wavefronts per load (the
     // volumes with the costly conflicts; ~5 us of host time per searched volume)
-    const bool search = bc > 2 * kBankSamples;
+    static const bool always = getenv("W3D_BANK_MODEL") && getenv("W3D_BANK_MODEL")[0] == '2';
+    const bool search = always || bc > 2 * kBankSamples;
     for (int Wc = W0; search && Wc <= W0 + kC && bc > kBankSamples; Wc += kC)
       for (int h = H0; h < H0 + 8 && bc > kBankSamples; ++h) {
         if (int64_t(Wc) * h * D > cap || (Wc == best_w && h == best_h)) continue;
