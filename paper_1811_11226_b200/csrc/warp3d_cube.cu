@@ -70,7 +70,10 @@ bool cube_tma_supported(const WarpArgs& a) { return cube_supported(a); }
 // corner offset, which rotates every lane's bank alike), so the shared-memory
 // wavefronts of a load depend on the plane pitch (W, W h) and on A.  kBankSamples
 // warp-rows of two sample tiles; their floors do not depend on the pitch.
-constexpr int kBankSamples = 4;
+#ifndef W3D_BANK_SAMPLES
+#define W3D_BANK_SAMPLES 4
+#endif
+constexpr int kBankSamples = W3D_BANK_SAMPLES;
 struct BankFloors {
   int32_t f[kBankSamples][3][32];
 };
