@@ -186,7 +186,11 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[
   // (f32 16-row boxes; W3D_BANK_MODEL=0 restores the residue rule alone)
   static const bool bank_model = !(getenv("W3D_BANK_MODEL") && getenv("W3D_BANK_MODEL")[0] == '0');
   // (float32 only: for int16 boxes the model's pick measured no change, 282.9 vs 282.9)
-  if (bank_model && elem_bytes == 4) {
+  // (float32 boxes of volumes with >= 256 output tiles: for a few tiles the call is
+  // launch- and host-bound and the ~5 us of modelling would show)
+  const int64_t ntiles = int64_t((out[0] + TX - 1) / TX) * ((out[1] + tile_rows - 1) / tile_rows) *
+                         ((out[2] + TZ - 1) / TZ);
+  if (bank_model && elem_bytes == 4 && ntiles >= 256) {
     const int eshift = 0;
     BankFloors F;
     bank_floors(A, out, tile_rows, F);
