@@ -678,7 +678,7 @@ def main():
     # e2e: pinned host buffers -> H2D -> warp -> D2H, inside the timed region
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(W, torch, dev, imgs, lbls, params, shape, min(args.steps, 20), world,
+        e2e = run_e2e(W, torch, dev, imgs, lbls, params, shape, min(args.steps, 60), world,
                       global_batch, nvox_out, args.pipe_vols)
 
     cpu = None

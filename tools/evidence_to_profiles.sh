@@ -35,3 +35,4 @@ if [ -f $G/ev_${TAG}_resample.ncu-rep ]; then
   python3 tools/ncu_summary.py $G/ev_${TAG}_resample.ncu-rep 134217728 > $OUT/ncu_full_resample_${TAG}.txt 2>&1
 fi
 python3 tools/ncu_traffic.py $TAG > /dev/null
+[ -f $G/ev_${TAG}_pcie.json ] && cp $G/ev_${TAG}_pcie.json $OUT/pcie_probe_${TAG}.json

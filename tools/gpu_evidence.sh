@@ -9,6 +9,7 @@ if [ "${SKIP_TESTS:-0}" != "1" ]; then
   timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/ev_${TAG}_gpu_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/ev_${TAG}_gpu_tests.log
   timeout 300 python __graft_entry__.py smoke > gpurun_out/ev_${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
 fi
+python tools/pcie_probe.py > gpurun_out/ev_${TAG}_pcie.json 2>&1; echo "pcie rc=$?"; head -1 gpurun_out/ev_${TAG}_pcie.json | cut -c1-160
 b() { name=$1; shift; timeout 900 python bench.py "$@" > gpurun_out/ev_${TAG}_bench_${name}.log 2>&1; echo "bench $name rc=$?"; tail -1 gpurun_out/ev_${TAG}_bench_${name}.log | cut -c1-140; }
 b c3
 b c1 --workload c1 --no-e2e
