@@ -78,11 +78,9 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
 #endif
 constexpr int kFuseR = 8, MX = 32, MZ = W3D_SM_MZ, kStages = W3D_SM_STAGES,
               kSmThreads = W3D_SM_THREADS;
-#ifdef W3D_SM_PAIR  // A/B knob: two planes per barrier
-constexpr int kLook = kStages - 2, kXBuf = 4;  // planes loaded ahead; x-result buffers
-#else
+// planes loaded ahead of the compute; x-result buffers (two planes per barrier --
+// four buffers, kStages - 2 ahead -- measured slower, profiles/round2/HISTORY.md)
 constexpr int kLook = kStages - 1, kXBuf = 2;
-#endif
 struct Taps3 {
   float wx[2 * kFuseR + 1], wy[2 * kFuseR + 1], wz[2 * kFuseR + 1];
   int32_t rx, ry, rz;
@@ -277,7 +275,6 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
         po += plane;
       }
     };
-#ifndef W3D_SM_PAIR
     // One barrier per plane: the x pass of plane i (into X buffer i & 1) and the y /
     // z passes of plane i - 1 (from buffer (i - 1) & 1) share a phase.  Behind the
     // barrier of step i: plane i has landed, buffer (i - 1) & 1 is complete, buffer
@@ -296,36 +293,6 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
     };
     for (int i0 = 0; i0 <= nin; i0 += P)
       for_each_slot(plane_step, i0, nin + 1, std::make_integer_sequence<int, P>());
-#else
-    // Two planes per barrier: step s x-passes planes 2s, 2s + 1 into buffers
-    // X[s & 1][0 / 1] and y / z-passes planes 2s - 2, 2s - 1 from X[(s - 1) & 1].
-    // Behind the barrier of step s: planes up to 2s + 1 have landed, X[(s - 1) & 1]
-    // is complete, X[s & 1] was last read in step s - 1, and the stages the next
-    // two loads overwrite (planes 2s + kLook, + 1; kStages >= kLook + 2) were last
-    // read by step s - 1's x passes.
-    auto pair_step = [&](int st, auto slot_tag) {
-      constexpr int u = decltype(slot_tag)::value;  // step st = u (mod P)
-      const int ia = 2 * st;
-      cp_async_wait<kLook - 2>();
-      __syncthreads();
-      float* Xc = X + (st & 1) * (2 * AY * MX);
-      if (ia < nin) xpass(ia, Xc);
-      if (ia + 1 < nin) xpass(ia + 1, Xc + AY * MX);
-      if (ia + kLook < nin) load_plane(ia + kLook);
-      cp_async_commit();
-      if (ia + 1 + kLook < nin) load_plane(ia + 1 + kLook);
-      cp_async_commit();
-      if (st >= 1) {
-        const float* Xp = X + ((st - 1) & 1) * (2 * AY * MX);
-        if (ia - 2 < nin) yzpass(ia - 2, std::integral_constant<int, (2 * u + 2 * P - 2) % P>(), Xp);
-        if (ia - 1 < nin)
-          yzpass(ia - 1, std::integral_constant<int, (2 * u + 2 * P - 1) % P>(), Xp + AY * MX);
-      }
-    };
-    const int nsteps = (nin + 1) / 2 + 1;
-    for (int s0 = 0; s0 < nsteps; s0 += P)
-      for_each_slot(pair_step, s0, nsteps, std::make_integer_sequence<int, P>());
-#endif
   }
 }
 
