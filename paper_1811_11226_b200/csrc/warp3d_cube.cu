@@ -87,9 +87,10 @@ static void bank_floors(const float A[12], const int out[3], int tile_rows, Bank
     const int r = (smp & 1) ? tile_rows - 1 : (smp * tile_rows) / (2 * kBankSamples);
     for (int l = 0; l < 32; ++l) {
       const float x = float(ox + (l & 15)), y = float(oy + r), z = float(oz + 2 * w + (l >> 4));
-      for (int k = 0; k < 3; ++k)
-        F.f[smp][k][l] = static_cast<int32_t>(
-            std::floor(A[4 * k] * x + A[4 * k + 1] * y + A[4 * k + 2] * z + A[4 * k + 3]));
+      for (int k = 0; k < 3; ++k) {  // clamped: far-off volumes must not overflow the cast
+        const float q = std::floor(A[4 * k] * x + A[4 * k + 1] * y + A[4 * k + 2] * z + A[4 * k + 3]);
+        F.f[smp][k][l] = static_cast<int32_t>(std::fmin(std::fmax(q, -1073741824.0f), 1073741824.0f));
+      }
     }
   }
 }
@@ -99,11 +100,15 @@ static int bank_cost(const BankFloors& F, int W, int h, int eshift) {
   const int32_t Pp = W * h;
   int tot = 0;
   for (int smp = 0; smp < kBankSamples; ++smp) {
-    int32_t tab[32][4];
+    uint32_t tab[32][4];
     uint8_t n[32] = {};
     int worst = 1;
     for (int l = 0; l < 32; ++l) {
-      const int32_t idx = (F.f[smp][0][l] + W * F.f[smp][1][l] + Pp * F.f[smp][2][l]) >> eshift;
+      // modulo 2^32 (unsigned: only the bank and equality matter)
+      const uint32_t idx = (static_cast<uint32_t>(F.f[smp][0][l]) +
+                            static_cast<uint32_t>(W) * static_cast<uint32_t>(F.f[smp][1][l]) +
+                            static_cast<uint32_t>(Pp) * static_cast<uint32_t>(F.f[smp][2][l])) >>
+                           eshift;
       const int b = idx & 31;
       bool dup = false;
       for (int k = 0; k < n[b]; ++k) dup |= tab[b][k] == idx;
