@@ -216,6 +216,17 @@ w3d_status warp3d_compose_affine(const w3d_geom* g, w3d_dims in_dims, w3d_dims o
                                  float affine_out[12]);
 
 /*
+ * warp3d_compose_params_batched -- host only: out[i].affine = warp3d_compose_affine(
+ * geoms[i]) and out[i].ph = ph[i] for i < n (one call per training batch instead of
+ * one per volume; the per-volume draws of PAPER.md:403-446 stay the caller's).
+ * Arrays of n elements, caller-owned; the photometric fields are validated as
+ * warp3d_affine_batched would.  W3D_ERR_INVALID_ARG names the first bad volume.
+ */
+w3d_status warp3d_compose_params_batched(int32_t n, const w3d_geom* geoms,
+                                         const w3d_photometric* ph, w3d_dims in_dims,
+                                         w3d_dims out_dims, w3d_volume_params* out);
+
+/*
  * warp3d_noise -- test hook: out[v] = sigma * n(seed, volume_id, v) over a
  * dense volume of `dims` (the noise term of PAPER.md:442 alone, R10).
  */

@@ -29,7 +29,7 @@ EXPORTS = (
     "warp3d_pipeline_destroy", "warp3d_resample_sigma", "warp3d_resample_dims",
     "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample",
     "warp3d_affine_batched_i16", "warp3d_affine_batched_i16_ex", "warp3d_affine_batched_v",
-    "warp3d_pipeline_create_ex", "warp3d_pipeline_vols_per_job",
+    "warp3d_pipeline_create_ex", "warp3d_pipeline_vols_per_job", "warp3d_compose_params_batched",
 )
 
 
@@ -94,6 +94,7 @@ def load():
     L.warp3d_affine_batched_ex.argtypes = [I32, P, P, Dims, P, I32, F, ctypes.c_uint8, P, P, Dims,
                                            I32, P]
     L.warp3d_compose_affine.argtypes = [P, Dims, Dims, P]
+    L.warp3d_compose_params_batched.argtypes = [I32, P, P, Dims, Dims, P]
     L.warp3d_noise.argtypes = [P, Dims, F, U64, U64, P]
     L.warp3d_philox4x32_10.argtypes = [P, U64, P, I64, P]
     L.warp3d_footprint_batched.argtypes = [I32, Dims, P, Dims, P, P, P]

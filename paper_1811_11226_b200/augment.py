@@ -9,8 +9,11 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
+from . import _lib as L
 from . import api
-from ._lib import PH_CLAMP, PH_GAMMA, PH_NOISE, PH_OCCLUDE, PH_WINDOW, VolumeParams
+from ._lib import PH_CLAMP, PH_GAMMA, PH_NOISE, PH_OCCLUDE, PH_WINDOW, Geom, Photometric, VolumeParams
 
 FULL = PH_NOISE | PH_WINDOW | PH_CLAMP | PH_GAMMA
 
@@ -28,19 +31,66 @@ def photometric_from_draw(draw, flags, seed, volume_id):
                            occ_z0=getattr(draw, "occ_z0", 0.0), occ_height=occ)
 
 
+def params_from_arrays(in_shape_zyx, rot_rad, scale, shear=None, flip=None, disp=None,
+                       generic=None, *, out_shape_zyx=None, flags=FULL, window=(0.0, 1.0),
+                       gamma=1.0, sigma=0.0, seed=0, volume_ids=None, occ_z0=None,
+                       occ_height=None):
+    """ctypes array of n VolumeParams from per-volume arrays (x, y, z columns): rot_rad,
+    scale, shear, disp [n, 3] float, flip [n, 3] bool, generic [n, 9] (G - I, row-major,
+    the w3d_geom convention) or None (G = I), window [n, 2] or one pair, gamma / sigma [n] or scalars, volume_ids [n]
+    (default 0..n-1), occ_z0 / occ_height [n] or None (an occ_height >= 0 sets
+    PH_OCCLUDE for that volume).  The affines are composed by one library call
+    (warp3d_compose_params_batched); no per-volume Python."""
+    out_shape_zyx = in_shape_zyx if out_shape_zyx is None else out_shape_zyx
+    rot_rad = np.asarray(rot_rad, dtype=np.float64).reshape(-1, 3)
+    n = rot_rad.shape[0]
+    geoms = (Geom * n)()
+    g = np.frombuffer(geoms, dtype=np.dtype(Geom))
+    g["rot_rad"] = rot_rad
+    g["scale"] = np.asarray(scale, dtype=np.float64).reshape(n, 3)
+    g["shear"] = 0.0 if shear is None else np.asarray(shear, dtype=np.float64).reshape(n, 3)
+    g["flip"] = 0 if flip is None else np.asarray(flip, dtype=bool).reshape(n, 3)
+    g["disp"] = 0.0 if disp is None else np.asarray(disp, dtype=np.float64).reshape(n, 3)
+    if generic is not None:
+        g["generic"] = np.asarray(generic, dtype=np.float64).reshape(n, 9)
+    phs = (Photometric * n)()
+    p = np.frombuffer(phs, dtype=np.dtype(Photometric))
+    fl = np.full(n, int(flags), dtype=np.uint32)
+    occ_h = np.zeros(n) if occ_height is None else np.asarray(occ_height, dtype=np.float64)
+    occ = occ_h >= 0.0 if occ_height is not None else np.zeros(n, dtype=bool)
+    fl[occ] |= PH_OCCLUDE
+    p["flags"] = fl
+    w = np.broadcast_to(np.asarray(window, dtype=np.float64), (n, 2))
+    p["window_lo"], p["window_hi"] = w[:, 0], w[:, 1]
+    p["gamma"] = gamma
+    p["noise_sigma"] = sigma
+    p["seed"] = int(seed)
+    p["volume_id"] = np.arange(n) if volume_ids is None else np.asarray(volume_ids, np.uint64)
+    p["occ_z0"] = 0.0 if occ_z0 is None else occ_z0
+    p["occ_height"] = np.where(occ, occ_h, 0.0)
+    out = (VolumeParams * n)()
+    L.check(L.load().warp3d_compose_params_batched(n, geoms, phs, L.dims(in_shape_zyx),
+                                                   L.dims(out_shape_zyx), out))
+    return out
+
+
 def build_params(draws, volume_ids, in_shape_zyx, out_shape_zyx=None, flags=FULL, seed=0,
                  sigma_override=None):
     """ctypes array of VolumeParams, volume i keyed by GLOBAL volume_ids[i]."""
-    out_shape_zyx = in_shape_zyx if out_shape_zyx is None else out_shape_zyx
-    arr = (VolumeParams * len(draws))()
-    for i, (d, vid) in enumerate(zip(draws, volume_ids)):
-        g = api.make_geom(d.rot_rad, d.scale, d.shear, d.flip, d.generic, d.disp)
-        A = api.warp3d_compose_affine(g, in_shape_zyx, out_shape_zyx)
-        ph = photometric_from_draw(d, flags, seed, vid)
-        if sigma_override is not None:
-            ph.noise_sigma = float(sigma_override)
-        arr[i] = api.volume_params(A, ph)
-    return arr
+    generic = None
+    if any(d.generic is not None for d in draws):
+        generic = [np.zeros(9) if d.generic is None else np.asarray(d.generic, dtype=np.float64)
+                   for d in draws]
+    occ_h = [getattr(d, "occ_height", -1.0) for d in draws]
+    occ_h = [(-1.0 if h is None else h) for h in occ_h]
+    return params_from_arrays(
+        in_shape_zyx, [d.rot_rad for d in draws], [d.scale for d in draws],
+        [d.shear for d in draws], [d.flip for d in draws], [d.disp for d in draws], generic,
+        out_shape_zyx=out_shape_zyx, flags=flags, window=[d.window for d in draws],
+        gamma=[d.gamma for d in draws],
+        sigma=[d.sigma for d in draws] if sigma_override is None else float(sigma_override),
+        seed=seed, volume_ids=list(volume_ids), occ_z0=[getattr(d, "occ_z0", 0.0) for d in draws],
+        occ_height=occ_h)
 
 
 class AugmentBatch:

@@ -723,6 +723,21 @@ w3d_status warp3d_compose_affine(const w3d_geom* g, w3d_dims in_dims, w3d_dims o
   return ok();
 }
 
+w3d_status warp3d_compose_params_batched(int32_t n, const w3d_geom* geoms,
+                                         const w3d_photometric* ph, w3d_dims in_dims,
+                                         w3d_dims out_dims, w3d_volume_params* out) {
+  if (n < 0 || (n > 0 && (!geoms || !ph || !out)))
+    return fail(W3D_ERR_INVALID_ARG, "n >= 0 and non-NULL geoms / ph / out");
+  for (int32_t i = 0; i < n; ++i) {
+    w3d_status st = check_ph(ph[i], i);
+    if (st != W3D_OK) return st;
+    if ((st = warp3d_compose_affine(&geoms[i], in_dims, out_dims, out[i].affine)) != W3D_OK)
+      return st;
+    out[i].ph = ph[i];
+  }
+  return ok();
+}
+
 // ---------------------------------------------------------------------------
 // Resampling to r mm (NEXT-3; readings R22-R25)
 // ---------------------------------------------------------------------------
