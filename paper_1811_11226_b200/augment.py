@@ -113,6 +113,18 @@ class AugmentBatch:
         # training steps if the caller draws new transforms)
         self._call = None
 
+    def set_params(self, params):
+        """Next step's per-volume parameters (a ctypes array of the same length, e.g. from
+        params_from_arrays), copied into the array the prepared call reads."""
+        if len(params) != len(self.params):
+            raise ValueError(f"{len(params)} params for a batch of {len(self.params)}")
+        if not isinstance(self.params, ctypes.Array):
+            self.params = (VolumeParams * len(self.params))(*self.params)
+            self._call = None
+        ctypes.memmove(self.params, (VolumeParams * len(params))(*params)
+                       if not isinstance(params, ctypes.Array) else params,
+                       ctypes.sizeof(VolumeParams) * len(params))
+
     def run(self):
         if self._call is None:
             api.warp3d_affine_batched(self.image, self.labels, self.params, fill=self.fill,

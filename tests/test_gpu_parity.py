@@ -975,3 +975,30 @@ def test_int16_with_occlusion_matches_float(W, interp):
     r_img, r_lbl = O.warp_volume(img, lbl, A, None, interp, -1000.0, 0, O.photometric(flags, **kw))
     assert np.array_equal(l32[0].cpu().numpy(), r_lbl)
     assert_image_close(o32[0].cpu().numpy(), r_img, d.window, d.gamma, True, "i16 occl")
+
+
+def test_augment_batch_new_params_each_step(W):
+    """A training loop: one AugmentBatch, new per-volume parameters each step through
+    set_params (built by params_from_arrays); every step equals the checked entry point
+    (itself oracle-checked above) on the same parameters bitwise."""
+    from paper_1811_11226_b200.augment import params_from_arrays
+    shape, B = (24, 32, 48), 3
+    imgs, lbls, ds, As = _batch_inputs(shape, B, synth.TRAIN)
+    img, lbl = torch.from_numpy(imgs).cuda(), torch.from_numpy(lbls).cuda()
+    rng = np.random.default_rng(5)
+    batch = None
+    for step in range(3):
+        rot = rng.uniform(-0.25, 0.25, (B, 3))
+        scale = rng.uniform(0.9, 1.1, (B, 3))
+        p = params_from_arrays(shape, rot, scale, disp=rng.uniform(-3, 3, (B, 3)),
+                               window=(-1000.0, 500.0), gamma=rng.uniform(0.7, 1.5, B),
+                               sigma=rng.uniform(0, 20, B), seed=9, volume_ids=[10 * step + i
+                                                                              for i in range(B)])
+        if batch is None:
+            batch = W.AugmentBatch(img, lbl, p, fill=-1000.0)
+        else:
+            batch.set_params(p)
+        out, out_l = batch.run()
+        ref, ref_l = W.warp3d_affine_batched(img, lbl, p, fill=-1000.0)
+        assert torch.equal(out, ref) and torch.equal(out_l, ref_l), f"step {step}"
+    torch.cuda.synchronize()
