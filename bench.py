@@ -23,6 +23,7 @@ import argparse
 import concurrent.futures as cf
 import ctypes
 import json
+import math
 import os
 import socket
 import statistics
@@ -78,6 +79,8 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pipe-vols", type=int, default=0,
                     help="e2e leg: volumes per pipeline job (0: the library's choice)")
+    ap.add_argument("--no-train-loop", action="store_true",
+                    help="skip the c3 line's train_loop key (new parameters every step)")
     ap.add_argument("--no-c5", action="store_true",
                     help="skip the configs[4] strong-scaling key of the c3 line")
     ap.add_argument("--input", choices=["f32", "i16"], default="f32",
@@ -578,6 +581,49 @@ def time_steps(W, batch, dev, steps, warmup, world, dist, torch, flush):
     return total, step_ms, launches, clk.summary()
 
 
+def train_loop(W, batch, dev, torch, shape, vids, steps):
+    """A training loop's augmentation: every step draws new per-volume transforms and
+    photometrics (numpy, the DESIGN.md Sec. 6 train ranges), builds the batch's
+    parameters in one library call (augment.params_from_arrays), hands them to the
+    prepared batch (set_params) and launches -- host work inside the timed region.
+    Device time from the first launch to the last (CUDA events), no L2 flush."""
+    from paper_1811_11226_b200.augment import FULL, params_from_arrays
+    B = len(vids)
+    rng = np.random.default_rng([synth.MASTER_SEED, 0x7121])
+    saved = type(batch.params)()  # the bench's own parameters, restored afterwards
+    ctypes.memmove(saved, batch.params, ctypes.sizeof(saved))
+
+    def step(k):
+        d = math.pi / 12.0
+        p = params_from_arrays(
+            shape, rng.uniform(-d, d, (B, 3)), rng.uniform(0.9, 1.1, (B, 3)),
+            rng.uniform(-0.1, 0.1, (B, 3)), rng.random((B, 3)) < 0.5,
+            rng.uniform(-8.0, 8.0, (B, 3)), flags=FULL,
+            window=np.stack([rng.uniform(-1000, -150, B), rng.uniform(230, 1500, B)], 1),
+            gamma=rng.uniform(0.7, 1.5, B), sigma=rng.uniform(0.0, 20.0, B),
+            seed=synth.MASTER_SEED, volume_ids=[v + B * k for v in vids])
+        batch.set_params(p)
+        batch.run()
+
+    for k in range(3):
+        step(k)
+    torch.cuda.synchronize(dev)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    s.record()
+    for k in range(steps):
+        step(3 + k)
+    host = time.perf_counter() - t0
+    e.record()
+    torch.cuda.synchronize(dev)
+    ms = s.elapsed_time(e)
+    batch.set_params(saved)
+    return {"value": B * int(np.prod(shape)) * steps / (ms * 1e-3) / 1e9, "unit": UNIT,
+            "steps": steps, "ms_per_step": ms / steps, "host_us_per_step": host / steps * 1e6,
+            "note": "new transforms + photometrics every step (params_from_arrays + "
+                    "set_params + launch on the host, inside the timed region), no L2 flush"}
+
+
 def latency_modes(W, batch, dev, torch, reps=50, rounds=20):
     """C1/C2 latency: the same pass as back-to-back launches (no
     flush, one event pair around `reps` passes) and as a CUDA graph of `reps` passes
@@ -657,6 +703,11 @@ def main():
     latency = None
     if args.workload in ("c1", "c2"):
         latency = latency_modes(W, batch, dev, torch)
+    # a training loop with new parameters every step (host work included)
+    tloop = None
+    if (args.workload == "c3" and not args.no_train_loop and not args.occlusion
+            and args.variant == "auto" and args.input == "f32" and not args.no_labels):
+        tloop = train_loop(W, batch, dev, torch, shape, vids, min(args.steps, 100))
 
     # configs[4] next to the weak-scaling c3 line: 256 volumes sharded over the ranks
     c5 = None
@@ -735,6 +786,8 @@ def main():
             line["c5"] = c5
         if latency is not None:
             line["latency"] = latency
+        if tloop is not None:
+            line["train_loop"] = tloop
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -87,36 +87,34 @@ static void bank_floors(const float A[12], const int out[3], int tile_rows, Bank
     const int r = (smp & 1) ? tile_rows - 1 : (smp * tile_rows) / (2 * kBankSamples);
     for (int l = 0; l < 32; ++l) {
       const float x = float(ox + (l & 15)), y = float(oy + r), z = float(oz + 2 * w + (l >> 4));
-      for (int k = 0; k < 3; ++k) {  // clamped: far-off volumes must not overflow the cast
-        const float q = std::floor(A[4 * k] * x + A[4 * k + 1] * y + A[4 * k + 2] * z + A[4 * k + 3]);
-        F.f[smp][k][l] = static_cast<int32_t>(std::fmin(std::fmax(q, -1073741824.0f), 1073741824.0f));
+      for (int k = 0; k < 3; ++k) {  // clamped (no overflowing cast), floor inline (no libm)
+        float q = A[4 * k] * x + A[4 * k + 1] * y + A[4 * k + 2] * z + A[4 * k + 3];
+        q = q < -1073741824.0f ? -1073741824.0f : (q > 1073741824.0f ? 1073741824.0f : q);
+        const int32_t t = static_cast<int32_t>(q);
+        F.f[smp][k][l] = t - (q < static_cast<float>(t) ? 1 : 0);
       }
     }
   }
 }
-// mean over the samples of max over banks of the distinct words addressed (<= 4 tracked);
+// mean over the samples of max over banks of the distinct words addressed: per bank a
+// 64-bit set of the words' rows (word >> 5) mod 64 -- branch-free; rows 2048 words
+// apart would alias, farther than one warp's loads reach in a staged box;
 // eshift: log2 of the elements per 4-byte word (0 for float32, 1 for int16)
-static int bank_cost(const BankFloors& F, int W, int h, int eshift) {
-  const int32_t Pp = W * h;
+static int bank_cost(const BankFloors& F, int W, int h, int eshift, int bound = 1 << 30) {
+  const uint32_t Wu = static_cast<uint32_t>(W), Pu = static_cast<uint32_t>(W * h);
   int tot = 0;
-  for (int smp = 0; smp < kBankSamples; ++smp) {
-    uint32_t tab[32][4];
-    uint8_t n[32] = {};
-    int worst = 1;
+  for (int smp = 0; smp < kBankSamples && tot <= bound; ++smp) {  // stop once worse
+    uint64_t rows[32] = {};
     for (int l = 0; l < 32; ++l) {
       // modulo 2^32 (unsigned: only the bank and equality matter)
       const uint32_t idx = (static_cast<uint32_t>(F.f[smp][0][l]) +
-                            static_cast<uint32_t>(W) * static_cast<uint32_t>(F.f[smp][1][l]) +
-                            static_cast<uint32_t>(Pp) * static_cast<uint32_t>(F.f[smp][2][l])) >>
+                            Wu * static_cast<uint32_t>(F.f[smp][1][l]) +
+                            Pu * static_cast<uint32_t>(F.f[smp][2][l])) >>
                            eshift;
-      const int b = idx & 31;
-      bool dup = false;
-      for (int k = 0; k < n[b]; ++k) dup |= tab[b][k] == idx;
-      if (!dup && n[b] < 4) {
-        tab[b][n[b]++] = idx;
-        worst = std::max(worst, int(n[b]));
-      }
+      rows[idx & 31] |= uint64_t(1) << ((idx >> 5) & 63);
     }
+    int worst = 1;
+    for (int bk = 0; bk < 32; ++bk) worst = std::max(worst, __builtin_popcountll(rows[bk]));
     tot += worst;
   }
   return tot;  // in units of 1 / kBankSamples wavefronts per load
@@ -205,12 +203,20 @@ void cube_cp_box(const float A[12], VolDev& P, int elem_bytes, const int /*in*/[
     // volumes with the costly conflicts; ~5 us of host time per searched volume)
     static const bool always = getenv("W3D_BANK_MODEL") && getenv("W3D_BANK_MODEL")[0] == '2';
     const bool search = always || bc > 2 * kBankSamples;
+    // a candidate's banks depend on (W mod 32, W h mod 32) only (up to rare equal
+    // addresses): one evaluation per residue pair, the smallest box first
+    uint32_t seen[8] = {};
+    seen[(best_w & 31) >> 2] |= 1u << ((best_w * best_h) & 31);
     for (int Wc = W0; search && Wc <= W0 + kC && bc > kBankSamples; Wc += kC)
       for (int h = H0; h < H0 + 8 && bc > kBankSamples; ++h) {
         if (int64_t(Wc) * h * D > cap || (Wc == best_w && h == best_h)) continue;
         const bool lbl = img_bytes_of(int64_t(Wc) * h) + lbl_bytes <= room && Wl <= 256;
         if (want_lbl && !lbl) continue;
-        const int c = bank_cost(F, Wc, h, eshift);
+        uint32_t& sw = seen[(Wc & 31) >> 2];
+        const uint32_t bit = 1u << ((Wc * h) & 31);
+        if (sw & bit) continue;
+        sw |= bit;
+        const int c = bank_cost(F, Wc, h, eshift, bc);
         if (c < bc || (c == bc && int64_t(Wc) * h < int64_t(best_w) * best_h)) {
           bc = c;
           best_w = Wc;
