@@ -227,6 +227,25 @@ w3d_status warp3d_compose_params_batched(int32_t n, const w3d_geom* geoms,
                                          w3d_dims out_dims, w3d_volume_params* out);
 
 /*
+ * warp3d_params_from_arrays -- host only: the same from per-volume arrays (a training
+ * loop's draws as numpy columns, no structs to fill): rot / scale / shear / disp
+ * double [n][3] (x, y, z), flip uint8 [n][3] (nonzero = flip), generic double [n][9]
+ * (G - I, row-major) or NULL, window double [n][2] (lo, hi), gamma / sigma double [n],
+ * volume_ids uint64 [n] or NULL (0 .. n-1), occ_z0 / occ_height double [n] or NULL
+ * (occ_height[i] >= 0 adds W3D_PH_OCCLUDE to `flags` for volume i); the photometric
+ * values are rounded to the float32 fields of w3d_photometric.  shear, flip,
+ * disp: NULL = zeros.  Validation and errors as warp3d_compose_params_batched.
+ */
+w3d_status warp3d_params_from_arrays(int32_t n, w3d_dims in_dims, w3d_dims out_dims,
+                                     const double* rot, const double* scale, const double* shear,
+                                     const uint8_t* flip, const double* disp,
+                                     const double* generic, uint32_t flags,
+                                     const double* window, const double* gamma, const double* sigma,
+                                     uint64_t seed, const uint64_t* volume_ids,
+                                     const double* occ_z0, const double* occ_height,
+                                     w3d_volume_params* out);
+
+/*
  * warp3d_noise -- test hook: out[v] = sigma * n(seed, volume_id, v) over a
  * dense volume of `dims` (the noise term of PAPER.md:442 alone, R10).
  */

@@ -30,6 +30,7 @@ EXPORTS = (
     "warp3d_resample_affine", "warp3d_smooth3d", "warp3d_resample",
     "warp3d_affine_batched_i16", "warp3d_affine_batched_i16_ex", "warp3d_affine_batched_v",
     "warp3d_pipeline_create_ex", "warp3d_pipeline_vols_per_job", "warp3d_compose_params_batched",
+    "warp3d_params_from_arrays",
 )
 
 
@@ -95,6 +96,8 @@ def load():
                                            I32, P]
     L.warp3d_compose_affine.argtypes = [P, Dims, Dims, P]
     L.warp3d_compose_params_batched.argtypes = [I32, P, P, Dims, Dims, P]
+    L.warp3d_params_from_arrays.argtypes = [I32, Dims, Dims, P, P, P, P, P, P, ctypes.c_uint32,
+                                            P, P, P, U64, P, P, P, P]
     L.warp3d_noise.argtypes = [P, Dims, F, U64, U64, P]
     L.warp3d_philox4x32_10.argtypes = [P, U64, P, I64, P]
     L.warp3d_footprint_batched.argtypes = [I32, Dims, P, Dims, P, P, P]

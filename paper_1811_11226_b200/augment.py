@@ -13,7 +13,7 @@ import numpy as np
 
 from . import _lib as L
 from . import api
-from ._lib import PH_CLAMP, PH_GAMMA, PH_NOISE, PH_OCCLUDE, PH_WINDOW, Geom, Photometric, VolumeParams
+from ._lib import PH_CLAMP, PH_GAMMA, PH_NOISE, PH_OCCLUDE, PH_WINDOW, VolumeParams
 
 FULL = PH_NOISE | PH_WINDOW | PH_CLAMP | PH_GAMMA
 
@@ -31,46 +31,52 @@ def photometric_from_draw(draw, flags, seed, volume_id):
                            occ_z0=getattr(draw, "occ_z0", 0.0), occ_height=occ)
 
 
+def _col(x, n, k, dtype):
+    """x as a C-contiguous [n, k] (or [n]) array of dtype, scalars broadcast."""
+    shape = (n,) if k == 1 else (n, k)
+    if isinstance(x, np.ndarray) and x.dtype == dtype and x.shape == shape and x.flags.c_contiguous:
+        return x
+    a = np.asarray(x, dtype=dtype)
+    if a.shape != shape:
+        a = np.broadcast_to(a, shape)
+    return np.ascontiguousarray(a)
+
+
+def _ptr(a):
+    # (ndarray.ctypes builds a helper object per call: ~10x the cost of the interface)
+    return None if a is None else a.__array_interface__["data"][0]
+
+
 def params_from_arrays(in_shape_zyx, rot_rad, scale, shear=None, flip=None, disp=None,
                        generic=None, *, out_shape_zyx=None, flags=FULL, window=(0.0, 1.0),
                        gamma=1.0, sigma=0.0, seed=0, volume_ids=None, occ_z0=None,
                        occ_height=None):
     """ctypes array of n VolumeParams from per-volume arrays (x, y, z columns): rot_rad,
     scale, shear, disp [n, 3] float, flip [n, 3] bool, generic [n, 9] (G - I, row-major,
-    the w3d_geom convention) or None (G = I), window [n, 2] or one pair, gamma / sigma [n] or scalars, volume_ids [n]
-    (default 0..n-1), occ_z0 / occ_height [n] or None (an occ_height >= 0 sets
-    PH_OCCLUDE for that volume).  The affines are composed by one library call
-    (warp3d_compose_params_batched); no per-volume Python."""
+    the w3d_geom convention) or None (G = I), window [n, 2] or one pair, gamma / sigma
+    [n] or scalars, volume_ids [n] (default 0..n-1), occ_z0 / occ_height [n] or None (an
+    occ_height >= 0 sets PH_OCCLUDE for that volume).  One library call
+    (warp3d_params_from_arrays) composes the affines and fills the photometrics; no
+    per-volume Python."""
     out_shape_zyx = in_shape_zyx if out_shape_zyx is None else out_shape_zyx
-    rot_rad = np.asarray(rot_rad, dtype=np.float64).reshape(-1, 3)
-    n = rot_rad.shape[0]
-    geoms = (Geom * n)()
-    g = np.frombuffer(geoms, dtype=np.dtype(Geom))
-    g["rot_rad"] = rot_rad
-    g["scale"] = np.asarray(scale, dtype=np.float64).reshape(n, 3)
-    g["shear"] = 0.0 if shear is None else np.asarray(shear, dtype=np.float64).reshape(n, 3)
-    g["flip"] = 0 if flip is None else np.asarray(flip, dtype=bool).reshape(n, 3)
-    g["disp"] = 0.0 if disp is None else np.asarray(disp, dtype=np.float64).reshape(n, 3)
-    if generic is not None:
-        g["generic"] = np.asarray(generic, dtype=np.float64).reshape(n, 9)
-    phs = (Photometric * n)()
-    p = np.frombuffer(phs, dtype=np.dtype(Photometric))
-    fl = np.full(n, int(flags), dtype=np.uint32)
-    occ_h = np.zeros(n) if occ_height is None else np.asarray(occ_height, dtype=np.float64)
-    occ = occ_h >= 0.0 if occ_height is not None else np.zeros(n, dtype=bool)
-    fl[occ] |= PH_OCCLUDE
-    p["flags"] = fl
-    w = np.broadcast_to(np.asarray(window, dtype=np.float64), (n, 2))
-    p["window_lo"], p["window_hi"] = w[:, 0], w[:, 1]
-    p["gamma"] = gamma
-    p["noise_sigma"] = sigma
-    p["seed"] = int(seed)
-    p["volume_id"] = np.arange(n) if volume_ids is None else np.asarray(volume_ids, np.uint64)
-    p["occ_z0"] = 0.0 if occ_z0 is None else occ_z0
-    p["occ_height"] = np.where(occ, occ_h, 0.0)
+    rot = np.ascontiguousarray(np.asarray(rot_rad, dtype=np.float64).reshape(-1, 3))
+    n = rot.shape[0]
+    keep = [rot, _col(scale, n, 3, np.float64),
+            None if shear is None else _col(shear, n, 3, np.float64),
+            None if flip is None else _col(np.asarray(flip, dtype=bool), n, 3, np.uint8),
+            None if disp is None else _col(disp, n, 3, np.float64),
+            None if generic is None else _col(np.asarray(generic, np.float64).reshape(n, 9), n, 9,
+                                              np.float64),
+            _col(window, n, 2, np.float64), _col(gamma, n, 1, np.float64),
+            _col(sigma, n, 1, np.float64),
+            None if volume_ids is None else _col(volume_ids, n, 1, np.uint64),
+            None if occ_z0 is None else _col(occ_z0, n, 1, np.float64),
+            None if occ_height is None else _col(occ_height, n, 1, np.float64)]
     out = (VolumeParams * n)()
-    L.check(L.load().warp3d_compose_params_batched(n, geoms, phs, L.dims(in_shape_zyx),
-                                                   L.dims(out_shape_zyx), out))
+    L.check(L.load().warp3d_params_from_arrays(
+        n, L.dims(in_shape_zyx), L.dims(out_shape_zyx), *[_ptr(k) for k in keep[:6]],
+        int(flags), *[_ptr(k) for k in keep[6:9]], int(seed), *[_ptr(k) for k in keep[9:]],
+        out))
     return out
 
 

@@ -764,6 +764,48 @@ w3d_status warp3d_compose_params_batched(int32_t n, const w3d_geom* geoms,
   return ok();
 }
 
+w3d_status warp3d_params_from_arrays(int32_t n, w3d_dims in_dims, w3d_dims out_dims,
+                                     const double* rot, const double* scale, const double* shear,
+                                     const uint8_t* flip, const double* disp,
+                                     const double* generic, uint32_t flags,
+                                     const double* window, const double* gamma, const double* sigma,
+                                     uint64_t seed, const uint64_t* volume_ids,
+                                     const double* occ_z0, const double* occ_height,
+                                     w3d_volume_params* out) {
+  if (n < 0 || (n > 0 && (!rot || !scale || !window || !gamma || !sigma || !out)))
+    return fail(W3D_ERR_INVALID_ARG, "n >= 0 and non-NULL rot / scale / window / gamma / sigma / out");
+  for (int32_t i = 0; i < n; ++i) {
+    w3d_geom g;
+    std::memset(&g, 0, sizeof(g));
+    for (int k = 0; k < 3; ++k) {
+      g.rot_rad[k] = rot[3 * i + k];
+      g.scale[k] = scale[3 * i + k];
+      g.shear[k] = shear ? shear[3 * i + k] : 0.0;
+      g.flip[k] = flip ? (flip[3 * i + k] != 0) : 0;
+      g.disp[k] = disp ? disp[3 * i + k] : 0.0;
+    }
+    if (generic)
+      for (int k = 0; k < 9; ++k) g.generic[k] = generic[9 * i + k];
+    w3d_photometric ph;
+    std::memset(&ph, 0, sizeof(ph));
+    const bool occ = occ_height && occ_height[i] >= 0.0;
+    ph.flags = flags | (occ ? uint32_t(W3D_PH_OCCLUDE) : 0u);
+    ph.window_lo = static_cast<float>(window[2 * i]);
+    ph.window_hi = static_cast<float>(window[2 * i + 1]);
+    ph.gamma = static_cast<float>(gamma[i]);
+    ph.noise_sigma = static_cast<float>(sigma[i]);
+    ph.seed = seed;
+    ph.volume_id = volume_ids ? volume_ids[i] : uint64_t(i);
+    ph.occ_z0 = occ_z0 ? static_cast<float>(occ_z0[i]) : 0.0f;
+    ph.occ_height = occ ? static_cast<float>(occ_height[i]) : 0.0f;
+    w3d_status st = check_ph(ph, i);
+    if (st != W3D_OK) return st;
+    if ((st = warp3d_compose_affine(&g, in_dims, out_dims, out[i].affine)) != W3D_OK) return st;
+    out[i].ph = ph;
+  }
+  return ok();
+}
+
 // ---------------------------------------------------------------------------
 // Resampling to r mm (NEXT-3; readings R22-R25)
 // ---------------------------------------------------------------------------
