@@ -942,14 +942,47 @@ w3d_status warp3d_resample(const float* in, const uint8_t* in_labels, w3d_dims i
       overlap(in, bi * 4, out, bo * 4) || overlap(in_labels, bi, out_labels, bo))
     return fail(W3D_ERR_INVALID_ARG, "buffers overlap");
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float A[12];
+  warp3d_resample_affine(in_dims, out_dims, spacing_mm, target_mm, A);
   // smoothed image in tmp[0 .. bi) (scratch tmp[bi .. 2 bi)), never the labels
   const float* src = in;
   if (sigma[0] > 0.0 || sigma[1] > 0.0 || sigma[2] > 0.0) {
-    if ((st = smooth_passes(in, in_dims, sigma, tmp, tmp + bi, s)) != W3D_OK) return st;
+    // The interpolation reads the smoothed image only at the trilinear corners of the
+    // output grid: p_k = fma(a_k, j, b_k) (R4 with a diagonal affine: the zero terms are
+    // exact), corners floor(p_k) and floor(p_k) + 1.  With the fused lowpass only those
+    // coordinates are computed and stored (the rest of tmp is left as it was); the
+    // values that are computed are the full lowpass's, bit for bit.
+    static const bool dense = getenv("W3D_RESAMPLE_DENSE") && getenv("W3D_RESAMPLE_DENSE")[0] == '1';
+    const int nin[3] = {in_dims.nx, in_dims.ny, in_dims.nz};
+    const int nout[3] = {out_dims.nx, out_dims.ny, out_dims.nz};
+    const bool maskable = !dense && smooth_fusable(sigma) && nin[0] <= kSmoothMaskMax &&
+                          nin[1] <= kSmoothMaskMax && nin[2] <= kSmoothMaskMax;
+    if (maskable) {
+      constexpr int kW = kSmoothMaskMax / 32;
+      static thread_local uint32_t mask[3 * kW];
+      std::memset(mask, 0, sizeof(mask));
+      for (int k = 0; k < 3; ++k) {
+        const float a = A[4 * k + k], b = A[4 * k + 3];
+        for (int j = 0; j < nout[k]; ++j) {
+          const float pk = std::fmaf(a, static_cast<float>(j), b);
+          const double f = std::floor(static_cast<double>(pk));
+          for (int c = 0; c < 2; ++c) {
+            const double i = f + c;
+            if (i >= 0.0 && i < nin[k]) {
+              const int ii = static_cast<int>(i);
+              mask[k * kW + (ii >> 5)] |= 1u << (ii & 31);
+            }
+          }
+        }
+      }
+      const cudaError_t e =
+          launch_smooth_fused(in, tmp, in_dims.nx, in_dims.ny, in_dims.nz, sigma, s, mask);
+      if (e != cudaSuccess) return cuda_fail(e, "warp3d_resample lowpass");
+    } else if ((st = smooth_passes(in, in_dims, sigma, tmp, tmp + bi, s)) != W3D_OK) {
+      return st;
+    }
     src = tmp;
   }
-  float A[12];
-  warp3d_resample_affine(in_dims, out_dims, spacing_mm, target_mm, A);
   const float* Ap = A;
   const w3d_photometric* none = nullptr;
   return run_batched(1, src, in_labels, in_dims, &Ap, &none, W3D_INTERP_LINEAR, fill, label_fill,

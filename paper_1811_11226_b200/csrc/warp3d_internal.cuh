@@ -142,8 +142,12 @@ cudaError_t launch_smooth_axis(int axis, const float* in, float* out, int nx, in
                                double sigma, cudaStream_t s);
 // all three passes in one kernel (radius <= 8 per axis), bit-identical to the passes
 bool smooth_fusable(const double sigma[3]);
+// mask (optional): 3 x kSmoothMaskMax / 32 words, bit i of axis k (x, y, z) set = output
+// coordinate i is needed; the others are neither computed nor stored (dims <= kSmoothMaskMax)
+constexpr int kSmoothMaskMax = 4096;
 cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int nz,
-                                const double sigma[3], cudaStream_t s);
+                                const double sigma[3], cudaStream_t s,
+                                const uint32_t* mask = nullptr);
 // warp3d_aux.cu (test hooks, measurement)
 cudaError_t launch_noise(float* out, int mx, int my, int mz, float sigma, uint32_t k0,
                          uint32_t k1, uint32_t v0, uint32_t v1, cudaStream_t s);

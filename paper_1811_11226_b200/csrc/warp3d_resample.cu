@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(256) smooth_axis_kernel(const float* __restric
 #define W3D_SM_MINB 1
 #endif
 constexpr int kFuseR = 8, MX = 32, MZ = W3D_SM_MZ, kStages = W3D_SM_STAGES,
+              kSmoothMaskWords = kSmoothMaskMax / 32,
               kSmThreads = W3D_SM_THREADS;
 // planes loaded ahead of the compute; x-result buffers (two planes per barrier --
 // four buffers, kStages - 2 ahead -- measured slower, profiles/round2/HISTORY.md)
@@ -84,6 +85,10 @@ constexpr int kLook = kStages - 1, kXBuf = 2;
 struct Taps3 {
   float wx[2 * kFuseR + 1], wy[2 * kFuseR + 1], wz[2 * kFuseR + 1];
   int32_t rx, ry, rz;
+  // optional output mask (warp3d_resample: only the voxels the 3 mm grid's trilinear
+  // corners read are computed and stored): bit i of mask[k] = coordinate i of axis k
+  int32_t masked;
+  uint32_t mask[3][kSmoothMaskWords];
 };
 
 extern __shared__ __align__(128) float fuse_smem[];
@@ -204,9 +209,14 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
     }
     const int gx = ox + lx, gy0 = oy + NYT * w;
     float* po = out + (static_cast<size_t>(oz) * ny + gy0) * nx + gx;
-    bool ok[NYT];  // store bounds per row
+    bool ok[NYT];  // store bounds per row (and the output mask's x / y bits)
+    const bool xneed = !t.masked || (gx < nx && ((t.mask[0][gx >> 5] >> (gx & 31)) & 1u));
 #pragma unroll
-    for (int q = 0; q < NYT; ++q) ok[q] = gx < nx && gy0 + q < ny;
+    for (int q = 0; q < NYT; ++q) {
+      const int gy = gy0 + q;
+      ok[q] = gx < nx && gy < ny && xneed &&
+              (!t.masked || ((t.mask[1][gy >> 5] >> (gy & 31)) & 1u));
+    }
     // x pass of plane i (its stage) into Xb
     auto xpass = [&](int i, float* Xb) {
       const float* A = fuse_smem + (i % kStages) * PL;
@@ -257,7 +267,10 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
         for (int k = 0; k <= 2 * RM; ++k) yv = __fmaf_rn(wy[k], xv[q + k], yv);
         ring[q][S] = yv;
       }
-      if (j >= 2 * RM) {
+      // output plane oz + j - 2 RM once the window is full; a masked-out plane skips
+      // its z pass and stores (CTA-uniform)
+      const int zo = oz + j - 2 * RM;
+      if (j >= 2 * RM && (!t.masked || ((t.mask[2][zo >> 5] >> (zo & 31)) & 1u))) {
         float acc[NYT];
 #pragma unroll
         for (int q = 0; q < NYT; ++q) {
@@ -272,8 +285,8 @@ __global__ void __launch_bounds__(kSmThreads, W3D_SM_MINB)
           if (ok[q]) *pq = acc[q];
           pq += nx;
         }
-        po += plane;
       }
+      if (j >= 2 * RM) po += plane;
     };
     // One barrier per plane: the x pass of plane i (into X buffer i & 1) and the y /
     // z passes of plane i - 1 (from buffer (i - 1) & 1) share a phase.  Behind the
@@ -333,8 +346,11 @@ bool smooth_fusable(const double sigma[3]) {
 }
 
 cudaError_t launch_smooth_fused(const float* in, float* out, int nx, int ny, int nz,
-                                const double sigma[3], cudaStream_t s) {
+                                const double sigma[3], cudaStream_t s, const uint32_t* mask) {
   Taps3 t;
+  t.masked = mask != nullptr;
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < kSmoothMaskWords; ++i) t.mask[k][i] = mask ? mask[k * kSmoothMaskWords + i] : 0u;
   t.rx = gauss_radius(sigma[0]);
   t.ry = gauss_radius(sigma[1]);
   t.rz = gauss_radius(sigma[2]);
