@@ -27,5 +27,6 @@ if [ "${NCU:-1}" == "1" ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_${TAG}_launches_c3.csv $CMD > /dev/null 2>&1; echo "ncu launches rc=$?"
   ncu --set full --clock-control none --import-source on -k regex:warp3d_cube -s 3 -c 1 -o gpurun_out/ev_${TAG}_c3 -f $CMD > /dev/null 2>&1; echo "ncu c3 rc=$?"
   ncu --set full --clock-control none --import-source on -k regex:warp3d_cube -s 3 -c 1 -o gpurun_out/ev_${TAG}_c4 -f $CMD --workload c4 > /dev/null 2>&1; echo "ncu c4 rc=$?"
-  ncu --set full --clock-control none --import-source on -k regex:smooth_fused -s 3 -c 1 -o gpurun_out/ev_${TAG}_resample -f $CMD --workload resample > /dev/null 2>&1; echo "ncu resample rc=$?"
+  # -s 6: skip the resample steps' (masked) lowpass launches, capture the first dense one (warp3d_smooth3d, what the roofline times)
+  ncu --set full --clock-control none --import-source on -k regex:smooth_fused -s 6 -c 1 -o gpurun_out/ev_${TAG}_resample -f $CMD --workload resample > /dev/null 2>&1; echo "ncu resample rc=$?"
 fi

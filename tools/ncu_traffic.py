@@ -11,8 +11,8 @@ caps = {
     "c3/auto": ("c3", "1 launch of warp3d_cube_kernel<float,16,3,1,0,1,0,16>, C3 16x128x128x160"),
     "c4/auto": ("c4", "1 launch of warp3d_cube_kernel<float,8,3,1,0,1,0,16>, C4 512^3, "
                       "8-row tiles in bricks"),
-    "resample/auto": ("resample", "1 launch of smooth_fused_kernel<2,4>, 512^3 f32, sigma 2/3 "
-                                  "voxel per axis"),
+    "resample/auto": ("resample", "1 launch of smooth_fused_kernel<2,4>, dense (warp3d_smooth3d), "
+                                  "512^3 f32, sigma 2/3 voxel per axis"),
 }
 out = {}
 for key, (w, what) in caps.items():
