@@ -41,7 +41,9 @@
 extern "C" {
 #endif
 
-#define WARP3D_ABI_VERSION 2
+/* 3: + warp3d_pipeline_create_ex / warp3d_pipeline_vols_per_job (multi-volume jobs),
+ *      warp3d_compose_params_batched, warp3d_params_from_arrays (additive) */
+#define WARP3D_ABI_VERSION 3
 
 typedef enum {
   W3D_OK = 0,

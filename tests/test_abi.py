@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported(W):
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(_lib.EXPORTS) == declared
-    assert W.warp3d_abi_version() == 2
+    assert W.warp3d_abi_version() == 3
 
 
 def test_struct_sizes_match_header(W):
